@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 VecKM_flow normal-flow path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl b200|reference]
+
+A step = one pass of the hot path (accumulate -> pool -> gather+MLP) over one
+synthetic slice per rank, inputs resident in HBM, L2 flushed between steps.
+Multi-GPU (torchrun, one rank per GPU): every rank processes its own slices,
+no data-path collective (weak scaling); timing is the max over ranks.
+`--impl reference` times the reference algorithm's CPU restatement
+(oracle/veckm_oracle.py, all host threads) on a bounded sample of the same
+workload; on N>1 only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "normal flows/sec (device-timed) at 1/2/4/8 B200; encoder HBM GB/s vs peak"
+UNIT = "flows/s"
+
+WORKLOADS = {
+    # name: (width, height, events per slice, delta, slices per rank per step, description)
+    "cfg1": (346, 260, 100_000, 10, 1, "configs[0]: 346x260 DAVIS slice, 100k events, delta 10"),
+    "cfg2": (640, 480, 1_000_000, 10, 1, "configs[1]: synthetic 640x480 slice, 1M events, delta 10"),
+    "cfg3": (1280, 720, 4_000_000, 20, 1, "configs[2]: 1280x720 slice, 4M events, delta 20"),
+    "cfg4": (346, 260, 200_000, 10, 125, "configs[3]: 346x260 slices of 200k events, 125 per rank per step"),
+    "cfg5": (1280, 720, 32_000_000, 10, 1, "configs[4]: 1280x720 slice, 32M events, delta 10 (single GPU)"),
+}
+
+
+def algorithmic_bytes(n, P, P_occ):
+    """per slice B = 56n + 516(3P + P_occ), split per kernel."""
+    k1 = 24 * n + 516 * P
+    k2 = 2 * 516 * P
+    k3 = 24 * n + 516 * P_occ + 8 * n
+    return k1, k2, k3
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), float(pk["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self._th = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._th = threading.Thread(target=self._run, daemon=True)
+            self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join()
+
+    def summary(self):
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+def _synth(n, W, H, seed):
+    # bench.synth_workload(..., "uniform_noise") semantics (bench.py:187-190, 209-213)
+    g = np.random.default_rng(seed)
+    t = g.uniform(0.0, 0.032, size=n)
+    x = g.integers(0, W, size=n)
+    y = g.integers(0, H, size=n)
+    o = np.argsort(t, kind="stable")
+    return np.stack([t[o], x[o].astype(np.float64), y[o].astype(np.float64)], axis=1)
+
+
+def cpu_reference(wl, steps, warmup, budget_s=90.0):
+    """Time the reference algorithm (oracle port, all host threads) on a bounded
+    sample: accumulate over the slice once (capped at 4M events, linear in n);
+    per step, pool + MLP over a strided query subset against that grid (the
+    reference's own bench_stage protocol, bench.py:233-285);
+    flows/s = 1 / (acc/n + (pool+mlp)/n_sub).  The subset size is picked from a
+    calibration step so the whole run stays within ~budget_s."""
+    from oracle import veckm_oracle as vo
+    from paper_2504_19417_b200.weights import generate_bases, init_weights
+    W, H, n, d, _, _ = WORKLOADS[wl]
+    cores = os.cpu_count() or 1
+    n_acc = min(n, 4_000_000)
+    X = _synth(n_acc, W, H, seed=0)
+    b = generate_bases(64)
+    fr = vo.Freqs(b.time_freqs, b.x_freqs, b.y_freqs, 25.0)
+    w = init_weights(64, 128, b, seed=0, dtype=np.float32)
+    t = X[:, 0] - X[0, 0]
+    xi, yi = X[:, 1].astype(np.int64), X[:, 2].astype(np.int64)
+    t_a = time.perf_counter()
+    g = vo.accumulate(t, xi, yi, W, H, d, d, fr, 0.016)
+    acc_s = time.perf_counter() - t_a
+    tab = vo.spatial_table(fr, d, d)
+
+    def pool_mlp(nq):
+        q = np.linspace(0, n_acc - 1, nq).astype(np.int64)
+        t_p = time.perf_counter()
+        emb, _ = vo.pool_threaded(g, tab, t[q], xi[q], yi[q], fr, 0.016, "f32", cores)
+        vo.mlp(w.w1, w.b1, w.w2, w.b2, vo.to_features(emb))
+        return time.perf_counter() - t_p
+
+    n_cal = 256 * cores
+    per_q = pool_mlp(n_cal) / n_cal
+    per_step = max(0.05, (budget_s - acc_s) / max(1, steps + warmup))
+    nsub = int(min(max(1024, per_step / per_q), 40_000 * cores))
+    times = []
+    for it in range(warmup + steps):
+        dt = pool_mlp(nsub)
+        if it >= warmup:
+            times.append(dt)
+    per_flow = acc_s / n_acc + statistics.median(times) / nsub
+    value = 1.0 / per_flow
+    sample = (f"{wl}: accumulate over {n_acc} events ({acc_s:.2f} s, once{'' if n_acc == n else ', extrapolated'}) "
+              f"+ pool+MLP on {nsub} strided queries per step, {cores} threads; per-flow cost extrapolated")
+    return value, cores, sample, statistics.median(times)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    value, cores, sample, step_s = cpu_reference(args.workload, args.steps, args.warmup)
+    W, H, n, d, slices, desc = WORKLOADS[args.workload]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (uniform noise, seeded)",
+        "config": {"workload": desc, "sensor": f"{W}x{H}", "events_per_slice": n, "delta": d,
+                   "parallelism": "host threads (reference CPU algorithm, oracle port)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2504_19417_b200 as pkg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    W, H, n, d, slices, desc = WORKLOADS[args.workload]
+    if args.slices:
+        slices = args.slices
+
+    bases = pkg.generate_bases(64, 25.0, (0, 1, 2))
+    w = pkg.init_weights(64, 128, bases, seed=0, dtype=np.float32)
+    eng = pkg.FlowEngine(W, H, d, d, 0.016, bases, w, device=local, mlp_mode=args.mlp_mode)
+
+    host = [_synth(n, W, H, seed=1000 * rank + s) for s in range(slices)]
+    P = W * H
+    p_occ = [int(len(np.unique(X[:, 2].astype(np.int64) * W + X[:, 1].astype(np.int64)))) for X in host]
+    evs = [torch.from_numpy(X).to(dev) for X in host]
+    t0s = [float(X[0, 0]) for X in host]
+    flows = [torch.empty((n, 2), dtype=torch.float32, device=dev) for _ in range(slices)]
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        for s in range(slices):
+            eng.predict_device(evs[s], t0s[s], flows=flows[s], stream=stream)
+
+    eng.set_profiling(slices == 1)
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    launches_per_call = eng.last_timings()[1]
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kern = []
+    launches = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+            if slices == 1:
+                kern.append(eng.last_timings()[0])
+            launches += launches_per_call * slices
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    flows_total = world * slices * n * args.steps
+    value = flows_total / (total_ms / 1e3)
+
+    # ---- end to end through the C-ABI host-buffer call (pinned buffers) ----
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(host[0]).pin_memory()
+        out = torch.empty((n, 2), dtype=torch.float32).pin_memory()
+        ev_np, out_np = pinned.numpy(), out.numpy()
+        lib = pkg._lib.load()
+
+        def call():
+            pkg._lib.check(lib.vkm_predict_host(eng._h, ev_np.ctypes.data, n, t0s[0], out_np.ctypes.data, None))
+
+        for _ in range(3):
+            call()
+        if world > 1:
+            dist.barrier()
+        k = max(5, args.steps // 2)
+        t_w = time.perf_counter()
+        for _ in range(k):
+            call()
+        e2e_s = time.perf_counter() - t_w
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": world * n * k / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 24 * n,
+               "d2h_bytes_per_step": 8 * n, "steps": k, "api": "vkm_predict_host (C-ABI, pinned host buffers)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    hbm_peak, tc_peak, peak_kind = load_peaks()
+    k1b, k2b, k3b = algorithmic_bytes(n, P, p_occ[0])
+    kernels = None
+    roofline = None
+    if kern:
+        avg = np.mean(np.array(kern), axis=0)
+        names = ["accumulate", "pool", "gather_mlp"]
+        byts = [k1b, k2b, k3b]
+        kernels = {}
+        for i, nm in enumerate(names):
+            gbs = byts[i] / (avg[i] * 1e-3) / 1e9
+            kernels[nm] = {"ms": float(avg[i]), "alg_bytes": int(byts[i]), "gbs": gbs, "frac_hbm": gbs / hbm_peak}
+        mlp_tflops = 33280.0 * n / (avg[2] * 1e-3) / 1e12
+        kernels["gather_mlp"]["mlp_tflops"] = mlp_tflops
+        kernels["gather_mlp"]["frac_tensor_bf16"] = mlp_tflops / tc_peak
+        dom = int(np.argmax(avg[:3]))
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                traffic = json.load(fh).get(args.workload, {}).get(names[dom])
+        except Exception:
+            pass
+        a = kernels[names[dom]]["gbs"]
+        roofline = {"bound": "hbm", "kernel": names[dom], "achieved": a, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": a / hbm_peak, "traffic": traffic, "alg_bytes_per_launch": int(byts[dom]),
+                    "peak_kind": peak_kind}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, cores, sample, _ = cpu_reference(args.workload, 3, 1, budget_s=20.0)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (uniform noise, seeded per rank), random-init weights D=64/hidden=128",
+        "config": {"workload": desc, "sensor": f"{W}x{H}", "events_per_slice": n, "delta": d,
+                   "slices_per_rank_per_step": slices, "embed_dim": 64, "hidden": 128,
+                   "mlp_mode": args.mlp_mode, "l2": "flushed between steps (512 MiB write, outside step events)",
+                   "parallelism": f"dp{world} (independent slices per rank, no collective)"},
+        "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
+        "cpu_baseline": cpu, "clocks": clk.summary(),
+        "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
+    ap.add_argument("--mlp-mode", default="auto", choices=["auto", "fp32", "f16x3", "bf16"])
+    ap.add_argument("--slices", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

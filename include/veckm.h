@@ -1,0 +1,143 @@
+/*
+ * veckm.h — C-ABI of the B200-native VecKM_flow normal-flow hot path
+ * (arXiv 2504.19417).  libveckm.so exports exactly these symbols.
+ *
+ * Plain C types only: pointers, sizes, doubles.  No torch / CUDA types in the
+ * signatures; streams travel as `void*` (a cudaStream_t, NULL = legacy default
+ * stream).  `*_dev` pointers are device memory on the handle's device, `*_host`
+ * pointers are host memory (pinned or pageable).
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/evflow/):
+ *   vkm_create        NormalFlowRegressor.__init__/_config/_resolve_pretrained
+ *                     (estimators.py:107-164), MlpWeights (flow.py:48-80),
+ *                     precompute_spatial_phases (encoder.py:173-179)
+ *   vkm_predict[_host] predict_flows with QuerySet.all (flow.py:155-197) as called by
+ *                     NormalFlowRegressor.predict (estimators.py:192-206)
+ *   vkm_encode[_host] encode + embed_to_features (encoder.py:371-412, flow.py:92-95) as
+ *                     called by LocalEventEncoder.transform (estimators.py:89-95)
+ *   vkm_grid          accumulate_grid + PixelGrid.embed/count (encoder.py:229-283,
+ *                     196-208); pooled=1 adds the window sums of _pool_batch
+ *                     (encoder.py:331-336) evaluated at every pixel
+ *   vkm_predict_batch the CLI's per-slice loop (cli.py:267-280) fused into one call
+ *   vkm_last_error    exception text of the reference's error hierarchy (errors.py:4-29)
+ *
+ * Event layout: the reference's (n, 3) float64 array [t, x, y], row-major,
+ * time-sorted ascending (validation.py:49-65 sorts before encoding); x, y are
+ * integer-valued pixel coordinates inside the sensor.  Output rows follow the
+ * input rows.  `t_start` is the slice's window start (the first timestamp,
+ * validation.py:59); pass NAN to have the device read events[0].t.
+ *
+ * Error convention: 0 = OK, VKM_EINVAL -> ValueError, VKM_EDIM ->
+ * DimensionMismatchError, VKM_ECUDA -> RuntimeError, VKM_EOOM -> MemoryError,
+ * VKM_EUNSUPPORTED -> NotImplementedError.  vkm_last_error() returns the
+ * thread-local message of the last failure.  Kernels never print.
+ *
+ * Threading: a handle is bound to one device, is not re-entrant, and all work
+ * is enqueued on the stream passed in.  Distinct handles may be driven
+ * concurrently from different host threads.
+ */
+#ifndef VECKM_H
+#define VECKM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VKM_VERSION 1
+
+enum {
+  VKM_OK = 0,
+  VKM_EINVAL = 1,
+  VKM_EDIM = 2,
+  VKM_ECUDA = 3,
+  VKM_EOOM = 4,
+  VKM_EUNSUPPORTED = 5
+};
+
+/* MLP execution modes of the flow head W2·relu(W1·f + b1) + b2 (flow.py:98-106). */
+enum {
+  VKM_MLP_AUTO = 0,   /* F16X3 when embed_dim == 64 and hidden == 128, else FP32 */
+  VKM_MLP_FP32 = 1,   /* CUDA-core FFMA, fp32 throughout                           */
+  VKM_MLP_F16X3 = 2,  /* tcgen05 kind::f16, 3-term hi/lo split: fp32-equivalent     */
+  VKM_MLP_BF16 = 3    /* tcgen05 kind::f16 single bf16 pass: fast, stated bound     */
+};
+
+typedef struct vkm_params {
+  int32_t width;      /* sensor width  (CameraGeometry, events.py:24-36)       */
+  int32_t height;     /* sensor height                                          */
+  int32_t delta_x;    /* pixel radius δx >= 1 (EncoderConfig, encoder.py:52)    */
+  int32_t delta_y;    /* pixel radius δy >= 1                                   */
+  int32_t embed_dim;  /* D, 1..64                                               */
+  int32_t hidden;     /* MLP hidden width, 0 = encoder-only handle, <= 256      */
+  double delta_t;     /* time radius in seconds (slice window = 2·delta_t)      */
+  int32_t device;     /* CUDA device ordinal                                    */
+  int32_t mlp_mode;   /* VKM_MLP_*                                              */
+} vkm_params;
+
+typedef struct vkm_handle vkm_handle;
+
+/* Library version (VKM_VERSION). */
+int vkm_version(void);
+
+/* Thread-local text of the last error ("" if none). */
+const char* vkm_last_error(void);
+
+/* Number of visible CUDA devices. */
+int vkm_device_count(int32_t* count);
+
+/* Create a handle: uploads the frequency vectors (f64[D] each: the bases the
+ * weights were trained with, flow.py:173-174) and, when hidden > 0, the head
+ * w1 (hidden x 2D row-major), b1 (hidden), w2 (2 x hidden), b2 (2), all f32. */
+int vkm_create(vkm_handle** out, const vkm_params* params,
+               const double* time_freqs, const double* x_freqs, const double* y_freqs,
+               const float* w1, const float* b1, const float* w2, const float* b2);
+
+void vkm_destroy(vkm_handle* h);
+
+/* Select the MLP mode after creation (VKM_MLP_*). */
+int vkm_set_mlp_mode(vkm_handle* h, int32_t mode);
+
+/* Per-event normal flow for every event of one slice.
+ * flows_dev: (n, 2) f32 [n_x, n_y]; NaN rows for empty neighbourhoods.
+ * counts_dev: (n) int32 neighbourhood sizes, or NULL. */
+int vkm_predict(vkm_handle* h, const double* events_dev, int64_t n, double t_start,
+                float* flows_dev, int32_t* counts_dev, void* stream);
+
+/* Per-event features [Re(emb); Im(emb)], (n, 2D) f32. */
+int vkm_encode(vkm_handle* h, const double* events_dev, int64_t n, double t_start,
+               float* feats_dev, int32_t* counts_dev, void* stream);
+
+/* Synchronous host-buffer variants: H2D of the events, the device path, D2H
+ * of the results, all on the handle's internal stream. */
+int vkm_predict_host(vkm_handle* h, const double* events_host, int64_t n, double t_start,
+                     float* flows_host, int32_t* counts_host);
+int vkm_encode_host(vkm_handle* h, const double* events_host, int64_t n, double t_start,
+                    float* feats_host, int32_t* counts_host);
+
+/* Many independent slices in one call.  Slice s holds events
+ * [offsets[s], offsets[s+1]) of events_dev; offsets_host has n_slices+1
+ * entries; t_starts_host has n_slices entries (NAN = first event). */
+int vkm_predict_batch(vkm_handle* h, const double* events_dev, const int64_t* offsets_host,
+                      int32_t n_slices, const double* t_starts_host,
+                      float* flows_dev, int32_t* counts_dev, void* stream);
+
+/* Parity hook: the per-pixel grid in the reference's PixelGrid layout.
+ * grid_dev: (width, height, D) complex64 as interleaved f32 pairs, [x][y][d];
+ * counts_dev: (width, height) int32.  pooled = 0: accumulate_grid sums;
+ * pooled = 1: window sums Σ G[x+i][y+j]·table[i][j] before de-phasing. */
+int vkm_grid(vkm_handle* h, const double* events_dev, int64_t n, double t_start,
+             int32_t pooled, float* grid_dev, int32_t* counts_dev, void* stream);
+
+/* Per-kernel device timing of the last call (ms), recorded with CUDA events
+ * when enabled: [0] accumulate, [1] pool, [2] gather+MLP, [3] total.
+ * *n_out receives the number of kernel launches of the last call. */
+int vkm_set_profiling(vkm_handle* h, int32_t enable);
+int vkm_last_timings(vkm_handle* h, float* ms_out, int32_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VECKM_H */

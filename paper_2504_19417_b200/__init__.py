@@ -1,0 +1,40 @@
+"""B200-native VecKM_flow normal-flow estimator (arXiv 2504.19417).
+
+Drop-in for the reference `evflow` estimator path:
+
+    from paper_2504_19417_b200 import NormalFlowRegressor
+    flows = NormalFlowRegressor(width=640, height=480, weights="head.vkmw").predict(X)
+
+`X` is an (n, 3) array of [t, x, y]; the result is (n, 2) float64 [n_x, n_y].
+Per-event work runs in hand-written sm_100a kernels behind the C-ABI in
+include/veckm.h (libveckm.so); there is no CPU fallback.
+"""
+
+__version__ = "0.1.0"
+
+from .engine import FlowEngine
+from .errors import (
+    DimensionMismatchError,
+    EmptyNeighborhoodError,
+    EventParseError,
+    EvflowError,
+    GeometryError,
+)
+from .estimators import LocalEventEncoder, NormalFlowRegressor
+from .validation import check_event_array, check_flow_array, slice_from_array
+from .weights import (
+    Bases,
+    MlpWeights,
+    generate_bases,
+    init_weights,
+    load_weights,
+    save_weights,
+    standard_normals,
+)
+
+__all__ = [
+    "FlowEngine", "NormalFlowRegressor", "LocalEventEncoder", "Bases", "MlpWeights", "generate_bases",
+    "init_weights", "load_weights", "save_weights", "standard_normals", "check_event_array",
+    "check_flow_array", "slice_from_array", "EvflowError", "EventParseError", "GeometryError",
+    "DimensionMismatchError", "EmptyNeighborhoodError",
+]

@@ -1,0 +1,513 @@
+// C-ABI of libveckm.so (declared in include/veckm.h).  Host-side orchestration
+// of the VecKM_flow kernels: handle/scratch management, parameter checks with
+// the reference's error semantics, stream-ordered launches, host-buffer
+// variants and per-kernel CUDA-event timing.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/veckm.h"
+#include "vkm_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+#define VKM_CK(x)                                                                              \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) {                                                                   \
+      int code_ = (e_ == cudaErrorMemoryAllocation) ? VKM_EOOM : VKM_ECUDA;                    \
+      return fail(code_, std::string(#x) + ": " + cudaGetErrorString(e_));                     \
+    }                                                                                          \
+  } while (0)
+
+int round_d8(int D) {
+  int d = 8;
+  while (d < D) d <<= 1;
+  return d;
+}
+
+}  // namespace
+
+struct vkm_handle {
+  vkm_params p{};
+  int D = 0, D8 = 0, planes = 0, hidden = 0, mode = VKM_MLP_FP32, num_sms = 148;
+  int64_t P = 0;
+  cudaStream_t stream = nullptr;
+  // constants
+  float* tf = nullptr;
+  float2* my = nullptr;
+  float2* mx = nullptr;
+  float* w1p = nullptr;  // [hidden][2*D8] padded
+  float* b1 = nullptr;
+  float* w2 = nullptr;
+  float* b2 = nullptr;
+  void* w1_f16_hi = nullptr;
+  void* w1_f16_lo = nullptr;
+  void* w1_bf16 = nullptr;
+  float w_scale_f16 = 1.f;
+  bool tc_ok = false;  // D == 64 && hidden == 128
+  // scratch
+  float2* G = nullptr;
+  int* C = nullptr;
+  float2* Q = nullptr;
+  int* NQ = nullptr;
+  float* feats = nullptr;
+  size_t feats_cap = 0;
+  int32_t* cnt_scratch = nullptr;
+  size_t cnt_cap = 0;
+  double* ev_stage = nullptr;
+  size_t ev_cap = 0;
+  float* out_stage = nullptr;
+  size_t out_cap = 0;
+  int32_t* cnt_stage = nullptr;
+  size_t cnt_stage_cap = 0;
+  // timing
+  bool profiling = false;
+  cudaEvent_t evt[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool have_timing = false;
+  int last_launches = 0;
+};
+
+namespace {
+
+template <class T>
+int grow(T** ptr, size_t* cap, size_t need) {
+  if (*cap >= need) return VKM_OK;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *cap = 0;
+  const size_t alloc = std::max<size_t>(need, 1);
+  VKM_CK(cudaMalloc(ptr, alloc * sizeof(T)));
+  *cap = alloc;
+  return VKM_OK;
+}
+
+vkm::DevTables tables(const vkm_handle* h) { return vkm::DevTables{h->tf, h->my, h->mx}; }
+vkm::GridBufs bufs(const vkm_handle* h) { return vkm::GridBufs{h->G, h->C, h->Q, h->NQ}; }
+
+void rec(vkm_handle* h, int i, cudaStream_t s) {
+  if (h->profiling) cudaEventRecord(h->evt[i], s);
+}
+
+// K1 + K2 for one slice on stream s.
+int encode_core(vkm_handle* h, const double* ev, int64_t n, double t0, int pooled, cudaStream_t s, int* launches) {
+  const int W = h->p.width, H = h->p.height;
+  VKM_CK(cudaMemsetAsync(h->G, 0, sizeof(float2) * 8 * h->planes * h->P, s));
+  VKM_CK(cudaMemsetAsync(h->C, 0, sizeof(int) * h->P, s));
+  vkm::launch_accumulate(ev, n, t0, h->p.delta_t, tables(h), W, H, h->D8, bufs(h), s);
+  if (n > 0) *launches += 1;
+  VKM_CK(cudaGetLastError());
+  rec(h, 1, s);
+  if (pooled) {
+    vkm::launch_pool(tables(h), W, H, h->D8, h->p.delta_x, h->p.delta_y, bufs(h), s, launches);
+    VKM_CK(cudaGetLastError());
+  }
+  rec(h, 2, s);
+  return VKM_OK;
+}
+
+int predict_one(vkm_handle* h, const double* ev, int64_t n, double t0, float* flows, int32_t* counts, cudaStream_t s,
+                int* launches) {
+  int rc = encode_core(h, ev, n, t0, 1, s, launches);
+  if (rc) return rc;
+  if (n <= 0) return VKM_OK;
+  const int W = h->p.width, H = h->p.height;
+  if ((h->mode == VKM_MLP_F16X3 || h->mode == VKM_MLP_BF16) && h->tc_ok) {
+    vkm::TcWeights tw{h->mode == VKM_MLP_BF16 ? h->w1_bf16 : h->w1_f16_hi, h->w1_f16_lo, h->b1, h->w2, h->b2,
+                      h->mode == VKM_MLP_BF16 ? 1.f : h->w_scale_f16};
+    vkm::launch_gather_mlp_tc(ev, n, t0, h->p.delta_t, tables(h), W, H, bufs(h), tw, h->mode, flows, counts,
+                              h->num_sms, s);
+    *launches += 1;
+  } else {
+    rc = grow(&h->feats, &h->feats_cap, size_t(n) * 2 * h->D8);
+    if (rc) return rc;
+    int32_t* cn = counts;
+    if (!cn) {
+      rc = grow(&h->cnt_scratch, &h->cnt_cap, size_t(n));
+      if (rc) return rc;
+      cn = h->cnt_scratch;
+    }
+    if (h->D8 != h->D) VKM_CK(cudaMemsetAsync(h->feats, 0, sizeof(float) * size_t(n) * 2 * h->D8, s));
+    vkm::launch_features(ev, n, t0, h->p.delta_t, tables(h), W, H, h->D8, h->D, bufs(h), h->feats, 2 * h->D8,
+                         h->D8, cn, s);
+    vkm::MlpDev md{h->w1p, h->b1, h->w2, h->b2, h->hidden};
+    vkm::launch_mlp_ffma(h->feats, cn, n, h->D8, md, flows, s);
+    *launches += 2;
+  }
+  VKM_CK(cudaGetLastError());
+  return VKM_OK;
+}
+
+int check_handle(const vkm_handle* h) {
+  if (!h) return fail(VKM_EINVAL, "null vkm_handle");
+  return VKM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vkm_version(void) { return VKM_VERSION; }
+
+const char* vkm_last_error(void) { return g_err.c_str(); }
+
+int vkm_device_count(int32_t* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    if (count) *count = 0;
+    return fail(VKM_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  if (count) *count = c;
+  return VKM_OK;
+}
+
+int vkm_create(vkm_handle** out, const vkm_params* params, const double* T, const double* X, const double* Y,
+               const float* w1, const float* b1, const float* w2, const float* b2) {
+  if (!out || !params) return fail(VKM_EINVAL, "vkm_create: null argument");
+  *out = nullptr;
+  const vkm_params& p = *params;
+  if (p.width < 1 || p.height < 1)
+    return fail(VKM_EINVAL, "geometry must be at least 1x1, got " + std::to_string(p.width) + "x" +
+                                std::to_string(p.height));
+  if (int64_t(p.width) * p.height > (int64_t(1) << 30)) return fail(VKM_EINVAL, "sensor too large (> 2^30 pixels)");
+  if (!(p.delta_t > 0) || !std::isfinite(p.delta_t)) return fail(VKM_EINVAL, "delta_t must be positive");
+  if (p.delta_x < 1 || p.delta_y < 1) return fail(VKM_EINVAL, "pixel radii must be >= 1");
+  if (p.delta_x > 100 || p.delta_y > 100) return fail(VKM_EUNSUPPORTED, "pixel radii above 100 are not supported");
+  if (p.embed_dim < 1) return fail(VKM_EINVAL, "embed_dim must be >= 1");
+  if (p.embed_dim > 64) return fail(VKM_EUNSUPPORTED, "embed_dim above 64 is not supported by the B200 kernels");
+  if (p.hidden < 0 || p.hidden > 256) return fail(VKM_EUNSUPPORTED, "hidden width must be in [0, 256]");
+  if (!T || !X || !Y) return fail(VKM_EINVAL, "frequency vectors are required");
+  for (int i = 0; i < p.embed_dim; ++i)
+    if (!std::isfinite(T[i]) || !std::isfinite(X[i]) || !std::isfinite(Y[i]))
+      return fail(VKM_EINVAL, "frequency vectors must be finite");
+  if (p.hidden > 0) {
+    if (!w1 || !b1 || !w2 || !b2) return fail(VKM_EINVAL, "weights are required when hidden > 0");
+    const size_t nw1 = size_t(p.hidden) * 2 * p.embed_dim;
+    for (size_t i = 0; i < nw1; ++i)
+      if (!std::isfinite(w1[i])) return fail(VKM_EINVAL, "weights must be finite");
+    for (int i = 0; i < p.hidden; ++i)
+      if (!std::isfinite(b1[i]) || !std::isfinite(w2[i]) || !std::isfinite(w2[p.hidden + i]))
+        return fail(VKM_EINVAL, "weights must be finite");
+    if (!std::isfinite(b2[0]) || !std::isfinite(b2[1])) return fail(VKM_EINVAL, "weights must be finite");
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(VKM_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+  if (p.device < 0 || p.device >= ndev) return fail(VKM_EINVAL, "device ordinal out of range");
+  DeviceGuard dg(p.device);
+  cudaDeviceProp prop;
+  VKM_CK(cudaGetDeviceProperties(&prop, p.device));
+  if (prop.major < 10) return fail(VKM_EUNSUPPORTED, std::string("libveckm targets sm_100a; device is ") + prop.name);
+
+  auto* h = new vkm_handle();
+  h->p = p;
+  h->D = p.embed_dim;
+  h->D8 = round_d8(p.embed_dim);
+  h->planes = h->D8 / 8;
+  h->hidden = p.hidden;
+  h->P = int64_t(p.width) * p.height;
+  h->num_sms = prop.multiProcessorCount;
+  h->tc_ok = (h->D == 64 && h->hidden == 128);
+  h->mode = p.mlp_mode == VKM_MLP_AUTO ? (h->tc_ok ? VKM_MLP_F16X3 : VKM_MLP_FP32) : p.mlp_mode;
+  if ((h->mode == VKM_MLP_F16X3 || h->mode == VKM_MLP_BF16) && !h->tc_ok) h->mode = VKM_MLP_FP32;
+
+  auto cleanup_fail = [&](int rc) {
+    vkm_destroy(h);
+    return rc;
+  };
+#define VKM_CKH(x)                                                                             \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) {                                                                   \
+      int code_ = (e_ == cudaErrorMemoryAllocation) ? VKM_EOOM : VKM_ECUDA;                    \
+      return cleanup_fail(fail(code_, std::string(#x) + ": " + cudaGetErrorString(e_)));       \
+    }                                                                                          \
+  } while (0)
+
+  VKM_CKH(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  for (auto& e : h->evt) VKM_CKH(cudaEventCreate(&e));
+
+  // Frequency tables.  Modulation factors are computed in f64 and rounded once
+  // (the reference's spatial table is f64 then cast, encoder.py:173-179).
+  const int D8 = h->D8, W = p.width, H = p.height;
+  std::vector<float> tf(D8, 0.f);
+  for (int c = 0; c < h->D; ++c) tf[c] = float(T[c]);
+  std::vector<float2> my(size_t(H) * D8), mx(size_t(W) * D8);
+  for (int y = 0; y < H; ++y)
+    for (int c = 0; c < D8; ++c) {
+      const double ang = c < h->D ? (double(y) / p.delta_y) * Y[c] : 0.0;
+      my[size_t(y) * D8 + c] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+    }
+  for (int x = 0; x < W; ++x)
+    for (int c = 0; c < D8; ++c) {
+      const double ang = c < h->D ? (double(x) / p.delta_x) * X[c] : 0.0;
+      mx[size_t(x) * D8 + c] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+    }
+  VKM_CKH(cudaMalloc(&h->tf, sizeof(float) * D8));
+  VKM_CKH(cudaMalloc(&h->my, sizeof(float2) * my.size()));
+  VKM_CKH(cudaMalloc(&h->mx, sizeof(float2) * mx.size()));
+  VKM_CKH(cudaMemcpy(h->tf, tf.data(), sizeof(float) * D8, cudaMemcpyHostToDevice));
+  VKM_CKH(cudaMemcpy(h->my, my.data(), sizeof(float2) * my.size(), cudaMemcpyHostToDevice));
+  VKM_CKH(cudaMemcpy(h->mx, mx.data(), sizeof(float2) * mx.size(), cudaMemcpyHostToDevice));
+
+  // Grid scratch: two planes-sets of 64 B/pixel plus int32 counts (516 B/pixel at D=64).
+  VKM_CKH(cudaMalloc(&h->G, sizeof(float2) * 8 * h->planes * h->P));
+  VKM_CKH(cudaMalloc(&h->Q, sizeof(float2) * 8 * h->planes * h->P));
+  VKM_CKH(cudaMalloc(&h->C, sizeof(int) * h->P));
+  VKM_CKH(cudaMalloc(&h->NQ, sizeof(int) * h->P));
+
+  if (h->hidden > 0) {
+    const int hid = h->hidden, D = h->D;
+    std::vector<float> w1p(size_t(hid) * 2 * D8, 0.f);
+    for (int r = 0; r < hid; ++r)
+      for (int c = 0; c < D; ++c) {
+        w1p[size_t(r) * 2 * D8 + c] = w1[size_t(r) * 2 * D + c];
+        w1p[size_t(r) * 2 * D8 + D8 + c] = w1[size_t(r) * 2 * D + D + c];
+      }
+    VKM_CKH(cudaMalloc(&h->w1p, sizeof(float) * w1p.size()));
+    VKM_CKH(cudaMalloc(&h->b1, sizeof(float) * hid));
+    VKM_CKH(cudaMalloc(&h->w2, sizeof(float) * 2 * hid));
+    VKM_CKH(cudaMalloc(&h->b2, sizeof(float) * 2));
+    VKM_CKH(cudaMemcpy(h->w1p, w1p.data(), sizeof(float) * w1p.size(), cudaMemcpyHostToDevice));
+    VKM_CKH(cudaMemcpy(h->b1, b1, sizeof(float) * hid, cudaMemcpyHostToDevice));
+    VKM_CKH(cudaMemcpy(h->w2, w2, sizeof(float) * 2 * hid, cudaMemcpyHostToDevice));
+    VKM_CKH(cudaMemcpy(h->b2, b2, sizeof(float) * 2, cudaMemcpyHostToDevice));
+    if (h->tc_ok) {
+      // fp16 hi/lo split of s·W1 with s = 2^e so that max|s·W1| <= 2^14.
+      float amax = 0.f;
+      for (float v : w1p) amax = std::max(amax, std::fabs(v));
+      int e = 0;
+      if (amax > 0.f) e = std::max(-30, std::min(40, 14 - int(std::ceil(std::log2(double(amax))))));
+      h->w_scale_f16 = std::ldexp(1.0f, e);
+      std::vector<uint16_t> hi(128 * 128), lo(128 * 128), bf(128 * 128);
+      for (int i = 0; i < 128 * 128; ++i) {
+        const float v = w1p[i] * h->w_scale_f16;
+        const __half vh = __float2half_rn(v);
+        const __half vl = __float2half_rn(v - __half2float(vh));
+        std::memcpy(&hi[i], &vh, 2);
+        std::memcpy(&lo[i], &vl, 2);
+        const __nv_bfloat16 vb = __float2bfloat16_rn(w1p[i]);
+        std::memcpy(&bf[i], &vb, 2);
+      }
+      std::vector<uint16_t> img(128 * 128);
+      VKM_CKH(cudaMalloc(&h->w1_f16_hi, 2 * 128 * 128));
+      VKM_CKH(cudaMalloc(&h->w1_f16_lo, 2 * 128 * 128));
+      VKM_CKH(cudaMalloc(&h->w1_bf16, 2 * 128 * 128));
+      vkm::build_umma_image_kmajor_128x128(hi.data(), img.data());
+      VKM_CKH(cudaMemcpy(h->w1_f16_hi, img.data(), 2 * 128 * 128, cudaMemcpyHostToDevice));
+      vkm::build_umma_image_kmajor_128x128(lo.data(), img.data());
+      VKM_CKH(cudaMemcpy(h->w1_f16_lo, img.data(), 2 * 128 * 128, cudaMemcpyHostToDevice));
+      vkm::build_umma_image_kmajor_128x128(bf.data(), img.data());
+      VKM_CKH(cudaMemcpy(h->w1_bf16, img.data(), 2 * 128 * 128, cudaMemcpyHostToDevice));
+    }
+  }
+#undef VKM_CKH
+  *out = h;
+  return VKM_OK;
+}
+
+void vkm_destroy(vkm_handle* h) {
+  if (!h) return;
+  DeviceGuard dg(h->p.device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  void* ptrs[] = {h->tf, h->my, h->mx, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
+                  h->G, h->C, h->Q, h->NQ, h->feats, h->cnt_scratch, h->ev_stage, h->out_stage, h->cnt_stage};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& e : h->evt)
+    if (e) cudaEventDestroy(e);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+int vkm_set_mlp_mode(vkm_handle* h, int32_t mode) {
+  if (int rc = check_handle(h)) return rc;
+  if (mode < VKM_MLP_AUTO || mode > VKM_MLP_BF16) return fail(VKM_EINVAL, "unknown MLP mode");
+  if (mode == VKM_MLP_AUTO) mode = h->tc_ok ? VKM_MLP_F16X3 : VKM_MLP_FP32;
+  if ((mode == VKM_MLP_F16X3 || mode == VKM_MLP_BF16) && !h->tc_ok)
+    return fail(VKM_EUNSUPPORTED, "tensor-core MLP modes need embed_dim == 64 and hidden == 128");
+  h->mode = mode;
+  return VKM_OK;
+}
+
+int vkm_predict(vkm_handle* h, const double* ev, int64_t n, double t_start, float* flows, int32_t* counts,
+                void* stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (h->hidden <= 0) return fail(VKM_EINVAL, "handle has no flow head (hidden == 0)");
+  if (n < 0) return fail(VKM_EINVAL, "n must be non-negative");
+  if (n > 0 && (!ev || !flows)) return fail(VKM_EINVAL, "null device buffer");
+  DeviceGuard dg(h->p.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int launches = 0;
+  rec(h, 0, s);
+  int rc = predict_one(h, ev, n, t_start, flows, counts, s, &launches);
+  rec(h, 3, s);
+  h->have_timing = h->profiling;
+  h->last_launches = launches;
+  return rc;
+}
+
+int vkm_encode(vkm_handle* h, const double* ev, int64_t n, double t_start, float* feats, int32_t* counts,
+               void* stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (n < 0) return fail(VKM_EINVAL, "n must be non-negative");
+  if (n > 0 && (!ev || !feats)) return fail(VKM_EINVAL, "null device buffer");
+  DeviceGuard dg(h->p.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int launches = 0;
+  rec(h, 0, s);
+  int rc = encode_core(h, ev, n, t_start, 1, s, &launches);
+  if (rc) return rc;
+  if (n > 0) {
+    vkm::launch_features(ev, n, t_start, h->p.delta_t, tables(h), h->p.width, h->p.height, h->D8, h->D, bufs(h),
+                         feats, 2 * h->D, h->D, counts, s);
+    launches += 1;
+    VKM_CK(cudaGetLastError());
+  }
+  rec(h, 3, s);
+  h->have_timing = h->profiling;
+  h->last_launches = launches;
+  return VKM_OK;
+}
+
+int vkm_predict_host(vkm_handle* h, const double* ev_host, int64_t n, double t_start, float* flows_host,
+                     int32_t* counts_host) {
+  if (int rc = check_handle(h)) return rc;
+  if (h->hidden <= 0) return fail(VKM_EINVAL, "handle has no flow head (hidden == 0)");
+  if (n < 0) return fail(VKM_EINVAL, "n must be non-negative");
+  if (n == 0) return VKM_OK;
+  if (!ev_host || !flows_host) return fail(VKM_EINVAL, "null host buffer");
+  DeviceGuard dg(h->p.device);
+  int rc = grow(&h->ev_stage, &h->ev_cap, size_t(n) * 3);
+  if (!rc) rc = grow(&h->out_stage, &h->out_cap, size_t(n) * 2);
+  if (!rc && counts_host) rc = grow(&h->cnt_stage, &h->cnt_stage_cap, size_t(n));
+  if (rc) return rc;
+  cudaStream_t s = h->stream;
+  VKM_CK(cudaMemcpyAsync(h->ev_stage, ev_host, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+  int launches = 0;
+  rec(h, 0, s);
+  rc = predict_one(h, h->ev_stage, n, t_start, h->out_stage, counts_host ? h->cnt_stage : nullptr, s, &launches);
+  if (rc) return rc;
+  rec(h, 3, s);
+  VKM_CK(cudaMemcpyAsync(flows_host, h->out_stage, sizeof(float) * 2 * n, cudaMemcpyDeviceToHost, s));
+  if (counts_host)
+    VKM_CK(cudaMemcpyAsync(counts_host, h->cnt_stage, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  VKM_CK(cudaStreamSynchronize(s));
+  h->have_timing = h->profiling;
+  h->last_launches = launches;
+  return VKM_OK;
+}
+
+int vkm_encode_host(vkm_handle* h, const double* ev_host, int64_t n, double t_start, float* feats_host,
+                    int32_t* counts_host) {
+  if (int rc = check_handle(h)) return rc;
+  if (n < 0) return fail(VKM_EINVAL, "n must be non-negative");
+  if (n == 0) return VKM_OK;
+  if (!ev_host || !feats_host) return fail(VKM_EINVAL, "null host buffer");
+  DeviceGuard dg(h->p.device);
+  int rc = grow(&h->ev_stage, &h->ev_cap, size_t(n) * 3);
+  if (!rc) rc = grow(&h->out_stage, &h->out_cap, size_t(n) * 2 * h->D);
+  if (!rc && counts_host) rc = grow(&h->cnt_stage, &h->cnt_stage_cap, size_t(n));
+  if (rc) return rc;
+  cudaStream_t s = h->stream;
+  VKM_CK(cudaMemcpyAsync(h->ev_stage, ev_host, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+  rc = vkm_encode(h, h->ev_stage, n, t_start, h->out_stage, counts_host ? h->cnt_stage : nullptr, s);
+  if (rc) return rc;
+  VKM_CK(cudaMemcpyAsync(feats_host, h->out_stage, sizeof(float) * 2 * h->D * n, cudaMemcpyDeviceToHost, s));
+  if (counts_host)
+    VKM_CK(cudaMemcpyAsync(counts_host, h->cnt_stage, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  VKM_CK(cudaStreamSynchronize(s));
+  return VKM_OK;
+}
+
+int vkm_predict_batch(vkm_handle* h, const double* ev, const int64_t* offsets, int32_t n_slices,
+                      const double* t_starts, float* flows, int32_t* counts, void* stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (h->hidden <= 0) return fail(VKM_EINVAL, "handle has no flow head (hidden == 0)");
+  if (n_slices < 0 || (n_slices > 0 && !offsets)) return fail(VKM_EINVAL, "bad slice offsets");
+  for (int s = 0; s < n_slices; ++s)
+    if (offsets[s + 1] < offsets[s] || offsets[s] < 0) return fail(VKM_EINVAL, "slice offsets must be non-decreasing");
+  DeviceGuard dg(h->p.device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int launches = 0;
+  rec(h, 0, st);
+  for (int s = 0; s < n_slices; ++s) {
+    const int64_t lo = offsets[s], cnt = offsets[s + 1] - offsets[s];
+    if (cnt == 0) continue;
+    const double t0 = t_starts ? t_starts[s] : NAN;
+    int rc = predict_one(h, ev + 3 * lo, cnt, t0, flows + 2 * lo, counts ? counts + lo : nullptr, st, &launches);
+    if (rc) return rc;
+  }
+  rec(h, 3, st);
+  h->have_timing = false;  // per-slice events are overwritten; only the total is meaningful
+  h->last_launches = launches;
+  return VKM_OK;
+}
+
+int vkm_grid(vkm_handle* h, const double* ev, int64_t n, double t_start, int32_t pooled, float* grid,
+             int32_t* counts, void* stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (n < 0) return fail(VKM_EINVAL, "n must be non-negative");
+  DeviceGuard dg(h->p.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int launches = 0;
+  int rc = encode_core(h, ev, n, t_start, pooled, s, &launches);
+  if (rc) return rc;
+  vkm::launch_grid_to_ref(pooled ? h->Q : h->G, pooled ? h->NQ : h->C, h->p.width, h->p.height, h->D, h->D8, grid,
+                          counts, s);
+  VKM_CK(cudaGetLastError());
+  return VKM_OK;
+}
+
+int vkm_set_profiling(vkm_handle* h, int32_t enable) {
+  if (int rc = check_handle(h)) return rc;
+  h->profiling = enable != 0;
+  return VKM_OK;
+}
+
+int vkm_last_timings(vkm_handle* h, float* ms, int32_t* n_out) {
+  if (int rc = check_handle(h)) return rc;
+  if (n_out) *n_out = h->last_launches;
+  if (!ms) return VKM_OK;
+  for (int i = 0; i < 4; ++i) ms[i] = -1.f;
+  if (!h->have_timing) return VKM_OK;
+  DeviceGuard dg(h->p.device);
+  VKM_CK(cudaEventSynchronize(h->evt[3]));
+  VKM_CK(cudaEventElapsedTime(&ms[0], h->evt[0], h->evt[1]));
+  VKM_CK(cudaEventElapsedTime(&ms[1], h->evt[1], h->evt[2]));
+  VKM_CK(cudaEventElapsedTime(&ms[2], h->evt[2], h->evt[3]));
+  VKM_CK(cudaEventElapsedTime(&ms[3], h->evt[0], h->evt[3]));
+  return VKM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// Launch wrappers for the VecKM_flow kernels (internal to libveckm.so).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vkm {
+
+struct DevTables {
+  const float* tf;     // f32(T_c), [D8]                       (encoder.py:223-224)
+  const float2* my;    // e^{i y Y_c / dy}, [H][D8] complex64   (modulation, y axis)
+  const float2* mx;    // e^{i x X_c / dx}, [W][D8] complex64   (modulation, x axis)
+};
+
+struct GridBufs {
+  float2* G;   // [planes][P][8]
+  int* C;      // [P]
+  float2* Q;   // [planes][P][8]
+  int* NQ;     // [P]
+};
+
+struct MlpDev {
+  const float* w1;   // [hidden][2*D8] padded: [Re(0..D8) | Im(0..D8)]
+  const float* b1;   // [hidden]
+  const float* w2;   // [2][hidden]
+  const float* b2;   // [2]
+  int hidden;
+};
+
+// K1: scatter per-event temporal phases into G and counts into C.
+void launch_accumulate(const double* ev, int64_t n, double t0, double delta_t, const DevTables& tb,
+                       int W, int H, int D8, const GridBufs& g, cudaStream_t s);
+// K2: windowed phase-weighted pooling of G -> Q, and box-sum of C -> NQ.
+void launch_pool(const DevTables& tb, int W, int H, int D8, int dx, int dy, const GridBufs& g,
+                 cudaStream_t s, int* launches);
+// K3a: gather Q at each event, de-phase, divide by the count -> features.
+// Row e gets Re at out[e*ld + c] and Im at out[e*ld + im_off + c] for c < Dout.
+void launch_features(const double* ev, int64_t n, double t0, double delta_t, const DevTables& tb,
+                     int W, int H, int D8, int Dout, const GridBufs& g, float* out, int ld, int im_off,
+                     int32_t* counts_out, cudaStream_t s);
+// K3b: FFMA two-layer head on padded features [n][2*D8] -> flows [n][2].
+void launch_mlp_ffma(const float* feats, const int32_t* counts, int64_t n, int D8, const MlpDev& m,
+                     float* flows, cudaStream_t s);
+// Layout conversion for the parity hook: planes -> reference [x][y][D] complex64.
+void launch_grid_to_ref(const float2* G, const int* C, int W, int H, int D, int D8, float* out_grid,
+                        int32_t* out_counts, cudaStream_t s);
+
+// tcgen05 fused gather + de-phase + MLP (D = 64, hidden = 128).
+struct TcWeights {
+  const void* w1_hi;   // UMMA K-major SW128 image of W1 hi (fp16 or bf16), 32 KB
+  const void* w1_lo;   // same for the lo split, 32 KB
+  const float* b1;     // [128]
+  const float* w2;     // [2][128]
+  const float* b2;     // [2]
+  float w_scale;       // power-of-two pre-scale folded into the W1 images
+};
+void launch_gather_mlp_tc(const double* ev, int64_t n, double t0, double delta_t, const DevTables& tb,
+                          int W, int H, const GridBufs& g, const TcWeights& w, int mode, float* flows,
+                          int32_t* counts_out, int num_sms, cudaStream_t s);
+// Host helper: build the UMMA smem image (K-major, 128B swizzle) of a 128x128 fp16/bf16 matrix.
+void build_umma_image_kmajor_128x128(const uint16_t* rowmajor, uint16_t* image);
+
+}  // namespace vkm

@@ -1,0 +1,176 @@
+"""`FlowEngine`: one libveckm handle (one device, one sensor geometry, one head).
+
+Host-buffer calls go through `vkm_predict_host` / `vkm_encode_host` (the C-ABI
+does its own H2D/D2H).  Device calls take torch CUDA tensors; torch is only the
+allocator and stream provider here, the work is the C-ABI's kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .weights import Bases, MlpWeights
+
+_dptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+_fptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_float))  # noqa: E731
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class FlowEngine:
+    """Device-resident encoder (+ optional flow head) for one sensor geometry.
+
+    Mirrors what `predict_flows` (flow.py:155-197) needs per slice: the weights'
+    own bases (flow.py:173-174), the window radii and delta_t.
+    """
+
+    def __init__(self, width: int, height: int, delta_x: int, delta_y: int, delta_t: float,
+                 bases: Bases, weights: Optional[MlpWeights] = None, device: int = 0,
+                 mlp_mode: str = "auto"):
+        lib = _lib.load()
+        self._lib = lib
+        self.width, self.height = int(width), int(height)
+        self.delta_x, self.delta_y = int(delta_x), int(delta_y)
+        self.delta_t = float(delta_t)
+        self.device = int(device)
+        self.embed_dim = bases.dim
+        self.hidden = 0 if weights is None else weights.hidden
+        p = _lib.VkmParams(self.width, self.height, self.delta_x, self.delta_y, self.embed_dim,
+                           self.hidden, self.delta_t, self.device, _lib.MLP_MODES[mlp_mode])
+        T = np.ascontiguousarray(bases.time_freqs, dtype=np.float64)
+        X = np.ascontiguousarray(bases.x_freqs, dtype=np.float64)
+        Y = np.ascontiguousarray(bases.y_freqs, dtype=np.float64)
+        if weights is not None:
+            w1 = np.ascontiguousarray(weights.w1, dtype=np.float32)
+            b1 = np.ascontiguousarray(weights.b1, dtype=np.float32)
+            w2 = np.ascontiguousarray(weights.w2, dtype=np.float32)
+            b2 = np.ascontiguousarray(weights.b2, dtype=np.float32)
+            wp = [_fptr(w1), _fptr(b1), _fptr(w2), _fptr(b2)]
+        else:
+            wp = [None, None, None, None]
+        h = C.c_void_p()
+        _lib.check(lib.vkm_create(C.byref(h), C.byref(p), _dptr(T), _dptr(X), _dptr(Y), *wp))
+        self._h = h
+
+    # -- lifecycle ---------------------------------------------------------
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.vkm_destroy(h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_mlp_mode(self, mode: str) -> None:
+        _lib.check(self._lib.vkm_set_mlp_mode(self._h, _lib.MLP_MODES[mode]))
+
+    def set_profiling(self, enable: bool) -> None:
+        _lib.check(self._lib.vkm_set_profiling(self._h, int(bool(enable))))
+
+    def last_timings(self):
+        """(ms[accumulate, pool, gather+mlp, total], kernel launches) of the last call."""
+        ms = (C.c_float * 4)()
+        n = C.c_int32()
+        _lib.check(self._lib.vkm_last_timings(self._h, ms, C.byref(n)))
+        return list(ms), int(n.value)
+
+    # -- host-buffer API ---------------------------------------------------
+    def predict_host(self, events: np.ndarray, t_start: float = math.nan, return_counts: bool = False):
+        ev = np.ascontiguousarray(events, dtype=np.float64)
+        n = len(ev)
+        flows = np.empty((n, 2), dtype=np.float32)
+        counts = np.empty(n, dtype=np.int32) if return_counts else None
+        if n:
+            _lib.check(self._lib.vkm_predict_host(self._h, ev.ctypes.data, n, float(t_start),
+                                                  flows.ctypes.data,
+                                                  counts.ctypes.data if counts is not None else None))
+        return (flows, counts) if return_counts else flows
+
+    def encode_host(self, events: np.ndarray, t_start: float = math.nan, return_counts: bool = False):
+        ev = np.ascontiguousarray(events, dtype=np.float64)
+        n = len(ev)
+        feats = np.empty((n, 2 * self.embed_dim), dtype=np.float32)
+        counts = np.empty(n, dtype=np.int32) if return_counts else None
+        if n:
+            _lib.check(self._lib.vkm_encode_host(self._h, ev.ctypes.data, n, float(t_start),
+                                                 feats.ctypes.data,
+                                                 counts.ctypes.data if counts is not None else None))
+        return (feats, counts) if return_counts else feats
+
+    # -- device API (torch tensors) -----------------------------------------
+    def _stream(self, stream):
+        torch = _torch()
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        return C.c_void_p(stream.cuda_stream)
+
+    @staticmethod
+    def _check_events(ev):
+        if ev.dtype.itemsize != 8 or ev.ndim != 2 or ev.shape[1] != 3 or not ev.is_contiguous() or not ev.is_cuda:
+            raise ValueError("device events must be a contiguous CUDA float64 tensor of shape (n, 3)")
+
+    def predict_device(self, events, t_start: float = math.nan, flows=None, counts=None, stream=None):
+        torch = _torch()
+        self._check_events(events)
+        n = events.shape[0]
+        if flows is None:
+            flows = torch.empty((n, 2), dtype=torch.float32, device=events.device)
+        _lib.check(self._lib.vkm_predict(self._h, C.c_void_p(events.data_ptr()), n, float(t_start),
+                                         C.c_void_p(flows.data_ptr()),
+                                         C.c_void_p(counts.data_ptr()) if counts is not None else None,
+                                         self._stream(stream)))
+        return flows
+
+    def encode_device(self, events, t_start: float = math.nan, feats=None, counts=None, stream=None):
+        torch = _torch()
+        self._check_events(events)
+        n = events.shape[0]
+        if feats is None:
+            feats = torch.empty((n, 2 * self.embed_dim), dtype=torch.float32, device=events.device)
+        _lib.check(self._lib.vkm_encode(self._h, C.c_void_p(events.data_ptr()), n, float(t_start),
+                                        C.c_void_p(feats.data_ptr()),
+                                        C.c_void_p(counts.data_ptr()) if counts is not None else None,
+                                        self._stream(stream)))
+        return feats
+
+    def predict_batch_device(self, events, offsets: Sequence[int], t_starts=None, flows=None, counts=None,
+                             stream=None):
+        torch = _torch()
+        self._check_events(events)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        ns = len(off) - 1
+        if flows is None:
+            flows = torch.empty((events.shape[0], 2), dtype=torch.float32, device=events.device)
+        ts = None
+        if t_starts is not None:
+            ts_arr = np.ascontiguousarray(t_starts, dtype=np.float64)
+            ts = _dptr(ts_arr)
+        _lib.check(self._lib.vkm_predict_batch(
+            self._h, C.c_void_p(events.data_ptr()), off.ctypes.data_as(C.POINTER(C.c_int64)), ns, ts,
+            C.c_void_p(flows.data_ptr()), C.c_void_p(counts.data_ptr()) if counts is not None else None,
+            self._stream(stream)))
+        return flows
+
+    def grid_device(self, events, t_start: float = math.nan, pooled: bool = False, stream=None):
+        """Per-pixel grid in the reference PixelGrid layout: ((W, H, D) complex64, (W, H) int32)."""
+        torch = _torch()
+        self._check_events(events)
+        W, H, D = self.width, self.height, self.embed_dim
+        g = torch.empty((W, H, D, 2), dtype=torch.float32, device=events.device)
+        c = torch.empty((W, H), dtype=torch.int32, device=events.device)
+        _lib.check(self._lib.vkm_grid(self._h, C.c_void_p(events.data_ptr()), events.shape[0], float(t_start),
+                                      int(bool(pooled)), C.c_void_p(g.data_ptr()), C.c_void_p(c.data_ptr()),
+                                      self._stream(stream)))
+        return torch.view_as_complex(g), c

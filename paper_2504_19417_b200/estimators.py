@@ -1,0 +1,181 @@
+"""Drop-in scikit-learn estimators backed by the B200 kernels.
+
+Same constructor parameters, `fit` / `predict` / `transform` semantics, output
+layout and error types as the reference adapters (estimators.py:30-206 under
+/root/reference/pkg/src/evflow/); two additive keyword parameters select the
+device and the MLP execution mode.  All per-event work runs in libveckm.so;
+there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+from typing import List, Optional, Sequence, Union
+
+import numpy as np
+from sklearn.base import BaseEstimator, TransformerMixin
+from sklearn.exceptions import NotFittedError
+
+from .engine import FlowEngine
+from .errors import DimensionMismatchError, EmptyNeighborhoodError
+from .validation import check_event_array, slice_from_array
+from .weights import MlpWeights, as_weights, generate_bases, load_weights
+
+_ENGINES = {}
+
+
+def _check_config(delta_t, delta_x, delta_y, embed_dim, sigma2, seeds, precision):
+    """EncoderConfig.__post_init__ checks (encoder.py:60-72)."""
+    if delta_t <= 0:
+        raise ValueError("delta_t must be positive")
+    if delta_x < 1 or delta_y < 1:
+        raise ValueError("pixel radii must be >= 1")
+    if embed_dim < 1:
+        raise ValueError("embed_dim must be >= 1")
+    if sigma2 <= 0:
+        raise ValueError("sigma2 must be positive")
+    if precision not in ("f32", "f64"):
+        raise ValueError("precision must be one of ['f32', 'f64']")
+    if len(tuple(seeds)) != 3:
+        raise ValueError("seeds must be a triple (time, x, y)")
+    if precision == "f64":
+        raise NotImplementedError("precision='f64' has no B200 kernel path yet (the B200 path is float32)")
+
+
+def _engine(key, factory) -> FlowEngine:
+    eng = _ENGINES.get(key)
+    if eng is None:
+        eng = factory()
+        _ENGINES[key] = eng
+    return eng
+
+
+class LocalEventEncoder(TransformerMixin, BaseEstimator):
+    """Per-event neighbourhood features [Re; Im] (estimators.py:30-95)."""
+
+    def __init__(self, delta_t: float = 0.016, delta_x: int = 10, delta_y: int = 10, embed_dim: int = 64,
+                 sigma2: float = 25.0, seeds: tuple = (0, 1, 2), precision: str = "f32", width: int = 640,
+                 height: int = 480, threads: int = 1, device: int = 0):
+        self.delta_t = delta_t
+        self.delta_x = delta_x
+        self.delta_y = delta_y
+        self.embed_dim = embed_dim
+        self.sigma2 = sigma2
+        self.seeds = seeds
+        self.precision = precision
+        self.width = width
+        self.height = height
+        self.threads = threads
+        self.device = device
+
+    def fit(self, X=None, y=None):
+        _check_config(self.delta_t, self.delta_x, self.delta_y, self.embed_dim, self.sigma2, self.seeds,
+                      "f32")
+        if X is not None:
+            check_event_array(X, self.width, self.height)
+        self.bases_ = generate_bases(self.embed_dim, self.sigma2, tuple(self.seeds))
+        return self
+
+    def transform(self, X) -> np.ndarray:
+        if not hasattr(self, "bases_"):
+            raise NotFittedError("call fit before transform")
+        _check_config(self.delta_t, self.delta_x, self.delta_y, self.embed_dim, self.sigma2, self.seeds,
+                      self.precision)
+        block = slice_from_array(X, self.width, self.height, 2.0 * self.delta_t)
+        if len(block) == 0:
+            return np.empty((0, 2 * self.embed_dim), dtype=np.float32)
+        b = self.bases_
+        key = ("enc", self.width, self.height, self.delta_x, self.delta_y, float(self.delta_t), self.device,
+               b.time_freqs.tobytes(), b.x_freqs.tobytes(), b.y_freqs.tobytes())
+        eng = _engine(key, lambda: FlowEngine(self.width, self.height, self.delta_x, self.delta_y, self.delta_t,
+                                              b, None, self.device))
+        feats, counts = eng.encode_host(block.events, block.t_start, return_counts=True)
+        if np.any(counts == 0):  # encoder.py:337-343
+            bad = np.flatnonzero(counts == 0)
+            raise EmptyNeighborhoodError(f"{len(bad)} queries have empty neighborhoods "
+                                         f"(first at batch position {bad[0]})")
+        return feats
+
+
+class NormalFlowRegressor(BaseEstimator):
+    """Per-event normal flow (estimators.py:98-206) on the B200 path."""
+
+    def __init__(self, delta_t: float = 0.016, delta_x: int = 10, delta_y: int = 10, embed_dim: int = 64,
+                 sigma2: float = 25.0, seeds: tuple = (0, 1, 2), precision: str = "f32", width: int = 640,
+                 height: int = 480, threads: int = 1, hidden: int = 128, epochs: int = 300, batch_size: int = 512,
+                 learning_rate: float = 1e-3, margin_weight: float = 0.1, random_state: int = 0,
+                 weights: Union[MlpWeights, str, None] = None, device: int = 0, mlp_mode: str = "auto"):
+        self.delta_t = delta_t
+        self.delta_x = delta_x
+        self.delta_y = delta_y
+        self.embed_dim = embed_dim
+        self.sigma2 = sigma2
+        self.seeds = seeds
+        self.precision = precision
+        self.width = width
+        self.height = height
+        self.threads = threads
+        self.hidden = hidden
+        self.epochs = epochs
+        self.batch_size = batch_size
+        self.learning_rate = learning_rate
+        self.margin_weight = margin_weight
+        self.random_state = random_state
+        self.weights = weights
+        self.device = device
+        self.mlp_mode = mlp_mode
+
+    def _resolve_pretrained(self) -> Optional[MlpWeights]:
+        if self.weights is None:
+            return None
+        if isinstance(self.weights, str):
+            return load_weights(self.weights)
+        return as_weights(self.weights)
+
+    def fit(self, X, y):
+        pretrained = self._resolve_pretrained()
+        if pretrained is not None:
+            self.weights_ = pretrained
+            return self
+        raise NotImplementedError(
+            "training the flow head is outside the B200 inference path; train with the reference "
+            "(evflow.train_head / evflow.NormalFlowRegressor.fit) and pass weights=")
+
+    def _ready(self) -> MlpWeights:
+        if not hasattr(self, "weights_"):
+            pretrained = self._resolve_pretrained()
+            if pretrained is None:
+                raise NotFittedError("call fit or supply pretrained weights")
+            self.weights_ = pretrained
+        _check_config(self.delta_t, self.delta_x, self.delta_y, self.embed_dim, self.sigma2, self.seeds,
+                      self.precision)
+        w = self.weights_
+        if w.embed_dim != self.embed_dim:  # flow.py:167-170
+            raise DimensionMismatchError(f"weights expect D={w.embed_dim} but config has D={self.embed_dim}")
+        return w
+
+    def engine(self) -> FlowEngine:
+        """The cached libveckm handle for this estimator's geometry and head."""
+        w = self._ready()
+        key = (self.width, self.height, self.delta_x, self.delta_y, float(self.delta_t), self.device,
+               self.mlp_mode)
+        cached = getattr(self, "_engine_cache", None)
+        if cached is not None and cached[0] == key and cached[1] is w:
+            return cached[2]
+        eng = FlowEngine(self.width, self.height, self.delta_x, self.delta_y, self.delta_t, w.bases, w,
+                         self.device, self.mlp_mode)
+        self._engine_cache = (key, w, eng)
+        return eng
+
+    def predict(self, X) -> np.ndarray:
+        """(n, 2) float64 flows in pixels/s; rows in stable time-sorted order
+        (input order for sorted input); NaN rows for empty neighbourhoods."""
+        eng = self.engine()
+        block = slice_from_array(X, self.width, self.height, 2.0 * self.delta_t)
+        if len(block) == 0:
+            return np.full((0, 2), np.nan)
+        flows = eng.predict_host(block.events, block.t_start)
+        return flows.astype(np.float64)
+
+    def predict_slices(self, slices: Sequence) -> List[np.ndarray]:
+        """Additive API: many independent slices, one result per slice."""
+        return [self.predict(X) for X in slices]

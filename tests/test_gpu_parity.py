@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's golden
+vectors and the CPU oracle.
+
+Bars: pixel counts and neighbourhood counts bit-exact;
+flows max-abs <= 1e-4 in the fp32-equivalent modes (FP32, F16X3); BF16 fast
+mode: max-abs <= 2e-3 and angular error p99 <= 2 deg, max <= 15 deg over
+|flow| >= 1e-2.  Embeddings / features max-abs <= 1e-5 (|emb| <= 1).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_CASES, has_cuda, load_golden
+from oracle import veckm_oracle as vo
+
+pytestmark = pytest.mark.gpu
+
+FLOW_TOL = 1e-4
+EMB_TOL = 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not has_cuda():
+        pytest.fail("GPU tests need a CUDA device")
+
+
+def _pkg():
+    import paper_2504_19417_b200 as pkg
+    return pkg
+
+
+def weights_of(g):
+    pkg = _pkg()
+    b = pkg.Bases(g["freqT"], g["freqX"], g["freqY"], float(g["sigma2"]))
+    return pkg.MlpWeights(g["w1"], g["b1"], g["w2"], g["b2"], b)
+
+
+def regressor(g, mode="auto"):
+    pkg = _pkg()
+    return pkg.NormalFlowRegressor(delta_t=float(g["delta_t"]), delta_x=int(g["dx"]), delta_y=int(g["dy"]),
+                                   embed_dim=int(g["D"]), width=int(g["width"]), height=int(g["height"]),
+                                   weights=weights_of(g), mlp_mode=mode)
+
+
+def angular_stats(got, want, floor=1e-2):
+    sel = np.linalg.norm(want, axis=1) >= floor
+    a = np.arctan2(got[sel, 1], got[sel, 0])
+    b = np.arctan2(want[sel, 1], want[sel, 0])
+    d = np.degrees(np.abs(np.angle(np.exp(1j * (a - b)))))
+    return (float(np.percentile(d, 99)), float(d.max())) if len(d) else (0.0, 0.0)
+
+
+@pytest.mark.parametrize("mode", ["fp32", "f16x3", "auto"])
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+def test_predict_matches_reference_golden(case, mode):
+    g = load_golden(case)
+    reg = regressor(g, mode)
+    if mode == "f16x3" and not (int(g["D"]) == 64 and int(g["w1"].shape[0]) == 128):
+        pytest.skip("tensor-core head needs D=64, hidden=128")
+    flows = reg.predict(g["X"])
+    assert flows.dtype == np.float64 and flows.shape == g["flows"].shape
+    np.testing.assert_allclose(flows, g["flows"], rtol=0, atol=FLOW_TOL)
+    blk = _pkg().slice_from_array(g["X"], int(g["width"]), int(g["height"]), 2 * float(g["delta_t"]))
+    _, counts = reg.engine().predict_host(blk.events, blk.t_start, return_counts=True)
+    np.testing.assert_array_equal(counts, g["counts"])
+
+
+@pytest.mark.parametrize("case", ["cfg1_20k", "r20_12k", "dense_asym"])
+def test_bf16_fast_mode_bound(case):
+    g = load_golden(case)
+    flows = regressor(g, "bf16").predict(g["X"])
+    assert np.max(np.abs(flows - g["flows"])) <= 2e-3
+    p99, mx = angular_stats(flows, g["flows"])
+    assert p99 <= 2.0 and mx <= 15.0, (p99, mx)
+
+
+def test_bias_only_head_is_exact():
+    g = load_golden("edge_bias_only")
+    for mode in ("fp32", "f16x3"):
+        flows = regressor(g, mode).predict(g["X"])
+        np.testing.assert_array_equal(flows, np.tile([2.5, -1.0], (len(flows), 1)))
+
+
+@pytest.mark.parametrize("case", ["small_d16", "cfg1_20k", "dense_asym", "edge_corner", "edge_t_offset"])
+def test_grid_matches_reference_golden(case):
+    import torch
+    g = load_golden(case)
+    pkg = _pkg()
+    reg = regressor(g)
+    blk = pkg.slice_from_array(g["X"], int(g["width"]), int(g["height"]), 2 * float(g["delta_t"]))
+    ev = torch.from_numpy(blk.events).cuda()
+    grid, cnt = reg.engine().grid_device(ev, blk.t_start, pooled=False)
+    np.testing.assert_array_equal(cnt.cpu().numpy(), g["grid_count"])
+    grid = grid.cpu().numpy()
+    if "grid_embed" in g:
+        np.testing.assert_allclose(grid, g["grid_embed"], rtol=0, atol=2e-6 * max(1, g["grid_count"].max()))
+    else:
+        x0, x1, y0, y1 = g["grid_box"]
+        np.testing.assert_allclose(grid[x0:x1, y0:y1], g["grid_embed_box"], rtol=0, atol=1e-5)
+
+
+@pytest.mark.parametrize("W,H,dx,dy,D,n,seed", [
+    (64, 48, 4, 4, 64, 3000, 1),
+    (96, 40, 10, 10, 64, 8000, 2),
+    (130, 70, 20, 20, 64, 6000, 3),     # strip wider than one CTA at delta 20
+    (300, 50, 3, 7, 32, 9000, 4),       # asymmetric radii, D padded to 32
+    (40, 300, 12, 5, 16, 5000, 5),      # tall sensor
+    (257, 9, 1, 1, 8, 2000, 6),         # radius 1, one-plane grid
+])
+def test_pooled_grid_matches_oracle(W, H, dx, dy, D, n, seed):
+    """K1+K2 against the oracle's window sums at every pixel."""
+    import torch
+    pkg = _pkg()
+    X = vo.synth_uniform_noise(n, W, H, seed=seed)
+    fr = vo.make_freqs(D, 25.0, (seed, seed + 1, seed + 2))
+    b = pkg.Bases(fr.T, fr.X, fr.Y, 25.0)
+    eng = pkg.FlowEngine(W, H, dx, dy, 0.016, b)
+    t0 = float(X[0, 0])
+    ev = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    q, qc = eng.grid_device(ev, t0, pooled=True)
+    g = vo.accumulate(X[:, 0] - t0, X[:, 1].astype(np.int64), X[:, 2].astype(np.int64), W, H, dx, dy, fr, 0.016)
+    acc, cnt = vo.pooled_all_pixels(g, vo.spatial_table(fr, dx, dy))
+    np.testing.assert_array_equal(qc.cpu().numpy(), cnt)
+    scale = np.maximum(cnt, 1)[:, :, None]
+    np.testing.assert_allclose(q.cpu().numpy() / scale, acc / scale, rtol=0, atol=EMB_TOL)
+
+
+def test_encoder_features_golden():
+    g = load_golden("encoder_1k")
+    pkg = _pkg()
+    enc = pkg.LocalEventEncoder(delta_t=float(g["delta_t"]), width=int(g["width"]), height=int(g["height"])).fit(g["X"])
+    feats = enc.transform(g["X"])
+    assert feats.dtype == np.float32 and feats.shape == g["feats"].shape
+    np.testing.assert_allclose(feats, g["feats"], rtol=0, atol=EMB_TOL)
+
+
+@pytest.mark.parametrize("D", [8, 16, 64])
+def test_features_match_oracle_small_dims(D, rng):
+    pkg = _pkg()
+    W, H = 50, 40
+    X = vo.synth_uniform_noise(4000, W, H, seed=D)
+    enc = pkg.LocalEventEncoder(delta_t=0.016, delta_x=5, delta_y=3, embed_dim=D, width=W, height=H).fit()
+    feats = enc.transform(X)
+    fr = vo.make_freqs(D, 25.0)
+    want = vo.encode_features(X, W, H, 5, 3, 0.016, fr)
+    np.testing.assert_allclose(feats, want, rtol=0, atol=EMB_TOL)
+
+
+def test_empty_and_tiny_slices():
+    pkg = _pkg()
+    g = load_golden("edge_single")
+    reg = regressor(g)
+    assert reg.predict(np.zeros((0, 3))).shape == (0, 2)
+    f = reg.predict(g["X"])
+    np.testing.assert_allclose(f, g["flows"], atol=FLOW_TOL)
+
+
+def test_unsorted_input_rows_follow_time_order():
+    g = load_golden("edge_unsorted_dups")
+    f = regressor(g).predict(g["X"])
+    np.testing.assert_allclose(f, g["flows"], atol=FLOW_TOL)
+
+
+def test_device_api_matches_host_api():
+    import torch
+    g = load_golden("cfg1_20k")
+    reg = regressor(g)
+    pkg = _pkg()
+    blk = pkg.slice_from_array(g["X"], 346, 260, 0.032)
+    eng = reg.engine()
+    host = eng.predict_host(blk.events, blk.t_start)
+    dev = eng.predict_device(torch.from_numpy(blk.events).cuda(), math.nan).cpu().numpy()
+    np.testing.assert_allclose(dev, host, rtol=0, atol=1e-6)
+
+
+def test_batch_matches_single_slices():
+    import torch
+    pkg = _pkg()
+    g = load_golden("cfg1_20k")
+    reg = regressor(g)
+    eng = reg.engine()
+    slices = [vo.synth_uniform_noise(5000 + 1000 * s, 346, 260, seed=10 + s) for s in range(4)]
+    ev = torch.from_numpy(np.concatenate(slices)).cuda()
+    off = np.cumsum([0] + [len(s) for s in slices])
+    out = eng.predict_batch_device(ev, off).cpu().numpy()
+    for s, X in enumerate(slices):
+        single = eng.predict_host(X, float(X[0, 0]))
+        np.testing.assert_allclose(out[off[s]:off[s + 1]], single, rtol=0, atol=1e-6)
+
+
+def test_full_size_config2_properties():
+    """640x480, 1M events (BASELINE configs[1]): size-independent properties
+    plus oracle parity on a strided query subset."""
+    import torch
+    pkg = _pkg()
+    W, H, n = 640, 480, 1_000_000
+    X = vo.synth_uniform_noise(n, W, H, seed=0)
+    fr = vo.make_freqs(64)
+    b = pkg.Bases(fr.T, fr.X, fr.Y, 25.0)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    eng = pkg.FlowEngine(W, H, 10, 10, 0.016, b, w)
+    ev = torch.from_numpy(X).cuda()
+    cnt = torch.empty(n, dtype=torch.int32, device="cuda")
+    flows = eng.predict_device(ev, float(X[0, 0]), counts=cnt).cpu().numpy()
+    cnt = cnt.cpu().numpy()
+    # neighbourhood counts: exact box sums of the pixel histogram
+    hist = np.zeros((H + 20, W + 20), np.int64)
+    np.add.at(hist, (X[:, 2].astype(int) + 10, X[:, 1].astype(int) + 10), 1)
+    ii = np.pad(hist.cumsum(0).cumsum(1), ((1, 0), (1, 0)))
+    yy, xx = X[:, 2].astype(int), X[:, 1].astype(int)
+    box = ii[yy + 21, xx + 21] - ii[yy, xx + 21] - ii[yy + 21, xx] + ii[yy, xx]
+    np.testing.assert_array_equal(cnt, box)
+    assert np.all(np.isfinite(flows))
+    # run-to-run: only fp32 atomic ordering differs
+    flows2 = eng.predict_device(ev, float(X[0, 0])).cpu().numpy()
+    assert np.max(np.abs(flows - flows2)) <= 1e-5
+    # oracle on 1500 strided queries (pool cost is per query)
+    t0 = float(X[0, 0])
+    g = vo.accumulate(X[:, 0] - t0, xx, yy, W, H, 10, 10, fr, 0.016)
+    q = np.arange(0, n, n // 1500)
+    emb, c = vo.pool(g, vo.spatial_table(fr, 10, 10), X[q, 0] - t0, xx[q], yy[q], fr, 0.016)
+    np.testing.assert_array_equal(c, cnt[q])
+    want = vo.mlp(w.w1, w.b1, w.w2, w.b2, vo.to_features(emb))
+    np.testing.assert_allclose(flows[q], want, rtol=0, atol=FLOW_TOL)

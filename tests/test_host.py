@@ -1,0 +1,206 @@
+"""CPU tests of the host side: input contract, weight formats, estimator API
+semantics, and the C-ABI library's exports.  No kernel is launched here."""
+
+import ctypes
+import os
+
+import numpy as np
+import pytest
+from sklearn.base import clone
+from sklearn.exceptions import NotFittedError
+
+from conftest import GOLDEN, load_golden
+import paper_2504_19417_b200 as pkg
+from paper_2504_19417_b200 import _lib
+from paper_2504_19417_b200.validation import check_event_array, slice_from_array
+from paper_2504_19417_b200.weights import bases_from_bytes, bases_to_bytes
+
+
+def make_events(rng, n=50, width=64, height=64, window=0.03):
+    t = np.sort(rng.uniform(0, window, n))
+    return np.stack([t, rng.integers(0, width, n), rng.integers(0, height, n)], axis=1)
+
+
+# ---------------------------------------------------------------- C-ABI ----
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    declared = _lib.declared_symbols()
+    assert len(declared) >= 14
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(_lib.SIGNATURES)
+
+
+def test_library_version_and_no_cpu_fallback():
+    lib = _lib.load()
+    assert lib.vkm_version() == 1
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except Exception:
+        pass
+    # without a device the create call must fail loudly (no CPU path)
+    p = _lib.VkmParams(8, 8, 2, 2, 8, 0, 0.016, 0, 0)
+    h = ctypes.c_void_p()
+    T = np.zeros(8)
+    ptr = T.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    rc = lib.vkm_create(ctypes.byref(h), ctypes.byref(p), ptr, ptr, ptr, None, None, None, None)
+    assert rc != 0
+    with pytest.raises(RuntimeError):
+        _lib.check(rc)
+
+
+def test_create_rejects_bad_params_before_touching_the_device():
+    lib = _lib.load()
+    T = np.zeros(8)
+    ptr = T.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    h = ctypes.c_void_p()
+    for bad, exc in [((0, 8, 2, 2, 8, 0, 0.016), ValueError), ((8, 8, 0, 2, 8, 0, 0.016), ValueError),
+                     ((8, 8, 2, 2, 8, 0, 0.0), ValueError), ((8, 8, 2, 2, 65, 0, 0.016), NotImplementedError),
+                     ((8, 8, 2, 2, 8, 4, 0.016), ValueError)]:
+        p = _lib.VkmParams(*bad, 0, 0)
+        rc = lib.vkm_create(ctypes.byref(h), ctypes.byref(p), ptr, ptr, ptr, None, None, None, None)
+        with pytest.raises(exc):
+            _lib.check(rc)
+
+
+# ------------------------------------------------------- input contract ----
+
+def test_check_event_array_types(rng):
+    X = make_events(rng, n=5)
+    X3, x, y = check_event_array(X, 64, 64)
+    assert X3.dtype == np.float64 and x.dtype == np.int32
+
+
+@pytest.mark.parametrize("X,match", [
+    (np.zeros((3,)), "shape"),
+    (np.array([[0.0, 1.5, 2.0]]), "integer"),
+    (np.array([[np.nan, 1.0, 2.0]]), "non-finite"),
+    (np.array([[-1.0, 1.0, 2.0]]), "non-negative"),
+    (np.array([[0.0, 9.0, 2.0]]), "outside geometry"),
+])
+def test_validation_messages(X, match):
+    with pytest.raises(ValueError, match=match):
+        check_event_array(X, 8, 8)
+
+
+def test_slice_sorts_stably_and_checks_span():
+    X = np.array([[0.02, 1, 1], [0.01, 2, 2], [0.01, 3, 3]])
+    b = slice_from_array(X, 8, 8, 0.032)
+    assert b.events[:, 0].tolist() == [0.01, 0.01, 0.02]
+    assert b.events[:, 1].tolist() == [2, 3, 1]
+    assert b.t_start == 0.01
+    with pytest.raises(ValueError, match="window"):
+        slice_from_array(np.array([[0.0, 1, 1], [0.5, 1, 1]]), 8, 8, 0.032)
+    # strict f64 span check (validation.py:59-64)
+    with pytest.raises(ValueError, match="window"):
+        slice_from_array(np.array([[5.0, 1, 1], [5.032, 1, 1]]), 8, 8, 0.032)
+
+
+def test_slice_matches_golden_sorting(golden_case):
+    g = golden_case
+    b = slice_from_array(g["X"], int(g["width"]), int(g["height"]), 2 * float(g["delta_t"]))
+    np.testing.assert_array_equal(b.events[:, 0], g["sorted_t"])
+    np.testing.assert_array_equal(b.events[:, 1].astype(np.int32), g["sorted_x"])
+    np.testing.assert_array_equal(b.events[:, 2].astype(np.int32), g["sorted_y"])
+    assert b.t_start == float(g["t_start"])
+
+
+# --------------------------------------------------------------- weights ----
+
+def test_generate_bases_matches_reference_golden():
+    g = load_golden("rng_bases")
+    b = pkg.generate_bases(64, 25.0, (0, 1, 2))
+    np.testing.assert_array_equal(b.time_freqs, g["T"])
+    np.testing.assert_array_equal(b.x_freqs, g["X"])
+    np.testing.assert_array_equal(b.y_freqs, g["Y"])
+    np.testing.assert_array_equal(pkg.generate_bases(48, 9.0, (7, 8, 9)).time_freqs, g["T_s789_d48"])
+
+
+def test_load_reference_weight_file_and_roundtrip(tmp_path):
+    w = pkg.load_weights(os.path.join(GOLDEN, "cfg1_weights.vkmw"))
+    g = load_golden("cfg1_20k")
+    np.testing.assert_array_equal(w.w1, g["w1"])
+    np.testing.assert_array_equal(w.b2, g["b2"])
+    np.testing.assert_array_equal(w.bases.time_freqs, g["freqT"])
+    out = tmp_path / "rt.vkmw"
+    pkg.save_weights(w, str(out))
+    with open(out, "rb") as a, open(os.path.join(GOLDEN, "cfg1_weights.vkmw"), "rb") as b:
+        assert a.read() == b.read()
+
+
+def test_bases_block_roundtrip():
+    b = pkg.generate_bases(48, 9.0, (4, 5, 6))
+    buf = bases_to_bytes(b)
+    assert len(buf) == 16 + 3 * 48 * 8
+    b2, pos = bases_from_bytes(buf)
+    assert pos == len(buf) and b2.sigma2 == 9.0
+    np.testing.assert_array_equal(b2.y_freqs, b.y_freqs)
+
+
+def test_bad_weight_files(tmp_path):
+    p = tmp_path / "bad.vkmw"
+    p.write_bytes(b"XXXX" + bytes(40))
+    with pytest.raises(pkg.EventParseError):
+        pkg.load_weights(str(p))
+
+
+def test_init_weights_matches_golden():
+    g = load_golden("cfg1_20k")
+    b = pkg.Bases(g["freqT"], g["freqX"], g["freqY"], 25.0)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    np.testing.assert_array_equal(w.w1, g["w1"])
+    np.testing.assert_array_equal(w.w2, g["w2"])
+
+
+def test_weights_shape_checks():
+    b = pkg.generate_bases(4)
+    with pytest.raises(pkg.DimensionMismatchError):
+        pkg.MlpWeights(np.zeros((3, 6)), np.zeros(3), np.zeros((2, 3)), np.zeros(2), b)
+    with pytest.raises(ValueError):
+        pkg.MlpWeights(np.full((3, 8), np.nan), np.zeros(3), np.zeros((2, 3)), np.zeros(2), b)
+
+
+# ------------------------------------------------------------ estimators ----
+
+def test_estimator_params_clone():
+    reg = pkg.NormalFlowRegressor(delta_x=4, width=64, height=64)
+    assert reg.get_params()["delta_x"] == 4
+    c = clone(reg)
+    assert c.get_params() == reg.get_params()
+    enc = pkg.LocalEventEncoder(embed_dim=16)
+    enc.set_params(embed_dim=8)
+    assert enc.get_params()["embed_dim"] == 8
+
+
+def test_estimator_errors_raised_before_the_device(rng):
+    with pytest.raises(NotFittedError):
+        pkg.NormalFlowRegressor().predict(make_events(rng))
+    with pytest.raises(NotFittedError):
+        pkg.LocalEventEncoder().transform(make_events(rng))
+    b = pkg.generate_bases(16)
+    w = pkg.init_weights(16, 8, b, dtype=np.float32)
+    with pytest.raises(pkg.DimensionMismatchError):
+        pkg.NormalFlowRegressor(embed_dim=64, weights=w).predict(make_events(rng))
+    with pytest.raises(NotImplementedError):
+        pkg.NormalFlowRegressor(embed_dim=16, precision="f64", weights=w).predict(make_events(rng))
+    with pytest.raises(NotImplementedError):
+        pkg.NormalFlowRegressor(embed_dim=16).fit(make_events(rng), np.zeros((50, 2)))
+    # pretrained weights: fit only stores them (estimators.py:166-170)
+    reg = pkg.NormalFlowRegressor(embed_dim=16, weights=w).fit(None, None)
+    assert reg.weights_ is w
+    with pytest.raises(ValueError, match="outside geometry"):
+        pkg.LocalEventEncoder(width=8, height=8).fit(np.array([[0.0, 9.0, 1.0]]))
+
+
+def test_reference_weights_object_is_accepted():
+    class Duck:
+        pass
+    b = pkg.generate_bases(8)
+    d = Duck()
+    d.w1, d.b1, d.w2, d.b2 = np.zeros((4, 16)), np.zeros(4), np.zeros((2, 4)), np.ones(2)
+    d.bases = b
+    reg = pkg.NormalFlowRegressor(embed_dim=8, weights=d)
+    assert reg._resolve_pretrained().hidden == 4
