@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) k_accumulate(const double* __restrict__ e
         float s0, c0, s1, c1;
         sincos_f32(__fmul_rn(aj, T0), s0, c0);
         sincos_f32(__fmul_rn(aj, T1), s1, c1);
-        atomicAdd(G4 + ((int64_t(plane) * P + pj) << 1) + q4, make_float4(c0, s0, c1, s1));
+        atomicAdd(G4 + ((int64_t(plane) * P + pj) << 2) + q4, make_float4(c0, s0, c1, s1));
       }
     }
   }
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(256) k_features(const double* __restrict__ ev,
       const int pj = __shfl_sync(kFull, pix, src & 31);
       const int cj = __shfl_sync(kFull, cnt, src & 31);
       if (src >= nv) continue;
-      const float4 acc = __ldg(Q4 + ((int64_t(plane) * P + pj) << 1) + q4);
+      const float4 acc = __ldg(Q4 + ((int64_t(plane) * P + pj) << 2) + q4);
       float s0, k0, s1, k1;
       sincos_f32(__fmul_rn(aj, T0), s0, k0);
       sincos_f32(__fmul_rn(aj, T1), s1, k1);

@@ -10,13 +10,13 @@
 //          Power-of-two pre-scales keep the lo parts out of fp16 subnormals.
 //   BF16   one bf16 pass, D = Fh·Whᵀ (fast mode, stated angular bound).
 //
-// Warp roles (288 threads, one persistent CTA per SM):
-//   warps 0-3  producers: one warp per 32 tile rows; gather the pooled grid
+// Warp roles (416 threads, one persistent CTA per SM):
+//   warps 0-7  producers: one warp per 16 tile rows; gather the pooled grid
 //              row of each event (coalesced 512 B), de-phase, ÷count, split,
 //              and store the fp16 A tile in the UMMA K-major SWIZZLE_128B layout
-//   warps 4-7  epilogue: tcgen05.ld of the accumulator (warp q owns TMEM lanes
-//              32q..32q+31 = tile rows), bias + ReLU + 128->2 on FFMA, store
-//   warp 8     TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 8-11 epilogue: tcgen05.ld of the accumulator (warp q = id % 4 owns
+//              TMEM lanes 32q..32q+31 = tile rows), bias + ReLU + 128->2, store
+//   warp 12    TMEM allocator + single-thread tcgen05.mma issuer
 // Pipelines: A stages (full/empty mbarriers, depth 2) and TMEM accumulators
 // (tfull/tempty, depth 2), so gather(i+1), MMA(i) and epilogue(i-1) overlap.
 #include <cuda_bf16.h>
@@ -38,7 +38,8 @@ constexpr int kStages = 2;
 constexpr int kAcc = 2;
 constexpr int kTileBytes = kM * kK * 2;        // 32 KB per fp16 operand image
 constexpr int kAtomBytes = kM * 128;           // one 64-wide K atom: 128 rows x 128 B
-constexpr int kThreads = 288;
+constexpr int kProdWarps = 8;                 // producer warps (16 tile rows each)
+constexpr int kThreads = (kProdWarps + 5) * 32; // + 4 epilogue warps + 1 MMA warp
 constexpr uint32_t kTmemCols = 256;
 
 struct Smem {
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       S.b2[1] = b2[1];
       S.scale = 1.f / (w_scale * f_scale);
       for (int s = 0; s < kStages; ++s) {
-        mbar_init(&S.full[s], 128);
+        mbar_init(&S.full[s], kProdWarps * 32);
         mbar_init(&S.empty[s], 1);
       }
       for (int a = 0; a < kAcc; ++a) {
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 8) {
+    if (warp == kProdWarps + 4) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
                    "r"(kTmemCols)
                    : "memory");
@@ -182,18 +183,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = S.tmem_base;
   const int64_t ntiles = (n + kM - 1) / kM;
 
-  if (warp < 4) {
+  if (warp < kProdWarps) {
     // ======================= producers =======================
+    // Warp w fills tile rows [16w, 16w+16).  Gathers are issued 8 events at a
+    // time before any is consumed, so each lane keeps 8 x 16 B in flight.
     const double t0 = ld_t0(ev, t0_in);
     const int c0 = 2 * lane;                      // this lane's channel pair
     const float T0 = __ldg(tf + c0), T1 = __ldg(tf + c0 + 1);
     const float4* Q4 = reinterpret_cast<const float4*>(Q);
     const int plane = lane >> 2, q4 = lane & 3;
+    constexpr int kRows = kM / kProdWarps;        // 16
+    constexpr int kBatch = 8;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int s = it & 1;
       const uint32_t ph = (it >> 1) & 1;
-      const int64_t e = tile * kM + warp * 32 + lane;
+      const int64_t e = tile * kM + warp * kRows + (lane & (kRows - 1));
       float a = 0.f;
       int pix = -1, cnt = 0;
       if (e < n) {
@@ -205,48 +210,57 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&S.empty[s], ph ^ 1);
       uint8_t* ah = S.ah[s];
       uint8_t* al = S.al[s];
-#pragma unroll 2
-      for (int j = 0; j < 32; ++j) {
-        const float aj = __shfl_sync(0xffffffffu, a, j);
-        const int pj = __shfl_sync(0xffffffffu, pix, j);
-        const int cj = __shfl_sync(0xffffffffu, cnt, j);
-        const uint32_t m = warp * 32 + j;
-        float re0 = 0.f, re1 = 0.f, im0 = 0.f, im1 = 0.f;
-        if (pj >= 0) {
-          const float4 acc = __ldg(Q4 + ((int64_t(plane) * P + pj) << 1) + q4);
-          float s0, k0, s1, k1;
-          sincos_f32(__fmul_rn(aj, T0), s0, k0);
-          sincos_f32(__fmul_rn(aj, T1), s1, k1);
-          const float den = float(max(cj, 1));
-          const float2 e0 = cmul_rn(make_float2(k0, -s0), make_float2(acc.x, acc.y));
-          const float2 e1 = cmul_rn(make_float2(k1, -s1), make_float2(acc.z, acc.w));
-          re0 = __fdiv_rn(e0.x, den) * f_scale;
-          re1 = __fdiv_rn(e1.x, den) * f_scale;
-          im0 = __fdiv_rn(e0.y, den) * f_scale;
-          im1 = __fdiv_rn(e1.y, den) * f_scale;
+#pragma unroll 1
+      for (int jb = 0; jb < kRows; jb += kBatch) {
+        float4 acc[kBatch];
+        int pjs[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          pjs[u] = __shfl_sync(0xffffffffu, pix, jb + u);
+          acc[u] = pjs[u] >= 0 ? __ldg(Q4 + ((int64_t(plane) * P + pjs[u]) << 2) + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        const uint32_t ore = umma_off(m, c0), oim = umma_off(m, 64 + c0);
-        if (kSplit) {
-          const __half2 hre = __floats2half2_rn(re0, re1);
-          const __half2 him = __floats2half2_rn(im0, im1);
-          const float2 fre = __half22float2(hre), fim = __half22float2(him);
-          const __half2 lre = __floats2half2_rn(re0 - fre.x, re1 - fre.y);
-          const __half2 lim = __floats2half2_rn(im0 - fim.x, im1 - fim.y);
-          *reinterpret_cast<__half2*>(ah + ore) = hre;
-          *reinterpret_cast<__half2*>(ah + oim) = him;
-          *reinterpret_cast<__half2*>(al + ore) = lre;
-          *reinterpret_cast<__half2*>(al + oim) = lim;
-        } else {
-          *reinterpret_cast<__nv_bfloat162*>(ah + ore) = __floats2bfloat162_rn(re0, re1);
-          *reinterpret_cast<__nv_bfloat162*>(ah + oim) = __floats2bfloat162_rn(im0, im1);
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const int j = jb + u;
+          const float aj = __shfl_sync(0xffffffffu, a, j);
+          const int cj = __shfl_sync(0xffffffffu, cnt, j);
+          const uint32_t m = warp * kRows + j;
+          float re0 = 0.f, re1 = 0.f, im0 = 0.f, im1 = 0.f;
+          if (pjs[u] >= 0) {
+            float s0, k0, s1, k1;
+            sincos_f32(__fmul_rn(aj, T0), s0, k0);
+            sincos_f32(__fmul_rn(aj, T1), s1, k1);
+            const float den = float(max(cj, 1));
+            const float2 e0 = cmul_rn(make_float2(k0, -s0), make_float2(acc[u].x, acc[u].y));
+            const float2 e1 = cmul_rn(make_float2(k1, -s1), make_float2(acc[u].z, acc[u].w));
+            re0 = __fdiv_rn(e0.x, den) * f_scale;
+            re1 = __fdiv_rn(e1.x, den) * f_scale;
+            im0 = __fdiv_rn(e0.y, den) * f_scale;
+            im1 = __fdiv_rn(e1.y, den) * f_scale;
+          }
+          const uint32_t ore = umma_off(m, c0), oim = umma_off(m, 64 + c0);
+          if (kSplit) {
+            const __half2 hre = __floats2half2_rn(re0, re1);
+            const __half2 him = __floats2half2_rn(im0, im1);
+            const float2 fre = __half22float2(hre), fim = __half22float2(him);
+            const __half2 lre = __floats2half2_rn(re0 - fre.x, re1 - fre.y);
+            const __half2 lim = __floats2half2_rn(im0 - fim.x, im1 - fim.y);
+            *reinterpret_cast<__half2*>(ah + ore) = hre;
+            *reinterpret_cast<__half2*>(ah + oim) = him;
+            *reinterpret_cast<__half2*>(al + ore) = lre;
+            *reinterpret_cast<__half2*>(al + oim) = lim;
+          } else {
+            *reinterpret_cast<__nv_bfloat162*>(ah + ore) = __floats2bfloat162_rn(re0, re1);
+            *reinterpret_cast<__nv_bfloat162*>(ah + oim) = __floats2bfloat162_rn(im0, im1);
+          }
         }
       }
       fence_proxy_async();
       mbar_arrive(&S.full[s]);
     }
-  } else if (warp < 8) {
+  } else if (warp < kProdWarps + 4) {
     // ======================= epilogue =======================
-    const int q = warp - 4;
+    const int q = warp & 3;   // TMEM lane quadrant = warp id % 4
     const float inv = S.scale;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -324,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kProdWarps + 4) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
   }
