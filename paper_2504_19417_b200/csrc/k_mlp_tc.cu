@@ -10,13 +10,13 @@
 //          Power-of-two pre-scales keep the lo parts out of fp16 subnormals.
 //   BF16   one bf16 pass, D = Fh·Whᵀ (fast mode, stated angular bound).
 //
-// Warp roles (416 threads, one persistent CTA per SM):
-//   warps 0-7  producers: one warp per 16 tile rows; gather the pooled grid
+// Warp roles (672 threads, one persistent CTA per SM):
+//   warps 0-15 producers: one warp per 8 tile rows; gather the pooled grid
 //              row of each event (coalesced 512 B), de-phase, ÷count, split,
 //              and store the fp16 A tile in the UMMA K-major SWIZZLE_128B layout
-//   warps 8-11 epilogue: tcgen05.ld of the accumulator (warp q = id % 4 owns
+//   warps 16-19 epilogue: tcgen05.ld of the accumulator (warp q = id % 4 owns
 //              TMEM lanes 32q..32q+31 = tile rows), bias + ReLU + 128->2, store
-//   warp 12    TMEM allocator + single-thread tcgen05.mma issuer
+//   warp 20    TMEM allocator + single-thread tcgen05.mma issuer
 // Pipelines: A stages (full/empty mbarriers, depth 2) and TMEM accumulators
 // (tfull/tempty, depth 2), so gather(i+1), MMA(i) and epilogue(i-1) overlap.
 #include <cuda_bf16.h>
@@ -38,7 +38,7 @@ constexpr int kStages = 2;
 constexpr int kAcc = 2;
 constexpr int kTileBytes = kM * kK * 2;        // 32 KB per fp16 operand image
 constexpr int kAtomBytes = kM * 128;           // one 64-wide K atom: 128 rows x 128 B
-constexpr int kProdWarps = 8;                 // producer warps (16 tile rows each)
+constexpr int kProdWarps = 16;                // producer warps (8 tile rows each)
 constexpr int kThreads = (kProdWarps + 5) * 32; // + 4 epilogue warps + 1 MMA warp
 constexpr uint32_t kTmemCols = 256;
 
@@ -49,7 +49,7 @@ struct Smem {
   uint8_t ah[kStages][kTileBytes];
   uint8_t al[kStages][kTileBytes];
   float b1[kN];
-  float w2[2 * kN];
+  float2 w2i[kN];   // (w2[0][n], w2[1][n]) interleaved for packed FFMA2
   float b2[2];
   float scale;
   uint32_t tmem_base;
@@ -130,8 +130,9 @@ __host__ __device__ __forceinline__ uint32_t umma_off(uint32_t m, uint32_t k) {
 
 template <int MODE>  // VKM_MLP_F16X3 or VKM_MLP_BF16
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gather_mlp_tc(const double* __restrict__ ev, int64_t n, double t0_in, double delta_t,
-                    const float* __restrict__ tf, int W, int64_t P, const float2* __restrict__ Q,
+    k_gather_mlp_tc(int64_t n, const int32_t* __restrict__ perm, const float* __restrict__ a_s,
+                    const int32_t* __restrict__ pix_s, const int* __restrict__ nvalid_ptr,
+                    const float* __restrict__ tf, int64_t P, const float2* __restrict__ Q,
                     const int* __restrict__ NQ, const uint4* __restrict__ w1h, const uint4* __restrict__ w1l,
                     const float* __restrict__ b1, const float* __restrict__ w2, const float* __restrict__ b2,
                     float w_scale, float* __restrict__ flows, int32_t* __restrict__ counts_out) {
@@ -152,8 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = threadIdx.x; i < kN; i += kThreads) {
       S.b1[i] = b1[i];
-      S.w2[i] = w2[i];
-      S.w2[kN + i] = w2[kN + i];
+      S.w2i[i] = make_float2(w2[i], w2[kN + i]);
     }
     if (threadIdx.x == 0) {
       S.b2[0] = b2[0];
@@ -182,81 +182,114 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   const uint32_t tmem = S.tmem_base;
   const int64_t ntiles = (n + kM - 1) / kM;
+  const int64_t nv = __ldg(nvalid_ptr);   // slots [0, nv) hold the in-sensor events
 
   if (warp < kProdWarps) {
     // ======================= producers =======================
-    // Warp w fills tile rows [16w, 16w+16).  Gathers are issued 8 events at a
-    // time before any is consumed, so each lane keeps 8 x 16 B in flight.
-    const double t0 = ld_t0(ev, t0_in);
+    // Warp w fills tile rows [8w, 8w+8) (pixel-sorted slots).  Its 8
+    // pooled-grid gathers are issued before the stage wait, the slot metadata
+    // (pixel, time argument, 1/count) is loaded a tile ahead, and one thread
+    // prefetches the pooled-grid rows of the next two tiles into L2 with bulk
+    // (TMA-engine) prefetches, so the gathers mostly hit L2.
     const int c0 = 2 * lane;                      // this lane's channel pair
-    const float T0 = __ldg(tf + c0), T1 = __ldg(tf + c0 + 1);
+    const uint64_t T01 = f2pack(__ldg(tf + c0), __ldg(tf + c0 + 1));
     const float4* Q4 = reinterpret_cast<const float4*>(Q);
     const int plane = lane >> 2, q4 = lane & 3;
-    constexpr int kRows = kM / kProdWarps;        // 16
-    constexpr int kBatch = 8;
+    constexpr int kRows = kM / kProdWarps;        // 8
+    const uint32_t lane_chunk = uint32_t(lane >> 2), lane_byte = uint32_t(lane & 3) * 4;
+    // lanes 0..7 hold the metadata of the warp's 8 rows
+    auto load_meta = [&](int64_t tl, float& a, int& pix, float& rs) {
+      const int64_t slot = tl * kM + warp * kRows + (lane & (kRows - 1));
+      a = 0.f;
+      pix = -1;
+      rs = 0.f;
+      if (tl < ntiles && slot < nv) {
+        pix = __ldg(pix_s + slot);
+        a = __ldg(a_s + slot);
+        const int cnt = __ldg(NQ + pix);
+        rs = cnt > 0 ? __frcp_rn(float(cnt)) * f_scale : 0.f;   // ÷count folded with the fp16 pre-scale
+      }
+    };
+    auto prefetch_l2 = [&](int64_t tl) {
+      if (tl >= ntiles) return;
+      const int64_t f = tl * kM;
+      if (f >= nv) return;
+      const int64_t l = (f + kM < nv ? f + kM : nv) - 1;
+      const int64_t p0 = __ldg(pix_s + f), p1 = __ldg(pix_s + l);
+      const uint32_t bytes = uint32_t((p1 - p0 + 1) < 2048 ? (p1 - p0 + 1) : 2048) * 64u;
+      for (int pl = 0; pl < 8; ++pl) {
+        const float2* src = Q + (int64_t(pl) * P + p0) * 8;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+      }
+    };
+    auto gather = [&](int pix_reg, float4 (&dst)[kRows]) {
+#pragma unroll
+      for (int u = 0; u < kRows; ++u) {
+        const int pj = __shfl_sync(0xffffffffu, pix_reg, u);
+        dst[u] = pj >= 0 ? __ldg(Q4 + ((int64_t(plane) * P + pj) << 2) + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    auto compute = [&](float a_reg, float rs_reg, const float4 (&src)[kRows], uint8_t* ah, uint8_t* al) {
+#pragma unroll
+      for (int u = 0; u < kRows; ++u) {
+        const float aj = __shfl_sync(0xffffffffu, a_reg, u);
+        const float rs = __shfl_sync(0xffffffffu, rs_reg, u);
+        const uint32_t m = warp * kRows + u;
+        uint64_t sn, cs;
+        sincos2p_f32(fmul2(f2pack(aj, aj), T01), sn, cs);
+        // conj(phase) * acc / cnt for channels (c0, c0+1), packed
+        const uint64_t ar = f2pack(src[u].x, src[u].z), ai = f2pack(src[u].y, src[u].w);
+        const uint64_t rs2 = f2pack(rs, rs);
+        const uint64_t re = fmul2(ffma2(sn, ai, fmul2(cs, ar)), rs2);
+        const uint64_t im = fmul2(ffma2(fneg2(sn), ar, fmul2(cs, ai)), rs2);
+        // umma_off(m, c0) and umma_off(m, 64 + c0) with the lane parts hoisted
+        const uint32_t ore = (m >> 3) * 1024 + (m & 7) * 128 + ((lane_chunk ^ (m & 7)) << 4) + lane_byte;
+        const uint32_t oim = ore + kAtomBytes;
+        float re0, re1, im0, im1;
+        f2unpack(re, re0, re1);
+        f2unpack(im, im0, im1);
+        if (kSplit) {
+          const __half2 hre = __floats2half2_rn(re0, re1);
+          const __half2 him = __floats2half2_rn(im0, im1);
+          const float2 fre = __half22float2(hre), fim = __half22float2(him);
+          float l0, l1, l2, l3;
+          f2unpack(fsub2(re, f2pack(fre.x, fre.y)), l0, l1);
+          f2unpack(fsub2(im, f2pack(fim.x, fim.y)), l2, l3);
+          *reinterpret_cast<__half2*>(ah + ore) = hre;
+          *reinterpret_cast<__half2*>(ah + oim) = him;
+          *reinterpret_cast<__half2*>(al + ore) = __floats2half2_rn(l0, l1);
+          *reinterpret_cast<__half2*>(al + oim) = __floats2half2_rn(l2, l3);
+        } else {
+          *reinterpret_cast<__nv_bfloat162*>(ah + ore) = __floats2bfloat162_rn(re0, re1);
+          *reinterpret_cast<__nv_bfloat162*>(ah + oim) = __floats2bfloat162_rn(im0, im1);
+        }
+      }
+    };
+
+    const int64_t G = gridDim.x;
+    float a_c, a_n, rs_c, rs_n;
+    int pix_c, pix_n;
+    load_meta(blockIdx.x, a_c, pix_c, rs_c);
+    load_meta(int64_t(blockIdx.x) + G, a_n, pix_n, rs_n);
+    if (warp == 0 && lane == 0) {
+      prefetch_l2(blockIdx.x);
+      prefetch_l2(int64_t(blockIdx.x) + G);
+    }
     int it = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++it) {
       const int s = it & 1;
       const uint32_t ph = (it >> 1) & 1;
-      const int64_t e = tile * kM + warp * kRows + (lane & (kRows - 1));
-      float a = 0.f;
-      int pix = -1, cnt = 0;
-      if (e < n) {
-        const double t = __ldg(ev + 3 * e), x = __ldg(ev + 3 * e + 1), y = __ldg(ev + 3 * e + 2);
-        pix = int(y) * W + int(x);
-        a = time_arg(t, t0, delta_t);
-        cnt = __ldg(NQ + pix);
-      }
+      if (warp == 0 && lane == 0) prefetch_l2(tile + 2 * G);
+      float4 acc[kRows];
+      gather(pix_c, acc);                           // in flight across the stage wait
       mbar_wait(&S.empty[s], ph ^ 1);
-      uint8_t* ah = S.ah[s];
-      uint8_t* al = S.al[s];
-#pragma unroll 1
-      for (int jb = 0; jb < kRows; jb += kBatch) {
-        float4 acc[kBatch];
-        int pjs[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          pjs[u] = __shfl_sync(0xffffffffu, pix, jb + u);
-          acc[u] = pjs[u] >= 0 ? __ldg(Q4 + ((int64_t(plane) * P + pjs[u]) << 2) + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-          const int j = jb + u;
-          const float aj = __shfl_sync(0xffffffffu, a, j);
-          const int cj = __shfl_sync(0xffffffffu, cnt, j);
-          const uint32_t m = warp * kRows + j;
-          float re0 = 0.f, re1 = 0.f, im0 = 0.f, im1 = 0.f;
-          if (pjs[u] >= 0) {
-            float s0, k0, s1, k1;
-            sincos_f32(__fmul_rn(aj, T0), s0, k0);
-            sincos_f32(__fmul_rn(aj, T1), s1, k1);
-            const float den = float(max(cj, 1));
-            const float2 e0 = cmul_rn(make_float2(k0, -s0), make_float2(acc[u].x, acc[u].y));
-            const float2 e1 = cmul_rn(make_float2(k1, -s1), make_float2(acc[u].z, acc[u].w));
-            re0 = __fdiv_rn(e0.x, den) * f_scale;
-            re1 = __fdiv_rn(e1.x, den) * f_scale;
-            im0 = __fdiv_rn(e0.y, den) * f_scale;
-            im1 = __fdiv_rn(e1.y, den) * f_scale;
-          }
-          const uint32_t ore = umma_off(m, c0), oim = umma_off(m, 64 + c0);
-          if (kSplit) {
-            const __half2 hre = __floats2half2_rn(re0, re1);
-            const __half2 him = __floats2half2_rn(im0, im1);
-            const float2 fre = __half22float2(hre), fim = __half22float2(him);
-            const __half2 lre = __floats2half2_rn(re0 - fre.x, re1 - fre.y);
-            const __half2 lim = __floats2half2_rn(im0 - fim.x, im1 - fim.y);
-            *reinterpret_cast<__half2*>(ah + ore) = hre;
-            *reinterpret_cast<__half2*>(ah + oim) = him;
-            *reinterpret_cast<__half2*>(al + ore) = lre;
-            *reinterpret_cast<__half2*>(al + oim) = lim;
-          } else {
-            *reinterpret_cast<__nv_bfloat162*>(ah + ore) = __floats2bfloat162_rn(re0, re1);
-            *reinterpret_cast<__nv_bfloat162*>(ah + oim) = __floats2bfloat162_rn(im0, im1);
-          }
-        }
-      }
+      compute(a_c, rs_c, acc, S.ah[s], S.al[s]);
       fence_proxy_async();
       mbar_arrive(&S.full[s]);
+      a_c = a_n;
+      pix_c = pix_n;
+      rs_c = rs_n;
+      load_meta(tile + 2 * G, a_n, pix_n, rs_n);
     }
   } else if (warp < kProdWarps + 4) {
     // ======================= epilogue =======================
@@ -266,15 +299,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
       const uint32_t ph = (it >> 1) & 1;
-      const int64_t e = tile * kM + q * 32 + lane;
+      const int64_t slot = tile * kM + q * 32 + lane;
       int cnt = 1;
-      if (e < n) {
-        const double x = __ldg(ev + 3 * e + 1), y = __ldg(ev + 3 * e + 2);
-        cnt = __ldg(NQ + int(y) * W + int(x));
+      int64_t e = -1;
+      if (slot < nv) {
+        e = __ldg(perm + slot);
+        cnt = __ldg(NQ + __ldg(pix_s + slot));
       }
       mbar_wait(&S.tfull[acc], ph);
       tc_fence_after();
-      float o0 = 0.f, o1 = 0.f;
+      uint64_t o = f2pack(0.f, 0.f);
       const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * kN);
 #pragma unroll
       for (int cb = 0; cb < kN; cb += 32) {
@@ -292,14 +326,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float hv = fmaxf(fmaf(__uint_as_float(r[i]), inv, 0.f) + S.b1[cb + i], 0.f);
-          o0 = fmaf(hv, S.w2[cb + i], o0);
-          o1 = fmaf(hv, S.w2[kN + cb + i], o1);
+          const float hv = fmaxf(fmaf(__uint_as_float(r[i]), inv, S.b1[cb + i]), 0.f);
+          const float2 w = S.w2i[cb + i];
+          o = ffma2(f2pack(hv, hv), f2pack(w.x, w.y), o);
         }
       }
       tc_fence_before();
       mbar_arrive(&S.tempty[acc]);
-      if (e < n) {
+      float o0, o1;
+      f2unpack(o, o0, o1);
+      if (e >= 0) {
         float2 r2 = make_float2(o0 + S.b2[0], o1 + S.b2[1]);
         if (cnt <= 0) r2 = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
         reinterpret_cast<float2*>(flows)[e] = r2;
@@ -351,23 +387,24 @@ void build_umma_image_kmajor_128x128(const uint16_t* rowmajor, uint16_t* image) 
     for (uint32_t k = 0; k < 128; ++k) image[tc::umma_off(m, k) / 2] = rowmajor[m * 128 + k];
 }
 
-void launch_gather_mlp_tc(const double* ev, int64_t n, double t0, double delta_t, const DevTables& tb, int W,
-                          int H, const GridBufs& g, const TcWeights& w, int mode, float* flows, int32_t* counts_out,
-                          int num_sms, cudaStream_t s) {
+void launch_gather_mlp_tc(int64_t n, const DevTables& tb, int W, int H, const GridBufs& g, const SortBufs& sb,
+                          const TcWeights& w, int mode, float* flows, int32_t* counts_out, int num_sms,
+                          cudaStream_t s) {
   if (n <= 0) return;
   const int64_t tiles = (n + tc::kM - 1) / tc::kM;
   const int grid = int(tiles < num_sms ? tiles : num_sms);
   const size_t smem = sizeof(tc::Smem) + 1024;
   const int64_t P = int64_t(W) * H;
+  const int* nvalid = sb.start + P;
   if (mode == VKM_MLP_BF16) {
     cudaFuncSetAttribute(tc::k_gather_mlp_tc<VKM_MLP_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     tc::k_gather_mlp_tc<VKM_MLP_BF16><<<grid, tc::kThreads, smem, s>>>(
-        ev, n, t0, delta_t, tb.tf, W, P, g.Q, g.NQ, static_cast<const uint4*>(w.w1_hi),
+        n, sb.perm, sb.a_s, sb.pix_s, nvalid, tb.tf, P, g.Q, g.NQ, static_cast<const uint4*>(w.w1_hi),
         static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out);
   } else {
     cudaFuncSetAttribute(tc::k_gather_mlp_tc<VKM_MLP_F16X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     tc::k_gather_mlp_tc<VKM_MLP_F16X3><<<grid, tc::kThreads, smem, s>>>(
-        ev, n, t0, delta_t, tb.tf, W, P, g.Q, g.NQ, static_cast<const uint4*>(w.w1_hi),
+        n, sb.perm, sb.a_s, sb.pix_s, nvalid, tb.tf, P, g.Q, g.NQ, static_cast<const uint4*>(w.w1_hi),
         static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out);
   }
 }

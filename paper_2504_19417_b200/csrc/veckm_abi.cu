@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -74,6 +75,8 @@ struct vkm_handle {
   float w_scale_f16 = 1.f;
   bool tc_ok = false;  // D == 64 && hidden == 128
   // scratch
+  vkm::SortBufs sb{};
+  size_t sort_cap = 0;
   float2* G = nullptr;
   int* C = nullptr;
   float2* Q = nullptr;
@@ -116,17 +119,43 @@ void rec(vkm_handle* h, int i, cudaStream_t s) {
   if (h->profiling) cudaEventRecord(h->evt[i], s);
 }
 
+int ensure_sort(vkm_handle* h, int64_t n) {
+  if (h->sort_cap >= size_t(std::max<int64_t>(n, 1))) return VKM_OK;
+  void* arrs[] = {h->sb.pix, h->sb.a, h->sb.iota, h->sb.perm, h->sb.a_s, h->sb.pix_s, h->sb.sort_temp};
+  for (void* p : arrs)
+    if (p) cudaFree(p);
+  h->sb.pix = nullptr; h->sb.a = nullptr; h->sb.iota = nullptr; h->sb.perm = nullptr;
+  h->sb.a_s = nullptr; h->sb.pix_s = nullptr; h->sb.sort_temp = nullptr;
+  const size_t cap = size_t(std::max<int64_t>(n, 1));
+  h->sort_cap = 0;
+  VKM_CK(cudaMalloc(&h->sb.pix, 4 * cap));
+  VKM_CK(cudaMalloc(&h->sb.a, 4 * cap));
+  VKM_CK(cudaMalloc(&h->sb.iota, 4 * cap));
+  VKM_CK(cudaMalloc(&h->sb.perm, 4 * cap));
+  VKM_CK(cudaMalloc(&h->sb.a_s, 4 * cap));
+  VKM_CK(cudaMalloc(&h->sb.pix_s, 4 * cap));
+  h->sb.sort_temp_bytes = vkm::sort_pairs_temp_bytes(int64_t(cap), h->P);
+  VKM_CK(cudaMalloc(&h->sb.sort_temp, std::max<size_t>(h->sb.sort_temp_bytes, 16)));
+  h->sort_cap = cap;
+  return VKM_OK;
+}
+
 // K1 + K2 for one slice on stream s.
-int encode_core(vkm_handle* h, const double* ev, int64_t n, double t0, int pooled, cudaStream_t s, int* launches) {
+int encode_core(vkm_handle* h, const double* ev, int64_t n, double t0, int pooled, cudaStream_t s, int* launches,
+                float* flows_invalid = nullptr, int32_t* counts_invalid = nullptr) {
   const int W = h->p.width, H = h->p.height;
-  VKM_CK(cudaMemsetAsync(h->G, 0, sizeof(float2) * 8 * h->planes * h->P, s));
-  VKM_CK(cudaMemsetAsync(h->C, 0, sizeof(int) * h->P, s));
-  vkm::launch_accumulate(ev, n, t0, h->p.delta_t, tables(h), W, H, h->D8, bufs(h), s);
-  if (n > 0) *launches += 1;
+  int rc = ensure_sort(h, n);
+  if (rc) return rc;
+  *launches += vkm::launch_accumulate_sorted(ev, n, t0, h->p.delta_t, tables(h), W, H, h->D8, bufs(h), h->sb,
+                                             flows_invalid, counts_invalid, s);
   VKM_CK(cudaGetLastError());
   rec(h, 1, s);
   if (pooled) {
-    vkm::launch_pool(tables(h), W, H, h->D8, h->p.delta_x, h->p.delta_y, bufs(h), s, launches);
+    // y-pass M(G) -> R(Q), x-pass R(Q) -> pooled(G); then swap so Q names the pooled grid
+    vkm::launch_pool_split(tables(h), W, H, h->D8, h->p.delta_x, h->p.delta_y, h->G, h->Q, h->G, s);
+    std::swap(h->G, h->Q);
+    vkm::launch_pool_count(W, H, h->p.delta_x, h->p.delta_y, bufs(h), s);
+    *launches += 3;
     VKM_CK(cudaGetLastError());
   }
   rec(h, 2, s);
@@ -135,15 +164,15 @@ int encode_core(vkm_handle* h, const double* ev, int64_t n, double t0, int poole
 
 int predict_one(vkm_handle* h, const double* ev, int64_t n, double t0, float* flows, int32_t* counts, cudaStream_t s,
                 int* launches) {
-  int rc = encode_core(h, ev, n, t0, 1, s, launches);
+  const bool tc = (h->mode == VKM_MLP_F16X3 || h->mode == VKM_MLP_BF16) && h->tc_ok;
+  int rc = encode_core(h, ev, n, t0, 1, s, launches, flows, counts);
   if (rc) return rc;
   if (n <= 0) return VKM_OK;
   const int W = h->p.width, H = h->p.height;
-  if ((h->mode == VKM_MLP_F16X3 || h->mode == VKM_MLP_BF16) && h->tc_ok) {
+  if (tc) {
     vkm::TcWeights tw{h->mode == VKM_MLP_BF16 ? h->w1_bf16 : h->w1_f16_hi, h->w1_f16_lo, h->b1, h->w2, h->b2,
                       h->mode == VKM_MLP_BF16 ? 1.f : h->w_scale_f16};
-    vkm::launch_gather_mlp_tc(ev, n, t0, h->p.delta_t, tables(h), W, H, bufs(h), tw, h->mode, flows, counts,
-                              h->num_sms, s);
+    vkm::launch_gather_mlp_tc(n, tables(h), W, H, bufs(h), h->sb, tw, h->mode, flows, counts, h->num_sms, s);
     *launches += 1;
   } else {
     rc = grow(&h->feats, &h->feats_cap, size_t(n) * 2 * h->D8);
@@ -283,8 +312,12 @@ int vkm_create(vkm_handle** out, const vkm_params* params, const double* T, cons
   // Grid scratch: two planes-sets of 64 B/pixel plus int32 counts (516 B/pixel at D=64).
   VKM_CKH(cudaMalloc(&h->G, sizeof(float2) * 8 * h->planes * h->P));
   VKM_CKH(cudaMalloc(&h->Q, sizeof(float2) * 8 * h->planes * h->P));
-  VKM_CKH(cudaMalloc(&h->C, sizeof(int) * h->P));
+  VKM_CKH(cudaMalloc(&h->C, sizeof(int) * (h->P + 1)));
   VKM_CKH(cudaMalloc(&h->NQ, sizeof(int) * h->P));
+  VKM_CKH(cudaMalloc(&h->sb.start, sizeof(int) * (h->P + 1)));
+  h->sb.temp_bytes = vkm::sort_scan_temp_bytes(h->P);
+  VKM_CKH(cudaMalloc(&h->sb.temp, std::max<size_t>(h->sb.temp_bytes, 16)));
+
 
   if (h->hidden > 0) {
     const int hid = h->hidden, D = h->D;
@@ -341,7 +374,9 @@ void vkm_destroy(vkm_handle* h) {
   DeviceGuard dg(h->p.device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   void* ptrs[] = {h->tf, h->my, h->mx, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
-                  h->G, h->C, h->Q, h->NQ, h->feats, h->cnt_scratch, h->ev_stage, h->out_stage, h->cnt_stage};
+                  h->G, h->C, h->Q, h->NQ, h->feats, h->cnt_scratch, h->ev_stage, h->out_stage, h->cnt_stage,
+                  h->sb.pix, h->sb.a, h->sb.iota, h->sb.start, h->sb.perm, h->sb.a_s, h->sb.pix_s, h->sb.temp,
+                  h->sb.sort_temp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->evt)
@@ -483,8 +518,8 @@ int vkm_grid(vkm_handle* h, const double* ev, int64_t n, double t_start, int32_t
   int launches = 0;
   int rc = encode_core(h, ev, n, t_start, pooled, s, &launches);
   if (rc) return rc;
-  vkm::launch_grid_to_ref(pooled ? h->Q : h->G, pooled ? h->NQ : h->C, h->p.width, h->p.height, h->D, h->D8, grid,
-                          counts, s);
+  vkm::launch_grid_to_ref(pooled ? h->Q : h->G, pooled ? h->NQ : h->C, h->p.width, h->p.height, h->D, h->D8,
+                          pooled ? nullptr : h->mx, pooled ? nullptr : h->my, grid, counts, s);
   VKM_CK(cudaGetLastError());
   return VKM_OK;
 }

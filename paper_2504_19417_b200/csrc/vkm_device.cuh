@@ -25,7 +25,10 @@ struct SliceGeom {
 // 1 ulp elsewhere.  Valid for |x| < ~1e5 (phase arguments here are < 100).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void sincos_f32(float x, float& s, float& c) {
-  const float q = rintf(x * 0.636619772f);
+  // q = rint(x·2/π) via the 1.5·2^23 magic constant (exact for |x·2/π| < 2^22):
+  // stays on the FMA/ALU pipes; the low mantissa bits carry the quadrant.
+  const float qb = __fadd_rn(__fmul_rn(x, 0.636619772f), 12582912.0f);
+  const float q = __fsub_rn(qb, 12582912.0f);
   float r = fmaf(q, -1.57079601e+00f, x);
   r = fmaf(q, -3.13916473e-07f, r);
   r = fmaf(q, -5.39030253e-15f, r);
@@ -41,11 +44,87 @@ __device__ __forceinline__ void sincos_f32(float x, float& s, float& c) {
   pc = fmaf(pc, u, 4.166661948e-02f);
   pc = fmaf(pc, u, -5.000000000e-01f);
   const float cr = fmaf(pc, u, 1.0f);
-  const int k = __float2int_rn(q);
-  float ss = (k & 1) ? cr : sr;
-  float cc = (k & 1) ? sr : cr;
-  s = (k & 2) ? -ss : ss;
-  c = ((k + 1) & 2) ? -cc : cc;
+  const int k = __float_as_int(qb);
+  const float ss = (k & 1) ? cr : sr;
+  const float cc = (k & 1) ? sr : cr;
+  s = __int_as_float(__float_as_int(ss) ^ ((k & 2) << 30));
+  c = __int_as_float(__float_as_int(cc) ^ (((k + 1) & 2) << 30));
+}
+
+// Packed f32x2 helpers (Blackwell FFMA2 / FMUL2): two lanes per instruction,
+// each lane IEEE round-to-nearest exactly like the scalar op.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fneg2(uint64_t a) { return a ^ 0x8000000080000000ull; }
+
+// Two sin/cos evaluations at once, bit-identical to two sincos_f32 calls
+// (same operations, paired into f32x2 instructions).
+__device__ __forceinline__ void sincos2_f32(float x0, float x1, float& s0, float& c0, float& s1, float& c1) {
+  const uint64_t x = f2pack(x0, x1);
+  const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
+  const uint64_t qb = fadd2(fmul2(x, f2pack(0.636619772f, 0.636619772f)), magic);
+  const uint64_t q = fsub2(qb, magic);
+  uint64_t r = ffma2(q, f2pack(-1.57079601e+00f, -1.57079601e+00f), x);
+  r = ffma2(q, f2pack(-3.13916473e-07f, -3.13916473e-07f), r);
+  r = ffma2(q, f2pack(-5.39030253e-15f, -5.39030253e-15f), r);
+  const uint64_t u = fmul2(r, r);
+  uint64_t ps = ffma2(f2pack(2.718123369e-06f, 2.718123369e-06f), u, f2pack(-1.983931288e-04f, -1.983931288e-04f));
+  ps = ffma2(ps, u, f2pack(8.333329111e-03f, 8.333329111e-03f));
+  ps = ffma2(ps, u, f2pack(-1.666666716e-01f, -1.666666716e-01f));
+  ps = fmul2(ps, u);
+  const uint64_t sr = ffma2(ps, r, r);
+  uint64_t pc = ffma2(f2pack(2.438358570e-05f, 2.438358570e-05f), u, f2pack(-1.388668199e-03f, -1.388668199e-03f));
+  pc = ffma2(pc, u, f2pack(4.166661948e-02f, 4.166661948e-02f));
+  pc = ffma2(pc, u, f2pack(-5.000000000e-01f, -5.000000000e-01f));
+  const uint64_t cr = ffma2(pc, u, f2pack(1.0f, 1.0f));
+  float sr0, sr1, cr0, cr1, qb0, qb1;
+  f2unpack(sr, sr0, sr1);
+  f2unpack(cr, cr0, cr1);
+  f2unpack(qb, qb0, qb1);
+  const int k0 = __float_as_int(qb0), k1 = __float_as_int(qb1);
+  float ss = (k0 & 1) ? cr0 : sr0, cc = (k0 & 1) ? sr0 : cr0;
+  s0 = __int_as_float(__float_as_int(ss) ^ ((k0 & 2) << 30));
+  c0 = __int_as_float(__float_as_int(cc) ^ (((k0 + 1) & 2) << 30));
+  ss = (k1 & 1) ? cr1 : sr1;
+  cc = (k1 & 1) ? sr1 : cr1;
+  s1 = __int_as_float(__float_as_int(ss) ^ ((k1 & 2) << 30));
+  c1 = __int_as_float(__float_as_int(cc) ^ (((k1 + 1) & 2) << 30));
+}
+
+// Packed-in/packed-out variant: theta = (x0, x1), returns (s0, s1), (c0, c1).
+__device__ __forceinline__ void sincos2p_f32(uint64_t theta, uint64_t& s01, uint64_t& c01) {
+  float x0, x1, s0, c0, s1, c1;
+  f2unpack(theta, x0, x1);
+  sincos2_f32(x0, x1, s0, c0, s1, c1);
+  s01 = f2pack(s0, s1);
+  c01 = f2pack(c0, c1);
 }
 
 // a = f32((t - t0) / delta_t): f64 rebase and divide, then one rounding to f32,
@@ -76,4 +155,84 @@ __device__ __forceinline__ double ld_t0(const double* ev, double t0) {
   return isnan(t0) ? __ldg(ev) : t0;
 }
 
+}  // namespace vkm
+
+namespace vkm {
+// L2 cache-policy helpers (createpolicy + .L2::cache_hint).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float2 ld_hint(const float2* ptr, uint64_t pol) {
+  float2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+               : "=f"(v.x), "=f"(v.y)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint(float2* ptr, float2 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(ptr), "f"(v.x), "f"(v.y),
+               "l"(pol)
+               : "memory");
+}
+}  // namespace vkm
+
+namespace vkm {
+// ---------------------------------------------------------------------------
+// mbarrier + bulk-copy (TMA engine, non-tensor) helpers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+// Bounded parity wait: a protocol bug traps instead of hanging the device.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = smem_addr(b);
+  for (uint32_t it = 0;; ++it) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (it > (1u << 26)) __trap();
+  }
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0, 16-B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+// shared -> global bulk copy (bulk-group completion)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 }  // namespace vkm

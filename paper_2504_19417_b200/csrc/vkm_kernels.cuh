@@ -12,10 +12,25 @@ struct DevTables {
 };
 
 struct GridBufs {
-  float2* G;   // [planes][P][8]
+  float2* G;   // [planes][P][8]  pre-modulated grid M = G·e^{i(xX/δx + yY/δy)}
   int* C;      // [P]
   float2* Q;   // [planes][P][8]
   int* NQ;     // [P]
+};
+
+// Pixel-sorted event order produced by the sorted K1 (k_sort.cu).
+struct SortBufs {
+  int32_t* pix;      // [n]  pixel key per event (P: outside the sensor)
+  float* a;          // [n]  f32 time argument per event
+  int32_t* iota;     // [n]  0..n-1 (sort values)
+  int* start;        // [P+1] exclusive scan of the counts (start[P] = valid events)
+  int32_t* perm;     // [n]  slot -> event (stable pixel-major order)
+  float* a_s;        // [n]  slot -> a
+  int32_t* pix_s;    // [n]  slot -> pixel
+  void* temp;        // CUB scan scratch
+  size_t temp_bytes;
+  void* sort_temp;   // CUB radix-sort scratch (grown with n)
+  size_t sort_temp_bytes;
 };
 
 struct MlpDev {
@@ -26,12 +41,18 @@ struct MlpDev {
   int hidden;
 };
 
-// K1: scatter per-event temporal phases into G and counts into C.
-void launch_accumulate(const double* ev, int64_t n, double t0, double delta_t, const DevTables& tb,
-                       int W, int H, int D8, const GridBufs& g, cudaStream_t s);
-// K2: windowed phase-weighted pooling of G -> Q, and box-sum of C -> NQ.
-void launch_pool(const DevTables& tb, int W, int H, int D8, int dx, int dy, const GridBufs& g,
-                 cudaStream_t s, int* launches);
+// K1 (sorted, default): prep + scan + scatter + per-pixel exact reduction.
+// Returns the number of kernel launches.  C must hold P+1 ints.
+int launch_accumulate_sorted(const double* ev, int64_t n, double t0, double delta_t, const DevTables& tb, int W,
+                             int H, int D8, const GridBufs& g, const SortBufs& sb, float* flows_invalid,
+                             int32_t* counts_invalid, cudaStream_t s);
+size_t sort_scan_temp_bytes(int64_t P);
+size_t sort_pairs_temp_bytes(int64_t n, int64_t P);
+// K2: box sum of the pre-modulated grid M (y-pass M -> R, x-pass + demodulation
+// R -> Qout); Qout may alias M (k_pool.cu).
+void launch_pool_split(const DevTables& tb, int W, int H, int D8, int dx, int dy, float2* M, float2* R,
+                       float2* Qout, cudaStream_t s);
+void launch_pool_count(int W, int H, int dx, int dy, const GridBufs& g, cudaStream_t s);
 // K3a: gather Q at each event, de-phase, divide by the count -> features.
 // Row e gets Re at out[e*ld + c] and Im at out[e*ld + im_off + c] for c < Dout.
 void launch_features(const double* ev, int64_t n, double t0, double delta_t, const DevTables& tb,
@@ -41,8 +62,9 @@ void launch_features(const double* ev, int64_t n, double t0, double delta_t, con
 void launch_mlp_ffma(const float* feats, const int32_t* counts, int64_t n, int D8, const MlpDev& m,
                      float* flows, cudaStream_t s);
 // Layout conversion for the parity hook: planes -> reference [x][y][D] complex64.
-void launch_grid_to_ref(const float2* G, const int* C, int W, int H, int D, int D8, float* out_grid,
-                        int32_t* out_counts, cudaStream_t s);
+// mx/my non-null: G holds the pre-modulated grid M and is demodulated on the way out.
+void launch_grid_to_ref(const float2* G, const int* C, int W, int H, int D, int D8, const float2* mx,
+                        const float2* my, float* out_grid, int32_t* out_counts, cudaStream_t s);
 
 // tcgen05 fused gather + de-phase + MLP (D = 64, hidden = 128).
 struct TcWeights {
@@ -53,9 +75,10 @@ struct TcWeights {
   const float* b2;     // [2]
   float w_scale;       // power-of-two pre-scale folded into the W1 images
 };
-void launch_gather_mlp_tc(const double* ev, int64_t n, double t0, double delta_t, const DevTables& tb,
-                          int W, int H, const GridBufs& g, const TcWeights& w, int mode, float* flows,
-                          int32_t* counts_out, int num_sms, cudaStream_t s);
+// Tiles run over the pixel-sorted slots of SortBufs (sequential pooled-grid reads).
+void launch_gather_mlp_tc(int64_t n, const DevTables& tb, int W, int H, const GridBufs& g, const SortBufs& sb,
+                          const TcWeights& w, int mode, float* flows, int32_t* counts_out, int num_sms,
+                          cudaStream_t s);
 // Host helper: build the UMMA smem image (K-major, 128B swizzle) of a 128x128 fp16/bf16 matrix.
 void build_umma_image_kmajor_128x128(const uint16_t* rowmajor, uint16_t* image);
 
