@@ -23,6 +23,7 @@
 #include <cuda_fp16.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/veckm.h"
 #include "vkm_device.cuh"
@@ -135,7 +136,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* __restrict__ tf, int64_t P, const float2* __restrict__ Q,
                     const int* __restrict__ NQ, const uint4* __restrict__ w1h, const uint4* __restrict__ w1l,
                     const float* __restrict__ b1, const float* __restrict__ w2, const float* __restrict__ b2,
-                    float w_scale, float* __restrict__ flows, int32_t* __restrict__ counts_out) {
+                    float w_scale, float* __restrict__ flows, int32_t* __restrict__ counts_out,
+                    int prefetch_on) {
   extern __shared__ uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -210,8 +212,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         rs = cnt > 0 ? __frcp_rn(float(cnt)) * f_scale : 0.f;   // ÷count folded with the fp16 pre-scale
       }
     };
+    // One thread prefetches the pooled-grid rows of a future tile into L2
+    // with bulk (TMA-engine) prefetches: the tile's pixel range x 8 planes.
+    // VKM_TC_PREFETCH=0 disables it (A/B evidence in profiles/).
     auto prefetch_l2 = [&](int64_t tl) {
-      if (tl >= ntiles) return;
+      if (!prefetch_on || tl >= ntiles || warp != 0 || lane != 0) return;
       const int64_t f = tl * kM;
       if (f >= nv) return;
       const int64_t l = (f + kM < nv ? f + kM : nv) - 1;
@@ -271,15 +276,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     int pix_c, pix_n;
     load_meta(blockIdx.x, a_c, pix_c, rs_c);
     load_meta(int64_t(blockIdx.x) + G, a_n, pix_n, rs_n);
-    if (warp == 0 && lane == 0) {
-      prefetch_l2(blockIdx.x);
-      prefetch_l2(int64_t(blockIdx.x) + G);
-    }
+    prefetch_l2(blockIdx.x);
+    prefetch_l2(int64_t(blockIdx.x) + G);
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++it) {
       const int s = it & 1;
       const uint32_t ph = (it >> 1) & 1;
-      if (warp == 0 && lane == 0) prefetch_l2(tile + 2 * G);
+      prefetch_l2(tile + 2 * G);
       float4 acc[kRows];
       gather(pix_c, acc);                           // in flight across the stage wait
       mbar_wait(&S.empty[s], ph ^ 1);
@@ -396,16 +399,20 @@ void launch_gather_mlp_tc(int64_t n, const DevTables& tb, int W, int H, const Gr
   const size_t smem = sizeof(tc::Smem) + 1024;
   const int64_t P = int64_t(W) * H;
   const int* nvalid = sb.start + P;
+  static const int prefetch = [] {
+    const char* e = std::getenv("VKM_TC_PREFETCH");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
   if (mode == VKM_MLP_BF16) {
     cudaFuncSetAttribute(tc::k_gather_mlp_tc<VKM_MLP_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     tc::k_gather_mlp_tc<VKM_MLP_BF16><<<grid, tc::kThreads, smem, s>>>(
         n, sb.perm, sb.a_s, sb.pix_s, nvalid, tb.tf, P, g.Q, g.NQ, static_cast<const uint4*>(w.w1_hi),
-        static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out);
+        static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out, prefetch);
   } else {
     cudaFuncSetAttribute(tc::k_gather_mlp_tc<VKM_MLP_F16X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     tc::k_gather_mlp_tc<VKM_MLP_F16X3><<<grid, tc::kThreads, smem, s>>>(
         n, sb.perm, sb.a_s, sb.pix_s, nvalid, tb.tf, P, g.Q, g.NQ, static_cast<const uint4*>(w.w1_hi),
-        static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out);
+        static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out, prefetch);
   }
 }
 

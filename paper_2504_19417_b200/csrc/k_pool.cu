@@ -116,13 +116,13 @@ void launch_pool_split(const DevTables& tb, int W, int H, int D8, int dx, int dy
   const double band = double(2 * dy + 1) * W * 512.0;
   const int s_max = std::max(1, int(64.0e6 / band));
   const int64_t col_threads = int64_t(W) * 8 * planes;
-  int segs = int(std::max<int64_t>(1, (148 * 2048 + col_threads - 1) / col_threads));
+  int segs = int(std::max<int64_t>(1, (148 * 1024 + col_threads - 1) / col_threads));   // ~32 warps per SM
   segs = std::max(1, std::min(segs, s_max));
   const int RS = (H + segs - 1) / segs;
   dim3 gy((W * 8 + 255) / 256, (H + RS - 1) / RS, planes);
   k_box_y<<<gy, 256, 0, s>>>(M, R, W, H, dy, RS, P);
   // x-pass: column segments of CS outputs (2δx halo re-reads are L1/L2 hits)
-  const int CS = std::max(32, 4 * dx);
+  const int CS = std::max(128, 8 * dx);   // halo re-reads 2δx/CS
   dim3 gx((W + CS - 1) / CS, (H * 8 + 255) / 256, planes);
   k_box_x<<<gx, 256, 0, s>>>(R, Qout, tb.mx, tb.my, W, H, D8, dx, CS, P);
 }

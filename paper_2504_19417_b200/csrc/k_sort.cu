@@ -64,8 +64,8 @@ __global__ void __launch_bounds__(256) k_reduce(const int* __restrict__ start, c
   const float4* mx4 = reinterpret_cast<const float4*>(mx);
   const float4* my4 = reinterpret_cast<const float4*>(my);
   // M[pixel] = (Σ e^{i a T}) · e^{i(x X/δx + y Y/δy)}: the pre-modulated grid K2 box-sums.
-  auto flush = [&](int64_t pix, uint64_t re, uint64_t im) {
-    const int y = int(pix / W), x = int(pix - int64_t(y) * W);
+  auto flush = [&](int pix, uint64_t re, uint64_t im) {
+    const int y = pix / W, x = pix - y * W;
     const float4 fx = __ldg(mx4 + ((int64_t(x) * 64) >> 1) + lane);
     const float4 fy = __ldg(my4 + ((int64_t(y) * 64) >> 1) + lane);
     const float2 m0 = cmul(make_float2(fx.x, fx.y), make_float2(fy.x, fy.y));
@@ -79,10 +79,10 @@ __global__ void __launch_bounds__(256) k_reduce(const int* __restrict__ start, c
   const uint64_t T01 = f2pack(__ldg(tf + 2 * lane), __ldg(tf + 2 * lane + 1));
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t p0 = warp * 32; p0 < P; p0 += nwarps * 32) {
-    const int64_t p1 = min(P, p0 + 32);
+  for (int64_t pw = warp * 32; pw < P; pw += nwarps * 32) {
+    const int p0 = int(pw), p1 = int(min(P, pw + 32));
     const int s0 = __ldg(start + p0), s1 = __ldg(start + p1);
-    int64_t cur = p0;                       // pixel being accumulated
+    int cur = p0;                           // pixel being accumulated
     uint64_t re = 0, im = 0;                // packed (ch c0, ch c0+1) sums, f32 in slot order
     for (int jb = s0; jb < s1; jb += 32) {
       const int j = jb + lane;
@@ -94,26 +94,27 @@ __global__ void __launch_bounds__(256) k_reduce(const int* __restrict__ start, c
         a_s[j] = av;
       }
       const int nj = min(32, s1 - jb);
+#pragma unroll 2
       for (int k = 0; k < nj; ++k) {
         const int pk = __shfl_sync(0xffffffffu, pv, k);
         const float ak = __shfl_sync(0xffffffffu, av, k);
-        while (cur < pk) {                  // flush finished pixels (and empty ones in between)
-          flush(cur, re, im);
-          re = 0;
-          im = 0;
-          ++cur;
-        }
         uint64_t sn, cs;
         sincos2p_f32(fmul2(f2pack(ak, ak), T01), sn, cs);
+        if (pk != cur) {                    // flush finished pixels (and empty ones in between)
+          do {
+            flush(cur, re, im);
+            re = 0;
+            im = 0;
+          } while (++cur < pk);
+        }
         re = fadd2(re, cs);
         im = fadd2(im, sn);
       }
     }
-    while (cur < p1) {
+    for (; cur < p1; ++cur) {
       flush(cur, re, im);
       re = 0;
       im = 0;
-      ++cur;
     }
   }
 }
