@@ -190,8 +190,14 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    shared = os.environ.get("VKM_BENCH_SHARED_GPU") == "1"   # test mode: all ranks on cuda:0, gloo
+    if shared:
+        local = 0
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     W, H, n, d, slices, desc = WORKLOADS[args.workload]
@@ -200,14 +206,29 @@ def run_b200(args):
 
     bases = pkg.generate_bases(64, 25.0, (0, 1, 2))
     w = pkg.init_weights(64, 128, bases, seed=0, dtype=np.float32)
-    eng = pkg.FlowEngine(W, H, d, d, 0.016, bases, w, device=local, mlp_mode=args.mlp_mode)
-
-    host = [_synth(n, W, H, seed=1000 * rank + s) for s in range(slices)]
-    P = W * H
+    spatial = args.split == "spatial"
+    if spatial:
+        # one slice split into row strips (event-halo duplication), strong scaling
+        from paper_2504_19417_b200 import sharding
+        full = _synth(n, W, H, seed=0)
+        rows = np.bincount(full[:, 2].astype(np.int64), minlength=H)
+        strips = sharding.row_strips(rows, world, d)
+        se = sharding.strip_events(full, strips[rank])
+        host = [se.events]
+        owned = int(se.owned.sum())
+        t_global = float(full[0, 0])
+        H_eff = strips[rank].height
+        slices = 1
+        del full
+    else:
+        host = [_synth(n, W, H, seed=1000 * rank + s) for s in range(slices)]
+        H_eff = H
+    eng = pkg.FlowEngine(W, H_eff, d, d, 0.016, bases, w, device=local, mlp_mode=args.mlp_mode)
+    P = W * H_eff
     p_occ = [int(len(np.unique(X[:, 2].astype(np.int64) * W + X[:, 1].astype(np.int64)))) for X in host]
-    evs = [torch.from_numpy(X).to(dev) for X in host]
-    t0s = [float(X[0, 0]) for X in host]
-    flows = [torch.empty((n, 2), dtype=torch.float32, device=dev) for _ in range(slices)]
+    evs = [torch.from_numpy(np.ascontiguousarray(X)).to(dev) for X in host]
+    t0s = [t_global] if spatial else [float(X[0, 0]) for X in host]
+    flows = [torch.empty((len(X), 2), dtype=torch.float32, device=dev) for X in host]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -247,19 +268,20 @@ def run_b200(args):
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    flows_total = world * slices * n * args.steps
+    flows_total = (n if spatial else world * slices * n) * args.steps
     value = flows_total / (total_ms / 1e3)
 
     # ---- end to end through the C-ABI host-buffer call (pinned buffers) ----
     e2e = None
     if not args.no_e2e:
-        pinned = torch.from_numpy(host[0]).pin_memory()
-        out = torch.empty((n, 2), dtype=torch.float32).pin_memory()
+        pinned = torch.from_numpy(np.ascontiguousarray(host[0])).pin_memory()
+        out = torch.empty((len(host[0]), 2), dtype=torch.float32).pin_memory()
+        n_e2e = len(host[0])
         ev_np, out_np = pinned.numpy(), out.numpy()
         lib = pkg._lib.load()
 
         def call():
-            pkg._lib.check(lib.vkm_predict_host(eng._h, ev_np.ctypes.data, n, t0s[0], out_np.ctypes.data, None))
+            pkg._lib.check(lib.vkm_predict_host(eng._h, ev_np.ctypes.data, n_e2e, t0s[0], out_np.ctypes.data, None))
 
         for _ in range(3):
             call()
@@ -274,8 +296,9 @@ def run_b200(args):
             t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        e2e = {"value": world * n * k / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 24 * n,
-               "d2h_bytes_per_step": 8 * n, "steps": k, "api": "vkm_predict_host (C-ABI, pinned host buffers)"}
+        per_step = n if spatial else world * n
+        e2e = {"value": per_step * k / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 24 * n_e2e,
+               "d2h_bytes_per_step": 8 * n_e2e, "steps": k, "api": "vkm_predict_host (C-ABI, pinned host buffers)"}
 
     if rank != 0:
         if world > 1:
@@ -283,7 +306,7 @@ def run_b200(args):
         return
 
     hbm_peak, tc_peak, peak_kind = load_peaks()
-    k1b, k2b, k3b = algorithmic_bytes(n, P, p_occ[0])
+    k1b, k2b, k3b = algorithmic_bytes(len(host[0]), P, p_occ[0])
     kernels = None
     roofline = None
     if kern:
@@ -317,12 +340,13 @@ def run_b200(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if spatial else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (uniform noise, seeded per rank), random-init weights D=64/hidden=128",
         "config": {"workload": desc, "sensor": f"{W}x{H}", "events_per_slice": n, "delta": d,
                    "slices_per_rank_per_step": slices, "embed_dim": 64, "hidden": 128,
                    "mlp_mode": args.mlp_mode, "l2": "flushed between steps (512 MiB write, outside step events)",
-                   "parallelism": f"dp{world} (independent slices per rank, no collective)"},
+                   "parallelism": (f"spatial{world} (row strips + {d}-row event halo, gather of owned flows)" if spatial
+                                   else f"dp{world} (independent slices per rank, no collective)")},
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
         "cpu_baseline": cpu, "clocks": clk.summary(),
         "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
@@ -341,6 +365,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--mlp-mode", default="auto", choices=["auto", "fp32", "f16x3", "bf16"])
     ap.add_argument("--slices", type=int, default=0)
+    ap.add_argument("--split", choices=["slices", "spatial"], default="slices",
+                    help="slices: independent slices per rank (weak); spatial: one slice in row strips (strong)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -54,7 +54,9 @@ __device__ __forceinline__ void sincos_f32(float x, float& s, float& c) {
 // Packed f32x2 helpers (Blackwell FFMA2 / FMUL2): two lanes per instruction,
 // each lane IEEE round-to-nearest exactly like the scalar op.
 __device__ __forceinline__ uint64_t f2pack(float a, float b) {
-  return (uint64_t(__float_as_uint(b)) << 32) | uint64_t(__float_as_uint(a));
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
 }
 __device__ __forceinline__ void f2unpack(uint64_t r, float& a, float& b) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));

@@ -225,3 +225,47 @@ def test_full_size_config2_properties():
     np.testing.assert_array_equal(c, cnt[q])
     want = vo.mlp(w.w1, w.b1, w.w2, w.b2, vo.to_features(emb))
     np.testing.assert_allclose(flows[q], want, rtol=0, atol=FLOW_TOL)
+
+
+def test_spatial_strip_split_matches_unsplit():
+    """Config-5 style row-strip split with a δ-row event halo (strips run one
+    after another on this GPU): counts bit-exact, flows within fp32 noise."""
+    pkg = _pkg()
+    from paper_2504_19417_b200 import sharding
+    W, H, d, n = 256, 120, 10, 200_000
+    X = vo.synth_uniform_noise(n, W, H, seed=11)
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    full = pkg.FlowEngine(W, H, d, d, 0.016, b, w)
+    f_full, c_full = full.predict_host(X, float(X[0, 0]), return_counts=True)
+    for world in (2, 3, 8):
+        rows = np.bincount(X[:, 2].astype(np.int64), minlength=H)
+        strips = sharding.row_strips(rows, world, d)
+        ses = [sharding.strip_events(X, s) for s in strips]
+        res = [pkg.FlowEngine(W, s.height, d, d, 0.016, b, w).predict_host(se.events, float(X[0, 0]), True)
+               for s, se in zip(strips, ses)]
+        flows, counts = sharding.assemble(n, ses, [r[0] for r in res], [r[1] for r in res])
+        np.testing.assert_array_equal(counts, c_full)
+        np.testing.assert_allclose(flows, f_full, rtol=0, atol=1e-5)
+
+
+def test_bench_multirank_shared_gpu(tmp_path):
+    """The torchrun (N=2) bench path, both ranks on this GPU (gloo plumbing)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VKM_BENCH_SHARED_GPU="1")
+    for split in ("slices", "spatial"):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+               "--master-addr", "127.0.0.1", "--master-port", str(29500 + (split == "spatial")),
+               os.path.join(root, "bench.py"), "--gpus", "2", "--workload", "cfg1", "--steps", "3",
+               "--warmup", "3", "--no-e2e", "--no-cpu-baseline", "--split", split]
+        out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=root)
+        assert out.returncode == 0, out.stderr[-2000:]
+        lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+        assert len(lines) == 1, out.stdout
+        rec = json.loads(lines[0])
+        assert rec["n_gpus"] == 2 and rec["value"] > 0
+        assert rec["scaling"] == ("strong" if split == "spatial" else "weak")
