@@ -131,8 +131,7 @@ __host__ __device__ __forceinline__ uint32_t umma_off(uint32_t m, uint32_t k) {
 
 template <int MODE>  // VKM_MLP_F16X3 or VKM_MLP_BF16
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gather_mlp_tc(int64_t n, const int32_t* __restrict__ perm, const float* __restrict__ a_s,
-                    const int32_t* __restrict__ pix_s, const int* __restrict__ nvalid_ptr,
+    k_gather_mlp_tc(int64_t n, const uint64_t* __restrict__ val_s, const int32_t* __restrict__ pix_s, const int* __restrict__ nvalid_ptr,
                     const float* __restrict__ tf, int64_t P, const float2* __restrict__ Q,
                     const int* __restrict__ NQ, const uint4* __restrict__ w1h, const uint4* __restrict__ w1l,
                     const float* __restrict__ b1, const float* __restrict__ w2, const float* __restrict__ b2,
@@ -207,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       rs = 0.f;
       if (tl < ntiles && slot < nv) {
         pix = __ldg(pix_s + slot);
-        a = __ldg(a_s + slot);
+        a = slot_arg(__ldg(val_s + slot));
         const int cnt = __ldg(NQ + pix);
         rs = cnt > 0 ? __frcp_rn(float(cnt)) * f_scale : 0.f;   // ÷count folded with the fp16 pre-scale
       }
@@ -306,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int cnt = 1;
       int64_t e = -1;
       if (slot < nv) {
-        e = __ldg(perm + slot);
+        e = slot_event(__ldg(val_s + slot));
         cnt = __ldg(NQ + __ldg(pix_s + slot));
       }
       mbar_wait(&S.tfull[acc], ph);
@@ -406,12 +405,12 @@ void launch_gather_mlp_tc(int64_t n, const DevTables& tb, int W, int H, const Gr
   if (mode == VKM_MLP_BF16) {
     cudaFuncSetAttribute(tc::k_gather_mlp_tc<VKM_MLP_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     tc::k_gather_mlp_tc<VKM_MLP_BF16><<<grid, tc::kThreads, smem, s>>>(
-        n, sb.perm, sb.a_s, sb.pix_s, nvalid, tb.tf, P, g.Q, g.NQ, static_cast<const uint4*>(w.w1_hi),
+        n, sb.val_s, sb.pix_s, nvalid, tb.tf, P, g.Q, g.NQ, static_cast<const uint4*>(w.w1_hi),
         static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out, prefetch);
   } else {
     cudaFuncSetAttribute(tc::k_gather_mlp_tc<VKM_MLP_F16X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     tc::k_gather_mlp_tc<VKM_MLP_F16X3><<<grid, tc::kThreads, smem, s>>>(
-        n, sb.perm, sb.a_s, sb.pix_s, nvalid, tb.tf, P, g.Q, g.NQ, static_cast<const uint4*>(w.w1_hi),
+        n, sb.val_s, sb.pix_s, nvalid, tb.tf, P, g.Q, g.NQ, static_cast<const uint4*>(w.w1_hi),
         static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out, prefetch);
   }
 }

@@ -28,9 +28,12 @@ constexpr int kU = 4;   // rows / columns per unrolled step
 }
 
 // idx = x*8 + ch within one plane row (W*8 float2); blockIdx.y = row segment,
-// blockIdx.z = plane.
+// blockIdx.z = plane.  DEMOD: the input is the x-pooled R of k_reduce_x and
+// each output is multiplied by conj(e^{i(xX/δx + yY/δy)}) (the pooled grid Q).
+template <bool DEMOD>
 __global__ void __launch_bounds__(256) k_box_y(const float2* __restrict__ M, float2* __restrict__ R, int W, int H,
-                                               int dy, int RS, int64_t P) {
+                                               int dy, int RS, int64_t P, const float2* __restrict__ mx,
+                                               const float2* __restrict__ my, int D8) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= W * 8) return;
   const int y0 = blockIdx.y * RS, y1 = min(H, y0 + RS);
@@ -39,6 +42,10 @@ __global__ void __launch_bounds__(256) k_box_y(const float2* __restrict__ M, flo
   const int64_t rs = int64_t(W) * 8;   // row stride in float2
   const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
   const float2 zero = make_float2(0.f, 0.f);
+  const int c = int(blockIdx.z) * 8 + (idx & 7);
+  float2 fx = zero;
+  const float2* myc = my + c;
+  if (DEMOD) fx = __ldg(mx + int64_t(idx >> 3) * D8 + c);
   float2 acc = zero;
   // warm-up: rows [y0-dy, y0+dy)
   {
@@ -54,18 +61,22 @@ __global__ void __launch_bounds__(256) k_box_y(const float2* __restrict__ M, flo
     for (; y < yb; ++y) acc = cadd(acc, ld_hint(Mp + int64_t(y) * rs, keep));
   }
   for (int y = y0; y < y1; y += kU) {
-    float2 ld[kU], tr[kU];
+    float2 ld[kU], tr[kU], fm[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int yy = y + u;
       ld[u] = (yy < y1 && yy + dy < H) ? ld_hint(Mp + int64_t(yy + dy) * rs, keep) : zero;
       tr[u] = (yy < y1 && yy - dy >= 0) ? ld_hint(Mp + int64_t(yy - dy) * rs, drop) : zero;
+      if (DEMOD) fm[u] = (yy < y1) ? __ldg(myc + int64_t(yy) * D8) : zero;
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       if (y + u >= y1) break;
       acc = cadd(acc, ld[u]);
-      Rp[int64_t(y + u) * rs] = acc;
+      if (DEMOD)
+        Rp[int64_t(y + u) * rs] = cmulc(acc, cmul(fx, fm[u]));   // · conj(e^{i(xX + yY)})
+      else
+        Rp[int64_t(y + u) * rs] = acc;
       acc = csub(acc, tr[u]);
     }
   }
@@ -108,23 +119,39 @@ __global__ void __launch_bounds__(256) k_box_x(const float2* __restrict__ R, flo
   }
 }
 
-void launch_pool_split(const DevTables& tb, int W, int H, int D8, int dx, int dy, float2* M, float2* R,
-                       float2* Qout, cudaStream_t s) {
-  const int planes = D8 / 8;
-  const int64_t P = int64_t(W) * H;
+namespace {
+int pick_segments(int W, int H, int dy, int planes) {
   // y-pass: segments bounded by an L2 budget for the live (2δy+1)-row windows
   const double band = double(2 * dy + 1) * W * 512.0;
   const int s_max = std::max(1, int(64.0e6 / band));
   const int64_t col_threads = int64_t(W) * 8 * planes;
   int segs = int(std::max<int64_t>(1, (148 * 1024 + col_threads - 1) / col_threads));   // ~32 warps per SM
-  segs = std::max(1, std::min(segs, s_max));
+  return std::max(1, std::min(segs, s_max));
+}
+}  // namespace
+
+void launch_pool_split(const DevTables& tb, int W, int H, int D8, int dx, int dy, float2* M, float2* R,
+                       float2* Qout, cudaStream_t s) {
+  const int planes = D8 / 8;
+  const int64_t P = int64_t(W) * H;
+  const int segs = pick_segments(W, H, dy, planes);
   const int RS = (H + segs - 1) / segs;
   dim3 gy((W * 8 + 255) / 256, (H + RS - 1) / RS, planes);
-  k_box_y<<<gy, 256, 0, s>>>(M, R, W, H, dy, RS, P);
+  k_box_y<false><<<gy, 256, 0, s>>>(M, R, W, H, dy, RS, P, nullptr, nullptr, D8);
   // x-pass: column segments of CS outputs (2δx halo re-reads are L1/L2 hits)
   const int CS = std::max(128, 8 * dx);   // halo re-reads 2δx/CS
   dim3 gx((W + CS - 1) / CS, (H * 8 + 255) / 256, planes);
   k_box_x<<<gx, 256, 0, s>>>(R, Qout, tb.mx, tb.my, W, H, D8, dx, CS, P);
+}
+
+void launch_pool_y_demod(const DevTables& tb, int W, int H, int D8, int dy, const float2* R, float2* Q,
+                         cudaStream_t s) {
+  const int planes = D8 / 8;
+  const int64_t P = int64_t(W) * H;
+  const int segs = pick_segments(W, H, dy, planes);
+  const int RS = (H + segs - 1) / segs;
+  dim3 gy((W * 8 + 255) / 256, (H + RS - 1) / RS, planes);
+  k_box_y<true><<<gy, 256, 0, s>>>(R, Q, W, H, dy, RS, P, tb.mx, tb.my, D8);
 }
 
 }  // namespace vkm

@@ -1,20 +1,21 @@
 // K1 (sorted): per-pixel accumulation in the reference's own summation order.
 //
-//   k_prep     event -> pixel key, f32 time argument a = f32((t - t0)/δt), the
-//              per-pixel count histogram (the reference's bincount,
-//              encoder.py:259) and the identity permutation
+//   k_prep     event -> pixel key, slot value (event index, f32 time argument
+//              a = f32((t - t0)/δt)) and the per-pixel count histogram (the
+//              reference's bincount, encoder.py:259)
 //   scan       exclusive prefix sum of the counts -> pixel run starts
-//   sort       stable LSD radix sort of (pixel key, event index): the same
+//   sort       stable LSD radix sort of (pixel key, slot value): the same
 //              stable pixel-major order as np.argsort(flat, kind="stable")
 //              (encoder.py:255-257), so each pixel's run is in time order
-//   k_reduce   one warp per range of 32 pixels walks the sorted runs and sums
-//              e^{i a T} per pixel sequentially in f32 — the order of the
-//              reference's np.add.reduceat (encoder.py:262-267) — then writes
-//              the pixel's 512-byte row of the pre-modulated grid
-//              M = G·e^{i(xX/δx + yY/δy)} exactly once (zeros for empty
-//              pixels); it also emits a in slot order for K3.
+//   k_reduce_x (default, D = 64) sums e^{i a T} per pixel sequentially in f32 —
+//              the order of the reference's np.add.reduceat (encoder.py:262-267)
+//              — and feeds the x half of the pooling window directly, so the
+//              raw grid never reaches HBM (see the kernel comment)
+//   k_reduce   raw-grid variant: writes each pixel's 512-byte row of the
+//              pre-modulated grid M = G·e^{i(xX/δx + yY/δy)} exactly once
+//              (split pooling path for large δx, and the raw-grid parity hook)
 //
-// Compared with scattering fp32 atomics this writes every grid row once (no
+// Compared with scattering fp32 atomics this writes every row once (no
 // memset, no L2 read-modify-write of a grid larger than L2), is bit-
 // deterministic, and reproduces the reference's per-pixel sums bit-for-bit
 // wherever the f32 phases agree (98.9% of sin/cos values).
@@ -22,16 +23,19 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "vkm_device.cuh"
 #include "vkm_kernels.cuh"
 
 namespace vkm {
 
+constexpr unsigned kFullMask = 0xffffffffu;
+
 __global__ void __launch_bounds__(256) k_prep(const double* __restrict__ ev, int64_t n, double t0_in, double delta_t,
                                               int W, int H, int32_t* __restrict__ pix_out,
-                                              float* __restrict__ a_out, int32_t* __restrict__ iota,
-                                              int* __restrict__ cnt, float* __restrict__ flows_invalid,
+                                              uint64_t* __restrict__ val_out, int* __restrict__ cnt,
+                                              float* __restrict__ flows_invalid,
                                               int32_t* __restrict__ counts_invalid) {
   const double t0 = ld_t0(ev, t0_in);
   const int P = W * H;
@@ -48,34 +52,21 @@ __global__ void __launch_bounds__(256) k_prep(const double* __restrict__ ev, int
       if (counts_invalid) counts_invalid[e] = 0;
     }
     pix_out[e] = pix;
-    a_out[e] = time_arg(t, t0, delta_t);
-    iota[e] = int32_t(e);
+    val_out[e] = slot_pack(int32_t(e), time_arg(t, t0, delta_t));
   }
 }
 
-// D8 == 64: a warp owns 32 consecutive pixels and their slot range; slots are
-// loaded 32 at a time (coalesced) and walked in order, lanes = channel pairs.
-__global__ void __launch_bounds__(256) k_reduce(const int* __restrict__ start, const int32_t* __restrict__ perm,
-                                                const int32_t* __restrict__ pix_s, const float* __restrict__ a,
-                                                const float* __restrict__ tf, const float2* __restrict__ mx,
-                                                const float2* __restrict__ my, int W, int64_t P,
-                                                float* __restrict__ a_s, float2* __restrict__ G) {
+// Raw grid, D8 == 64: a warp owns 32 consecutive pixels and their slot range;
+// slots are loaded 32 at a time (coalesced) and walked in order, lanes =
+// channel pairs.  Writes M[pixel] = (Σ e^{i a T}) · e^{i(x X/δx + y Y/δy)}.
+__global__ void __launch_bounds__(256) k_reduce(const int* __restrict__ start, const uint64_t* __restrict__ val_s,
+                                                const int32_t* __restrict__ pix_s, const float* __restrict__ tf,
+                                                const float2* __restrict__ mx, const float2* __restrict__ my, int W,
+                                                int64_t P, float2* __restrict__ G) {
   const int lane = threadIdx.x & 31;
-  const float4* mx4 = reinterpret_cast<const float4*>(mx);
-  const float4* my4 = reinterpret_cast<const float4*>(my);
-  // M[pixel] = (Σ e^{i a T}) · e^{i(x X/δx + y Y/δy)}: the pre-modulated grid K2 box-sums.
-  auto flush = [&](int pix, uint64_t re, uint64_t im) {
-    const int y = pix / W, x = pix - y * W;
-    const float4 fx = __ldg(mx4 + ((int64_t(x) * 64) >> 1) + lane);
-    const float4 fy = __ldg(my4 + ((int64_t(y) * 64) >> 1) + lane);
-    const float2 m0 = cmul(make_float2(fx.x, fx.y), make_float2(fy.x, fy.y));
-    const float2 m1 = cmul(make_float2(fx.z, fx.w), make_float2(fy.z, fy.w));
-    float r0, r1, i0, i1;
-    f2unpack(re, r0, r1);
-    f2unpack(im, i0, i1);
-    const float2 g0 = cmul(make_float2(r0, i0), m0), g1 = cmul(make_float2(r1, i1), m1);
-    reinterpret_cast<float4*>(G)[((int64_t(lane >> 2) * P + pix) << 2) + (lane & 3)] = make_float4(g0.x, g0.y, g1.x, g1.y);
-  };
+  const float4* mx4 = reinterpret_cast<const float4*>(mx) + lane;
+  const float4* my4 = reinterpret_cast<const float4*>(my) + lane;
+  float4* G4 = reinterpret_cast<float4*>(G) + ((int64_t(lane >> 2) * P) << 2) + (lane & 3);
   const uint64_t T01 = f2pack(__ldg(tf + 2 * lane), __ldg(tf + 2 * lane + 1));
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -83,48 +74,55 @@ __global__ void __launch_bounds__(256) k_reduce(const int* __restrict__ start, c
     const int p0 = int(pw), p1 = int(min(P, pw + 32));
     const int s0 = __ldg(start + p0), s1 = __ldg(start + p1);
     int cur = p0;                           // pixel being accumulated
+    int cy = p0 / W, cx = p0 - cy * W;      // its coordinates (advanced incrementally)
     uint64_t re = 0, im = 0;                // packed (ch c0, ch c0+1) sums, f32 in slot order
+    auto flush = [&]() {
+      const float4 fx = __ldg(mx4 + int64_t(cx) * 32), fy = __ldg(my4 + int64_t(cy) * 32);
+      const float2 m0 = cmul(make_float2(fx.x, fx.y), make_float2(fy.x, fy.y));
+      const float2 m1 = cmul(make_float2(fx.z, fx.w), make_float2(fy.z, fy.w));
+      float r0, r1, i0, i1;
+      f2unpack(re, r0, r1);
+      f2unpack(im, i0, i1);
+      const float2 g0 = cmul(make_float2(r0, i0), m0), g1 = cmul(make_float2(r1, i1), m1);
+      G4[int64_t(cur) << 2] = make_float4(g0.x, g0.y, g1.x, g1.y);
+      re = 0;
+      im = 0;
+      ++cur;
+      if (++cx == W) {
+        cx = 0;
+        ++cy;
+      }
+    };
     for (int jb = s0; jb < s1; jb += 32) {
       const int j = jb + lane;
       float av = 0.f;
       int pv = int(P);
       if (j < s1) {
         pv = __ldg(pix_s + j);
-        av = __ldg(a + __ldg(perm + j));
-        a_s[j] = av;
+        av = slot_arg(__ldg(val_s + j));
       }
       const int nj = min(32, s1 - jb);
 #pragma unroll 2
       for (int k = 0; k < nj; ++k) {
-        const int pk = __shfl_sync(0xffffffffu, pv, k);
-        const float ak = __shfl_sync(0xffffffffu, av, k);
+        const int pk = __shfl_sync(kFullMask, pv, k);
+        const float ak = __shfl_sync(kFullMask, av, k);
         uint64_t sn, cs;
         sincos2p_f32(fmul2(f2pack(ak, ak), T01), sn, cs);
-        if (pk != cur) {                    // flush finished pixels (and empty ones in between)
-          do {
-            flush(cur, re, im);
-            re = 0;
-            im = 0;
-          } while (++cur < pk);
-        }
+        while (cur < pk) flush();           // finished pixels (and empty ones in between)
         re = fadd2(re, cs);
         im = fadd2(im, sn);
       }
     }
-    for (; cur < p1; ++cur) {
-      flush(cur, re, im);
-      re = 0;
-      im = 0;
-    }
+    while (cur < p1) flush();
   }
 }
 
 // D8 < 64: one warp per pixel group with lanes = (pixel sub-index, channel pair).
 __global__ void __launch_bounds__(256) k_reduce_small(const int* __restrict__ start, const int* __restrict__ cnt,
-                                                      const int32_t* __restrict__ perm, const float* __restrict__ a,
+                                                      const uint64_t* __restrict__ val_s,
                                                       const float* __restrict__ tf, const float2* __restrict__ mx,
                                                       const float2* __restrict__ my, int W, int64_t P, int D8,
-                                                      float* __restrict__ a_s, float2* __restrict__ G) {
+                                                      float2* __restrict__ G) {
   const int lane = threadIdx.x & 31;
   const int cp = D8 >> 1;
   const int pair = lane % cp, sub = lane / cp, pps = 32 / cp;
@@ -139,8 +137,7 @@ __global__ void __launch_bounds__(256) k_reduce_small(const int* __restrict__ st
     const int s = __ldg(start + p), c = __ldg(cnt + p);
     uint64_t re = 0, im = 0;
     for (int j = s; j < s + c; ++j) {
-      const float av = __ldg(a + __ldg(perm + j));
-      if (pair == 0) a_s[j] = av;
+      const float av = slot_arg(__ldg(val_s + j));
       uint64_t sn, cs;
       sincos2p_f32(fmul2(f2pack(av, av), T01), sn, cs);
       re = fadd2(re, cs);
@@ -155,6 +152,136 @@ __global__ void __launch_bounds__(256) k_reduce_small(const int* __restrict__ st
     const float2 g0 = cmul(make_float2(r0, i0), cmul(__ldg(fx), __ldg(fy)));
     const float2 g1 = cmul(make_float2(r1, i1), cmul(__ldg(fx + 1), __ldg(fy + 1)));
     G4[((int64_t(plane) * P + p) << 2) + q4] = make_float4(g0.x, g0.y, g1.x, g1.y);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1 reduce fused with the x window (D8 == 64).
+//
+// One warp per (row y, segment of S output columns [x0, x1)); lanes = channel
+// pairs.  The warp sweeps input pixels x in [x0-δx, x1+δx): for each it sums
+// e^{i a T} over the pixel's time-ordered slot run in f32 (the reference's
+// reduceat order, encoder.py:262-267), modulates by e^{i x X/δx}, and keeps a
+// sliding window sum over the last 2δx+1 pixels (a per-lane ring in shared
+// memory).  The window centred on x-δx is complete after pixel x, so it is
+// multiplied by e^{i y Y/δy} and written:
+//   R[y][x] = e^{i y Y/δy} · Σ_{|i|<=δx} G[y][x+i] e^{i (x+i) X/δx}
+// The raw grid never reaches HBM; the y pass (k_box_y<true>) finishes the
+// window and demodulates.  Halo pixels (δx each side) are recomputed by the
+// two neighbouring segments.  Events are processed in groups for ILP; pixel
+// boundaries are tracked from start[] (32 run ends per coalesced load).
+// ---------------------------------------------------------------------------
+constexpr int kMaxFusedDx = 24;
+constexpr int kRxWarps = 2;
+constexpr int kRxMaxSeg = 128;
+constexpr int kRxEnds = kRxMaxSeg + 2 * kMaxFusedDx + 4;   // run ends of one segment sweep (+ sentinel)
+#ifndef VKM_RX_GROUP
+#define VKM_RX_GROUP 4
+#endif
+constexpr int kRxGroup = VKM_RX_GROUP;   // events per sin/cos group (divides 32)
+
+size_t reduce_x_smem(int dx) { return size_t(kRxWarps) * ((2 * dx + 1) * 512 + kRxEnds * 4); }
+
+__global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restrict__ start,
+                                                            const uint64_t* __restrict__ val_s,
+                                                            const float* __restrict__ tf,
+                                                            const float4* __restrict__ mxp,
+                                                            const float2* __restrict__ my, int W, int H, int dx,
+                                                            int S, int nseg, int64_t P, float2* __restrict__ R) {
+  extern __shared__ __align__(16) uint8_t rx_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int RL = 2 * dx + 1;
+  ulonglong2* const ring0 = reinterpret_cast<ulonglong2*>(rx_smem) + wib * RL * 32 + lane;
+  ulonglong2* const ring_end = ring0 + RL * 32;
+  int* const ends = reinterpret_cast<int*>(rx_smem + size_t(kRxWarps) * RL * 512) + wib * kRxEnds;
+  const uint64_t T01 = f2pack(__ldg(tf + 2 * lane), __ldg(tf + 2 * lane + 1));
+  const float4* mxl = mxp + lane;                   // mxl[x * 32]: (cos c0, cos c1, sin c0, sin c1) of x X/δx
+  const float4* my4 = reinterpret_cast<const float4*>(my) + lane;
+  float4* const R4 = reinterpret_cast<float4*>(R) + ((int64_t(lane >> 2) * P) << 2) + (lane & 3);
+  const int64_t items = int64_t(H) * nseg;
+  const int64_t nwarps = int64_t(gridDim.x) * kRxWarps;
+  for (int64_t it = int64_t(blockIdx.x) * kRxWarps + wib; it < items; it += nwarps) {
+    const int y = int(it / nseg);
+    const int x0 = int(it - int64_t(y) * nseg) * S, x1 = min(W, x0 + S);
+    const int xs = x0 - dx, nx = x1 + dx - xs;      // sweep x = xs + k, k in [0, nx)
+    const int* st = start + int64_t(y) * W;         // st[x]: first slot of pixel (x, y)
+    const int jfirst = __ldg(st + max(0, xs)), jend = __ldg(st + min(W, x1 + dx));
+    __syncwarp();
+    for (int k = lane; k <= nx; k += 32) {          // ends[k]: end slot of pixel xs + k's run
+      const int x = xs + k;
+      ends[k] = k == nx ? jend : (x < 0 ? jfirst : (x < W ? __ldg(st + x + 1) : jend));
+    }
+    for (int k = 0; k < RL; ++k) ring0[k * 32] = make_ulonglong2(0ull, 0ull);
+    __syncwarp();
+    const float4 fy4 = __ldg(my4 + int64_t(y) * 32);
+    const uint64_t fyr = f2pack(fy4.x, fy4.z), fyi = f2pack(fy4.y, fy4.w);
+    float4* out = R4 + ((int64_t(y) * W + x0) << 2);
+    auto ld_a = [&](int jj) { return jj < jend ? slot_arg(__ldg(val_s + jj)) : 0.f; };
+    int jb = jfirst;
+    float av0 = ld_a(jb + lane), av1 = ld_a(jb + 32 + lane);
+
+    int k = 0;                                      // sweep index of the pixel being summed
+    int je = ends[0];
+    float4 mc = __ldg(mxl + int64_t(min(max(xs, 0), W - 1)) * 32);
+    uint64_t gr = 0, gi = 0, ar = 0, ai = 0;
+    ulonglong2* pn = ring0;                          // ring slot of pixel k
+    ulonglong2* po = ring0 + 32;                     // ring slot of pixel k - 2δx
+    auto finish = [&]() {
+      const uint64_t mre = f2pack(mc.x, mc.y), mim = f2pack(mc.z, mc.w);
+      const uint64_t mr = fsub2(fmul2(gr, mre), fmul2(gi, mim));
+      const uint64_t mi = ffma2(gr, mim, fmul2(gi, mre));
+      const ulonglong2 old = *po;
+      *pn = make_ulonglong2(mr, mi);
+      ar = fadd2(ar, mr);
+      ai = fadd2(ai, mi);
+      if (k >= 2 * dx) {
+        const uint64_t orr = fsub2(fmul2(ar, fyr), fmul2(ai, fyi));
+        const uint64_t oi = ffma2(ar, fyi, fmul2(ai, fyr));
+        float r0, r1, i0, i1;
+        f2unpack(orr, r0, r1);
+        f2unpack(oi, i0, i1);
+        *out = make_float4(r0, i0, r1, i1);
+        out += 4;
+      }
+      ar = fsub2(ar, old.x);
+      ai = fsub2(ai, old.y);
+      gr = 0;
+      gi = 0;
+      pn = po;
+      po = (po + 32 == ring_end) ? ring0 : po + 32;
+      ++k;
+      je = ends[k];
+      mc = __ldg(mxl + int64_t(min(max(xs + k, 0), W - 1)) * 32);   // next pixel's factor, in flight early
+    };
+
+    // Events in groups of kRxGroup: the sin/cos of a whole group are computed
+    // back to back (independent chains), then added in slot order with the
+    // pixel boundaries resolved between them.  Groups never straddle a 32-slot
+    // batch (both advance from jfirst).
+    for (int j = jfirst; j < jend; j += kRxGroup) {
+      if (j - jb >= 32) {
+        jb += 32;
+        av0 = av1;
+        av1 = ld_a(jb + 32 + lane);
+      }
+      const int i0 = j - jb;
+      uint64_t cs[kRxGroup], sn[kRxGroup];
+#pragma unroll
+      for (int u = 0; u < kRxGroup; ++u) {
+        const float au = __shfl_sync(kFullMask, av0, i0 + u);
+        sincos2p_f32(fmul2(f2pack(au, au), T01), sn[u], cs[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kRxGroup; ++u) {
+        if (j + u >= je) {                           // pixel boundary (je <= jend)
+          if (j + u >= jend) break;
+          do finish(); while (j + u >= je);
+        }
+        gr = fadd2(gr, cs[u]);
+        gi = fadd2(gi, sn[u]);
+      }
+    }
+    while (k < nx) finish();
   }
 }
 
@@ -175,21 +302,19 @@ size_t sort_scan_temp_bytes(int64_t P) {
 size_t sort_pairs_temp_bytes(int64_t n, int64_t P) {
   size_t bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
-                                  static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr), int(n), 0,
+                                  static_cast<const uint64_t*>(nullptr), static_cast<uint64_t*>(nullptr), int(n), 0,
                                   key_bits(P));
   return bytes;
 }
 
-int launch_accumulate_sorted(const double* ev, int64_t n, double t0, double delta_t, const DevTables& tb, int W,
-                             int H, int D8, const GridBufs& g, const SortBufs& sb, float* flows_invalid,
-                             int32_t* counts_invalid, cudaStream_t s) {
+int launch_sort_events(const double* ev, int64_t n, double t0, double delta_t, int W, int H, const GridBufs& g,
+                       const SortBufs& sb, float* flows_invalid, int32_t* counts_invalid, cudaStream_t s) {
   const int64_t P = int64_t(W) * H;
   int launches = 0;
   cudaMemsetAsync(g.C, 0, sizeof(int) * (P + 1), s);
   if (n > 0) {
     const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
-    k_prep<<<blocks, 256, 0, s>>>(ev, n, t0, delta_t, W, H, sb.pix, sb.a, sb.iota, g.C, flows_invalid,
-                                  counts_invalid);
+    k_prep<<<blocks, 256, 0, s>>>(ev, n, t0, delta_t, W, H, sb.pix, sb.val, g.C, flows_invalid, counts_invalid);
     ++launches;
   }
   size_t scan_bytes = sb.temp_bytes;
@@ -197,22 +322,66 @@ int launch_accumulate_sorted(const double* ev, int64_t n, double t0, double delt
   launches += 2;   // CUB: init + scan
   if (n > 0) {
     size_t sort_bytes = sb.sort_temp_bytes;
-    cub::DeviceRadixSort::SortPairs(sb.sort_temp, sort_bytes, sb.pix, sb.pix_s, sb.iota, sb.perm, int(n), 0,
+    cub::DeviceRadixSort::SortPairs(sb.sort_temp, sort_bytes, sb.pix, sb.pix_s, sb.val, sb.val_s, int(n), 0,
                                     key_bits(P), s);
-    launches += 4;   // CUB onesweep: histogram, exclusive sum, digit passes
+    launches += 2 + (key_bits(P) + 7) / 8;   // CUB onesweep: histogram, exclusive sum, one pass per 8-bit digit
   }
+  return launches;
+}
+
+namespace {
+int resident_blocks(const void* fn, int threads, size_t smem) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
+  return std::max(1, per) * sms;
+}
+}  // namespace
+
+void launch_reduce_raw(const DevTables& tb, int W, int H, int D8, const GridBufs& g, const SortBufs& sb,
+                       cudaStream_t s) {
+  const int64_t P = int64_t(W) * H;
   if (D8 == 64) {
     const int64_t warps = (P + 31) / 32;
-    const int blocks = int(std::min<int64_t>((warps + 7) / 8, 148 * 64));
-    k_reduce<<<blocks, 256, 0, s>>>(sb.start, sb.perm, sb.pix_s, sb.a, tb.tf, tb.mx, tb.my, W, P, sb.a_s, g.G);
+    static const int res = resident_blocks(reinterpret_cast<const void*>(k_reduce), 256, 0);
+    const int blocks = int(std::min<int64_t>((warps + 7) / 8, res));
+    k_reduce<<<blocks, 256, 0, s>>>(sb.start, sb.val_s, sb.pix_s, tb.tf, tb.mx, tb.my, W, P, g.G);
   } else {
     const int cp = D8 >> 1, pps = 32 / cp;
     const int64_t warps = (P + pps - 1) / pps;
     const int blocks = int(std::min<int64_t>((warps + 7) / 8, 148 * 64));
-    k_reduce_small<<<blocks, 256, 0, s>>>(sb.start, g.C, sb.perm, sb.a, tb.tf, tb.mx, tb.my, W, P, D8, sb.a_s, g.G);
+    k_reduce_small<<<blocks, 256, 0, s>>>(sb.start, g.C, sb.val_s, tb.tf, tb.mx, tb.my, W, P, D8, g.G);
   }
-  ++launches;
-  return launches;
+}
+
+bool reduce_x_supported(int D8, int dx) { return D8 == 64 && dx >= 1 && dx <= kMaxFusedDx; }
+
+void launch_reduce_x(const DevTables& tb, int W, int H, int dx, const SortBufs& sb, float2* R, int num_sms,
+                     cudaStream_t s) {
+  const int64_t P = int64_t(W) * H;
+  const size_t smem = reduce_x_smem(dx);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_reduce_x, cudaFuncAttributeMaxDynamicSharedMemorySize, int(reduce_x_smem(kMaxFusedDx)));
+    attr = true;
+  }
+  int per = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reduce_x, kRxWarps * 32, smem);
+  const int64_t res_warps = int64_t(std::max(1, per)) * num_sms * kRxWarps;
+  // Segment width: long segments keep the recomputed 2δx halo small; shorter
+  // ones when a row split into 128-column segments would not fill the GPU.
+  static const int seg_env = [] {
+    const char* e = std::getenv("VKM_RX_SEG");
+    return e ? std::atoi(e) : 0;
+  }();
+  int S = seg_env > 0 ? std::min(seg_env, kRxMaxSeg) : kRxMaxSeg;
+  if (seg_env <= 0)
+    while (S > 32 && 4 * int64_t(H) * ((W + S - 1) / S) < 3 * res_warps) S >>= 1;
+  const int nseg = (W + S - 1) / S;
+  const int64_t items = int64_t(H) * nseg;
+  const int blocks = int(std::min<int64_t>((items + kRxWarps - 1) / kRxWarps, res_warps / kRxWarps));
+  k_reduce_x<<<blocks, kRxWarps * 32, smem, s>>>(sb.start, sb.val_s, tb.tf, tb.mxp, tb.my, W, H, dx, S, nseg, P, R);
 }
 
 }  // namespace vkm

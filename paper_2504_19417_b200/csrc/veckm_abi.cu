@@ -65,6 +65,7 @@ struct vkm_handle {
   float* tf = nullptr;
   float2* my = nullptr;
   float2* mx = nullptr;
+  float4* mxp = nullptr;
   float* w1p = nullptr;  // [hidden][2*D8] padded
   float* b1 = nullptr;
   float* w2 = nullptr;
@@ -74,6 +75,7 @@ struct vkm_handle {
   void* w1_bf16 = nullptr;
   float w_scale_f16 = 1.f;
   bool tc_ok = false;  // D == 64 && hidden == 128
+  bool force_split = false;  // VKM_POOL=split: raw grid + two-pass pooling (A/B and parity)
   // scratch
   vkm::SortBufs sb{};
   size_t sort_cap = 0;
@@ -112,7 +114,7 @@ int grow(T** ptr, size_t* cap, size_t need) {
   return VKM_OK;
 }
 
-vkm::DevTables tables(const vkm_handle* h) { return vkm::DevTables{h->tf, h->my, h->mx}; }
+vkm::DevTables tables(const vkm_handle* h) { return vkm::DevTables{h->tf, h->my, h->mx, h->mxp}; }
 vkm::GridBufs bufs(const vkm_handle* h) { return vkm::GridBufs{h->G, h->C, h->Q, h->NQ}; }
 
 void rec(vkm_handle* h, int i, cudaStream_t s) {
@@ -121,18 +123,16 @@ void rec(vkm_handle* h, int i, cudaStream_t s) {
 
 int ensure_sort(vkm_handle* h, int64_t n) {
   if (h->sort_cap >= size_t(std::max<int64_t>(n, 1))) return VKM_OK;
-  void* arrs[] = {h->sb.pix, h->sb.a, h->sb.iota, h->sb.perm, h->sb.a_s, h->sb.pix_s, h->sb.sort_temp};
+  void* arrs[] = {h->sb.pix, h->sb.val, h->sb.val_s, h->sb.pix_s, h->sb.sort_temp};
   for (void* p : arrs)
     if (p) cudaFree(p);
-  h->sb.pix = nullptr; h->sb.a = nullptr; h->sb.iota = nullptr; h->sb.perm = nullptr;
-  h->sb.a_s = nullptr; h->sb.pix_s = nullptr; h->sb.sort_temp = nullptr;
+  h->sb.pix = nullptr; h->sb.val = nullptr; h->sb.val_s = nullptr; h->sb.pix_s = nullptr;
+  h->sb.sort_temp = nullptr;
   const size_t cap = size_t(std::max<int64_t>(n, 1));
   h->sort_cap = 0;
   VKM_CK(cudaMalloc(&h->sb.pix, 4 * cap));
-  VKM_CK(cudaMalloc(&h->sb.a, 4 * cap));
-  VKM_CK(cudaMalloc(&h->sb.iota, 4 * cap));
-  VKM_CK(cudaMalloc(&h->sb.perm, 4 * cap));
-  VKM_CK(cudaMalloc(&h->sb.a_s, 4 * cap));
+  VKM_CK(cudaMalloc(&h->sb.val, 8 * cap));
+  VKM_CK(cudaMalloc(&h->sb.val_s, 8 * cap));
   VKM_CK(cudaMalloc(&h->sb.pix_s, 4 * cap));
   h->sb.sort_temp_bytes = vkm::sort_pairs_temp_bytes(int64_t(cap), h->P);
   VKM_CK(cudaMalloc(&h->sb.sort_temp, std::max<size_t>(h->sb.sort_temp_bytes, 16)));
@@ -140,23 +140,39 @@ int ensure_sort(vkm_handle* h, int64_t n) {
   return VKM_OK;
 }
 
-// K1 + K2 for one slice on stream s.
+// K1 + K2 for one slice on stream s.  pooled = 0 leaves the raw pre-modulated
+// grid in G (parity hook); otherwise the pooled grid ends in Q.
 int encode_core(vkm_handle* h, const double* ev, int64_t n, double t0, int pooled, cudaStream_t s, int* launches,
                 float* flows_invalid = nullptr, int32_t* counts_invalid = nullptr) {
   const int W = h->p.width, H = h->p.height;
   int rc = ensure_sort(h, n);
   if (rc) return rc;
-  *launches += vkm::launch_accumulate_sorted(ev, n, t0, h->p.delta_t, tables(h), W, H, h->D8, bufs(h), h->sb,
-                                             flows_invalid, counts_invalid, s);
-  VKM_CK(cudaGetLastError());
-  rec(h, 1, s);
-  if (pooled) {
-    // y-pass M(G) -> R(Q), x-pass R(Q) -> pooled(G); then swap so Q names the pooled grid
-    vkm::launch_pool_split(tables(h), W, H, h->D8, h->p.delta_x, h->p.delta_y, h->G, h->Q, h->G, s);
-    std::swap(h->G, h->Q);
-    vkm::launch_pool_count(W, H, h->p.delta_x, h->p.delta_y, bufs(h), s);
-    *launches += 3;
+  *launches += vkm::launch_sort_events(ev, n, t0, h->p.delta_t, W, H, bufs(h), h->sb, flows_invalid,
+                                       counts_invalid, s);
+  const bool fused = pooled && !h->force_split && vkm::reduce_x_supported(h->D8, h->p.delta_x);
+  if (fused) {
+    // x window fused into the reduction: R -> G, then y window + demodulation G -> Q
+    vkm::launch_reduce_x(tables(h), W, H, h->p.delta_x, h->sb, h->G, h->num_sms, s);
+    *launches += 1;
     VKM_CK(cudaGetLastError());
+    rec(h, 1, s);
+    vkm::launch_pool_y_demod(tables(h), W, H, h->D8, h->p.delta_y, h->G, h->Q, s);
+    vkm::launch_pool_count(W, H, h->p.delta_x, h->p.delta_y, bufs(h), s);
+    *launches += 2;
+    VKM_CK(cudaGetLastError());
+  } else {
+    vkm::launch_reduce_raw(tables(h), W, H, h->D8, bufs(h), h->sb, s);
+    *launches += 1;
+    VKM_CK(cudaGetLastError());
+    rec(h, 1, s);
+    if (pooled) {
+      // y-pass M(G) -> R(Q), x-pass R(Q) -> pooled(G); then swap so Q names the pooled grid
+      vkm::launch_pool_split(tables(h), W, H, h->D8, h->p.delta_x, h->p.delta_y, h->G, h->Q, h->G, s);
+      std::swap(h->G, h->Q);
+      vkm::launch_pool_count(W, H, h->p.delta_x, h->p.delta_y, bufs(h), s);
+      *launches += 3;
+      VKM_CK(cudaGetLastError());
+    }
   }
   rec(h, 2, s);
   return VKM_OK;
@@ -267,6 +283,10 @@ int vkm_create(vkm_handle** out, const vkm_params* params, const double* T, cons
   h->P = int64_t(p.width) * p.height;
   h->num_sms = prop.multiProcessorCount;
   h->tc_ok = (h->D == 64 && h->hidden == 128);
+  {
+    const char* e = std::getenv("VKM_POOL");
+    h->force_split = e && std::strcmp(e, "split") == 0;
+  }
   h->mode = p.mlp_mode == VKM_MLP_AUTO ? (h->tc_ok ? VKM_MLP_F16X3 : VKM_MLP_FP32) : p.mlp_mode;
   if ((h->mode == VKM_MLP_F16X3 || h->mode == VKM_MLP_BF16) && !h->tc_ok) h->mode = VKM_MLP_FP32;
 
@@ -308,6 +328,16 @@ int vkm_create(vkm_handle** out, const vkm_params* params, const double* T, cons
   VKM_CKH(cudaMemcpy(h->tf, tf.data(), sizeof(float) * D8, cudaMemcpyHostToDevice));
   VKM_CKH(cudaMemcpy(h->my, my.data(), sizeof(float2) * my.size(), cudaMemcpyHostToDevice));
   VKM_CKH(cudaMemcpy(h->mx, mx.data(), sizeof(float2) * mx.size(), cudaMemcpyHostToDevice));
+  if (D8 == 64) {   // lane-packed copy of the x table for k_reduce_x
+    std::vector<float4> mxp(size_t(W) * 32);
+    for (int x = 0; x < W; ++x)
+      for (int l = 0; l < 32; ++l) {
+        const float2 a = mx[size_t(x) * 64 + 2 * l], b = mx[size_t(x) * 64 + 2 * l + 1];
+        mxp[size_t(x) * 32 + l] = make_float4(a.x, b.x, a.y, b.y);
+      }
+    VKM_CKH(cudaMalloc(&h->mxp, sizeof(float4) * mxp.size()));
+    VKM_CKH(cudaMemcpy(h->mxp, mxp.data(), sizeof(float4) * mxp.size(), cudaMemcpyHostToDevice));
+  }
 
   // Grid scratch: two planes-sets of 64 B/pixel plus int32 counts (516 B/pixel at D=64).
   VKM_CKH(cudaMalloc(&h->G, sizeof(float2) * 8 * h->planes * h->P));
@@ -373,10 +403,9 @@ void vkm_destroy(vkm_handle* h) {
   if (!h) return;
   DeviceGuard dg(h->p.device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->tf, h->my, h->mx, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
+  void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
                   h->G, h->C, h->Q, h->NQ, h->feats, h->cnt_scratch, h->ev_stage, h->out_stage, h->cnt_stage,
-                  h->sb.pix, h->sb.a, h->sb.iota, h->sb.start, h->sb.perm, h->sb.a_s, h->sb.pix_s, h->sb.temp,
-                  h->sb.sort_temp};
+                  h->sb.pix, h->sb.val, h->sb.start, h->sb.val_s, h->sb.pix_s, h->sb.temp, h->sb.sort_temp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->evt)

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstring>
 
 namespace vkm {
 
@@ -9,6 +10,7 @@ struct DevTables {
   const float* tf;     // f32(T_c), [D8]                       (encoder.py:223-224)
   const float2* my;    // e^{i y Y_c / dy}, [H][D8] complex64   (modulation, y axis)
   const float2* mx;    // e^{i x X_c / dx}, [W][D8] complex64   (modulation, x axis)
+  const float4* mxp;   // D8 == 64: [W][32] (cos c0, cos c1, sin c0, sin c1) of x X_c/dx, c0 = 2·lane
 };
 
 struct GridBufs {
@@ -18,14 +20,27 @@ struct GridBufs {
   int* NQ;     // [P]
 };
 
-// Pixel-sorted event order produced by the sorted K1 (k_sort.cu).
+// Pixel-sorted event order produced by the sorted K1 (k_sort.cu).  Sort
+// values pack (event index, f32 time argument) so the consumers of a slot read
+// one coalesced 8-byte word instead of chasing perm[] into a[].
+__host__ __device__ inline uint64_t slot_pack(int32_t e, float a) {
+  uint32_t ab;
+  memcpy(&ab, &a, 4);
+  return uint64_t(uint32_t(e)) | (uint64_t(ab) << 32);
+}
+__host__ __device__ inline int32_t slot_event(uint64_t v) { return int32_t(uint32_t(v)); }
+__host__ __device__ inline float slot_arg(uint64_t v) {
+  const uint32_t ab = uint32_t(v >> 32);
+  float a;
+  memcpy(&a, &ab, 4);
+  return a;
+}
+
 struct SortBufs {
   int32_t* pix;      // [n]  pixel key per event (P: outside the sensor)
-  float* a;          // [n]  f32 time argument per event
-  int32_t* iota;     // [n]  0..n-1 (sort values)
+  uint64_t* val;     // [n]  slot_pack(e, a) per event (sort values)
   int* start;        // [P+1] exclusive scan of the counts (start[P] = valid events)
-  int32_t* perm;     // [n]  slot -> event (stable pixel-major order)
-  float* a_s;        // [n]  slot -> a
+  uint64_t* val_s;   // [n]  slot -> slot_pack(event, a), stable pixel-major order
   int32_t* pix_s;    // [n]  slot -> pixel
   void* temp;        // CUB scan scratch
   size_t temp_bytes;
@@ -41,17 +56,30 @@ struct MlpDev {
   int hidden;
 };
 
-// K1 (sorted, default): prep + scan + scatter + per-pixel exact reduction.
+// K1 (sorted): prep + scan + stable radix sort of (pixel, slot_pack) pairs.
 // Returns the number of kernel launches.  C must hold P+1 ints.
-int launch_accumulate_sorted(const double* ev, int64_t n, double t0, double delta_t, const DevTables& tb, int W,
-                             int H, int D8, const GridBufs& g, const SortBufs& sb, float* flows_invalid,
-                             int32_t* counts_invalid, cudaStream_t s);
+int launch_sort_events(const double* ev, int64_t n, double t0, double delta_t, int W, int H, const GridBufs& g,
+                       const SortBufs& sb, float* flows_invalid, int32_t* counts_invalid, cudaStream_t s);
+// K1 reduce, raw grid: per-pixel time-ordered sums, written pre-modulated
+// (M = G·e^{i(xX/δx + yY/δy)}) to g.G.  Used by the split pooling path and the
+// raw-grid parity hook.
+void launch_reduce_raw(const DevTables& tb, int W, int H, int D8, const GridBufs& g, const SortBufs& sb,
+                       cudaStream_t s);
+// K1 reduce fused with the x window (D8 == 64, dx <= kMaxFusedDx):
+//   R[y][x] = e^{i y Y/δy} · Σ_{|i|<=δx} G[y][x+i]·e^{i (x+i) X/δx}   -> R
+bool reduce_x_supported(int D8, int dx);
+void launch_reduce_x(const DevTables& tb, int W, int H, int dx, const SortBufs& sb, float2* R, int num_sms,
+                     cudaStream_t s);
 size_t sort_scan_temp_bytes(int64_t P);
 size_t sort_pairs_temp_bytes(int64_t n, int64_t P);
-// K2: box sum of the pre-modulated grid M (y-pass M -> R, x-pass + demodulation
-// R -> Qout); Qout may alias M (k_pool.cu).
+// K2 (split): box sum of the pre-modulated grid M (y-pass M -> R, x-pass +
+// demodulation R -> Qout); Qout may alias M (k_pool.cu).
 void launch_pool_split(const DevTables& tb, int W, int H, int D8, int dx, int dy, float2* M, float2* R,
                        float2* Qout, cudaStream_t s);
+// K2 (fused path): y window of the x-pooled R plus full demodulation
+//   Q[y][x] = conj(e^{i(xX/δx + yY/δy)}) · Σ_{|j|<=δy} R[y+j][x]
+void launch_pool_y_demod(const DevTables& tb, int W, int H, int D8, int dy, const float2* R, float2* Q,
+                         cudaStream_t s);
 void launch_pool_count(int W, int H, int dx, int dy, const GridBufs& g, cudaStream_t s);
 // K3a: gather Q at each event, de-phase, divide by the count -> features.
 // Row e gets Re at out[e*ld + c] and Im at out[e*ld + im_off + c] for c < Dout.
