@@ -141,8 +141,9 @@ __global__ void __launch_bounds__(256) k_features(const double* __restrict__ ev,
       float s0, k0, s1, k1;
       sincos2_f32(__fmul_rn(aj, T0), __fmul_rn(aj, T1), s0, k0, s1, k1);
       const float den = float(max(cj, 1));
-      const float2 e0 = cmul_rn(make_float2(k0, -s0), make_float2(acc.x, acc.y));
-      const float2 e1 = cmul_rn(make_float2(k1, -s1), make_float2(acc.z, acc.w));
+      // pooled grid chunk in packed-pair layout (re c0, re c1, im c0, im c1)
+      const float2 e0 = cmul_rn(make_float2(k0, -s0), make_float2(acc.x, acc.z));
+      const float2 e1 = cmul_rn(make_float2(k1, -s1), make_float2(acc.y, acc.w));
       float* row = out + (base + src) * int64_t(ld);
       if (c0 + 1 < Dout) {
         *reinterpret_cast<float2*>(row + c0) = make_float2(__fdiv_rn(e0.x, den), __fdiv_rn(e1.x, den));
@@ -242,7 +243,7 @@ void launch_mlp_ffma(const float* feats, const int32_t* counts, int64_t n, int D
 // Parity hook: plane layout -> reference PixelGrid layout [x][y][D] complex64.
 // ---------------------------------------------------------------------------
 __global__ void k_grid_to_ref(const float2* __restrict__ G, const int* __restrict__ C, int W, int H, int D, int D8,
-                              const float2* __restrict__ mx, const float2* __restrict__ my,
+                              const float2* __restrict__ mx, const float2* __restrict__ my, bool packed,
                               float2* __restrict__ out, int32_t* __restrict__ oc) {
   const int64_t P = int64_t(W) * H;
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -251,7 +252,13 @@ __global__ void k_grid_to_ref(const float2* __restrict__ G, const int* __restric
   const int64_t xy = i / D;            // x * H + y
   const int x = int(xy / H), y = int(xy % H);
   const int64_t pix = int64_t(y) * W + x;
-  float2 v = G[(int64_t(c >> 3) * P + pix) * 8 + (c & 7)];
+  float2 v;
+  if (packed) {
+    const float* f = reinterpret_cast<const float*>(G + (int64_t(c >> 3) * P + pix) * 8) + ((c & 7) >> 1) * 4 + (c & 1);
+    v = make_float2(f[0], f[2]);
+  } else {
+    v = G[(int64_t(c >> 3) * P + pix) * 8 + (c & 7)];
+  }
   if (mx) {   // the raw grid is stored pre-modulated (M = G·e^{i(xX+yY)}): undo it
     const float2 m = cmul(__ldg(mx + int64_t(x) * D8 + c), __ldg(my + int64_t(y) * D8 + c));
     v = cmulc(v, m);
@@ -261,9 +268,9 @@ __global__ void k_grid_to_ref(const float2* __restrict__ G, const int* __restric
 }
 
 void launch_grid_to_ref(const float2* G, const int* C, int W, int H, int D, int D8, const float2* mx,
-                        const float2* my, float* out_grid, int32_t* out_counts, cudaStream_t s) {
+                        const float2* my, bool packed, float* out_grid, int32_t* out_counts, cudaStream_t s) {
   const int64_t tot = int64_t(W) * H * D;
-  k_grid_to_ref<<<int((tot + 255) / 256), 256, 0, s>>>(G, C, W, H, D, D8, mx, my, reinterpret_cast<float2*>(out_grid),
+  k_grid_to_ref<<<int((tot + 255) / 256), 256, 0, s>>>(G, C, W, H, D, D8, mx, my, packed, reinterpret_cast<float2*>(out_grid),
                                                        out_counts);
 }
 

@@ -36,12 +36,13 @@ constexpr int kM = 128;             // events per tile (UMMA M)
 constexpr int kN = 128;             // hidden units (UMMA N)
 constexpr int kK = 128;             // features 2D (UMMA K total)
 constexpr int kStages = 2;
-constexpr int kAcc = 2;
+constexpr int kAcc = 4;                // TMEM accumulators (4 x 128 columns = all 512)
 constexpr int kTileBytes = kM * kK * 2;        // 32 KB per fp16 operand image
 constexpr int kAtomBytes = kM * 128;           // one 64-wide K atom: 128 rows x 128 B
 constexpr int kProdWarps = 16;                // producer warps (8 tile rows each)
 constexpr int kThreads = (kProdWarps + 5) * 32; // + 4 epilogue warps + 1 MMA warp
-constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kTmemCols = kAcc * kN;
+constexpr int kQD = 4;                          // per-warp cp.async ring of pooled rows (3 in flight)
 
 struct Smem {
   // operand images, each 1024-byte aligned (SWIZZLE_128B atoms)
@@ -49,6 +50,7 @@ struct Smem {
   uint8_t bl[kTileBytes];
   uint8_t ah[kStages][kTileBytes];
   uint8_t al[kStages][kTileBytes];
+  float4 qring[kProdWarps][kQD][32];   // per producer warp: pooled rows of its next kQD-1 events
   float b1[kN];
   float2 w2i[kN];   // (w2[0][n], w2[1][n]) interleaved for packed FFMA2
   float b2[2];
@@ -56,6 +58,8 @@ struct Smem {
   uint32_t tmem_base;
   unsigned long long full[kStages], empty[kStages], tfull[kAcc], tempty[kAcc];
 };
+
+static_assert(sizeof(Smem) + 1024 <= 232448, "K3 shared memory exceeds the 227 KB opt-in limit");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -73,15 +77,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
   const uint32_t a = smem_u32(b);
   uint32_t done = 0;
   for (uint32_t it = 0;; ++it) {
+    // suspend-time hint: a waiting warp sleeps in the barrier unit (up to
+    // ~20 us per try) instead of spinning on issue slots the producers need
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(20000u)
         : "memory");
     if (done) return;
-    if (it > (1u << 26)) __trap();
+    if (it > (1u << 20)) __trap();
   }
 }
 
@@ -187,11 +193,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp < kProdWarps) {
     // ======================= producers =======================
-    // Warp w fills tile rows [8w, 8w+8) (pixel-sorted slots).  Its 8
-    // pooled-grid gathers are issued before the stage wait, the slot metadata
-    // (pixel, time argument, 1/count) is loaded a tile ahead, and one thread
-    // prefetches the pooled-grid rows of the next two tiles into L2 with bulk
-    // (TMA-engine) prefetches, so the gathers mostly hit L2.
+    // Warp w fills tile rows [8w, 8w+8) (pixel-sorted slots).  Its pooled-
+    // grid rows stream through a cp.async ring (3 rows in flight), the slot
+    // metadata (pixel, time argument, 1/count) is loaded a tile ahead, and one
+    // thread prefetches the pooled-grid rows of the next two tiles into L2
+    // with bulk (TMA-engine) prefetches, so the ring mostly hits L2.
     const int c0 = 2 * lane;                      // this lane's channel pair
     const uint64_t T01 = f2pack(__ldg(tf + c0), __ldg(tf + c0 + 1));
     const float4* Q4 = reinterpret_cast<const float4*>(Q);
@@ -226,23 +232,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
       }
     };
-    auto gather = [&](int pix_reg, float4 (&dst)[kRows]) {
-#pragma unroll
-      for (int u = 0; u < kRows; ++u) {
-        const int pj = __shfl_sync(0xffffffffu, pix_reg, u);
-        dst[u] = pj >= 0 ? __ldg(Q4 + ((int64_t(plane) * P + pj) << 2) + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+    // Pooled rows stream through a per-warp ring in shared memory: row r is
+    // read from slot r % kQD while the rows r+1 .. r+kQD-1 are in flight
+    // (cp.async, 16 B per lane, zero-filled for empty slots), so the
+    // L2/HBM latency of the gathers overlaps the de-phase/split work.
+    float4* const ring = &S.qring[warp][0][lane];
+    auto issue_row = [&](int pj, int slot) {
+      const float4* src = Q4 + ((int64_t(plane) * P + (pj >= 0 ? pj : 0)) << 2) + q4;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n\tcp.async.commit_group;" ::"r"(
+                       smem_u32(ring + slot * 32)),
+                   "l"(src), "r"(pj >= 0 ? 16 : 0)
+                   : "memory");
     };
-    auto compute = [&](float a_reg, float rs_reg, const float4 (&src)[kRows], uint8_t* ah, uint8_t* al) {
+    auto compute = [&](float a_reg, float rs_reg, int pix_c, int pix_n, uint8_t* ah, uint8_t* al) {
 #pragma unroll
       for (int u = 0; u < kRows; ++u) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kQD - 2) : "memory");
+        const float4 src_u = ring[(u & (kQD - 1)) * 32];
+        {   // refill the slot read one row ago with the row kQD-1 ahead
+          const int un = u + kQD - 1;
+          const int pj = un < kRows ? __shfl_sync(0xffffffffu, pix_c, un) : __shfl_sync(0xffffffffu, pix_n, un - kRows);
+          issue_row(pj, un & (kQD - 1));
+        }
         const float aj = __shfl_sync(0xffffffffu, a_reg, u);
         const float rs = __shfl_sync(0xffffffffu, rs_reg, u);
         const uint32_t m = warp * kRows + u;
         uint64_t sn, cs;
         sincos2p_f32(fmul2(f2pack(aj, aj), T01), sn, cs);
         // conj(phase) * acc / cnt for channels (c0, c0+1), packed
-        const uint64_t ar = f2pack(src[u].x, src[u].z), ai = f2pack(src[u].y, src[u].w);
+        const uint64_t ar = f2pack(src_u.x, src_u.y), ai = f2pack(src_u.z, src_u.w);   // packed pairs
         const uint64_t rs2 = f2pack(rs, rs);
         const uint64_t re = fmul2(ffma2(sn, ai, fmul2(cs, ar)), rs2);
         const uint64_t im = fmul2(ffma2(fneg2(sn), ar, fmul2(cs, ai)), rs2);
@@ -277,15 +295,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     load_meta(int64_t(blockIdx.x) + G, a_n, pix_n, rs_n);
     prefetch_l2(blockIdx.x);
     prefetch_l2(int64_t(blockIdx.x) + G);
+#pragma unroll
+    for (int u = 0; u < kQD - 1; ++u) issue_row(__shfl_sync(0xffffffffu, pix_c, u), u);
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++it) {
       const int s = it & 1;
       const uint32_t ph = (it >> 1) & 1;
       prefetch_l2(tile + 2 * G);
-      float4 acc[kRows];
-      gather(pix_c, acc);                           // in flight across the stage wait
       mbar_wait(&S.empty[s], ph ^ 1);
-      compute(a_c, rs_c, acc, S.ah[s], S.al[s]);
+      compute(a_c, rs_c, pix_c, pix_n, S.ah[s], S.al[s]);
       fence_proxy_async();
       mbar_arrive(&S.full[s]);
       a_c = a_n;
@@ -293,14 +311,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       rs_c = rs_n;
       load_meta(tile + 2 * G, a_n, pix_n, rs_n);
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp < kProdWarps + 4) {
     // ======================= epilogue =======================
     const int q = warp & 3;   // TMEM lane quadrant = warp id % 4
     const float inv = S.scale;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const int acc = it & 1;
-      const uint32_t ph = (it >> 1) & 1;
+      const int acc = it & (kAcc - 1);
+      const uint32_t ph = (it / kAcc) & 1;
       const int64_t slot = tile * kM + q * 32 + lane;
       int cnt = 1;
       int64_t e = -1;
@@ -351,9 +370,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t bh = smem_u32(S.bh), bl = smem_u32(S.bl);
       int it = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int s = it & 1, acc = it & 1;
-        const uint32_t ph = (it >> 1) & 1;
-        mbar_wait(&S.tempty[acc], ph ^ 1);
+        const int s = it & 1, acc = it & (kAcc - 1);
+        const uint32_t ph = (it >> 1) & 1, pha = (it / kAcc) & 1;
+        mbar_wait(&S.tempty[acc], pha ^ 1);
         mbar_wait(&S.full[s], ph);
         tc_fence_after();
         const uint32_t d = tmem + uint32_t(acc * kN);

@@ -17,6 +17,7 @@
 // ahead of their use.  Out-of-image rows/columns contribute zero
 // (encoder.py:185-188).
 #include <algorithm>
+#include <cstdlib>
 
 #include "vkm_device.cuh"
 #include "vkm_kernels.cuh"
@@ -30,10 +31,10 @@ constexpr int kU = 4;   // rows / columns per unrolled step
 // idx = x*8 + ch within one plane row (W*8 float2); blockIdx.y = row segment,
 // blockIdx.z = plane.  DEMOD: the input is the x-pooled R of k_reduce_x and
 // each output is multiplied by conj(e^{i(xX/δx + yY/δy)}) (the pooled grid Q).
-template <bool DEMOD>
+// Raw y window (split path): idx = x*8 + ch within one plane row (W*8
+// float2, complex layout); blockIdx.y = row segment, blockIdx.z = plane.
 __global__ void __launch_bounds__(256) k_box_y(const float2* __restrict__ M, float2* __restrict__ R, int W, int H,
-                                               int dy, int RS, int64_t P, const float2* __restrict__ mx,
-                                               const float2* __restrict__ my, int D8) {
+                                               int dy, int RS, int64_t P) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= W * 8) return;
   const int y0 = blockIdx.y * RS, y1 = min(H, y0 + RS);
@@ -42,42 +43,86 @@ __global__ void __launch_bounds__(256) k_box_y(const float2* __restrict__ M, flo
   const int64_t rs = int64_t(W) * 8;   // row stride in float2
   const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
   const float2 zero = make_float2(0.f, 0.f);
-  const int c = int(blockIdx.z) * 8 + (idx & 7);
-  float2 fx = zero;
-  const float2* myc = my + c;
-  if (DEMOD) fx = __ldg(mx + int64_t(idx >> 3) * D8 + c);
   float2 acc = zero;
-  // warm-up: rows [y0-dy, y0+dy)
-  {
-    const int ya = max(0, y0 - dy), yb = min(H, y0 + dy);
-    int y = ya;
-    for (; y + kU <= yb; y += kU) {
-      float2 v[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) v[u] = ld_hint(Mp + int64_t(y + u) * rs, keep);
-#pragma unroll
-      for (int u = 0; u < kU; ++u) acc = cadd(acc, v[u]);
-    }
-    for (; y < yb; ++y) acc = cadd(acc, ld_hint(Mp + int64_t(y) * rs, keep));
-  }
+  for (int y = max(0, y0 - dy); y < min(H, y0 + dy); ++y) acc = cadd(acc, ld_nc_hint(Mp + int64_t(y) * rs, keep));
   for (int y = y0; y < y1; y += kU) {
-    float2 ld[kU], tr[kU], fm[kU];
+    float2 ld[kU], tr[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int yy = y + u;
-      ld[u] = (yy < y1 && yy + dy < H) ? ld_hint(Mp + int64_t(yy + dy) * rs, keep) : zero;
-      tr[u] = (yy < y1 && yy - dy >= 0) ? ld_hint(Mp + int64_t(yy - dy) * rs, drop) : zero;
-      if (DEMOD) fm[u] = (yy < y1) ? __ldg(myc + int64_t(yy) * D8) : zero;
+      ld[u] = (yy < y1 && yy + dy < H) ? ld_nc_hint(Mp + int64_t(yy + dy) * rs, keep) : zero;
+      tr[u] = (yy < y1 && yy - dy >= 0) ? ld_nc_hint(Mp + int64_t(yy - dy) * rs, drop) : zero;
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      if (y + u >= y1) break;
-      acc = cadd(acc, ld[u]);
-      if (DEMOD)
-        Rp[int64_t(y + u) * rs] = cmulc(acc, cmul(fx, fm[u]));   // · conj(e^{i(xX + yY)})
-      else
+      if (y + u < y1) {
+        acc = cadd(acc, ld[u]);
         Rp[int64_t(y + u) * rs] = acc;
-      acc = csub(acc, tr[u]);
+        acc = csub(acc, tr[u]);
+      }
+    }
+  }
+}
+
+// y window + demodulation on the packed-pair layout (fused path): idx =
+// x*4 + q, a thread owns channel pair q of one plane (16 B per pixel row):
+//   Q[y][x] = Σ_{|j|<=δy} R[y+j][x] · conj(e^{i(xX/δx + yY/δy)})
+// Complex arithmetic runs on f32x2 pairs (re c, re c+1), (im c, im c+1).
+__global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ Rin, float4* __restrict__ Q, int W,
+                                                     int H, int dy, int RS, int64_t P, const float4* __restrict__ mxp,
+                                                     const float4* __restrict__ myp, int D2) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= W * 4) return;
+  const int y0 = blockIdx.y * RS, y1 = min(H, y0 + RS);
+  const int pair = int(blockIdx.z) * 4 + (idx & 3);
+  const ulonglong2* Rp = reinterpret_cast<const ulonglong2*>(Rin) + int64_t(blockIdx.z) * P * 4 + idx;
+  ulonglong2* Qp = reinterpret_cast<ulonglong2*>(Q) + int64_t(blockIdx.z) * P * 4 + idx;
+  const int64_t rs = int64_t(W) * 4;   // row stride in 16-byte chunks
+  const float4 fx4 = __ldg(mxp + int64_t(idx >> 2) * D2 + pair);
+  const uint64_t fxr = f2pack(fx4.x, fx4.y), fxi = f2pack(fx4.z, fx4.w);
+  const float4* myc = myp + pair;
+  // lead rows stay in L2 (evict_last) until the trailing edge re-reads them
+  // 2δy+1 rows later (evict_first)
+  const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
+  auto ld = [&](const ulonglong2* p, uint64_t pol) {
+    ulonglong2 v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+        : "=l"(v.x), "=l"(v.y)
+        : "l"(p), "l"(pol));
+    return v;
+  };
+  uint64_t ar = 0, ai = 0;
+  for (int y = max(0, y0 - dy); y < min(H, y0 + dy); ++y) {
+    const ulonglong2 v = ld(Rp + int64_t(y) * rs, keep);
+    ar = fadd2(ar, v.x);
+    ai = fadd2(ai, v.y);
+  }
+  for (int y = y0; y < y1; y += kU) {
+    ulonglong2 lv[kU], tv[kU];
+    float4 fm[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int yy = y + u;
+      const bool ok = yy < y1;
+      lv[u] = (ok && yy + dy < H) ? ld(Rp + int64_t(yy + dy) * rs, keep) : make_ulonglong2(0ull, 0ull);
+      tv[u] = (ok && yy - dy >= 0) ? ld(Rp + int64_t(yy - dy) * rs, drop) : make_ulonglong2(0ull, 0ull);
+      fm[u] = ok ? __ldg(myc + int64_t(yy) * D2) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (y + u < y1) {
+        ar = fadd2(ar, lv[u].x);
+        ai = fadd2(ai, lv[u].y);
+        const uint64_t fyr = f2pack(fm[u].x, fm[u].y), fyi = f2pack(fm[u].z, fm[u].w);
+        // f = e^{i xX}·e^{i yY};  out = acc · conj(f)
+        const uint64_t fr = fsub2(fmul2(fxr, fyr), fmul2(fxi, fyi));
+        const uint64_t fi = ffma2(fxr, fyi, fmul2(fxi, fyr));
+        const uint64_t orr = ffma2(ar, fr, fmul2(ai, fi));
+        const uint64_t oi = fsub2(fmul2(ai, fr), fmul2(ar, fi));
+        Qp[int64_t(y + u) * rs] = make_ulonglong2(orr, oi);
+        ar = fsub2(ar, tv[u].x);
+        ai = fsub2(ai, tv[u].y);
+      }
     }
   }
 }
@@ -94,7 +139,8 @@ __global__ void __launch_bounds__(256) k_box_x(const float2* __restrict__ R, flo
   const int x0 = blockIdx.x * CS, x1 = min(W, x0 + CS);
   const int c = plane * 8 + ch;
   const float2* Rr = R + int64_t(plane) * P * 8 + int64_t(y) * W * 8 + ch;
-  float2* Qr = Q + int64_t(plane) * P * 8 + int64_t(y) * W * 8 + ch;
+  float2* Qr = Q + int64_t(plane) * P * 8 + int64_t(y) * W * 8 + (ch >> 1) * 2;   // + (ch & 1) floats below
+  Qr = reinterpret_cast<float2*>(reinterpret_cast<float*>(Qr) + (ch & 1));
   float2 dmy = __ldg(my + int64_t(y) * D8 + c);
   dmy.y = -dmy.y;
   const float2 zero = make_float2(0.f, 0.f);
@@ -113,19 +159,24 @@ __global__ void __launch_bounds__(256) k_box_x(const float2* __restrict__ R, flo
     for (int u = 0; u < kU; ++u) {
       if (x + u >= x1) break;
       acc = cadd(acc, ld[u]);
-      Qr[int64_t(x + u) * 8] = cmulc(cmul(acc, dmy), m[u]);   // · conj(e^{iyY}) · conj(e^{ixX})
+      const float2 o = cmulc(cmul(acc, dmy), m[u]);   // · conj(e^{iyY}) · conj(e^{ixX})
+      float* qo = reinterpret_cast<float*>(Qr + int64_t(x + u) * 8);   // packed pairs: re at +0, im at +2
+      qo[0] = o.x;
+      qo[2] = o.y;
       acc = csub(acc, tr[u]);
     }
   }
 }
 
 namespace {
-int pick_segments(int W, int H, int dy, int planes) {
-  // y-pass: segments bounded by an L2 budget for the live (2δy+1)-row windows
+// Row segments per column: enough threads for ~32 resident warps per SM, but
+// bounded so the live (2δy+1)-row windows of all segments stay in an L2 budget
+// (the trailing edge must hit L2) and the 2δy warm-up rows stay a minority.
+int pick_segments(int W, int H, int dy, int planes, int threads_per_row, int threads_per_sm) {
   const double band = double(2 * dy + 1) * W * 512.0;
-  const int s_max = std::max(1, int(64.0e6 / band));
-  const int64_t col_threads = int64_t(W) * 8 * planes;
-  int segs = int(std::max<int64_t>(1, (148 * 1024 + col_threads - 1) / col_threads));   // ~32 warps per SM
+  const int s_max = std::max(1, std::min(int(64.0e6 / band), H / std::max(1, 3 * dy)));
+  const int64_t col_threads = int64_t(threads_per_row) * planes;
+  const int segs = int(std::max<int64_t>(1, (int64_t(148) * threads_per_sm + col_threads - 1) / col_threads));
   return std::max(1, std::min(segs, s_max));
 }
 }  // namespace
@@ -134,10 +185,10 @@ void launch_pool_split(const DevTables& tb, int W, int H, int D8, int dx, int dy
                        float2* Qout, cudaStream_t s) {
   const int planes = D8 / 8;
   const int64_t P = int64_t(W) * H;
-  const int segs = pick_segments(W, H, dy, planes);
+  const int segs = pick_segments(W, H, dy, planes, W * 8, 1024);
   const int RS = (H + segs - 1) / segs;
   dim3 gy((W * 8 + 255) / 256, (H + RS - 1) / RS, planes);
-  k_box_y<false><<<gy, 256, 0, s>>>(M, R, W, H, dy, RS, P, nullptr, nullptr, D8);
+  k_box_y<<<gy, 256, 0, s>>>(M, R, W, H, dy, RS, P);
   // x-pass: column segments of CS outputs (2δx halo re-reads are L1/L2 hits)
   const int CS = std::max(128, 8 * dx);   // halo re-reads 2δx/CS
   dim3 gx((W + CS - 1) / CS, (H * 8 + 255) / 256, planes);
@@ -148,10 +199,15 @@ void launch_pool_y_demod(const DevTables& tb, int W, int H, int D8, int dy, cons
                          cudaStream_t s) {
   const int planes = D8 / 8;
   const int64_t P = int64_t(W) * H;
-  const int segs = pick_segments(W, H, dy, planes);
+  static const int env_segs = [] {
+    const char* e = std::getenv("VKM_YSEGS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int segs = env_segs > 0 ? env_segs : pick_segments(W, H, dy, planes, W * 4, 512);
   const int RS = (H + segs - 1) / segs;
-  dim3 gy((W * 8 + 255) / 256, (H + RS - 1) / RS, planes);
-  k_box_y<true><<<gy, 256, 0, s>>>(R, Q, W, H, dy, RS, P, tb.mx, tb.my, D8);
+  dim3 gy((W * 4 + 255) / 256, (H + RS - 1) / RS, planes);
+  k_box_y_demod<<<gy, 256, 0, s>>>(reinterpret_cast<const float4*>(R), reinterpret_cast<float4*>(Q), W, H, dy, RS, P,
+                                   tb.mxp, tb.myp, D8 / 2);
 }
 
 }  // namespace vkm

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(256) k_reduce_small(const int* __restrict__ st
 // reduceat order, encoder.py:262-267), modulates by e^{i x X/δx}, and keeps a
 // sliding window sum over the last 2δx+1 pixels (a per-lane ring in shared
 // memory).  The window centred on x-δx is complete after pixel x, so it is
-// multiplied by e^{i y Y/δy} and written:
+// multiplied by e^{i y Y/δy} and written (packed-pair layout, see k_pool.cu):
 //   R[y][x] = e^{i y Y/δy} · Σ_{|i|<=δx} G[y][x+i] e^{i (x+i) X/δx}
 // The raw grid never reaches HBM; the y pass (k_box_y<true>) finishes the
 // window and demodulates.  Halo pixels (δx each side) are recomputed by the
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
                                                             const uint64_t* __restrict__ val_s,
                                                             const float* __restrict__ tf,
                                                             const float4* __restrict__ mxp,
-                                                            const float2* __restrict__ my, int W, int H, int dx,
+                                                            const float4* __restrict__ myp, int W, int H, int dx,
                                                             int S, int nseg, int64_t P, float2* __restrict__ R) {
   extern __shared__ __align__(16) uint8_t rx_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
   int* const ends = reinterpret_cast<int*>(rx_smem + size_t(kRxWarps) * RL * 512) + wib * kRxEnds;
   const uint64_t T01 = f2pack(__ldg(tf + 2 * lane), __ldg(tf + 2 * lane + 1));
   const float4* mxl = mxp + lane;                   // mxl[x * 32]: (cos c0, cos c1, sin c0, sin c1) of x X/δx
-  const float4* my4 = reinterpret_cast<const float4*>(my) + lane;
+  const float4* myl = myp + lane;                   // (cos c0, cos c1, sin c0, sin c1) of y Y/δy
   float4* const R4 = reinterpret_cast<float4*>(R) + ((int64_t(lane >> 2) * P) << 2) + (lane & 3);
   const int64_t items = int64_t(H) * nseg;
   const int64_t nwarps = int64_t(gridDim.x) * kRxWarps;
@@ -213,8 +213,8 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
     }
     for (int k = 0; k < RL; ++k) ring0[k * 32] = make_ulonglong2(0ull, 0ull);
     __syncwarp();
-    const float4 fy4 = __ldg(my4 + int64_t(y) * 32);
-    const uint64_t fyr = f2pack(fy4.x, fy4.z), fyi = f2pack(fy4.y, fy4.w);
+    const float4 fy4 = __ldg(myl + int64_t(y) * 32);
+    const uint64_t fyr = f2pack(fy4.x, fy4.y), fyi = f2pack(fy4.z, fy4.w);
     float4* out = R4 + ((int64_t(y) * W + x0) << 2);
     auto ld_a = [&](int jj) { return jj < jend ? slot_arg(__ldg(val_s + jj)) : 0.f; };
     int jb = jfirst;
@@ -237,10 +237,7 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
       if (k >= 2 * dx) {
         const uint64_t orr = fsub2(fmul2(ar, fyr), fmul2(ai, fyi));
         const uint64_t oi = ffma2(ar, fyi, fmul2(ai, fyr));
-        float r0, r1, i0, i1;
-        f2unpack(orr, r0, r1);
-        f2unpack(oi, i0, i1);
-        *out = make_float4(r0, i0, r1, i1);
+        *reinterpret_cast<ulonglong2*>(out) = make_ulonglong2(orr, oi);   // packed-pair layout
         out += 4;
       }
       ar = fsub2(ar, old.x);
@@ -381,7 +378,7 @@ void launch_reduce_x(const DevTables& tb, int W, int H, int dx, const SortBufs& 
   const int nseg = (W + S - 1) / S;
   const int64_t items = int64_t(H) * nseg;
   const int blocks = int(std::min<int64_t>((items + kRxWarps - 1) / kRxWarps, res_warps / kRxWarps));
-  k_reduce_x<<<blocks, kRxWarps * 32, smem, s>>>(sb.start, sb.val_s, tb.tf, tb.mxp, tb.my, W, H, dx, S, nseg, P, R);
+  k_reduce_x<<<blocks, kRxWarps * 32, smem, s>>>(sb.start, sb.val_s, tb.tf, tb.mxp, tb.myp, W, H, dx, S, nseg, P, R);
 }
 
 }  // namespace vkm

@@ -66,6 +66,7 @@ struct vkm_handle {
   float2* my = nullptr;
   float2* mx = nullptr;
   float4* mxp = nullptr;
+  float4* myp = nullptr;
   float* w1p = nullptr;  // [hidden][2*D8] padded
   float* b1 = nullptr;
   float* w2 = nullptr;
@@ -114,7 +115,7 @@ int grow(T** ptr, size_t* cap, size_t need) {
   return VKM_OK;
 }
 
-vkm::DevTables tables(const vkm_handle* h) { return vkm::DevTables{h->tf, h->my, h->mx, h->mxp}; }
+vkm::DevTables tables(const vkm_handle* h) { return vkm::DevTables{h->tf, h->my, h->mx, h->mxp, h->myp}; }
 vkm::GridBufs bufs(const vkm_handle* h) { return vkm::GridBufs{h->G, h->C, h->Q, h->NQ}; }
 
 void rec(vkm_handle* h, int i, cudaStream_t s) {
@@ -328,15 +329,22 @@ int vkm_create(vkm_handle** out, const vkm_params* params, const double* T, cons
   VKM_CKH(cudaMemcpy(h->tf, tf.data(), sizeof(float) * D8, cudaMemcpyHostToDevice));
   VKM_CKH(cudaMemcpy(h->my, my.data(), sizeof(float2) * my.size(), cudaMemcpyHostToDevice));
   VKM_CKH(cudaMemcpy(h->mx, mx.data(), sizeof(float2) * mx.size(), cudaMemcpyHostToDevice));
-  if (D8 == 64) {   // lane-packed copy of the x table for k_reduce_x
-    std::vector<float4> mxp(size_t(W) * 32);
-    for (int x = 0; x < W; ++x)
-      for (int l = 0; l < 32; ++l) {
-        const float2 a = mx[size_t(x) * 64 + 2 * l], b = mx[size_t(x) * 64 + 2 * l + 1];
-        mxp[size_t(x) * 32 + l] = make_float4(a.x, b.x, a.y, b.y);
-      }
+  {   // packed-pair copies (cos c, cos c+1, sin c, sin c+1) of both tables
+    auto pack = [&](const std::vector<float2>& t, int rows, std::vector<float4>& out) {
+      out.resize(size_t(rows) * (D8 / 2));
+      for (int r = 0; r < rows; ++r)
+        for (int q = 0; q < D8 / 2; ++q) {
+          const float2 a = t[size_t(r) * D8 + 2 * q], b = t[size_t(r) * D8 + 2 * q + 1];
+          out[size_t(r) * (D8 / 2) + q] = make_float4(a.x, b.x, a.y, b.y);
+        }
+    };
+    std::vector<float4> mxp, myp;
+    pack(mx, W, mxp);
+    pack(my, H, myp);
     VKM_CKH(cudaMalloc(&h->mxp, sizeof(float4) * mxp.size()));
+    VKM_CKH(cudaMalloc(&h->myp, sizeof(float4) * myp.size()));
     VKM_CKH(cudaMemcpy(h->mxp, mxp.data(), sizeof(float4) * mxp.size(), cudaMemcpyHostToDevice));
+    VKM_CKH(cudaMemcpy(h->myp, myp.data(), sizeof(float4) * myp.size(), cudaMemcpyHostToDevice));
   }
 
   // Grid scratch: two planes-sets of 64 B/pixel plus int32 counts (516 B/pixel at D=64).
@@ -403,7 +411,7 @@ void vkm_destroy(vkm_handle* h) {
   if (!h) return;
   DeviceGuard dg(h->p.device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
+  void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->myp, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
                   h->G, h->C, h->Q, h->NQ, h->feats, h->cnt_scratch, h->ev_stage, h->out_stage, h->cnt_stage,
                   h->sb.pix, h->sb.val, h->sb.start, h->sb.val_s, h->sb.pix_s, h->sb.temp, h->sb.sort_temp};
   for (void* p : ptrs)
@@ -548,7 +556,7 @@ int vkm_grid(vkm_handle* h, const double* ev, int64_t n, double t_start, int32_t
   int rc = encode_core(h, ev, n, t_start, pooled, s, &launches);
   if (rc) return rc;
   vkm::launch_grid_to_ref(pooled ? h->Q : h->G, pooled ? h->NQ : h->C, h->p.width, h->p.height, h->D, h->D8,
-                          pooled ? nullptr : h->mx, pooled ? nullptr : h->my, grid, counts, s);
+                          pooled ? nullptr : h->mx, pooled ? nullptr : h->my, pooled != 0, grid, counts, s);
   VKM_CK(cudaGetLastError());
   return VKM_OK;
 }

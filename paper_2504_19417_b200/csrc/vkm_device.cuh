@@ -176,6 +176,15 @@ __device__ __forceinline__ float2 ld_hint(const float2* ptr, uint64_t pol) {
                : "l"(ptr), "l"(pol));
   return v;
 }
+// Same load without `volatile`: the compiler may batch and reorder it (the data
+// is read-only for the kernel's lifetime).
+__device__ __forceinline__ float2 ld_nc_hint(const float2* ptr, uint64_t pol) {
+  float2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+      : "=f"(v.x), "=f"(v.y)
+      : "l"(ptr), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ void st_hint(float2* ptr, float2 v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(ptr), "f"(v.x), "f"(v.y),
                "l"(pol)

@@ -10,13 +10,18 @@ struct DevTables {
   const float* tf;     // f32(T_c), [D8]                       (encoder.py:223-224)
   const float2* my;    // e^{i y Y_c / dy}, [H][D8] complex64   (modulation, y axis)
   const float2* mx;    // e^{i x X_c / dx}, [W][D8] complex64   (modulation, x axis)
-  const float4* mxp;   // D8 == 64: [W][32] (cos c0, cos c1, sin c0, sin c1) of x X_c/dx, c0 = 2·lane
+  const float4* mxp;   // [W][D8/2] (cos c0, cos c1, sin c0, sin c1) of x X_c/dx, c0 = 2·pair (packed pairs)
+  const float4* myp;   // [H][D8/2] same for y Y_c/dy
 };
 
+// Grid layouts, [plane = channel/8][pixel][64 B]:
+//   complex layout  8 × (re, im) complex64          (raw grid G of k_reduce)
+//   packed pairs    4 × (re c, re c+1, im c, im c+1) (x-pooled R, pooled Q):
+//                   one 16-byte chunk is a channel pair in f32x2-ready form
 struct GridBufs {
-  float2* G;   // [planes][P][8]  pre-modulated grid M = G·e^{i(xX/δx + yY/δy)}
+  float2* G;   // [planes][P][8]  pre-modulated grid M = G·e^{i(xX/δx + yY/δy)} (complex layout)
   int* C;      // [P]
-  float2* Q;   // [planes][P][8]
+  float2* Q;   // [planes][P][8]  pooled grid (packed pairs)
   int* NQ;     // [P]
 };
 
@@ -91,8 +96,9 @@ void launch_mlp_ffma(const float* feats, const int32_t* counts, int64_t n, int D
                      float* flows, cudaStream_t s);
 // Layout conversion for the parity hook: planes -> reference [x][y][D] complex64.
 // mx/my non-null: G holds the pre-modulated grid M and is demodulated on the way out.
+// packed: G uses the packed-pair layout (the pooled grid Q).
 void launch_grid_to_ref(const float2* G, const int* C, int W, int H, int D, int D8, const float2* mx,
-                        const float2* my, float* out_grid, int32_t* out_counts, cudaStream_t s);
+                        const float2* my, bool packed, float* out_grid, int32_t* out_counts, cudaStream_t s);
 
 // tcgen05 fused gather + de-phase + MLP (D = 64, hidden = 128).
 struct TcWeights {
