@@ -20,6 +20,9 @@
  *                     196-208); pooled=1 adds the window sums of _pool_batch
  *                     (encoder.py:331-336) evaluated at every pixel
  *   vkm_predict_batch the CLI's per-slice loop (cli.py:267-280) fused into one call
+ *   vkm_predict_batch_host  the same loop over host buffers, with the H2D of
+ *                     slice s+1 and the D2H of slice s-1 overlapping the kernels of
+ *                     slice s (NormalFlowRegressor.predict_slices)
  *   vkm_last_error    exception text of the reference's error hierarchy (errors.py:4-29)
  *
  * Event layout: the reference's (n, 3) float64 array [t, x, y], row-major,
@@ -123,6 +126,15 @@ int vkm_encode_host(vkm_handle* h, const double* events_host, int64_t n, double 
 int vkm_predict_batch(vkm_handle* h, const double* events_dev, const int64_t* offsets_host,
                       int32_t n_slices, const double* t_starts_host,
                       float* flows_dev, int32_t* counts_dev, void* stream);
+
+/* Host-buffer batch: like vkm_predict_batch, but events_host / flows_host /
+ * counts_host (may be NULL) are host memory.  Slices are pipelined over three
+ * streams (copy-in, kernels, copy-out) with two device staging buffers, so
+ * transfers overlap compute; pass page-locked buffers for the copies to be
+ * asynchronous.  Returns after the last result has landed in host memory. */
+int vkm_predict_batch_host(vkm_handle* h, const double* events_host, const int64_t* offsets_host,
+                           int32_t n_slices, const double* t_starts_host, float* flows_host,
+                           int32_t* counts_host);
 
 /* Parity hook: the per-pixel grid in the reference's PixelGrid layout.
  * grid_dev: (width, height, D) complex64 as interleaved f32 pairs, [x][y][d];

@@ -94,6 +94,15 @@ struct vkm_handle {
   size_t out_cap = 0;
   int32_t* cnt_stage = nullptr;
   size_t cnt_stage_cap = 0;
+  // pipelined host batches: copy-in / copy-out streams, two staging slots
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t in_ready[2] = {nullptr, nullptr}, computed[2] = {nullptr, nullptr}, out_done[2] = {nullptr, nullptr};
+  double* pev[2] = {nullptr, nullptr};
+  size_t pev_cap[2] = {0, 0};
+  float* pout[2] = {nullptr, nullptr};
+  size_t pout_cap[2] = {0, 0};
+  int32_t* pcnt[2] = {nullptr, nullptr};
+  size_t pcnt_cap[2] = {0, 0};
   // timing
   bool profiling = false;
   cudaEvent_t evt[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -418,6 +427,14 @@ void vkm_destroy(vkm_handle* h) {
     if (p) cudaFree(p);
   for (auto& e : h->evt)
     if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    for (void* p : {static_cast<void*>(h->pev[i]), static_cast<void*>(h->pout[i]), static_cast<void*>(h->pcnt[i])})
+      if (p) cudaFree(p);
+    for (cudaEvent_t e : {h->in_ready[i], h->computed[i], h->out_done[i]})
+      if (e) cudaEventDestroy(e);
+  }
+  if (h->s_in) cudaStreamSynchronize(h->s_in), cudaStreamDestroy(h->s_in);
+  if (h->s_out) cudaStreamSynchronize(h->s_out), cudaStreamDestroy(h->s_out);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -542,6 +559,65 @@ int vkm_predict_batch(vkm_handle* h, const double* ev, const int64_t* offsets, i
   }
   rec(h, 3, st);
   h->have_timing = false;  // per-slice events are overwritten; only the total is meaningful
+  h->last_launches = launches;
+  return VKM_OK;
+}
+
+int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* offsets, int32_t n_slices,
+                           const double* t_starts, float* flows_host, int32_t* counts_host) {
+  if (int rc = check_handle(h)) return rc;
+  if (h->hidden <= 0) return fail(VKM_EINVAL, "handle has no flow head (hidden == 0)");
+  if (n_slices < 0 || (n_slices > 0 && !offsets)) return fail(VKM_EINVAL, "bad slice offsets");
+  int64_t nmax = 0;
+  for (int s = 0; s < n_slices; ++s) {
+    if (offsets[s + 1] < offsets[s] || offsets[s] < 0) return fail(VKM_EINVAL, "slice offsets must be non-decreasing");
+    nmax = std::max(nmax, offsets[s + 1] - offsets[s]);
+  }
+  if (n_slices == 0 || offsets[n_slices] == offsets[0]) return VKM_OK;
+  if (!ev_host || !flows_host) return fail(VKM_EINVAL, "null host buffer");
+  DeviceGuard dg(h->p.device);
+  if (!h->s_in) {
+    VKM_CK(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+    VKM_CK(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      VKM_CK(cudaEventCreateWithFlags(&h->in_ready[i], cudaEventDisableTiming));
+      VKM_CK(cudaEventCreateWithFlags(&h->computed[i], cudaEventDisableTiming));
+      VKM_CK(cudaEventCreateWithFlags(&h->out_done[i], cudaEventDisableTiming));
+    }
+  }
+  for (int i = 0; i < 2; ++i) {
+    int rc = grow(&h->pev[i], &h->pev_cap[i], size_t(nmax) * 3);
+    if (!rc) rc = grow(&h->pout[i], &h->pout_cap[i], size_t(nmax) * 2);
+    if (!rc && counts_host) rc = grow(&h->pcnt[i], &h->pcnt_cap[i], size_t(nmax));
+    if (rc) return rc;
+  }
+  cudaStream_t sc = h->stream;
+  // slot k = s % 2.  copy-in(s) waits until compute(s-2) stopped reading the slot;
+  // compute(s) waits for copy-in(s) and for copy-out(s-2) to drain the output slot.
+  int launches = 0, used = 0;
+  for (int s = 0; s < n_slices; ++s) {
+    const int64_t lo = offsets[s], n = offsets[s + 1] - lo;
+    if (n == 0) continue;
+    const int k = used & 1;
+    if (used >= 2) VKM_CK(cudaStreamWaitEvent(h->s_in, h->computed[k], 0));
+    VKM_CK(cudaMemcpyAsync(h->pev[k], ev_host + 3 * lo, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, h->s_in));
+    VKM_CK(cudaEventRecord(h->in_ready[k], h->s_in));
+    VKM_CK(cudaStreamWaitEvent(sc, h->in_ready[k], 0));
+    if (used >= 2) VKM_CK(cudaStreamWaitEvent(sc, h->out_done[k], 0));
+    const double t0 = t_starts ? t_starts[s] : NAN;
+    int rc = predict_one(h, h->pev[k], n, t0, h->pout[k], counts_host ? h->pcnt[k] : nullptr, sc, &launches);
+    if (rc) return rc;
+    VKM_CK(cudaEventRecord(h->computed[k], sc));
+    VKM_CK(cudaStreamWaitEvent(h->s_out, h->computed[k], 0));
+    VKM_CK(cudaMemcpyAsync(flows_host + 2 * lo, h->pout[k], sizeof(float) * 2 * n, cudaMemcpyDeviceToHost, h->s_out));
+    if (counts_host)
+      VKM_CK(cudaMemcpyAsync(counts_host + lo, h->pcnt[k], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, h->s_out));
+    VKM_CK(cudaEventRecord(h->out_done[k], h->s_out));
+    ++used;
+  }
+  VKM_CK(cudaStreamSynchronize(h->s_out));
+  VKM_CK(cudaStreamSynchronize(sc));
+  h->have_timing = false;
   h->last_launches = launches;
   return VKM_OK;
 }

@@ -98,6 +98,27 @@ class FlowEngine:
                                                   counts.ctypes.data if counts is not None else None))
         return (flows, counts) if return_counts else flows
 
+    def predict_batch_host(self, events: np.ndarray, offsets: Sequence[int], t_starts=None,
+                           flows: Optional[np.ndarray] = None, return_counts: bool = False):
+        """Many slices from host memory in one pipelined call (copy-in of slice
+        s+1 and copy-out of slice s-1 overlap the kernels of slice s).  Pass
+        page-locked `events` / `flows` (e.g. torch pin_memory().numpy()) for
+        the copies to run asynchronously."""
+        ev = np.ascontiguousarray(events, dtype=np.float64)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        ns = len(off) - 1
+        if flows is None:
+            flows = np.empty((len(ev), 2), dtype=np.float32)
+        counts = np.empty(len(ev), dtype=np.int32) if return_counts else None
+        ts = None
+        if t_starts is not None:
+            ts_arr = np.ascontiguousarray(t_starts, dtype=np.float64)
+            ts = _dptr(ts_arr)
+        _lib.check(self._lib.vkm_predict_batch_host(
+            self._h, ev.ctypes.data, off.ctypes.data_as(C.POINTER(C.c_int64)), ns, ts, flows.ctypes.data,
+            counts.ctypes.data if counts is not None else None))
+        return (flows, counts) if return_counts else flows
+
     def encode_host(self, events: np.ndarray, t_start: float = math.nan, return_counts: bool = False):
         ev = np.ascontiguousarray(events, dtype=np.float64)
         n = len(ev)

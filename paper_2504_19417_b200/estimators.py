@@ -177,5 +177,35 @@ class NormalFlowRegressor(BaseEstimator):
         return flows.astype(np.float64)
 
     def predict_slices(self, slices: Sequence) -> List[np.ndarray]:
-        """Additive API: many independent slices, one result per slice."""
-        return [self.predict(X) for X in slices]
+        """Additive API: many independent slices, one result
+        per slice, each with `predict`'s semantics.  The slices are validated
+        on the host, packed into one page-locked buffer and streamed through
+        vkm_predict_batch_host, which overlaps the copies of neighbouring
+        slices with the kernels."""
+        eng = self.engine()
+        blocks = [slice_from_array(X, self.width, self.height, 2.0 * self.delta_t) for X in slices]
+        sizes = [len(b) for b in blocks]
+        total = int(sum(sizes))
+        if total == 0:
+            return [np.full((0, 2), np.nan) for _ in blocks]
+        ev, out = _pinned_pair(total)
+        offsets = np.zeros(len(blocks) + 1, dtype=np.int64)
+        np.cumsum(sizes, out=offsets[1:])
+        for b, lo in zip(blocks, offsets[:-1]):
+            if len(b):
+                ev[lo:lo + len(b)] = b.events
+        t_starts = np.array([b.t_start if len(b) else 0.0 for b in blocks], dtype=np.float64)
+        eng.predict_batch_host(ev, offsets, t_starts, flows=out)
+        return [out[lo:hi].astype(np.float64) for lo, hi in zip(offsets[:-1], offsets[1:])]
+
+
+def _pinned_pair(n: int):
+    """Page-locked (n, 3) f64 event and (n, 2) f32 flow buffers (torch's host
+    allocator; plain numpy memory when torch is unavailable)."""
+    try:
+        import torch
+        ev = torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy()
+        out = torch.empty((n, 2), dtype=torch.float32).pin_memory().numpy()
+        return ev, out
+    except Exception:
+        return np.empty((n, 3), dtype=np.float64), np.empty((n, 2), dtype=np.float32)

@@ -269,3 +269,50 @@ def test_bench_multirank_shared_gpu(tmp_path):
         rec = json.loads(lines[0])
         assert rec["n_gpus"] == 2 and rec["value"] > 0
         assert rec["scaling"] == ("strong" if split == "spatial" else "weak")
+
+
+def test_predict_slices_pipelined_host_batch():
+    """predict_slices (vkm_predict_batch_host: copy-in / kernels / copy-out on
+    three streams) returns, per slice, exactly what predict returns; empty
+    slices in the middle and slices of very different sizes included."""
+    pkg = _pkg()
+    g = load_golden("cfg1_20k")
+    reg = regressor(g)
+    sizes = [4000, 0, 25000, 1, 9000, 0, 17000]
+    slices = [vo.synth_uniform_noise(n, 346, 260, seed=40 + i) if n else np.zeros((0, 3)) for i, n in
+              enumerate(sizes)]
+    got = reg.predict_slices(slices)
+    assert len(got) == len(slices)
+    for X, f in zip(slices, got):
+        assert f.shape == (len(X), 2) and f.dtype == np.float64
+        if len(X):
+            np.testing.assert_array_equal(f, reg.predict(X))
+    # counts through the engine call
+    eng = reg.engine()
+    ev = np.concatenate([s for s in slices if len(s)])
+    off = np.cumsum([0] + [len(s) for s in slices if len(s)])
+    flows, counts = eng.predict_batch_host(ev, off, [float(s[0, 0]) for s in slices if len(s)], return_counts=True)
+    for i, s in enumerate([s for s in slices if len(s)]):
+        f1, c1 = eng.predict_host(s, float(s[0, 0]), return_counts=True)
+        np.testing.assert_array_equal(flows[off[i]:off[i + 1]], f1)
+        np.testing.assert_array_equal(counts[off[i]:off[i + 1]], c1)
+
+
+@pytest.mark.parametrize("d", [1, 10, 24, 25])
+def test_fused_x_window_matches_split_pooling(d, monkeypatch):
+    """k_reduce_x (x window fused into the per-pixel reduction) against the
+    raw-grid + two-pass pooling path (VKM_POOL=split) on the same slice:
+    counts bit-exact, flows within f32 summation-order noise.  d = 25 is past
+    the fused kernel's radius limit, so both handles run the split path."""
+    pkg = _pkg()
+    W, H, n = 200, 150, 60000
+    X = vo.synth_uniform_noise(n, W, H, seed=d)
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    fused = pkg.FlowEngine(W, H, d, d, 0.016, b, w)
+    monkeypatch.setenv("VKM_POOL", "split")
+    split = pkg.FlowEngine(W, H, d, d, 0.016, b, w)
+    f1, c1 = fused.predict_host(X, float(X[0, 0]), return_counts=True)
+    f2, c2 = split.predict_host(X, float(X[0, 0]), return_counts=True)
+    np.testing.assert_array_equal(c1, c2)
+    np.testing.assert_allclose(f1, f2, rtol=0, atol=1e-5)
