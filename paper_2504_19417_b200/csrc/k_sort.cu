@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
 #pragma unroll
       for (int u = 0; u < kRxGroup; ++u) {
         const float au = __shfl_sync(kFullMask, av0, i0 + u);
-        sincos2p_f32(fmul2(f2pack(au, au), T01), sn[u], cs[u]);
+        VKM_SINCOS_HOT(fmul2(f2pack(au, au), T01), sn[u], cs[u]);
       }
 #pragma unroll
       for (int u = 0; u < kRxGroup; ++u) {

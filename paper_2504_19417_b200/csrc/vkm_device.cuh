@@ -118,6 +118,38 @@ __device__ __forceinline__ void sincos2_f32(float x0, float x1, float& s0, float
   c1 = __int_as_float(__float_as_int(cc) ^ (((k1 + 1) & 2) << 30));
 }
 
+// Two sin/cos pairs with the reduction by pi (r in [-pi/2, pi/2]): the only
+// quadrant fix-up is a common sign (-1)^k, applied with one shift and one
+// LOP3 per value, so the whole evaluation is 17 packed FMA-pipe instructions
+// plus 6 integer ones (31 for sincos2p_f32).  Degree-11 sin / degree-12 cos
+// minimax polynomials (tools/fit_sincos.py); max abs error 1.5e-7 over
+// |x| < 60 (sincos2p_f32: 7.3e-8), i.e. ~2.5 ulp of 1.0.
+__device__ __forceinline__ void sincos2p_pi(uint64_t x, uint64_t& s01, uint64_t& c01) {
+  const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
+  const uint64_t qb = ffma2(x, f2pack(0.318309886f, 0.318309886f), magic);
+  const uint64_t q = fsub2(qb, magic);
+  uint64_t r = ffma2(q, f2pack(-3.14159203e+00f, -3.14159203e+00f), x);
+  r = ffma2(q, f2pack(-6.27832946e-07f, -6.27832946e-07f), r);
+  r = ffma2(q, f2pack(-1.07806051e-14f, -1.07806051e-14f), r);
+  const uint64_t u = fmul2(r, r);
+  uint64_t ps = ffma2(f2pack(-2.384669173e-08f, -2.384669173e-08f), u, f2pack(2.752261935e-06f, 2.752261935e-06f));
+  ps = ffma2(ps, u, f2pack(-1.984080445e-04f, -1.984080445e-04f));
+  ps = ffma2(ps, u, f2pack(8.333330043e-03f, 8.333330043e-03f));
+  ps = ffma2(ps, u, f2pack(-1.666666716e-01f, -1.666666716e-01f));
+  ps = fmul2(ps, u);
+  const uint64_t sr = ffma2(ps, r, r);
+  uint64_t pc = ffma2(f2pack(1.991995235e-09f, 1.991995235e-09f), u, f2pack(-2.752566104e-07f, -2.752566104e-07f));
+  pc = ffma2(pc, u, f2pack(2.480107105e-05f, 2.480107105e-05f));
+  pc = ffma2(pc, u, f2pack(-1.388888457e-03f, -1.388888457e-03f));
+  pc = ffma2(pc, u, f2pack(4.166666791e-02f, 4.166666791e-02f));
+  pc = ffma2(pc, u, f2pack(-5.000000000e-01f, -5.000000000e-01f));
+  const uint64_t cr = ffma2(pc, u, f2pack(1.0f, 1.0f));
+  // (-1)^k: the parity of k sits in bit 0 of each f32 lane of qb
+  const uint64_t sgn = (qb << 31) & 0x8000000080000000ull;
+  s01 = sr ^ sgn;
+  c01 = cr ^ sgn;
+}
+
 // Packed-in/packed-out variant: theta = (x0, x1), returns (s0, s1), (c0, c1).
 __device__ __forceinline__ void sincos2p_f32(uint64_t theta, uint64_t& s01, uint64_t& c01) {
   float x0, x1, s0, c0, s1, c1;
@@ -126,6 +158,17 @@ __device__ __forceinline__ void sincos2p_f32(uint64_t theta, uint64_t& s01, uint
   s01 = f2pack(s0, s1);
   c01 = f2pack(c0, c1);
 }
+
+// sin/cos used by the two hot kernels (k_reduce_x, k_gather_mlp_tc).  The
+// pi-reduced variant issues 23 instead of 31 instructions per pair but
+// measured no faster on B200 (both kernels are dependency-latency bound:
+// k_reduce_x 128 -> 132 us, K3 ~equal, ncu cfg2) and is 2x less accurate, so
+// the pi/2-reduced version is the default; -DVKM_SINCOS_PI selects the other.
+#ifdef VKM_SINCOS_PI
+#define VKM_SINCOS_HOT sincos2p_pi
+#else
+#define VKM_SINCOS_HOT sincos2p_f32
+#endif
 
 // a = f32((t - t0) / delta_t): f64 rebase and divide, then one rounding to f32,
 // exactly as rebase_slice (events.py:390-407) + _temporal_phases
