@@ -232,7 +232,17 @@ def run_b200(args):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    if slices > 1:
+        # independent slices of one rank: one device buffer, batched launch
+        # sequences (vkm_predict_batch: up to 64 slices share each kernel)
+        ev_all = torch.cat(evs)
+        fl_all = torch.empty((ev_all.shape[0], 2), dtype=torch.float32, device=dev)
+        offs_all = np.cumsum([0] + [len(X) for X in host])
+
     def step():
+        if slices > 1:
+            eng.predict_batch_device(ev_all, offs_all, t0s, flows=fl_all, stream=stream)
+            return
         for s in range(slices):
             eng.predict_device(evs[s], t0s[s], flows=flows[s], stream=stream)
 
@@ -258,7 +268,7 @@ def run_b200(args):
             ends[i].record(stream)
             if slices == 1:
                 kern.append(eng.last_timings()[0])
-            launches += launches_per_call * slices
+            launches += launches_per_call if slices > 1 else launches_per_call * slices
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

@@ -23,8 +23,11 @@ constexpr int kRB = 8;   // rows per batch of the count pooling kernel
 // Exact int32 box sum of the per-pixel counts (bit-exact neighbourhood sizes,
 // the cnt of encoder.py:336).  Same strip/segment tiling, one channel.
 constexpr int kCountSW = 256;
-__global__ void __launch_bounds__(256) k_pool_count(const int* __restrict__ C, int* __restrict__ NQ, int W, int H,
-                                                    int dx, int dy, int RS) {
+__global__ void __launch_bounds__(256) k_pool_count(const int* __restrict__ Cin, int* __restrict__ NQout, int W,
+                                                    int H, int dx, int dy, int RS) {
+  // blockIdx.z = slice of a batch (its own W x H pixel block)
+  const int* __restrict__ C = Cin + int64_t(blockIdx.z) * W * H;
+  int* __restrict__ NQ = NQout + int64_t(blockIdx.z) * W * H;
   constexpr int SW = kCountSW;
   constexpr int ROW = SW + SW / 8;
   __shared__ int buf[kRB * ROW];
@@ -90,11 +93,11 @@ static int pick_rs(int H, int strips, int planes) {
   return rs;
 }
 
-void launch_pool_count(int W, int H, int dx, int dy, const GridBufs& g, cudaStream_t s) {
+void launch_pool_count(int W, int H, int nb, int dx, int dy, const GridBufs& g, cudaStream_t s) {
   const int TXc = kCountSW - 2 * dx;
   const int strips = (W + TXc - 1) / TXc;
   const int RS = pick_rs(H, strips, 1);
-  dim3 grid(strips, (H + RS - 1) / RS);
+  dim3 grid(strips, (H + RS - 1) / RS, nb);
   k_pool_count<<<grid, kCountSW, 0, s>>>(g.C, g.NQ, W, H, dx, dy, RS);
 }
 

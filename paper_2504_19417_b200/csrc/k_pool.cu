@@ -68,15 +68,20 @@ __global__ void __launch_bounds__(256) k_box_y(const float2* __restrict__ M, flo
 // x*4 + q, a thread owns channel pair q of one plane (16 B per pixel row):
 //   Q[y][x] = Σ_{|j|<=δy} R[y+j][x] · conj(e^{i(xX/δx + yY/δy)})
 // Complex arithmetic runs on f32x2 pairs (re c, re c+1), (im c, im c+1).
+// blockIdx.y = slice * segs + segment (batched slices stack vertically, rows
+// never mix across slices); P is the plane stride (nb·W·H).
 __global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ Rin, float4* __restrict__ Q, int W,
-                                                     int H, int dy, int RS, int64_t P, const float4* __restrict__ mxp,
+                                                     int H, int segs, int dy, int RS, int64_t P,
+                                                     const float4* __restrict__ mxp,
                                                      const float4* __restrict__ myp, int D2) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= W * 4) return;
-  const int y0 = blockIdx.y * RS, y1 = min(H, y0 + RS);
+  const int slice = blockIdx.y / segs;
+  const int y0 = (blockIdx.y - slice * segs) * RS, y1 = min(H, y0 + RS);
   const int pair = int(blockIdx.z) * 4 + (idx & 3);
-  const ulonglong2* Rp = reinterpret_cast<const ulonglong2*>(Rin) + int64_t(blockIdx.z) * P * 4 + idx;
-  ulonglong2* Qp = reinterpret_cast<ulonglong2*>(Q) + int64_t(blockIdx.z) * P * 4 + idx;
+  const int64_t base = (int64_t(blockIdx.z) * P + int64_t(slice) * H * W) * 4 + idx;
+  const ulonglong2* Rp = reinterpret_cast<const ulonglong2*>(Rin) + base;
+  ulonglong2* Qp = reinterpret_cast<ulonglong2*>(Q) + base;
   const int64_t rs = int64_t(W) * 4;   // row stride in 16-byte chunks
   const float4 fx4 = __ldg(mxp + int64_t(idx >> 2) * D2 + pair);
   const uint64_t fxr = f2pack(fx4.x, fx4.y), fxi = f2pack(fx4.z, fx4.w);
@@ -195,19 +200,21 @@ void launch_pool_split(const DevTables& tb, int W, int H, int D8, int dx, int dy
   k_box_x<<<gx, 256, 0, s>>>(R, Qout, tb.mx, tb.my, W, H, D8, dx, CS, P);
 }
 
-void launch_pool_y_demod(const DevTables& tb, int W, int H, int D8, int dy, const float2* R, float2* Q,
+void launch_pool_y_demod(const DevTables& tb, int W, int H, int nb, int D8, int dy, const float2* R, float2* Q,
                          cudaStream_t s) {
   const int planes = D8 / 8;
-  const int64_t P = int64_t(W) * H;
+  const int64_t P = int64_t(W) * H * nb;
   static const int env_segs = [] {
     const char* e = std::getenv("VKM_YSEGS");
     return e ? std::atoi(e) : 0;
   }();
-  const int segs = env_segs > 0 ? env_segs : pick_segments(W, H, dy, planes, W * 4, 512);
+  int segs = env_segs > 0 ? env_segs : pick_segments(W, H, dy, planes, W * 4, 512);
+  segs = std::max(1, segs / nb);   // batched slices already multiply the parallelism
   const int RS = (H + segs - 1) / segs;
-  dim3 gy((W * 4 + 255) / 256, (H + RS - 1) / RS, planes);
-  k_box_y_demod<<<gy, 256, 0, s>>>(reinterpret_cast<const float4*>(R), reinterpret_cast<float4*>(Q), W, H, dy, RS, P,
-                                   tb.mxp, tb.myp, D8 / 2);
+  segs = (H + RS - 1) / RS;
+  dim3 gy((W * 4 + 255) / 256, segs * nb, planes);
+  k_box_y_demod<<<gy, 256, 0, s>>>(reinterpret_cast<const float4*>(R), reinterpret_cast<float4*>(Q), W, H, segs, dy,
+                                   RS, P, tb.mxp, tb.myp, D8 / 2);
 }
 
 }  // namespace vkm

@@ -32,19 +32,23 @@ namespace vkm {
 
 constexpr unsigned kFullMask = 0xffffffffu;
 
-__global__ void __launch_bounds__(256) k_prep(const double* __restrict__ ev, int64_t n, double t0_in, double delta_t,
+__global__ void __launch_bounds__(256) k_prep(const double* __restrict__ ev, const SliceTab st, double delta_t,
                                               int W, int H, int32_t* __restrict__ pix_out,
                                               uint64_t* __restrict__ val_out, int* __restrict__ cnt,
                                               float* __restrict__ flows_invalid,
                                               int32_t* __restrict__ counts_invalid) {
-  const double t0 = ld_t0(ev, t0_in);
   const int P = W * H;
+  const int64_t n = st.off[st.nb];
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    int b = 0;   // slice of event e (upper_bound over the offsets)
+    for (int step = kMaxBatch / 2; step > 0; step >>= 1)
+      if (b + step < st.nb && st.off[b + step] <= e) b += step;
+    const double t0 = ld_t0(ev + 3 * st.off[b], st.t0[b]);
     const double t = __ldg(ev + 3 * e), x = __ldg(ev + 3 * e + 1), y = __ldg(ev + 3 * e + 2);
     const int xi = int(x), yi = int(y);
-    int pix = P;   // out-of-sensor events sort after every pixel run
+    int pix = st.nb * P;   // out-of-sensor events sort after every pixel run
     if (xi >= 0 && xi < W && yi >= 0 && yi < H && x == double(xi) && y == double(yi)) {
-      pix = yi * W + xi;
+      pix = b * P + yi * W + xi;
       atomicAdd(cnt + pix, 1);
     } else {
       if (flows_invalid)
@@ -186,8 +190,9 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
                                                             const uint64_t* __restrict__ val_s,
                                                             const float* __restrict__ tf,
                                                             const float4* __restrict__ mxp,
-                                                            const float4* __restrict__ myp, int W, int H, int dx,
-                                                            int S, int nseg, int64_t P, float2* __restrict__ R) {
+                                                            const float4* __restrict__ myp, int W, int H, int nb,
+                                                            int dx, int S, int nseg, int64_t P,
+                                                            float2* __restrict__ R) {
   extern __shared__ __align__(16) uint8_t rx_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int RL = 2 * dx + 1;
@@ -198,10 +203,10 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
   const float4* mxl = mxp + lane;                   // mxl[x * 32]: (cos c0, cos c1, sin c0, sin c1) of x X/δx
   const float4* myl = myp + lane;                   // (cos c0, cos c1, sin c0, sin c1) of y Y/δy
   float4* const R4 = reinterpret_cast<float4*>(R) + ((int64_t(lane >> 2) * P) << 2) + (lane & 3);
-  const int64_t items = int64_t(H) * nseg;
+  const int64_t items = int64_t(nb) * H * nseg;   // (virtual row, segment); P = nb·W·H
   const int64_t nwarps = int64_t(gridDim.x) * kRxWarps;
   for (int64_t it = int64_t(blockIdx.x) * kRxWarps + wib; it < items; it += nwarps) {
-    const int y = int(it / nseg);
+    const int y = int(it / nseg);                  // virtual row: slice y / H, sensor row y % H
     const int x0 = int(it - int64_t(y) * nseg) * S, x1 = min(W, x0 + S);
     const int xs = x0 - dx, nx = x1 + dx - xs;      // sweep x = xs + k, k in [0, nx)
     const int* st = start + int64_t(y) * W;         // st[x]: first slot of pixel (x, y)
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
     }
     for (int k = 0; k < RL; ++k) ring0[k * 32] = make_ulonglong2(0ull, 0ull);
     __syncwarp();
-    const float4 fy4 = __ldg(myl + int64_t(y) * 32);
+    const float4 fy4 = __ldg(myl + int64_t(y % H) * 32);
     const uint64_t fyr = f2pack(fy4.x, fy4.y), fyi = f2pack(fy4.z, fy4.w);
     float4* out = R4 + ((int64_t(y) * W + x0) << 2);
     auto ld_a = [&](int jj) { return jj < jend ? slot_arg(__ldg(val_s + jj)) : 0.f; };
@@ -304,14 +309,15 @@ size_t sort_pairs_temp_bytes(int64_t n, int64_t P) {
   return bytes;
 }
 
-int launch_sort_events(const double* ev, int64_t n, double t0, double delta_t, int W, int H, const GridBufs& g,
+int launch_sort_events(const double* ev, const SliceTab& st, double delta_t, int W, int H, const GridBufs& g,
                        const SortBufs& sb, float* flows_invalid, int32_t* counts_invalid, cudaStream_t s) {
-  const int64_t P = int64_t(W) * H;
+  const int64_t P = int64_t(W) * H * st.nb;
+  const int64_t n = st.off[st.nb];
   int launches = 0;
   cudaMemsetAsync(g.C, 0, sizeof(int) * (P + 1), s);
   if (n > 0) {
     const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
-    k_prep<<<blocks, 256, 0, s>>>(ev, n, t0, delta_t, W, H, sb.pix, sb.val, g.C, flows_invalid, counts_invalid);
+    k_prep<<<blocks, 256, 0, s>>>(ev, st, delta_t, W, H, sb.pix, sb.val, g.C, flows_invalid, counts_invalid);
     ++launches;
   }
   size_t scan_bytes = sb.temp_bytes;
@@ -354,9 +360,9 @@ void launch_reduce_raw(const DevTables& tb, int W, int H, int D8, const GridBufs
 
 bool reduce_x_supported(int D8, int dx) { return D8 == 64 && dx >= 1 && dx <= kMaxFusedDx; }
 
-void launch_reduce_x(const DevTables& tb, int W, int H, int dx, const SortBufs& sb, float2* R, int num_sms,
-                     cudaStream_t s) {
-  const int64_t P = int64_t(W) * H;
+void launch_reduce_x(const DevTables& tb, int W, int H, int nb, int dx, const SortBufs& sb, float2* R,
+                     int num_sms, cudaStream_t s) {
+  const int64_t P = int64_t(W) * H * nb;
   const size_t smem = reduce_x_smem(dx);
   static bool attr = false;
   if (!attr) {
@@ -374,11 +380,11 @@ void launch_reduce_x(const DevTables& tb, int W, int H, int dx, const SortBufs& 
   }();
   int S = seg_env > 0 ? std::min(seg_env, kRxMaxSeg) : kRxMaxSeg;
   if (seg_env <= 0)
-    while (S > 32 && 4 * int64_t(H) * ((W + S - 1) / S) < 3 * res_warps) S >>= 1;
+    while (S > 32 && 4 * int64_t(H) * nb * ((W + S - 1) / S) < 3 * res_warps) S >>= 1;
   const int nseg = (W + S - 1) / S;
-  const int64_t items = int64_t(H) * nseg;
+  const int64_t items = int64_t(H) * nb * nseg;
   const int blocks = int(std::min<int64_t>((items + kRxWarps - 1) / kRxWarps, res_warps / kRxWarps));
-  k_reduce_x<<<blocks, kRxWarps * 32, smem, s>>>(sb.start, sb.val_s, tb.tf, tb.mxp, tb.myp, W, H, dx, S, nseg, P, R);
+  k_reduce_x<<<blocks, kRxWarps * 32, smem, s>>>(sb.start, sb.val_s, tb.tf, tb.mxp, tb.myp, W, H, nb, dx, S, nseg, P, R);
 }
 
 }  // namespace vkm

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <utility>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -77,6 +79,8 @@ struct vkm_handle {
   float w_scale_f16 = 1.f;
   bool tc_ok = false;  // D == 64 && hidden == 128
   bool force_split = false;  // VKM_POOL=split: raw grid + two-pass pooling (A/B and parity)
+  int64_t grid_cap = 0;      // pixels the grid scratch holds (nb·W·H of the largest batch so far)
+  int64_t batch_pixels = int64_t(1) << 22;   // pixel budget of one batched launch sequence
   // scratch
   vkm::SortBufs sb{};
   size_t sort_cap = 0;
@@ -131,46 +135,87 @@ void rec(vkm_handle* h, int i, cudaStream_t s) {
   if (h->profiling) cudaEventRecord(h->evt[i], s);
 }
 
-int ensure_sort(vkm_handle* h, int64_t n) {
-  if (h->sort_cap >= size_t(std::max<int64_t>(n, 1))) return VKM_OK;
+int ensure_sort(vkm_handle* h, int64_t n, int64_t Pv) {
+  const size_t cap = size_t(std::max<int64_t>(n, 1));
+  const size_t temp = vkm::sort_pairs_temp_bytes(int64_t(cap), Pv);
+  if (h->sort_cap >= cap && h->sb.sort_temp_bytes >= temp) return VKM_OK;
   void* arrs[] = {h->sb.pix, h->sb.val, h->sb.val_s, h->sb.pix_s, h->sb.sort_temp};
   for (void* p : arrs)
     if (p) cudaFree(p);
   h->sb.pix = nullptr; h->sb.val = nullptr; h->sb.val_s = nullptr; h->sb.pix_s = nullptr;
   h->sb.sort_temp = nullptr;
-  const size_t cap = size_t(std::max<int64_t>(n, 1));
   h->sort_cap = 0;
+  h->sb.sort_temp_bytes = 0;
   VKM_CK(cudaMalloc(&h->sb.pix, 4 * cap));
   VKM_CK(cudaMalloc(&h->sb.val, 8 * cap));
   VKM_CK(cudaMalloc(&h->sb.val_s, 8 * cap));
   VKM_CK(cudaMalloc(&h->sb.pix_s, 4 * cap));
-  h->sb.sort_temp_bytes = vkm::sort_pairs_temp_bytes(int64_t(cap), h->P);
-  VKM_CK(cudaMalloc(&h->sb.sort_temp, std::max<size_t>(h->sb.sort_temp_bytes, 16)));
+  VKM_CK(cudaMalloc(&h->sb.sort_temp, std::max<size_t>(temp, 16)));
+  h->sb.sort_temp_bytes = temp;
   h->sort_cap = cap;
   return VKM_OK;
 }
 
-// K1 + K2 for one slice on stream s.  pooled = 0 leaves the raw pre-modulated
-// grid in G (parity hook); otherwise the pooled grid ends in Q.
-int encode_core(vkm_handle* h, const double* ev, int64_t n, double t0, int pooled, cudaStream_t s, int* launches,
+// Grid scratch for Pv = nb·W·H pixels: two grids of 64 B/pixel per plane,
+// counts, pooled counts, run starts and the scan scratch.
+int ensure_grid(vkm_handle* h, int64_t Pv) {
+  if (h->grid_cap >= Pv) return VKM_OK;
+  void* arrs[] = {h->G, h->Q, h->C, h->NQ, h->sb.start, h->sb.temp};
+  for (void* p : arrs)
+    if (p) cudaFree(p);
+  h->G = h->Q = nullptr;
+  h->C = h->NQ = h->sb.start = nullptr;
+  h->sb.temp = nullptr;
+  h->grid_cap = 0;
+  VKM_CK(cudaMalloc(&h->G, sizeof(float2) * 8 * h->planes * Pv));
+  VKM_CK(cudaMalloc(&h->Q, sizeof(float2) * 8 * h->planes * Pv));
+  VKM_CK(cudaMalloc(&h->C, sizeof(int) * (Pv + 1)));
+  VKM_CK(cudaMalloc(&h->NQ, sizeof(int) * Pv));
+  VKM_CK(cudaMalloc(&h->sb.start, sizeof(int) * (Pv + 1)));
+  h->sb.temp_bytes = vkm::sort_scan_temp_bytes(Pv);
+  VKM_CK(cudaMalloc(&h->sb.temp, std::max<size_t>(h->sb.temp_bytes, 16)));
+  h->grid_cap = Pv;
+  return VKM_OK;
+}
+
+vkm::SliceTab one_slice(int64_t n, double t0) {
+  vkm::SliceTab st{};
+  st.nb = 1;
+  st.off[0] = 0;
+  st.off[1] = n;
+  st.t0[0] = t0;
+  return st;
+}
+
+bool use_tc(const vkm_handle* h) { return (h->mode == VKM_MLP_F16X3 || h->mode == VKM_MLP_BF16) && h->tc_ok; }
+bool fused_ok(const vkm_handle* h) { return !h->force_split && vkm::reduce_x_supported(h->D8, h->p.delta_x); }
+// Several slices per launch sequence: the fused encoder and the tensor-core head.
+bool batchable(const vkm_handle* h) { return use_tc(h) && fused_ok(h); }
+
+// K1 + K2 for the slices of st on stream s.  pooled = 0 leaves the raw
+// pre-modulated grid in G (parity hook, one slice); otherwise the pooled grid
+// ends in Q.  More than one slice requires the fused path.
+int encode_core(vkm_handle* h, const double* ev, const vkm::SliceTab& st, int pooled, cudaStream_t s, int* launches,
                 float* flows_invalid = nullptr, int32_t* counts_invalid = nullptr) {
-  const int W = h->p.width, H = h->p.height;
-  int rc = ensure_sort(h, n);
+  const int W = h->p.width, H = h->p.height, nb = st.nb;
+  const int64_t n = st.off[nb], Pv = h->P * nb;
+  int rc = ensure_grid(h, Pv);
+  if (!rc) rc = ensure_sort(h, n, Pv);
   if (rc) return rc;
-  *launches += vkm::launch_sort_events(ev, n, t0, h->p.delta_t, W, H, bufs(h), h->sb, flows_invalid,
-                                       counts_invalid, s);
-  const bool fused = pooled && !h->force_split && vkm::reduce_x_supported(h->D8, h->p.delta_x);
-  if (fused) {
+  *launches += vkm::launch_sort_events(ev, st, h->p.delta_t, W, H, bufs(h), h->sb, flows_invalid, counts_invalid,
+                                       s);
+  if (pooled && fused_ok(h)) {
     // x window fused into the reduction: R -> G, then y window + demodulation G -> Q
-    vkm::launch_reduce_x(tables(h), W, H, h->p.delta_x, h->sb, h->G, h->num_sms, s);
+    vkm::launch_reduce_x(tables(h), W, H, nb, h->p.delta_x, h->sb, h->G, h->num_sms, s);
     *launches += 1;
     VKM_CK(cudaGetLastError());
     rec(h, 1, s);
-    vkm::launch_pool_y_demod(tables(h), W, H, h->D8, h->p.delta_y, h->G, h->Q, s);
-    vkm::launch_pool_count(W, H, h->p.delta_x, h->p.delta_y, bufs(h), s);
+    vkm::launch_pool_y_demod(tables(h), W, H, nb, h->D8, h->p.delta_y, h->G, h->Q, s);
+    vkm::launch_pool_count(W, H, nb, h->p.delta_x, h->p.delta_y, bufs(h), s);
     *launches += 2;
     VKM_CK(cudaGetLastError());
   } else {
+    if (nb != 1) return fail(VKM_EINVAL, "internal: batched slices need the fused encoder");
     vkm::launch_reduce_raw(tables(h), W, H, h->D8, bufs(h), h->sb, s);
     *launches += 1;
     VKM_CK(cudaGetLastError());
@@ -179,7 +224,7 @@ int encode_core(vkm_handle* h, const double* ev, int64_t n, double t0, int poole
       // y-pass M(G) -> R(Q), x-pass R(Q) -> pooled(G); then swap so Q names the pooled grid
       vkm::launch_pool_split(tables(h), W, H, h->D8, h->p.delta_x, h->p.delta_y, h->G, h->Q, h->G, s);
       std::swap(h->G, h->Q);
-      vkm::launch_pool_count(W, H, h->p.delta_x, h->p.delta_y, bufs(h), s);
+      vkm::launch_pool_count(W, H, 1, h->p.delta_x, h->p.delta_y, bufs(h), s);
       *launches += 3;
       VKM_CK(cudaGetLastError());
     }
@@ -188,19 +233,24 @@ int encode_core(vkm_handle* h, const double* ev, int64_t n, double t0, int poole
   return VKM_OK;
 }
 
-int predict_one(vkm_handle* h, const double* ev, int64_t n, double t0, float* flows, int32_t* counts, cudaStream_t s,
-                int* launches) {
-  const bool tc = (h->mode == VKM_MLP_F16X3 || h->mode == VKM_MLP_BF16) && h->tc_ok;
-  int rc = encode_core(h, ev, n, t0, 1, s, launches, flows, counts);
+// Flows for the slices of st (one launch sequence).
+int predict_chunk(vkm_handle* h, const double* ev, const vkm::SliceTab& st, float* flows, int32_t* counts,
+                  cudaStream_t s, int* launches) {
+  const bool tc = use_tc(h);
+  int rc = encode_core(h, ev, st, 1, s, launches, flows, counts);
   if (rc) return rc;
+  const int64_t n = st.off[st.nb];
   if (n <= 0) return VKM_OK;
   const int W = h->p.width, H = h->p.height;
   if (tc) {
     vkm::TcWeights tw{h->mode == VKM_MLP_BF16 ? h->w1_bf16 : h->w1_f16_hi, h->w1_f16_lo, h->b1, h->w2, h->b2,
                       h->mode == VKM_MLP_BF16 ? 1.f : h->w_scale_f16};
-    vkm::launch_gather_mlp_tc(n, tables(h), W, H, bufs(h), h->sb, tw, h->mode, flows, counts, h->num_sms, s);
+    vkm::launch_gather_mlp_tc(n, tables(h), W, H * st.nb, bufs(h), h->sb, tw, h->mode, flows, counts, h->num_sms,
+                              s);
     *launches += 1;
   } else {
+    if (st.nb != 1) return fail(VKM_EINVAL, "internal: batched slices need the tensor-core head");
+    const double t0 = st.t0[0];
     rc = grow(&h->feats, &h->feats_cap, size_t(n) * 2 * h->D8);
     if (rc) return rc;
     int32_t* cn = counts;
@@ -218,6 +268,34 @@ int predict_one(vkm_handle* h, const double* ev, int64_t n, double t0, float* fl
   }
   VKM_CK(cudaGetLastError());
   return VKM_OK;
+}
+
+int predict_one(vkm_handle* h, const double* ev, int64_t n, double t0, float* flows, int32_t* counts, cudaStream_t s,
+                int* launches) {
+  return predict_chunk(h, ev, one_slice(n, t0), flows, counts, s, launches);
+}
+
+// Group consecutive slices [s0, s1) into one SliceTab (offsets relative to
+// offsets[s0]); empty slices are skipped; at most max_events events unless a
+// single slice is larger.  Returns s1.
+int next_chunk(const vkm_handle* h, const int64_t* offsets, int32_t n_slices, const double* t_starts, int s0,
+               vkm::SliceTab& st, int64_t max_events = INT64_MAX) {
+  const int maxb = batchable(h) ? int(std::max<int64_t>(1, std::min<int64_t>(vkm::kMaxBatch,
+                                                                             h->batch_pixels / h->P)))
+                                : 1;
+  st = vkm::SliceTab{};
+  st.nb = 0;
+  const int64_t base = offsets[s0];
+  int s = s0;
+  for (; s < n_slices && st.nb < maxb; ++s) {
+    if (offsets[s + 1] == offsets[s]) continue;
+    if (st.nb > 0 && offsets[s + 1] - base > max_events) break;   // keep chunks small enough to pipeline
+    st.off[st.nb] = offsets[s] - base;
+    st.t0[st.nb] = t_starts ? t_starts[s] : NAN;
+    ++st.nb;
+  }
+  st.off[st.nb] = offsets[s] - base;
+  return s;
 }
 
 int check_handle(const vkm_handle* h) {
@@ -356,14 +434,13 @@ int vkm_create(vkm_handle** out, const vkm_params* params, const double* T, cons
     VKM_CKH(cudaMemcpy(h->myp, myp.data(), sizeof(float4) * myp.size(), cudaMemcpyHostToDevice));
   }
 
-  // Grid scratch: two planes-sets of 64 B/pixel plus int32 counts (516 B/pixel at D=64).
-  VKM_CKH(cudaMalloc(&h->G, sizeof(float2) * 8 * h->planes * h->P));
-  VKM_CKH(cudaMalloc(&h->Q, sizeof(float2) * 8 * h->planes * h->P));
-  VKM_CKH(cudaMalloc(&h->C, sizeof(int) * (h->P + 1)));
-  VKM_CKH(cudaMalloc(&h->NQ, sizeof(int) * h->P));
-  VKM_CKH(cudaMalloc(&h->sb.start, sizeof(int) * (h->P + 1)));
-  h->sb.temp_bytes = vkm::sort_scan_temp_bytes(h->P);
-  VKM_CKH(cudaMalloc(&h->sb.temp, std::max<size_t>(h->sb.temp_bytes, 16)));
+  // Grid scratch for one slice (grown on demand for batches): two plane sets
+  // of 64 B/pixel plus int32 counts (516 B/pixel at D=64).
+  if (int rc = ensure_grid(h, h->P)) return cleanup_fail(rc);
+  {
+    const char* e = std::getenv("VKM_BATCH_PIXELS");
+    if (e && std::atoll(e) > 0) h->batch_pixels = std::atoll(e);
+  }
 
 
   if (h->hidden > 0) {
@@ -475,7 +552,7 @@ int vkm_encode(vkm_handle* h, const double* ev, int64_t n, double t_start, float
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int launches = 0;
   rec(h, 0, s);
-  int rc = encode_core(h, ev, n, t_start, 1, s, &launches);
+  int rc = encode_core(h, ev, one_slice(n, t_start), 1, s, &launches);
   if (rc) return rc;
   if (n > 0) {
     vkm::launch_features(ev, n, t_start, h->p.delta_t, tables(h), h->p.width, h->p.height, h->D8, h->D, bufs(h),
@@ -547,18 +624,22 @@ int vkm_predict_batch(vkm_handle* h, const double* ev, const int64_t* offsets, i
   for (int s = 0; s < n_slices; ++s)
     if (offsets[s + 1] < offsets[s] || offsets[s] < 0) return fail(VKM_EINVAL, "slice offsets must be non-decreasing");
   DeviceGuard dg(h->p.device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaStream_t sm = static_cast<cudaStream_t>(stream);
   int launches = 0;
-  rec(h, 0, st);
-  for (int s = 0; s < n_slices; ++s) {
-    const int64_t lo = offsets[s], cnt = offsets[s + 1] - offsets[s];
-    if (cnt == 0) continue;
-    const double t0 = t_starts ? t_starts[s] : NAN;
-    int rc = predict_one(h, ev + 3 * lo, cnt, t0, flows + 2 * lo, counts ? counts + lo : nullptr, st, &launches);
-    if (rc) return rc;
+  rec(h, 0, sm);
+  // chunks of up to kMaxBatch slices (pixel budget batch_pixels) share one launch sequence
+  for (int s = 0; s < n_slices;) {
+    vkm::SliceTab st;
+    const int s1 = next_chunk(h, offsets, n_slices, t_starts, s, st);
+    const int64_t lo = offsets[s];
+    if (st.nb > 0) {
+      int rc = predict_chunk(h, ev + 3 * lo, st, flows + 2 * lo, counts ? counts + lo : nullptr, sm, &launches);
+      if (rc) return rc;
+    }
+    s = s1;
   }
-  rec(h, 3, st);
-  h->have_timing = false;  // per-slice events are overwritten; only the total is meaningful
+  rec(h, 3, sm);
+  h->have_timing = false;  // per-chunk events are overwritten; only the total is meaningful
   h->last_launches = launches;
   return VKM_OK;
 }
@@ -568,14 +649,25 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
   if (int rc = check_handle(h)) return rc;
   if (h->hidden <= 0) return fail(VKM_EINVAL, "handle has no flow head (hidden == 0)");
   if (n_slices < 0 || (n_slices > 0 && !offsets)) return fail(VKM_EINVAL, "bad slice offsets");
-  int64_t nmax = 0;
-  for (int s = 0; s < n_slices; ++s) {
+  for (int s = 0; s < n_slices; ++s)
     if (offsets[s + 1] < offsets[s] || offsets[s] < 0) return fail(VKM_EINVAL, "slice offsets must be non-decreasing");
-    nmax = std::max(nmax, offsets[s + 1] - offsets[s]);
-  }
   if (n_slices == 0 || offsets[n_slices] == offsets[0]) return VKM_OK;
   if (!ev_host || !flows_host) return fail(VKM_EINVAL, "null host buffer");
   DeviceGuard dg(h->p.device);
+  // chunks (each one launch sequence), then the largest chunk sizes the staging slots
+  // at most 2M events (or a quarter of the call) per chunk so copies overlap kernels
+  const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(int64_t(1) << 21, (offsets[n_slices] - offsets[0]) / 4));
+  std::vector<std::pair<int, vkm::SliceTab>> chunks;
+  int64_t nmax = 0;
+  for (int s = 0; s < n_slices;) {
+    vkm::SliceTab st;
+    const int s1 = next_chunk(h, offsets, n_slices, t_starts, s, st, cap);
+    if (st.nb > 0) {
+      chunks.emplace_back(s, st);
+      nmax = std::max(nmax, st.off[st.nb]);
+    }
+    s = s1;
+  }
   if (!h->s_in) {
     VKM_CK(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
     VKM_CK(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
@@ -592,20 +684,19 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
     if (rc) return rc;
   }
   cudaStream_t sc = h->stream;
-  // slot k = s % 2.  copy-in(s) waits until compute(s-2) stopped reading the slot;
-  // compute(s) waits for copy-in(s) and for copy-out(s-2) to drain the output slot.
-  int launches = 0, used = 0;
-  for (int s = 0; s < n_slices; ++s) {
-    const int64_t lo = offsets[s], n = offsets[s + 1] - lo;
-    if (n == 0) continue;
-    const int k = used & 1;
-    if (used >= 2) VKM_CK(cudaStreamWaitEvent(h->s_in, h->computed[k], 0));
+  // slot k = chunk % 2.  copy-in(c) waits until compute(c-2) stopped reading the
+  // slot; compute(c) waits for copy-in(c) and for copy-out(c-2) to drain its output.
+  int launches = 0;
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    const vkm::SliceTab& st = chunks[c].second;
+    const int64_t lo = offsets[chunks[c].first], n = st.off[st.nb];
+    const int k = int(c & 1);
+    if (c >= 2) VKM_CK(cudaStreamWaitEvent(h->s_in, h->computed[k], 0));
     VKM_CK(cudaMemcpyAsync(h->pev[k], ev_host + 3 * lo, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, h->s_in));
     VKM_CK(cudaEventRecord(h->in_ready[k], h->s_in));
     VKM_CK(cudaStreamWaitEvent(sc, h->in_ready[k], 0));
-    if (used >= 2) VKM_CK(cudaStreamWaitEvent(sc, h->out_done[k], 0));
-    const double t0 = t_starts ? t_starts[s] : NAN;
-    int rc = predict_one(h, h->pev[k], n, t0, h->pout[k], counts_host ? h->pcnt[k] : nullptr, sc, &launches);
+    if (c >= 2) VKM_CK(cudaStreamWaitEvent(sc, h->out_done[k], 0));
+    int rc = predict_chunk(h, h->pev[k], st, h->pout[k], counts_host ? h->pcnt[k] : nullptr, sc, &launches);
     if (rc) return rc;
     VKM_CK(cudaEventRecord(h->computed[k], sc));
     VKM_CK(cudaStreamWaitEvent(h->s_out, h->computed[k], 0));
@@ -613,7 +704,6 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
     if (counts_host)
       VKM_CK(cudaMemcpyAsync(counts_host + lo, h->pcnt[k], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, h->s_out));
     VKM_CK(cudaEventRecord(h->out_done[k], h->s_out));
-    ++used;
   }
   VKM_CK(cudaStreamSynchronize(h->s_out));
   VKM_CK(cudaStreamSynchronize(sc));
@@ -629,7 +719,7 @@ int vkm_grid(vkm_handle* h, const double* ev, int64_t n, double t_start, int32_t
   DeviceGuard dg(h->p.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int launches = 0;
-  int rc = encode_core(h, ev, n, t_start, pooled, s, &launches);
+  int rc = encode_core(h, ev, one_slice(n, t_start), pooled, s, &launches);
   if (rc) return rc;
   vkm::launch_grid_to_ref(pooled ? h->Q : h->G, pooled ? h->NQ : h->C, h->p.width, h->p.height, h->D, h->D8,
                           pooled ? nullptr : h->mx, pooled ? nullptr : h->my, pooled != 0, grid, counts, s);

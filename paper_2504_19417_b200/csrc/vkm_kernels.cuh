@@ -53,6 +53,17 @@ struct SortBufs {
   size_t sort_temp_bytes;
 };
 
+// Slices processed by one launch sequence (batched fused path): slice b owns
+// events [off[b], off[b+1]) and the pixel block [b·P, (b+1)·P) of a virtual
+// W x (nb·H) sensor whose windows never cross slice borders.  t0[b] = NaN
+// reads the slice's first event.  Passed by value as a kernel parameter.
+constexpr int kMaxBatch = 64;
+struct SliceTab {
+  int32_t nb;
+  int64_t off[kMaxBatch + 1];
+  double t0[kMaxBatch];
+};
+
 struct MlpDev {
   const float* w1;   // [hidden][2*D8] padded: [Re(0..D8) | Im(0..D8)]
   const float* b1;   // [hidden]
@@ -63,7 +74,8 @@ struct MlpDev {
 
 // K1 (sorted): prep + scan + stable radix sort of (pixel, slot_pack) pairs.
 // Returns the number of kernel launches.  C must hold P+1 ints.
-int launch_sort_events(const double* ev, int64_t n, double t0, double delta_t, int W, int H, const GridBufs& g,
+// Keys live in [0, nb·W·H]; nb·W·H + 1 counters in g.C.
+int launch_sort_events(const double* ev, const SliceTab& st, double delta_t, int W, int H, const GridBufs& g,
                        const SortBufs& sb, float* flows_invalid, int32_t* counts_invalid, cudaStream_t s);
 // K1 reduce, raw grid: per-pixel time-ordered sums, written pre-modulated
 // (M = G·e^{i(xX/δx + yY/δy)}) to g.G.  Used by the split pooling path and the
@@ -73,8 +85,8 @@ void launch_reduce_raw(const DevTables& tb, int W, int H, int D8, const GridBufs
 // K1 reduce fused with the x window (D8 == 64, dx <= kMaxFusedDx):
 //   R[y][x] = e^{i y Y/δy} · Σ_{|i|<=δx} G[y][x+i]·e^{i (x+i) X/δx}   -> R
 bool reduce_x_supported(int D8, int dx);
-void launch_reduce_x(const DevTables& tb, int W, int H, int dx, const SortBufs& sb, float2* R, int num_sms,
-                     cudaStream_t s);
+void launch_reduce_x(const DevTables& tb, int W, int H, int nb, int dx, const SortBufs& sb, float2* R,
+                     int num_sms, cudaStream_t s);
 size_t sort_scan_temp_bytes(int64_t P);
 size_t sort_pairs_temp_bytes(int64_t n, int64_t P);
 // K2 (split): box sum of the pre-modulated grid M (y-pass M -> R, x-pass +
@@ -83,9 +95,9 @@ void launch_pool_split(const DevTables& tb, int W, int H, int D8, int dx, int dy
                        float2* Qout, cudaStream_t s);
 // K2 (fused path): y window of the x-pooled R plus full demodulation
 //   Q[y][x] = conj(e^{i(xX/δx + yY/δy)}) · Σ_{|j|<=δy} R[y+j][x]
-void launch_pool_y_demod(const DevTables& tb, int W, int H, int D8, int dy, const float2* R, float2* Q,
+void launch_pool_y_demod(const DevTables& tb, int W, int H, int nb, int D8, int dy, const float2* R, float2* Q,
                          cudaStream_t s);
-void launch_pool_count(int W, int H, int dx, int dy, const GridBufs& g, cudaStream_t s);
+void launch_pool_count(int W, int H, int nb, int dx, int dy, const GridBufs& g, cudaStream_t s);
 // K3a: gather Q at each event, de-phase, divide by the count -> features.
 // Row e gets Re at out[e*ld + c] and Im at out[e*ld + im_off + c] for c < Dout.
 void launch_features(const double* ev, int64_t n, double t0, double delta_t, const DevTables& tb,
@@ -110,6 +122,7 @@ struct TcWeights {
   float w_scale;       // power-of-two pre-scale folded into the W1 images
 };
 // Tiles run over the pixel-sorted slots of SortBufs (sequential pooled-grid reads).
+// H is the (virtual, nb·H for a batch) grid height.
 void launch_gather_mlp_tc(int64_t n, const DevTables& tb, int W, int H, const GridBufs& g, const SortBufs& sb,
                           const TcWeights& w, int mode, float* flows, int32_t* counts_out, int num_sms,
                           cudaStream_t s);

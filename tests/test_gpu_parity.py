@@ -186,9 +186,11 @@ def test_batch_matches_single_slices():
     ev = torch.from_numpy(np.concatenate(slices)).cuda()
     off = np.cumsum([0] + [len(s) for s in slices])
     out = eng.predict_batch_device(ev, off).cpu().numpy()
+    # batched and single launches pick different x-segment widths in
+    # k_reduce_x, so the sliding window sums round differently (~1e-7 rel.)
     for s, X in enumerate(slices):
         single = eng.predict_host(X, float(X[0, 0]))
-        np.testing.assert_allclose(out[off[s]:off[s + 1]], single, rtol=0, atol=1e-6)
+        np.testing.assert_allclose(out[off[s]:off[s + 1]], single, rtol=0, atol=1e-5)
 
 
 def test_full_size_config2_properties():
@@ -285,8 +287,8 @@ def test_predict_slices_pipelined_host_batch():
     assert len(got) == len(slices)
     for X, f in zip(slices, got):
         assert f.shape == (len(X), 2) and f.dtype == np.float64
-        if len(X):
-            np.testing.assert_array_equal(f, reg.predict(X))
+        if len(X):   # batched launches: other x-segment widths -> f32 rounding noise
+            np.testing.assert_allclose(f, reg.predict(X), rtol=0, atol=1e-5)
     # counts through the engine call
     eng = reg.engine()
     ev = np.concatenate([s for s in slices if len(s)])
@@ -294,7 +296,7 @@ def test_predict_slices_pipelined_host_batch():
     flows, counts = eng.predict_batch_host(ev, off, [float(s[0, 0]) for s in slices if len(s)], return_counts=True)
     for i, s in enumerate([s for s in slices if len(s)]):
         f1, c1 = eng.predict_host(s, float(s[0, 0]), return_counts=True)
-        np.testing.assert_array_equal(flows[off[i]:off[i + 1]], f1)
+        np.testing.assert_allclose(flows[off[i]:off[i + 1]], f1, rtol=0, atol=1e-5)
         np.testing.assert_array_equal(counts[off[i]:off[i + 1]], c1)
 
 
@@ -316,3 +318,39 @@ def test_fused_x_window_matches_split_pooling(d, monkeypatch):
     f2, c2 = split.predict_host(X, float(X[0, 0]), return_counts=True)
     np.testing.assert_array_equal(c1, c2)
     np.testing.assert_allclose(f1, f2, rtol=0, atol=1e-5)
+
+
+def test_batched_slices_many_chunks_edge_cases():
+    """Batched launch sequences (up to 64 slices stacked as one virtual
+    W x (nb·H) sensor with hard slice borders): 70 slices of mixed sizes ->
+    more than one chunk; empty slices, a single-event slice, an out-of-sensor
+    event (NaN row, count 0), explicit and NaN t_starts.  Each slice must match
+    its own single-slice run (counts exact, flows to f32 rounding)."""
+    import torch
+    pkg = _pkg()
+    W, H = 120, 90
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    eng = pkg.FlowEngine(W, H, 10, 10, 0.016, b, w)
+    rng = np.random.default_rng(5)
+    slices = []
+    for i in range(70):
+        n = int(rng.choice([0, 1, 700, 3000, 9000]))
+        X = vo.synth_uniform_noise(n, W, H, seed=100 + i) if n else np.zeros((0, 3))
+        if n and i % 9 == 0:
+            X[n // 2, 1] = W + 3   # outside the sensor
+        slices.append(X)
+    off = np.cumsum([0] + [len(s) for s in slices])
+    ts = [float(s[0, 0]) if (len(s) and i % 2) else math.nan for i, s in enumerate(slices)]
+    ev = torch.from_numpy(np.ascontiguousarray(np.concatenate([s for s in slices if len(s)]))).cuda()
+    cnt = torch.empty(len(ev), dtype=torch.int32, device="cuda")
+    flows = eng.predict_batch_device(ev, off, ts, counts=cnt).cpu().numpy()
+    cnt = cnt.cpu().numpy()
+    for i, X in enumerate(slices):
+        if not len(X):
+            continue
+        f1, c1 = eng.predict_host(X, float(X[0, 0]), return_counts=True)
+        np.testing.assert_array_equal(cnt[off[i]:off[i + 1]], c1)
+        np.testing.assert_allclose(flows[off[i]:off[i + 1]], f1, rtol=0, atol=1e-5)
+        if i % 9 == 0:
+            assert np.isnan(flows[off[i] + len(X) // 2]).all() and cnt[off[i] + len(X) // 2] == 0
