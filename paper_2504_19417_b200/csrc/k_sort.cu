@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "vkm_device.cuh"
 #include "vkm_kernels.cuh"
@@ -287,6 +288,104 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
   }
 }
 
+// ---------------------------------------------------------------------------
+// Counting sort (default): the histogram and run starts exist already
+// (k_prep + scan), so each event's slot is start[pixel] + a per-pixel atomic
+// cursor.  That scatter is stable only up to the order of the atomics; the
+// runs are then put back into event (= time) order, which is exactly the
+// stable pixel-major order of np.argsort(kind="stable") (encoder.py:255-257):
+//   k_runsort   one thread per pixel, insertion sort of runs <= 32 events;
+//               longer runs go to a list
+//   k_longsort  one CTA per listed run: bitonic sort (ascending-only network,
+//               so the virtual +inf padding never moves) in shared memory for
+//               runs <= 4096, in global memory beyond (pathological hot pixels)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_scatter(const int32_t* __restrict__ pix, const uint64_t* __restrict__ val,
+                                                 int64_t n, int64_t P, const int* __restrict__ start,
+                                                 int* __restrict__ cursor, uint64_t* __restrict__ val_s,
+                                                 int32_t* __restrict__ pix_s) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    const int p = __ldg(pix + e);
+    if (p >= P) continue;   // outside the sensor: no slot (slots [start[P], n) are never read)
+    const int slot = __ldg(start + p) + atomicAdd(cursor + p, 1);
+    val_s[slot] = __ldg(val + e);
+    pix_s[slot] = p;
+  }
+}
+
+constexpr int kShortRun = 32;
+constexpr int kSmemRun = 4096;
+
+__global__ void __launch_bounds__(256) k_runsort(const int* __restrict__ start, int64_t P,
+                                                 uint64_t* __restrict__ val_s, int* __restrict__ longlist,
+                                                 int* __restrict__ longcount) {
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < P; p += int64_t(gridDim.x) * blockDim.x) {
+    const int s = __ldg(start + p), L = __ldg(start + p + 1) - s;
+    if (L <= 1) continue;
+    if (L > kShortRun) {
+      longlist[atomicAdd(longcount, 1)] = int(p);
+      continue;
+    }
+    uint64_t* r = val_s + s;
+    for (int i = 1; i < L; ++i) {   // by event index (low 32 bits), unique within a run
+      const uint64_t v = r[i];
+      const uint32_t k = uint32_t(v);
+      int j = i - 1;
+      while (j >= 0 && uint32_t(r[j]) > k) {
+        r[j + 1] = r[j];
+        --j;
+      }
+      r[j + 1] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ void cas_slot(uint64_t& a, uint64_t& b) {
+  if (uint32_t(a) > uint32_t(b)) {
+    const uint64_t t = a;
+    a = b;
+    b = t;
+  }
+}
+
+__global__ void __launch_bounds__(512) k_longsort(const int* __restrict__ start, uint64_t* __restrict__ val_s,
+                                                  const int* __restrict__ longlist,
+                                                  const int* __restrict__ longcount) {
+  __shared__ uint64_t sm[kSmemRun];
+  const int nl = *longcount;
+  for (int li = blockIdx.x; li < nl; li += gridDim.x) {
+    const int p = longlist[li];
+    const int s = start[p], L = start[p + 1] - s;
+    int N = 1;
+    while (N < L) N <<= 1;
+    const bool in_smem = N <= kSmemRun;
+    uint64_t* a = in_smem ? sm : val_s + s;
+    if (in_smem)
+      for (int i = threadIdx.x; i < L; i += blockDim.x) sm[i] = val_s[s + i];
+    __syncthreads();
+    // bitonic sort, ascending-only form: merge stage k first compares i with
+    // its mirror in the 2k block, then half-cleaners; partners >= L are +inf
+    for (int k = 2; k <= N; k <<= 1) {
+      for (int i = threadIdx.x; i < N / 2; i += blockDim.x) {
+        const int lo = (i / (k / 2)) * k + (i % (k / 2));
+        const int hi = (i / (k / 2)) * k + k - 1 - (i % (k / 2));
+        if (hi < L) cas_slot(a[lo], a[hi]);
+      }
+      __syncthreads();
+      for (int j = k / 4; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < N / 2; i += blockDim.x) {
+          const int lo = (i / j) * 2 * j + (i % j), hi = lo + j;
+          if (hi < L) cas_slot(a[lo], a[hi]);
+        }
+        __syncthreads();
+      }
+    }
+    if (in_smem)
+      for (int i = threadIdx.x; i < L; i += blockDim.x) val_s[s + i] = sm[i];
+    __syncthreads();
+  }
+}
+
 namespace {
 int key_bits(int64_t P) {   // keys are in [0, P] (P = out-of-sensor)
   int b = 1;
@@ -323,7 +422,20 @@ int launch_sort_events(const double* ev, const SliceTab& st, double delta_t, int
   size_t scan_bytes = sb.temp_bytes;
   cub::DeviceScan::ExclusiveSum(sb.temp, scan_bytes, g.C, sb.start, int(P + 1), s);
   launches += 2;   // CUB: init + scan
-  if (n > 0) {
+  static const bool use_cub = [] {
+    const char* e = std::getenv("VKM_SORT");
+    return e && std::strcmp(e, "cub") == 0;
+  }();
+  if (n > 0 && !use_cub) {
+    cudaMemsetAsync(sb.cursor, 0, sizeof(int) * P, s);
+    cudaMemsetAsync(sb.longcount, 0, sizeof(int), s);
+    const int eb = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_scatter<<<eb, 256, 0, s>>>(sb.pix, sb.val, n, P, sb.start, sb.cursor, sb.val_s, sb.pix_s);
+    const int pb = int(std::min<int64_t>((P + 255) / 256, 148 * 16));
+    k_runsort<<<pb, 256, 0, s>>>(sb.start, P, sb.val_s, sb.longlist, sb.longcount);
+    k_longsort<<<148, 512, 0, s>>>(sb.start, sb.val_s, sb.longlist, sb.longcount);
+    launches += 3;
+  } else if (n > 0) {
     size_t sort_bytes = sb.sort_temp_bytes;
     cub::DeviceRadixSort::SortPairs(sb.sort_temp, sort_bytes, sb.pix, sb.pix_s, sb.val, sb.val_s, int(n), 0,
                                     key_bits(P), s);

@@ -160,11 +160,11 @@ int ensure_sort(vkm_handle* h, int64_t n, int64_t Pv) {
 // counts, pooled counts, run starts and the scan scratch.
 int ensure_grid(vkm_handle* h, int64_t Pv) {
   if (h->grid_cap >= Pv) return VKM_OK;
-  void* arrs[] = {h->G, h->Q, h->C, h->NQ, h->sb.start, h->sb.temp};
+  void* arrs[] = {h->G, h->Q, h->C, h->NQ, h->sb.start, h->sb.temp, h->sb.cursor, h->sb.longlist, h->sb.longcount};
   for (void* p : arrs)
     if (p) cudaFree(p);
   h->G = h->Q = nullptr;
-  h->C = h->NQ = h->sb.start = nullptr;
+  h->C = h->NQ = h->sb.start = h->sb.cursor = h->sb.longlist = h->sb.longcount = nullptr;
   h->sb.temp = nullptr;
   h->grid_cap = 0;
   VKM_CK(cudaMalloc(&h->G, sizeof(float2) * 8 * h->planes * Pv));
@@ -172,6 +172,9 @@ int ensure_grid(vkm_handle* h, int64_t Pv) {
   VKM_CK(cudaMalloc(&h->C, sizeof(int) * (Pv + 1)));
   VKM_CK(cudaMalloc(&h->NQ, sizeof(int) * Pv));
   VKM_CK(cudaMalloc(&h->sb.start, sizeof(int) * (Pv + 1)));
+  VKM_CK(cudaMalloc(&h->sb.cursor, sizeof(int) * (Pv + 1)));
+  VKM_CK(cudaMalloc(&h->sb.longlist, sizeof(int) * Pv));
+  VKM_CK(cudaMalloc(&h->sb.longcount, sizeof(int)));
   h->sb.temp_bytes = vkm::sort_scan_temp_bytes(Pv);
   VKM_CK(cudaMalloc(&h->sb.temp, std::max<size_t>(h->sb.temp_bytes, 16)));
   h->grid_cap = Pv;
@@ -499,7 +502,8 @@ void vkm_destroy(vkm_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->myp, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
                   h->G, h->C, h->Q, h->NQ, h->feats, h->cnt_scratch, h->ev_stage, h->out_stage, h->cnt_stage,
-                  h->sb.pix, h->sb.val, h->sb.start, h->sb.val_s, h->sb.pix_s, h->sb.temp, h->sb.sort_temp};
+                  h->sb.pix, h->sb.val, h->sb.start, h->sb.val_s, h->sb.pix_s, h->sb.temp, h->sb.sort_temp,
+                  h->sb.cursor, h->sb.longlist, h->sb.longcount};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->evt)

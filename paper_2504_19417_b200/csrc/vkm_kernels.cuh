@@ -51,6 +51,9 @@ struct SortBufs {
   size_t temp_bytes;
   void* sort_temp;   // CUB radix-sort scratch (grown with n)
   size_t sort_temp_bytes;
+  int* cursor;       // [P+1] per-pixel fill cursors of the counting scatter
+  int* longlist;     // [P]   pixels whose run is longer than one warp sort
+  int* longcount;    // [1]
 };
 
 // Slices processed by one launch sequence (batched fused path): slice b owns
