@@ -70,6 +70,10 @@ __global__ void __launch_bounds__(256) k_box_y(const float2* __restrict__ M, flo
 // Complex arithmetic runs on f32x2 pairs (re c, re c+1), (im c, im c+1).
 // blockIdx.y = slice * segs + segment (batched slices stack vertically, rows
 // never mix across slices); P is the plane stride (nb·W·H).
+#ifndef VKM_YU
+#define VKM_YU 4
+#endif
+constexpr int kYU = VKM_YU;   // rows per batched step of the packed y pass
 __global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ Rin, float4* __restrict__ Q, int W,
                                                      int H, int segs, int dy, int RS, int64_t P,
                                                      const float4* __restrict__ mxp,
@@ -102,11 +106,11 @@ __global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ 
     ar = fadd2(ar, v.x);
     ai = fadd2(ai, v.y);
   }
-  for (int y = y0; y < y1; y += kU) {
-    ulonglong2 lv[kU], tv[kU];
-    float4 fm[kU];
+  for (int y = y0; y < y1; y += kYU) {
+    ulonglong2 lv[kYU], tv[kYU];
+    float4 fm[kYU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < kYU; ++u) {
       const int yy = y + u;
       const bool ok = yy < y1;
       lv[u] = (ok && yy + dy < H) ? ld(Rp + int64_t(yy + dy) * rs, keep) : make_ulonglong2(0ull, 0ull);
@@ -114,7 +118,7 @@ __global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ 
       fm[u] = ok ? __ldg(myc + int64_t(yy) * D2) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < kYU; ++u) {
       if (y + u < y1) {
         ar = fadd2(ar, lv[u].x);
         ai = fadd2(ai, lv[u].y);
