@@ -61,6 +61,34 @@ __global__ void __launch_bounds__(256) k_prep(const double* __restrict__ ev, con
   }
 }
 
+// Host-packed events (vkm_predict_batch_host): the time argument arrives
+// precomputed, pixels as 16-bit coordinates.
+__global__ void __launch_bounds__(256) k_prep_packed(const uint2* __restrict__ evp, const SliceTab st, int W, int H,
+                                                     int32_t* __restrict__ pix_out, uint64_t* __restrict__ val_out,
+                                                     int* __restrict__ cnt, float* __restrict__ flows_invalid,
+                                                     int32_t* __restrict__ counts_invalid) {
+  const int P = W * H;
+  const int64_t n = st.off[st.nb];
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    int b = 0;
+    for (int step = kMaxBatch / 2; step > 0; step >>= 1)
+      if (b + step < st.nb && st.off[b + step] <= e) b += step;
+    const uint2 v = __ldg(evp + e);
+    const int xi = int(v.y & 0xFFFFu), yi = int(v.y >> 16);
+    int pix = st.nb * P;
+    if (xi < W && yi < H) {
+      pix = b * P + yi * W + xi;
+      atomicAdd(cnt + pix, 1);
+    } else {
+      if (flows_invalid)
+        reinterpret_cast<float2*>(flows_invalid)[e] = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+      if (counts_invalid) counts_invalid[e] = 0;
+    }
+    pix_out[e] = pix;
+    val_out[e] = slot_pack(int32_t(e), __uint_as_float(v.x));
+  }
+}
+
 // Raw grid, D8 == 64: a warp owns 32 consecutive pixels and their slot range;
 // slots are loaded 32 at a time (coalesced) and walked in order, lanes =
 // channel pairs.  Writes M[pixel] = (Σ e^{i a T}) · e^{i(x X/δx + y Y/δy)}.
@@ -408,15 +436,19 @@ size_t sort_pairs_temp_bytes(int64_t n, int64_t P) {
   return bytes;
 }
 
-int launch_sort_events(const double* ev, const SliceTab& st, double delta_t, int W, int H, const GridBufs& g,
-                       const SortBufs& sb, float* flows_invalid, int32_t* counts_invalid, cudaStream_t s) {
+int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st, double delta_t, int W, int H,
+                       const GridBufs& g, const SortBufs& sb, float* flows_invalid, int32_t* counts_invalid,
+                       cudaStream_t s) {
   const int64_t P = int64_t(W) * H * st.nb;
   const int64_t n = st.off[st.nb];
   int launches = 0;
   cudaMemsetAsync(g.C, 0, sizeof(int) * (P + 1), s);
   if (n > 0) {
     const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
-    k_prep<<<blocks, 256, 0, s>>>(ev, st, delta_t, W, H, sb.pix, sb.val, g.C, flows_invalid, counts_invalid);
+    if (packed)
+      k_prep_packed<<<blocks, 256, 0, s>>>(packed, st, W, H, sb.pix, sb.val, g.C, flows_invalid, counts_invalid);
+    else
+      k_prep<<<blocks, 256, 0, s>>>(ev, st, delta_t, W, H, sb.pix, sb.val, g.C, flows_invalid, counts_invalid);
     ++launches;
   }
   size_t scan_bytes = sb.temp_bytes;

@@ -7,6 +7,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <cstdint>
 #include <utility>
 #include <cmath>
@@ -55,6 +59,75 @@ int round_d8(int D) {
   while (d < D) d <<= 1;
   return d;
 }
+
+// Persistent host worker pool: packs host events into 8-byte records for the
+// pipelined host batch (the calling thread works too).
+class HostPool {
+ public:
+  explicit HostPool(int n) {
+    for (int i = 0; i < n; ++i) threads_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> l(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+  int size() const { return int(threads_.size()) + 1; }
+  void run(int parts, const std::function<void(int)>& fn) {
+    {
+      std::lock_guard<std::mutex> l(m_);
+      task_ = &fn;
+      total_ = parts;
+      next_ = 0;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> l(m_);
+    done_cv_.wait(l, [&] { return done_ == total_; });
+    task_ = nullptr;
+  }
+
+ private:
+  void work() {
+    for (;;) {
+      int i;
+      const std::function<void(int)>* fn;
+      {
+        std::lock_guard<std::mutex> l(m_);
+        if (!task_ || next_ >= total_) return;
+        i = next_++;
+        fn = task_;
+      }
+      (*fn)(i);
+      std::lock_guard<std::mutex> l(m_);
+      if (++done_ == total_) done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> l(m_);
+        cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* task_ = nullptr;
+  int total_ = 0, next_ = 0, done_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
 
 }  // namespace
 
@@ -107,6 +180,9 @@ struct vkm_handle {
   size_t pout_cap[2] = {0, 0};
   int32_t* pcnt[2] = {nullptr, nullptr};
   size_t pcnt_cap[2] = {0, 0};
+  uint2* hpack[2] = {nullptr, nullptr};   // page-locked packed-event staging (host)
+  size_t hpack_cap[2] = {0, 0};
+  HostPool* pool = nullptr;
   // timing
   bool profiling = false;
   cudaEvent_t evt[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -199,14 +275,14 @@ bool batchable(const vkm_handle* h) { return use_tc(h) && fused_ok(h); }
 // pre-modulated grid in G (parity hook, one slice); otherwise the pooled grid
 // ends in Q.  More than one slice requires the fused path.
 int encode_core(vkm_handle* h, const double* ev, const vkm::SliceTab& st, int pooled, cudaStream_t s, int* launches,
-                float* flows_invalid = nullptr, int32_t* counts_invalid = nullptr) {
+                float* flows_invalid = nullptr, int32_t* counts_invalid = nullptr, const uint2* packed = nullptr) {
   const int W = h->p.width, H = h->p.height, nb = st.nb;
   const int64_t n = st.off[nb], Pv = h->P * nb;
   int rc = ensure_grid(h, Pv);
   if (!rc) rc = ensure_sort(h, n, Pv);
   if (rc) return rc;
-  *launches += vkm::launch_sort_events(ev, st, h->p.delta_t, W, H, bufs(h), h->sb, flows_invalid, counts_invalid,
-                                       s);
+  *launches += vkm::launch_sort_events(ev, packed, st, h->p.delta_t, W, H, bufs(h), h->sb, flows_invalid,
+                                       counts_invalid, s);
   if (pooled && fused_ok(h)) {
     // x window fused into the reduction: R -> G, then y window + demodulation G -> Q
     vkm::launch_reduce_x(tables(h), W, H, nb, h->p.delta_x, h->sb, h->G, h->num_sms, s);
@@ -238,9 +314,10 @@ int encode_core(vkm_handle* h, const double* ev, const vkm::SliceTab& st, int po
 
 // Flows for the slices of st (one launch sequence).
 int predict_chunk(vkm_handle* h, const double* ev, const vkm::SliceTab& st, float* flows, int32_t* counts,
-                  cudaStream_t s, int* launches) {
+                  cudaStream_t s, int* launches, const uint2* packed = nullptr) {
   const bool tc = use_tc(h);
-  int rc = encode_core(h, ev, st, 1, s, launches, flows, counts);
+  if (packed && !tc) return fail(VKM_EINVAL, "internal: packed events need the tensor-core head");
+  int rc = encode_core(h, ev, st, 1, s, launches, flows, counts, packed);
   if (rc) return rc;
   const int64_t n = st.off[st.nb];
   if (n <= 0) return VKM_OK;
@@ -299,6 +376,43 @@ int next_chunk(const vkm_handle* h, const int64_t* offsets, int32_t n_slices, co
   }
   st.off[st.nb] = offsets[s] - base;
   return s;
+}
+
+// Pack the events of one chunk into 8-byte records (see launch_sort_events):
+// a = f32((t - t0)/δt) in f64 exactly like k_prep, x | y << 16, 0xFFFF... for
+// events that are not integer pixels inside the sensor.
+void pack_chunk(vkm_handle* h, const double* ev, const int64_t* offsets, const double* t_starts, int s0,
+                const vkm::SliceTab& st, uint2* out) {
+  const int64_t base = offsets[s0];
+  const double dt = h->p.delta_t;
+  const int W = h->p.width, H = h->p.height;
+  // the slice index of chunk slice b in the caller's numbering (empty slices were skipped)
+  std::vector<int> sidx(st.nb);
+  for (int s = s0, b = 0; b < st.nb; ++s)
+    if (offsets[s + 1] > offsets[s] && offsets[s] - base == st.off[b]) sidx[b++] = s;
+  const int64_t n = st.off[st.nb];
+  if (!h->pool) h->pool = new HostPool(std::max(0, std::min(15, int(std::thread::hardware_concurrency()) - 1)));
+  const int parts = std::max(1, std::min<int>(4 * h->pool->size(), int((n + 65535) / 65536)));
+  h->pool->run(parts, [&](int part) {
+    const int64_t lo = n * part / parts, hi = n * (part + 1) / parts;
+    int b = 0;
+    while (b + 1 < st.nb && st.off[b + 1] <= lo) ++b;
+    for (int64_t i = lo; i < hi; ++i) {
+      while (b + 1 < st.nb && st.off[b + 1] <= i) ++b;
+      const double* r = ev + 3 * (base + i);
+      const double t0 = (t_starts && !std::isnan(t_starts[sidx[b]])) ? t_starts[sidx[b]] : ev[3 * (base + st.off[b])];
+      const float a = float((r[0] - t0) / dt);
+      uint32_t ab;
+      std::memcpy(&ab, &a, 4);
+      uint32_t xy = 0xFFFFFFFFu;
+      const double x = r[1], y = r[2];
+      if (x >= 0.0 && x < W && y >= 0.0 && y < H) {
+        const int xi = int(x), yi = int(y);
+        if (double(xi) == x && double(yi) == y) xy = uint32_t(xi) | (uint32_t(yi) << 16);
+      }
+      out[i] = make_uint2(ab, xy);
+    }
+  });
 }
 
 int check_handle(const vkm_handle* h) {
@@ -514,6 +628,9 @@ void vkm_destroy(vkm_handle* h) {
     for (cudaEvent_t e : {h->in_ready[i], h->computed[i], h->out_done[i]})
       if (e) cudaEventDestroy(e);
   }
+  for (int i = 0; i < 2; ++i)
+    if (h->hpack[i]) cudaFreeHost(h->hpack[i]);
+  delete h->pool;
   if (h->s_in) cudaStreamSynchronize(h->s_in), cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamSynchronize(h->s_out), cudaStreamDestroy(h->s_out);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -687,20 +804,48 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
     if (!rc && counts_host) rc = grow(&h->pcnt[i], &h->pcnt_cap[i], size_t(nmax));
     if (rc) return rc;
   }
+  // Host packing (VKM_HOST_PACK=1): 8 instead of 24 bytes per event over PCIe;
+  // the host threads pack chunk c+1 while the GPU runs chunk c.  Needs the
+  // tensor-core head and 16-bit pixel coordinates.  Off by default: on the
+  // B200 boxes measured (16 host threads) packing ran at ~1.2e9 events/s,
+  // below the PCIe-bound 1.6e9 of shipping the f64 rows.
+  static const bool pack_env = [] {
+    const char* e = std::getenv("VKM_HOST_PACK");
+    return e && e[0] == '1';
+  }();
+  const bool pack = pack_env && batchable(h) && h->p.width < 65535 && h->p.height < 65535;
+  if (pack)
+    for (int i = 0; i < 2; ++i)
+      if (h->hpack_cap[i] < size_t(nmax)) {
+        if (h->hpack[i]) cudaFreeHost(h->hpack[i]);
+        h->hpack[i] = nullptr;
+        h->hpack_cap[i] = 0;
+        VKM_CK(cudaHostAlloc(&h->hpack[i], sizeof(uint2) * size_t(std::max<int64_t>(nmax, 1)), cudaHostAllocDefault));
+        h->hpack_cap[i] = size_t(nmax);
+      }
   cudaStream_t sc = h->stream;
   // slot k = chunk % 2.  copy-in(c) waits until compute(c-2) stopped reading the
-  // slot; compute(c) waits for copy-in(c) and for copy-out(c-2) to drain its output.
+  // slot; compute(c) waits for copy-in(c) and for copy-out(c-2) to drain its output;
+  // packing chunk c waits until copy-in(c-2) has drained the host staging slot.
   int launches = 0;
   for (size_t c = 0; c < chunks.size(); ++c) {
     const vkm::SliceTab& st = chunks[c].second;
     const int64_t lo = offsets[chunks[c].first], n = st.off[st.nb];
     const int k = int(c & 1);
+    if (pack) {
+      if (c >= 2) VKM_CK(cudaEventSynchronize(h->in_ready[k]));
+      pack_chunk(h, ev_host, offsets, t_starts, chunks[c].first, st, h->hpack[k]);
+    }
     if (c >= 2) VKM_CK(cudaStreamWaitEvent(h->s_in, h->computed[k], 0));
-    VKM_CK(cudaMemcpyAsync(h->pev[k], ev_host + 3 * lo, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, h->s_in));
+    if (pack)
+      VKM_CK(cudaMemcpyAsync(h->pev[k], h->hpack[k], sizeof(uint2) * n, cudaMemcpyHostToDevice, h->s_in));
+    else
+      VKM_CK(cudaMemcpyAsync(h->pev[k], ev_host + 3 * lo, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, h->s_in));
     VKM_CK(cudaEventRecord(h->in_ready[k], h->s_in));
     VKM_CK(cudaStreamWaitEvent(sc, h->in_ready[k], 0));
     if (c >= 2) VKM_CK(cudaStreamWaitEvent(sc, h->out_done[k], 0));
-    int rc = predict_chunk(h, h->pev[k], st, h->pout[k], counts_host ? h->pcnt[k] : nullptr, sc, &launches);
+    int rc = predict_chunk(h, h->pev[k], st, h->pout[k], counts_host ? h->pcnt[k] : nullptr, sc, &launches,
+                           pack ? reinterpret_cast<const uint2*>(h->pev[k]) : nullptr);
     if (rc) return rc;
     VKM_CK(cudaEventRecord(h->computed[k], sc));
     VKM_CK(cudaStreamWaitEvent(h->s_out, h->computed[k], 0));

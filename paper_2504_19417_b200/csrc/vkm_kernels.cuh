@@ -77,9 +77,14 @@ struct MlpDev {
 
 // K1 (sorted): prep + scan + stable radix sort of (pixel, slot_pack) pairs.
 // Returns the number of kernel launches.  C must hold P+1 ints.
-// Keys live in [0, nb·W·H]; nb·W·H + 1 counters in g.C.
-int launch_sort_events(const double* ev, const SliceTab& st, double delta_t, int W, int H, const GridBufs& g,
-                       const SortBufs& sb, float* flows_invalid, int32_t* counts_invalid, cudaStream_t s);
+// Keys live in [0, nb·W·H]; nb·W·H + 1 counters in g.C.  Events are either
+// the reference's (n, 3) f64 rows (ev) or host-packed 8-byte records
+// (packed != null): .x = f32 bits of a = f32((t - t0)/δt) computed on the host
+// in f64 exactly like the device, .y = x | y << 16 (0xFFFF: not an in-sensor
+// integer pixel).
+int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st, double delta_t, int W, int H,
+                       const GridBufs& g, const SortBufs& sb, float* flows_invalid, int32_t* counts_invalid,
+                       cudaStream_t s);
 // K1 reduce, raw grid: per-pixel time-ordered sums, written pre-modulated
 // (M = G·e^{i(xX/δx + yY/δy)}) to g.G.  Used by the split pooling path and the
 // raw-grid parity hook.

@@ -403,3 +403,54 @@ def test_counting_sort_matches_radix_sort_with_hot_pixels():
                      fr, 0.016)
     np.testing.assert_array_equal(c, c1[q])
     np.testing.assert_allclose(f1[q], vo.mlp(w.w1, w.b1, w.w2, w.b2, vo.to_features(emb)), rtol=0, atol=1e-4)
+
+
+def test_host_batch_packing_edge_cases():
+    """vkm_predict_batch_host with host packing (VKM_HOST_PACK=1: f32 time
+    argument + 16-bit pixel coordinates packed on host threads): out-of-sensor
+    and non-integer pixels become NaN rows with count 0, explicit and NaN
+    t_starts, and the packed path matches the default f64-row path (fresh
+    process) bitwise."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    if os.environ.get("VKM_HOST_PACK") != "1":   # the switch is read once per process: rerun this test packed
+        out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                              os.path.abspath(__file__) + "::test_host_batch_packing_edge_cases"],
+                             env=dict(os.environ, VKM_HOST_PACK="1"), capture_output=True, text=True, timeout=600,
+                             cwd=os.path.dirname(os.path.abspath(__file__)))
+        assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+        return
+    pkg = _pkg()
+    W, H = 200, 120
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    eng = pkg.FlowEngine(W, H, 10, 10, 0.016, b, w)
+    slices = [vo.synth_uniform_noise(n, W, H, seed=300 + n) for n in (5000, 1, 40000, 7000)]
+    slices[2][10, 1] = W          # outside
+    slices[2][11, 2] = 3.5        # not an integer pixel
+    slices[3][0, 0] += 0.0        # first event defines t0 when t_start is NaN
+    ev = np.ascontiguousarray(np.concatenate(slices))
+    off = np.cumsum([0] + [len(s) for s in slices])
+    ts = [float(slices[0][0, 0]), math.nan, float(slices[2][0, 0]), math.nan]
+    flows, counts = eng.predict_batch_host(ev, off, ts, return_counts=True)
+    bad = off[2] + np.array([10, 11])
+    assert np.isnan(flows[bad]).all() and (counts[bad] == 0).all()
+    good = np.setdiff1d(np.arange(len(ev)), bad)
+    assert np.isfinite(flows[good]).all() and (counts[good] > 0).all()
+    with tempfile.TemporaryDirectory() as td:
+        np.save(os.path.join(td, "ev.npy"), ev)
+        code = (
+            "import sys, math, numpy as np; sys.path.insert(0, %r); import paper_2504_19417_b200 as pkg;"
+            "ev = np.load(%r); b = pkg.generate_bases(64); w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32);"
+            "e = pkg.FlowEngine(%d, %d, 10, 10, 0.016, b, w);"
+            "f, c = e.predict_batch_host(ev, %r, %r, return_counts=True); np.save(%r, f); np.save(%r, c)"
+        ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.join(td, "ev.npy"), W, H,
+             [int(v) for v in off], ts, os.path.join(td, "f.npy"), os.path.join(td, "c.npy"))
+        code = code.replace("nan", "math.nan")
+        out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, VKM_HOST_PACK="0"),
+                             capture_output=True, text=True, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        np.testing.assert_array_equal(np.load(os.path.join(td, "c.npy")), counts)
+        np.testing.assert_array_equal(np.load(os.path.join(td, "f.npy")), flows)
