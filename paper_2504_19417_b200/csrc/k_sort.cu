@@ -341,30 +341,49 @@ __global__ void __launch_bounds__(256) k_scatter(const int32_t* __restrict__ pix
   }
 }
 
-constexpr int kShortRun = 32;
+constexpr int kShortRun = 256;   // runs up to this length: one thread, insertion sort
 constexpr int kSmemRun = 4096;
 
-__global__ void __launch_bounds__(256) k_runsort(const int* __restrict__ start, int64_t P,
+// A block owns ppb consecutive pixels per step, i.e. one contiguous slot range:
+// it is staged through shared memory (coalesced in and out) when it fits, and
+// each thread insertion-sorts its pixel's run there by event index.  ppb is
+// chosen on the host from the mean run length so the range usually fits.
+constexpr int kRunsortStage = 3072;   // slots staged per block (24 KB)
+
+__global__ void __launch_bounds__(256) k_runsort(const int* __restrict__ start, int64_t P, int ppb,
                                                  uint64_t* __restrict__ val_s, int* __restrict__ longlist,
                                                  int* __restrict__ longcount) {
-  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < P; p += int64_t(gridDim.x) * blockDim.x) {
-    const int s = __ldg(start + p), L = __ldg(start + p + 1) - s;
-    if (L <= 1) continue;
-    if (L > kShortRun) {
-      longlist[atomicAdd(longcount, 1)] = int(p);
-      continue;
-    }
-    uint64_t* r = val_s + s;
-    for (int i = 1; i < L; ++i) {   // by event index (low 32 bits), unique within a run
-      const uint64_t v = r[i];
-      const uint32_t k = uint32_t(v);
-      int j = i - 1;
-      while (j >= 0 && uint32_t(r[j]) > k) {
-        r[j + 1] = r[j];
-        --j;
+  __shared__ uint64_t stage[kRunsortStage];
+  for (int64_t p0 = int64_t(blockIdx.x) * ppb; p0 < P; p0 += int64_t(gridDim.x) * ppb) {
+    const int64_t p = p0 + threadIdx.x;
+    const int64_t pe = min(P, p0 + int64_t(ppb));
+    const int b0 = __ldg(start + p0), b1 = __ldg(start + pe);
+    const bool staged = b1 - b0 <= kRunsortStage;
+    if (staged)
+      for (int i = threadIdx.x; i < b1 - b0; i += blockDim.x) stage[i] = val_s[b0 + i];
+    __syncthreads();
+    if (threadIdx.x < ppb && p < P) {
+      const int s = __ldg(start + p), L = __ldg(start + p + 1) - s;
+      if (L > kShortRun) {
+        longlist[atomicAdd(longcount, 1)] = int(p);
+      } else if (L > 1) {
+        uint64_t* r = staged ? stage + (s - b0) : val_s + s;
+        for (int i = 1; i < L; ++i) {   // by event index (low 32 bits), unique within a run
+          const uint64_t v = r[i];
+          const uint32_t k = uint32_t(v);
+          int j = i - 1;
+          while (j >= 0 && uint32_t(r[j]) > k) {
+            r[j + 1] = r[j];
+            --j;
+          }
+          r[j + 1] = v;
+        }
       }
-      r[j + 1] = v;
     }
+    __syncthreads();
+    if (staged)
+      for (int i = threadIdx.x; i < b1 - b0; i += blockDim.x) val_s[b0 + i] = stage[i];
+    __syncthreads();
   }
 }
 
@@ -458,13 +477,21 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
     const char* e = std::getenv("VKM_SORT");
     return e && std::strcmp(e, "cub") == 0;
   }();
-  if (n > 0 && !use_cub) {
+  // Counting scatter for sparse-to-moderate slices; dense slices (mean run >
+  // 8 events, e.g. config 5 at 35 events/pixel) sort faster with CUB's
+  // bandwidth-bound onesweep passes (cfg5 K1 3.7 ms vs 6.0 ms).
+  const bool counting = !use_cub && double(n) <= 8.0 * double(P);
+  if (n > 0 && counting) {
     cudaMemsetAsync(sb.cursor, 0, sizeof(int) * P, s);
     cudaMemsetAsync(sb.longcount, 0, sizeof(int), s);
     const int eb = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
     k_scatter<<<eb, 256, 0, s>>>(sb.pix, sb.val, n, P, sb.start, sb.cursor, sb.val_s, sb.pix_s);
-    const int pb = int(std::min<int64_t>((P + 255) / 256, 148 * 16));
-    k_runsort<<<pb, 256, 0, s>>>(sb.start, P, sb.val_s, sb.longlist, sb.longcount);
+    // pixels per runsort block step: ~2000 expected slots (fits the stage), 16..256 pixels
+    const double mean_run = double(n) / double(std::max<int64_t>(P, 1));
+    int ppb = 256;
+    while (ppb > 16 && ppb * mean_run > 2000.0) ppb >>= 1;
+    const int pb = int(std::min<int64_t>((P + ppb - 1) / ppb, 148 * 16));
+    k_runsort<<<pb, 256, 0, s>>>(sb.start, P, ppb, sb.val_s, sb.longlist, sb.longcount);
     k_longsort<<<148, 512, 0, s>>>(sb.start, sb.val_s, sb.longlist, sb.longcount);
     launches += 3;
   } else if (n > 0) {
