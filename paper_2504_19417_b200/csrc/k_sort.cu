@@ -207,9 +207,9 @@ __global__ void __launch_bounds__(256) k_reduce_small(const int* __restrict__ st
 constexpr int kMaxFusedDx = 24;
 constexpr int kRxWarps = 2;
 constexpr int kRxMaxSeg = 128;
-constexpr int kRxEnds = kRxMaxSeg + 2 * kMaxFusedDx + 4;   // run ends of one segment sweep (+ sentinel)
+constexpr int kRxEnds = kRxMaxSeg + 2 * kMaxFusedDx + 4 + 64;   // run ends of one sweep (+ sentinel) + 64-float stage
 #ifndef VKM_RX_GROUP
-#define VKM_RX_GROUP 4
+#define VKM_RX_GROUP 4   // k_reduce_x1 assumes 4 (one float4 of time arguments per group)
 #endif
 constexpr int kRxGroup = VKM_RX_GROUP;   // events per sin/cos group (divides 32)
 
@@ -433,6 +433,118 @@ __global__ void __launch_bounds__(512) k_longsort(const int* __restrict__ start,
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_reduce_x1: the same computation with one channel per lane and two warps
+// per (row, segment) item (channels 0-31 and 32-63).  Each lane packs two
+// consecutive events of its channel into one f32x2 sin/cos and adds them in
+// slot order, so sums keep the reference's order.  Same instruction count as
+// k_reduce_x, half the shared memory per warp (the ring holds one complex per
+// lane) and twice the warps, i.e. twice the latency hiding.
+// ---------------------------------------------------------------------------
+constexpr int kRx1Warps = 4;   // two items per block
+size_t reduce_x1_smem(int dx) { return size_t(kRx1Warps) * ((2 * dx + 1) * 256 + kRxEnds * 4); }
+
+__global__ void __launch_bounds__(kRx1Warps * 32) k_reduce_x1(const int* __restrict__ start,
+                                                              const uint64_t* __restrict__ val_s,
+                                                              const float* __restrict__ tf,
+                                                              const float2* __restrict__ mx,
+                                                              const float2* __restrict__ my, int W, int H, int nb,
+                                                              int dx, int S, int nseg, int64_t P,
+                                                              float2* __restrict__ R) {
+  extern __shared__ __align__(16) uint8_t rx_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int half = wib & 1;                        // channel half of this warp
+  const int c = half * 32 + lane;                  // this lane's channel
+  const int RL = 2 * dx + 1;
+  float2* const ring0 = reinterpret_cast<float2*>(rx_smem) + wib * RL * 32 + lane;
+  float2* const ring_end = ring0 + RL * 32;
+  int* const ends = reinterpret_cast<int*>(rx_smem + size_t(kRx1Warps) * RL * 256) + wib * kRxEnds;
+  const float Tc = __ldg(tf + c);
+  const uint64_t TT = f2pack(Tc, Tc);
+  const float2* mxc = mx + c;                      // mxc[x * 64]
+  // packed-pair output position of channel c inside a pixel's 64-B plane chunk
+  float* const Rf = reinterpret_cast<float*>(R) + int64_t(c >> 3) * P * 16 + ((c & 7) >> 1) * 4 + (c & 1);
+  const int64_t items = int64_t(nb) * H * nseg;
+  const int64_t nwarp_items = int64_t(gridDim.x) * (kRx1Warps / 2);
+  for (int64_t it = int64_t(blockIdx.x) * (kRx1Warps / 2) + (wib >> 1); it < items; it += nwarp_items) {
+    const int y = int(it / nseg);
+    const int x0 = int(it - int64_t(y) * nseg) * S, x1 = min(W, x0 + S);
+    const int xs = x0 - dx, nx = x1 + dx - xs;
+    const int* st = start + int64_t(y) * W;
+    const int jfirst = __ldg(st + max(0, xs)), jend = __ldg(st + min(W, x1 + dx));
+    __syncwarp();
+    for (int k = lane; k <= nx; k += 32) {
+      const int x = xs + k;
+      ends[k] = k == nx ? jend : (x < 0 ? jfirst : (x < W ? __ldg(st + x + 1) : jend));
+    }
+    for (int k = 0; k < RL; ++k) ring0[k * 32] = make_float2(0.f, 0.f);
+    __syncwarp();
+    const float2 fy = __ldg(my + int64_t(y % H) * 64 + c);
+    float* out = Rf + (int64_t(y) * W + x0) * 16;
+    // time arguments of the item's slots, staged 32 at a time in shared memory
+    // (one LDS.128 broadcast per group of 4 events instead of 4 shuffles)
+    float* const abuf = reinterpret_cast<float*>(ends + kRxEnds - 64);   // 2 x 32 floats at the end of ends[]
+    auto ld_a = [&](int jj) { return jj < jend ? slot_arg(__ldg(val_s + jj)) : 0.f; };
+    int jb = jfirst;
+    float av1 = ld_a(jb + 32 + lane);
+    abuf[lane] = ld_a(jb + lane);
+    __syncwarp();
+
+    int k = 0;
+    int je = ends[0];
+    float2 mc = __ldg(mxc + int64_t(min(max(xs, 0), W - 1)) * 64);
+    uint64_t g = 0;                                  // packed (re, im) sum of the current pixel
+    float ar = 0.f, ai = 0.f;
+    float2* pn = ring0;
+    float2* po = ring0 + 32;
+    auto finish = [&]() {
+      float gr, gi;
+      f2unpack(g, gr, gi);
+      const float mr = fmaf(gr, mc.x, -gi * mc.y), mi = fmaf(gr, mc.y, gi * mc.x);
+      const float2 old = *po;
+      *pn = make_float2(mr, mi);
+      ar += mr;
+      ai += mi;
+      if (k >= 2 * dx) {
+        out[0] = fmaf(ar, fy.x, -ai * fy.y);
+        out[2] = fmaf(ar, fy.y, ai * fy.x);
+        out += 16;
+      }
+      ar -= old.x;
+      ai -= old.y;
+      g = 0;
+      pn = po;
+      po = (po + 32 == ring_end) ? ring0 : po + 32;
+      ++k;
+      je = ends[k];
+      mc = __ldg(mxc + int64_t(min(max(xs + k, 0), W - 1)) * 64);
+    };
+
+    for (int j = jfirst; j < jend; j += kRxGroup) {
+      if (j - jb >= 32) {
+        jb += 32;
+        __syncwarp();
+        abuf[lane] = av1;
+        __syncwarp();
+        av1 = ld_a(jb + 32 + lane);
+      }
+      const float4 a4 = *reinterpret_cast<const float4*>(abuf + (j - jb));
+      uint64_t cs[kRxGroup];
+      VKM_SINCOS_CS(fmul2(f2pack(a4.x, a4.y), TT), cs[0], cs[1]);
+      VKM_SINCOS_CS(fmul2(f2pack(a4.z, a4.w), TT), cs[2], cs[3]);
+#pragma unroll
+      for (int u = 0; u < kRxGroup; ++u) {
+        if (j + u >= je) {
+          if (j + u >= jend) break;
+          do finish(); while (j + u >= je);
+        }
+        g = fadd2(g, cs[u]);
+      }
+    }
+    while (k < nx) finish();
+  }
+}
+
 namespace {
 int key_bits(int64_t P) {   // keys are in [0, P] (P = out-of-sensor)
   int b = 1;
@@ -534,6 +646,34 @@ bool reduce_x_supported(int D8, int dx) { return D8 == 64 && dx >= 1 && dx <= kM
 void launch_reduce_x(const DevTables& tb, int W, int H, int nb, int dx, const SortBufs& sb, float2* R,
                      int num_sms, cudaStream_t s) {
   const int64_t P = int64_t(W) * H * nb;
+  static const int variant_env = [] {
+    const char* e = std::getenv("VKM_RX");
+    return e ? std::atoi(e) : -1;
+  }();
+  // k_reduce_x1 issues ~35 % more instructions but runs twice the warps: it
+  // wins where the (2δx+1)-pixel ring limits occupancy (cfg3, δ = 20: -3.6 %),
+  // loses slightly at δ = 10 (cfg2: +2 %).
+  const int variant = variant_env >= 0 ? variant_env : (dx >= 16 ? 1 : 0);
+  if (variant == 1) {   // one channel per lane, two warps per item
+    const size_t smem = reduce_x1_smem(dx);
+    static bool attr1 = false;
+    if (!attr1) {
+      cudaFuncSetAttribute(k_reduce_x1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(reduce_x1_smem(kMaxFusedDx)));
+      attr1 = true;
+    }
+    int per = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reduce_x1, kRx1Warps * 32, smem);
+    const int64_t res_items = int64_t(std::max(1, per)) * num_sms * (kRx1Warps / 2);
+    int S = kRxMaxSeg;
+    while (S > 32 && 4 * int64_t(H) * nb * ((W + S - 1) / S) < 3 * res_items) S >>= 1;
+    const int nseg = (W + S - 1) / S;
+    const int64_t items = int64_t(H) * nb * nseg;
+    const int blocks = int(std::min<int64_t>((items + 1) / 2, res_items / 2));
+    k_reduce_x1<<<blocks, kRx1Warps * 32, smem, s>>>(sb.start, sb.val_s, tb.tf, tb.mx, tb.my, W, H, nb, dx, S, nseg,
+                                                     P, R);
+    return;
+  }
   const size_t smem = reduce_x_smem(dx);
   static bool attr = false;
   if (!attr) {

@@ -150,6 +150,17 @@ __device__ __forceinline__ void sincos2p_pi(uint64_t x, uint64_t& s01, uint64_t&
   c01 = cr ^ sgn;
 }
 
+// theta = (x0, x1) -> (cos x0, sin x0), (cos x1, sin x1): the quadrant
+// fix-up writes scalars anyway, so pairing each argument's cos and sin costs
+// nothing and lets a complex accumulator (re, im) add them with one add.f32x2.
+__device__ __forceinline__ void sincos2_cs(uint64_t theta, uint64_t& cs0, uint64_t& cs1) {
+  float x0, x1, s0, c0, s1, c1;
+  f2unpack(theta, x0, x1);
+  sincos2_f32(x0, x1, s0, c0, s1, c1);
+  cs0 = f2pack(c0, s0);
+  cs1 = f2pack(c1, s1);
+}
+
 // Packed-in/packed-out variant: theta = (x0, x1), returns (s0, s1), (c0, c1).
 __device__ __forceinline__ void sincos2p_f32(uint64_t theta, uint64_t& s01, uint64_t& c01) {
   float x0, x1, s0, c0, s1, c1;
@@ -169,6 +180,7 @@ __device__ __forceinline__ void sincos2p_f32(uint64_t theta, uint64_t& s01, uint
 #else
 #define VKM_SINCOS_HOT sincos2p_f32
 #endif
+#define VKM_SINCOS_CS sincos2_cs
 
 // a = f32((t - t0) / delta_t): f64 rebase and divide, then one rounding to f32,
 // exactly as rebase_slice (events.py:390-407) + _temporal_phases
