@@ -205,17 +205,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kRows = kM / kProdWarps;        // 8
     const uint32_t lane_chunk = uint32_t(lane >> 2), lane_byte = uint32_t(lane & 3) * 4;
     // lanes 0..7 hold the metadata of the warp's 8 rows
-    auto load_meta = [&](int64_t tl, float& a, int& pix, float& rs) {
+    // Slot metadata is pipelined over three tiles so no load is consumed right
+    // after it issues: (pixel, time argument) two tiles ahead, the pooled count
+    // NQ[pixel] one tile ahead (it depends on the pixel), 1/count on use.
+    auto load_slot = [&](int64_t tl, float& a, int& pix) {
       const int64_t slot = tl * kM + warp * kRows + (lane & (kRows - 1));
       a = 0.f;
       pix = -1;
-      rs = 0.f;
       if (tl < ntiles && slot < nv) {
         pix = __ldg(pix_s + slot);
         a = slot_arg(__ldg(val_s + slot));
-        const int cnt = __ldg(NQ + pix);
-        rs = cnt > 0 ? __frcp_rn(float(cnt)) * f_scale : 0.f;   // ÷count folded with the fp16 pre-scale
       }
+    };
+    auto load_cnt = [&](int pix) { return pix >= 0 ? __ldg(NQ + pix) : 0; };
+    auto recip = [&](int cnt) {   // ÷count folded with the fp16 pre-scale
+      return cnt > 0 ? __frcp_rn(float(cnt)) * f_scale : 0.f;
     };
     // One thread prefetches the pooled-grid rows of a future tile into L2
     // with bulk (TMA-engine) prefetches: the tile's pixel range x 8 planes.
@@ -289,10 +293,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
 
     const int64_t G = gridDim.x;
-    float a_c, a_n, rs_c, rs_n;
-    int pix_c, pix_n;
-    load_meta(blockIdx.x, a_c, pix_c, rs_c);
-    load_meta(int64_t(blockIdx.x) + G, a_n, pix_n, rs_n);
+    float a_c, a_n, a_nn, rs_c;
+    int pix_c, pix_n, pix_nn, cnt_n;
+    load_slot(blockIdx.x, a_c, pix_c);
+    load_slot(int64_t(blockIdx.x) + G, a_n, pix_n);
+    load_slot(int64_t(blockIdx.x) + 2 * G, a_nn, pix_nn);
+    rs_c = recip(load_cnt(pix_c));
+    cnt_n = load_cnt(pix_n);
     prefetch_l2(blockIdx.x);
     prefetch_l2(int64_t(blockIdx.x) + G);
 #pragma unroll
@@ -308,8 +315,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&S.full[s]);
       a_c = a_n;
       pix_c = pix_n;
-      rs_c = rs_n;
-      load_meta(tile + 2 * G, a_n, pix_n, rs_n);
+      rs_c = recip(cnt_n);
+      a_n = a_nn;
+      pix_n = pix_nn;
+      cnt_n = load_cnt(pix_nn);
+      load_slot(tile + 3 * G, a_nn, pix_nn);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp < kProdWarps + 4) {
