@@ -352,7 +352,7 @@ constexpr int kRunsortStage = 3072;   // slots staged per block (24 KB)
 
 __global__ void __launch_bounds__(256) k_runsort(const int* __restrict__ start, int64_t P, int ppb,
                                                  uint64_t* __restrict__ val_s, int* __restrict__ longlist,
-                                                 int* __restrict__ longcount) {
+                                                 int* __restrict__ longcount, int* __restrict__ cursor) {
   __shared__ uint64_t stage[kRunsortStage];
   for (int64_t p0 = int64_t(blockIdx.x) * ppb; p0 < P; p0 += int64_t(gridDim.x) * ppb) {
     const int64_t p = p0 + threadIdx.x;
@@ -363,6 +363,7 @@ __global__ void __launch_bounds__(256) k_runsort(const int* __restrict__ start, 
       for (int i = threadIdx.x; i < b1 - b0; i += blockDim.x) stage[i] = val_s[b0 + i];
     __syncthreads();
     if (threadIdx.x < ppb && p < P) {
+      cursor[p] = 0;   // ready for the next call's scatter (saves a memset)
       const int s = __ldg(start + p), L = __ldg(start + p + 1) - s;
       if (L > kShortRun) {
         longlist[atomicAdd(longcount, 1)] = int(p);
@@ -594,8 +595,7 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
   // bandwidth-bound onesweep passes (cfg5 K1 3.7 ms vs 6.0 ms).
   const bool counting = !use_cub && double(n) <= 8.0 * double(P);
   if (n > 0 && counting) {
-    cudaMemsetAsync(sb.cursor, 0, sizeof(int) * P, s);
-    cudaMemsetAsync(sb.longcount, 0, sizeof(int), s);
+    cudaMemsetAsync(sb.longcount, 0, sizeof(int), s);   // sb.cursor is zero (allocation, then k_runsort)
     const int eb = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
     k_scatter<<<eb, 256, 0, s>>>(sb.pix, sb.val, n, P, sb.start, sb.cursor, sb.val_s, sb.pix_s);
     // pixels per runsort block step: ~2000 expected slots (fits the stage), 16..256 pixels
@@ -603,7 +603,7 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
     int ppb = 256;
     while (ppb > 16 && ppb * mean_run > 2000.0) ppb >>= 1;
     const int pb = int(std::min<int64_t>((P + ppb - 1) / ppb, 148 * 16));
-    k_runsort<<<pb, 256, 0, s>>>(sb.start, P, ppb, sb.val_s, sb.longlist, sb.longcount);
+    k_runsort<<<pb, 256, 0, s>>>(sb.start, P, ppb, sb.val_s, sb.longlist, sb.longcount, sb.cursor);
     k_longsort<<<148, 512, 0, s>>>(sb.start, sb.val_s, sb.longlist, sb.longcount);
     launches += 3;
   } else if (n > 0) {

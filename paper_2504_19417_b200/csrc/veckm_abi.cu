@@ -186,6 +186,9 @@ struct vkm_handle {
   // timing
   bool profiling = false;
   cudaEvent_t evt[4] = {nullptr, nullptr, nullptr, nullptr};
+  // side stream: the count pooling overlaps k_reduce_x (it only needs the counts)
+  cudaStream_t s_side = nullptr;
+  cudaEvent_t e_fork = nullptr, e_join = nullptr;
   bool have_timing = false;
   int last_launches = 0;
 };
@@ -249,6 +252,7 @@ int ensure_grid(vkm_handle* h, int64_t Pv) {
   VKM_CK(cudaMalloc(&h->NQ, sizeof(int) * Pv));
   VKM_CK(cudaMalloc(&h->sb.start, sizeof(int) * (Pv + 1)));
   VKM_CK(cudaMalloc(&h->sb.cursor, sizeof(int) * (Pv + 1)));
+  VKM_CK(cudaMemset(h->sb.cursor, 0, sizeof(int) * (Pv + 1)));   // k_runsort re-zeroes it after each use
   VKM_CK(cudaMalloc(&h->sb.longlist, sizeof(int) * Pv));
   VKM_CK(cudaMalloc(&h->sb.longcount, sizeof(int)));
   h->sb.temp_bytes = vkm::sort_scan_temp_bytes(Pv);
@@ -284,13 +288,19 @@ int encode_core(vkm_handle* h, const double* ev, const vkm::SliceTab& st, int po
   *launches += vkm::launch_sort_events(ev, packed, st, h->p.delta_t, W, H, bufs(h), h->sb, flows_invalid,
                                        counts_invalid, s);
   if (pooled && fused_ok(h)) {
-    // x window fused into the reduction: R -> G, then y window + demodulation G -> Q
+    // count pooling on the side stream (needs only the counts), overlapping
+    // the reduction; x window fused into the reduction: R -> G, then y window
+    // + demodulation G -> Q; join before the head reads NQ
+    VKM_CK(cudaEventRecord(h->e_fork, s));
+    VKM_CK(cudaStreamWaitEvent(h->s_side, h->e_fork, 0));
+    vkm::launch_pool_count(W, H, nb, h->p.delta_x, h->p.delta_y, bufs(h), h->s_side);
+    VKM_CK(cudaEventRecord(h->e_join, h->s_side));
     vkm::launch_reduce_x(tables(h), W, H, nb, h->p.delta_x, h->sb, h->G, h->num_sms, s);
     *launches += 1;
     VKM_CK(cudaGetLastError());
     rec(h, 1, s);
     vkm::launch_pool_y_demod(tables(h), W, H, nb, h->D8, h->p.delta_y, h->G, h->Q, s);
-    vkm::launch_pool_count(W, H, nb, h->p.delta_x, h->p.delta_y, bufs(h), s);
+    VKM_CK(cudaStreamWaitEvent(s, h->e_join, 0));
     *launches += 2;
     VKM_CK(cudaGetLastError());
   } else {
@@ -509,6 +519,9 @@ int vkm_create(vkm_handle** out, const vkm_params* params, const double* T, cons
   } while (0)
 
   VKM_CKH(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  VKM_CKH(cudaStreamCreateWithFlags(&h->s_side, cudaStreamNonBlocking));
+  VKM_CKH(cudaEventCreateWithFlags(&h->e_fork, cudaEventDisableTiming));
+  VKM_CKH(cudaEventCreateWithFlags(&h->e_join, cudaEventDisableTiming));
   for (auto& e : h->evt) VKM_CKH(cudaEventCreate(&e));
 
   // Frequency tables.  Modulation factors are computed in f64 and rounded once
@@ -633,6 +646,9 @@ void vkm_destroy(vkm_handle* h) {
   delete h->pool;
   if (h->s_in) cudaStreamSynchronize(h->s_in), cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamSynchronize(h->s_out), cudaStreamDestroy(h->s_out);
+  if (h->s_side) cudaStreamSynchronize(h->s_side), cudaStreamDestroy(h->s_side);
+  if (h->e_fork) cudaEventDestroy(h->e_fork);
+  if (h->e_join) cudaEventDestroy(h->e_join);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
