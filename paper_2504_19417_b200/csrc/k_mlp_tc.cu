@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr bool kSplit = (MODE == VKM_MLP_F16X3);
   const float f_scale = kSplit ? 256.f : 1.f;   // features |f| <= 1 -> keep lo parts normal
 
-  // ---- one-time setup ----
+  pdl_trigger();
+  // ---- one-time setup (reads only the weights, never the predecessor's outputs) ----
   {
     const int nvec = kTileBytes / 16;
     uint4* dh = reinterpret_cast<uint4*>(S.bh);
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
   }
+  pdl_wait();   // setup above overlapped the predecessor's tail; its outputs are read below
   const uint32_t tmem = S.tmem_base;
   const int64_t ntiles = (n + kM - 1) / kM;
   const int64_t nv = __ldg(nvalid_ptr);   // slots [0, nv) hold the in-sensor events
@@ -433,14 +435,16 @@ void launch_gather_mlp_tc(int64_t n, const DevTables& tb, int W, int H, const Gr
   }();
   if (mode == VKM_MLP_BF16) {
     cudaFuncSetAttribute(tc::k_gather_mlp_tc<VKM_MLP_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    tc::k_gather_mlp_tc<VKM_MLP_BF16><<<grid, tc::kThreads, smem, s>>>(
-        n, sb.val_s, sb.pix_s, nvalid, tb.tf, P, g.Q, g.NQ, static_cast<const uint4*>(w.w1_hi),
-        static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out, prefetch);
+    launch_pdl(tc::k_gather_mlp_tc<VKM_MLP_BF16>, grid, tc::kThreads, smem, s, n,
+               static_cast<const uint64_t*>(sb.val_s), static_cast<const int32_t*>(sb.pix_s), nvalid, tb.tf, P,
+               static_cast<const float2*>(g.Q), static_cast<const int*>(g.NQ), static_cast<const uint4*>(w.w1_hi),
+               static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out, prefetch);
   } else {
     cudaFuncSetAttribute(tc::k_gather_mlp_tc<VKM_MLP_F16X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    tc::k_gather_mlp_tc<VKM_MLP_F16X3><<<grid, tc::kThreads, smem, s>>>(
-        n, sb.val_s, sb.pix_s, nvalid, tb.tf, P, g.Q, g.NQ, static_cast<const uint4*>(w.w1_hi),
-        static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out, prefetch);
+    launch_pdl(tc::k_gather_mlp_tc<VKM_MLP_F16X3>, grid, tc::kThreads, smem, s, n,
+               static_cast<const uint64_t*>(sb.val_s), static_cast<const int32_t*>(sb.pix_s), nvalid, tb.tf, P,
+               static_cast<const float2*>(g.Q), static_cast<const int*>(g.NQ), static_cast<const uint4*>(w.w1_hi),
+               static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out, prefetch);
   }
 }
 

@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ 
                                                      int H, int segs, int dy, int RS, int64_t P,
                                                      const float4* __restrict__ mxp,
                                                      const float4* __restrict__ myp, int D2) {
+  pdl_wait();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= W * 4) return;
   const int slice = blockIdx.y / segs;
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ 
       }
     }
   }
+  pdl_trigger();   // dependents may launch as this grid drains
 }
 
 // Thread -> (row y, channel ch) of plane blockIdx.z, columns [x0, x0+CS).
@@ -217,8 +219,8 @@ void launch_pool_y_demod(const DevTables& tb, int W, int H, int nb, int D8, int 
   const int RS = (H + segs - 1) / segs;
   segs = (H + RS - 1) / RS;
   dim3 gy((W * 4 + 255) / 256, segs * nb, planes);
-  k_box_y_demod<<<gy, 256, 0, s>>>(reinterpret_cast<const float4*>(R), reinterpret_cast<float4*>(Q), W, H, segs, dy,
-                                   RS, P, tb.mxp, tb.myp, D8 / 2);
+  launch_pdl(k_box_y_demod, gy, 256, 0, s, reinterpret_cast<const float4*>(R), reinterpret_cast<float4*>(Q), W, H,
+             segs, dy, RS, P, static_cast<const float4*>(tb.mxp), static_cast<const float4*>(tb.myp), D8 / 2);
 }
 
 }  // namespace vkm

@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
                                                             const float4* __restrict__ myp, int W, int H, int nb,
                                                             int dx, int S, int nseg, int64_t P,
                                                             float2* __restrict__ R) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t rx_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int RL = 2 * dx + 1;
@@ -314,6 +315,7 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
     }
     while (k < nx) finish();
   }
+  pdl_trigger();   // dependents may launch as this grid drains
 }
 
 // ---------------------------------------------------------------------------
@@ -332,6 +334,7 @@ __global__ void __launch_bounds__(256) k_scatter(const int32_t* __restrict__ pix
                                                  int64_t n, int64_t P, const int* __restrict__ start,
                                                  int* __restrict__ cursor, uint64_t* __restrict__ val_s,
                                                  int32_t* __restrict__ pix_s) {
+  pdl_wait();
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
     const int p = __ldg(pix + e);
     if (p >= P) continue;   // outside the sensor: no slot (slots [start[P], n) are never read)
@@ -339,6 +342,7 @@ __global__ void __launch_bounds__(256) k_scatter(const int32_t* __restrict__ pix
     val_s[slot] = __ldg(val + e);
     pix_s[slot] = p;
   }
+  pdl_trigger();   // dependents may launch as this grid drains
 }
 
 constexpr int kShortRun = 256;   // runs up to this length: one thread, insertion sort
@@ -353,6 +357,7 @@ constexpr int kRunsortStage = 3072;   // slots staged per block (24 KB)
 __global__ void __launch_bounds__(256) k_runsort(const int* __restrict__ start, int64_t P, int ppb,
                                                  uint64_t* __restrict__ val_s, int* __restrict__ longlist,
                                                  int* __restrict__ longcount, int* __restrict__ cursor) {
+  pdl_wait();
   __shared__ uint64_t stage[kRunsortStage];
   for (int64_t p0 = int64_t(blockIdx.x) * ppb; p0 < P; p0 += int64_t(gridDim.x) * ppb) {
     const int64_t p = p0 + threadIdx.x;
@@ -386,6 +391,7 @@ __global__ void __launch_bounds__(256) k_runsort(const int* __restrict__ start, 
       for (int i = threadIdx.x; i < b1 - b0; i += blockDim.x) val_s[b0 + i] = stage[i];
     __syncthreads();
   }
+  pdl_trigger();   // dependents may launch as this grid drains
 }
 
 __device__ __forceinline__ void cas_slot(uint64_t& a, uint64_t& b) {
@@ -399,6 +405,7 @@ __device__ __forceinline__ void cas_slot(uint64_t& a, uint64_t& b) {
 __global__ void __launch_bounds__(512) k_longsort(const int* __restrict__ start, uint64_t* __restrict__ val_s,
                                                   const int* __restrict__ longlist,
                                                   const int* __restrict__ longcount) {
+  pdl_wait();
   __shared__ uint64_t sm[kSmemRun];
   const int nl = *longcount;
   for (int li = blockIdx.x; li < nl; li += gridDim.x) {
@@ -432,6 +439,7 @@ __global__ void __launch_bounds__(512) k_longsort(const int* __restrict__ start,
       for (int i = threadIdx.x; i < L; i += blockDim.x) val_s[s + i] = sm[i];
     __syncthreads();
   }
+  pdl_trigger();   // dependents may launch as this grid drains
 }
 
 // ---------------------------------------------------------------------------
@@ -452,6 +460,7 @@ __global__ void __launch_bounds__(kRx1Warps * 32) k_reduce_x1(const int* __restr
                                                               const float2* __restrict__ my, int W, int H, int nb,
                                                               int dx, int S, int nseg, int64_t P,
                                                               float2* __restrict__ R) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t rx_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int half = wib & 1;                        // channel half of this warp
@@ -544,6 +553,7 @@ __global__ void __launch_bounds__(kRx1Warps * 32) k_reduce_x1(const int* __restr
     }
     while (k < nx) finish();
   }
+  pdl_trigger();   // dependents may launch as this grid drains
 }
 
 namespace {
@@ -597,14 +607,14 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
   if (n > 0 && counting) {
     cudaMemsetAsync(sb.longcount, 0, sizeof(int), s);   // sb.cursor is zero (allocation, then k_runsort)
     const int eb = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
-    k_scatter<<<eb, 256, 0, s>>>(sb.pix, sb.val, n, P, sb.start, sb.cursor, sb.val_s, sb.pix_s);
+    launch_pdl(k_scatter, eb, 256, 0, s, sb.pix, sb.val, n, P, sb.start, sb.cursor, sb.val_s, sb.pix_s);
     // pixels per runsort block step: ~2000 expected slots (fits the stage), 16..256 pixels
     const double mean_run = double(n) / double(std::max<int64_t>(P, 1));
     int ppb = 256;
     while (ppb > 16 && ppb * mean_run > 2000.0) ppb >>= 1;
     const int pb = int(std::min<int64_t>((P + ppb - 1) / ppb, 148 * 16));
-    k_runsort<<<pb, 256, 0, s>>>(sb.start, P, ppb, sb.val_s, sb.longlist, sb.longcount, sb.cursor);
-    k_longsort<<<148, 512, 0, s>>>(sb.start, sb.val_s, sb.longlist, sb.longcount);
+    launch_pdl(k_runsort, pb, 256, 0, s, sb.start, P, ppb, sb.val_s, sb.longlist, sb.longcount, sb.cursor);
+    launch_pdl(k_longsort, 148, 512, 0, s, sb.start, sb.val_s, sb.longlist, sb.longcount);
     launches += 3;
   } else if (n > 0) {
     size_t sort_bytes = sb.sort_temp_bytes;
@@ -670,8 +680,8 @@ void launch_reduce_x(const DevTables& tb, int W, int H, int nb, int dx, const So
     const int nseg = (W + S - 1) / S;
     const int64_t items = int64_t(H) * nb * nseg;
     const int blocks = int(std::min<int64_t>((items + 1) / 2, res_items / 2));
-    k_reduce_x1<<<blocks, kRx1Warps * 32, smem, s>>>(sb.start, sb.val_s, tb.tf, tb.mx, tb.my, W, H, nb, dx, S, nseg,
-                                                     P, R);
+    launch_pdl(k_reduce_x1, blocks, kRx1Warps * 32, smem, s, sb.start, sb.val_s, tb.tf, tb.mx, tb.my, W, H, nb, dx,
+               S, nseg, P, R);
     return;
   }
   const size_t smem = reduce_x_smem(dx);
@@ -695,7 +705,8 @@ void launch_reduce_x(const DevTables& tb, int W, int H, int nb, int dx, const So
   const int nseg = (W + S - 1) / S;
   const int64_t items = int64_t(H) * nb * nseg;
   const int blocks = int(std::min<int64_t>((items + kRxWarps - 1) / kRxWarps, res_warps / kRxWarps));
-  k_reduce_x<<<blocks, kRxWarps * 32, smem, s>>>(sb.start, sb.val_s, tb.tf, tb.mxp, tb.myp, W, H, nb, dx, S, nseg, P, R);
+  launch_pdl(k_reduce_x, blocks, kRxWarps * 32, smem, s, sb.start, sb.val_s, tb.tf, tb.mxp, tb.myp, W, H, nb, dx, S,
+             nseg, P, R);
 }
 
 }  // namespace vkm

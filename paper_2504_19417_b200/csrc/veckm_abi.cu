@@ -299,8 +299,8 @@ int encode_core(vkm_handle* h, const double* ev, const vkm::SliceTab& st, int po
     *launches += 1;
     VKM_CK(cudaGetLastError());
     rec(h, 1, s);
+    VKM_CK(cudaStreamWaitEvent(s, h->e_join, 0));   // long done: it ran beside the reduction
     vkm::launch_pool_y_demod(tables(h), W, H, nb, h->D8, h->p.delta_y, h->G, h->Q, s);
-    VKM_CK(cudaStreamWaitEvent(s, h->e_join, 0));
     *launches += 2;
     VKM_CK(cudaGetLastError());
   } else {
