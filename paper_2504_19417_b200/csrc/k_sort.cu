@@ -209,7 +209,7 @@ constexpr int kRxWarps = 2;
 constexpr int kRxMaxSeg = 128;
 constexpr int kRxEnds = kRxMaxSeg + 2 * kMaxFusedDx + 4 + 64;   // run ends of one sweep (+ sentinel) + 64-float stage
 #ifndef VKM_RX_GROUP
-#define VKM_RX_GROUP 4   // k_reduce_x1 assumes 4 (one float4 of time arguments per group)
+#define VKM_RX_GROUP 8   // events per sin/cos group of k_reduce_x (8: -1 % vs 4)
 #endif
 constexpr int kRxGroup = VKM_RX_GROUP;   // events per sin/cos group (divides 32)
 
@@ -451,6 +451,7 @@ __global__ void __launch_bounds__(512) k_longsort(const int* __restrict__ start,
 // lane) and twice the warps, i.e. twice the latency hiding.
 // ---------------------------------------------------------------------------
 constexpr int kRx1Warps = 4;   // two items per block
+constexpr int kRx1Group = 4;   // events per group: one float4 of time arguments
 size_t reduce_x1_smem(int dx) { return size_t(kRx1Warps) * ((2 * dx + 1) * 256 + kRxEnds * 4); }
 
 __global__ void __launch_bounds__(kRx1Warps * 32) k_reduce_x1(const int* __restrict__ start,
@@ -530,7 +531,7 @@ __global__ void __launch_bounds__(kRx1Warps * 32) k_reduce_x1(const int* __restr
       mc = __ldg(mxc + int64_t(min(max(xs + k, 0), W - 1)) * 64);
     };
 
-    for (int j = jfirst; j < jend; j += kRxGroup) {
+    for (int j = jfirst; j < jend; j += kRx1Group) {
       if (j - jb >= 32) {
         jb += 32;
         __syncwarp();
@@ -539,11 +540,11 @@ __global__ void __launch_bounds__(kRx1Warps * 32) k_reduce_x1(const int* __restr
         av1 = ld_a(jb + 32 + lane);
       }
       const float4 a4 = *reinterpret_cast<const float4*>(abuf + (j - jb));
-      uint64_t cs[kRxGroup];
+      uint64_t cs[kRx1Group];
       VKM_SINCOS_CS(fmul2(f2pack(a4.x, a4.y), TT), cs[0], cs[1]);
       VKM_SINCOS_CS(fmul2(f2pack(a4.z, a4.w), TT), cs[2], cs[3]);
 #pragma unroll
-      for (int u = 0; u < kRxGroup; ++u) {
+      for (int u = 0; u < kRx1Group; ++u) {
         if (j + u >= je) {
           if (j + u >= jend) break;
           do finish(); while (j + u >= je);
