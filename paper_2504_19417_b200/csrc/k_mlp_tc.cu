@@ -51,8 +51,11 @@ struct Smem {
   uint8_t ah[kStages][kTileBytes];
   uint8_t al[kStages][kTileBytes];
   float4 qring[kProdWarps][kQD][32];   // per producer warp: pooled rows of its next kQD-1 events
-  float b1[kN];
-  float2 w2i[kN];   // (w2[0][n], w2[1][n]) interleaved for packed FFMA2
+  // head constants with the power-of-two operand scale s = w_scale·f_scale
+  // folded in: relu(acc/s + b1)·w2 == relu(acc + s·b1)·(w2/s) exactly
+  float b1s[kN];    // s·b1
+  float w2a[kN];    // w2[0][n] / s
+  float w2b[kN];    // w2[1][n] / s
   float b2[2];
   float scale;
   uint32_t tmem_base;
@@ -159,9 +162,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       dh[i] = __ldg(w1h + i);
       if (kSplit) dl[i] = __ldg(w1l + i);
     }
+    const float sc = w_scale * f_scale;   // a power of two: exact scaling
     for (int i = threadIdx.x; i < kN; i += kThreads) {
-      S.b1[i] = b1[i];
-      S.w2i[i] = make_float2(w2[i], w2[kN + i]);
+      S.b1s[i] = b1[i] * sc;
+      S.w2a[i] = w2[i] / sc;
+      S.w2b[i] = w2[kN + i] / sc;
     }
     if (threadIdx.x == 0) {
       S.b2[0] = b2[0];
@@ -327,7 +332,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < kProdWarps + 4) {
     // ======================= epilogue =======================
     const int q = warp & 3;   // TMEM lane quadrant = warp id % 4
-    const float inv = S.scale;
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int acc = it & (kAcc - 1);
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&S.tfull[acc], ph);
       tc_fence_after();
-      uint64_t o = f2pack(0.f, 0.f);
+      uint64_t oa = 0, ob = 0;   // (even, odd) hidden partial sums of the two outputs
       const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * kN);
 #pragma unroll
       for (int cb = 0; cb < kN; cb += 32) {
@@ -358,16 +362,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             : "r"(taddr + cb));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float hv = fmaxf(fmaf(__uint_as_float(r[i]), inv, S.b1[cb + i]), 0.f);
-          const float2 w = S.w2i[cb + i];
-          o = ffma2(f2pack(hv, hv), f2pack(w.x, w.y), o);
+        for (int i = 0; i < 32; i += 4) {   // 4 hidden units: 3 LDS.128, 2 FADD2, 4 FMNMX, 4 FFMA2
+          const float4 bb = *reinterpret_cast<const float4*>(S.b1s + cb + i);
+          const float4 wa = *reinterpret_cast<const float4*>(S.w2a + cb + i);
+          const float4 wb = *reinterpret_cast<const float4*>(S.w2b + cb + i);
+          float h0, h1, h2, h3;
+          f2unpack(fadd2(f2pack(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), f2pack(bb.x, bb.y)), h0, h1);
+          f2unpack(fadd2(f2pack(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])), f2pack(bb.z, bb.w)), h2, h3);
+          const uint64_t h01 = f2pack(fmaxf(h0, 0.f), fmaxf(h1, 0.f)), h23 = f2pack(fmaxf(h2, 0.f), fmaxf(h3, 0.f));
+          oa = ffma2(h01, f2pack(wa.x, wa.y), oa);
+          oa = ffma2(h23, f2pack(wa.z, wa.w), oa);
+          ob = ffma2(h01, f2pack(wb.x, wb.y), ob);
+          ob = ffma2(h23, f2pack(wb.z, wb.w), ob);
         }
       }
       tc_fence_before();
       mbar_arrive(&S.tempty[acc]);
-      float o0, o1;
-      f2unpack(o, o0, o1);
+      float oa0, oa1, ob0, ob1;
+      f2unpack(oa, oa0, oa1);
+      f2unpack(ob, ob0, ob1);
+      const float o0 = oa0 + oa1, o1 = ob0 + ob1;
       if (e >= 0) {
         float2 r2 = make_float2(o0 + S.b2[0], o1 + S.b2[1]);
         if (cnt <= 0) r2 = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
