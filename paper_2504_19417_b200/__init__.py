@@ -6,6 +6,9 @@ Drop-in for the reference `evflow` estimator path:
     flows = NormalFlowRegressor(width=640, height=480, weights="head.vkmw").predict(X)
 
 `X` is an (n, 3) array of [t, x, y]; the result is (n, 2) float64 [n_x, n_y].
+`paper_2504_19417_b200.stream` loads EVN1/CSV event files, slices streams like
+the reference's `slice_stream`, and `NormalFlowRegressor.predict_stream` runs
+every window through one pipelined batch.
 `paper_2504_19417_b200.bindings` mirrors the reference's array-in/array-out
 `evflow_bindings` (encode / predict / load_config_preset).
 Per-event work runs in hand-written sm_100a kernels behind the C-ABI in

@@ -199,6 +199,17 @@ class NormalFlowRegressor(BaseEstimator):
         return [out[lo:hi].astype(np.float64) for lo, hi in zip(offsets[:-1], offsets[1:])]
 
 
+def _stream_predict(self, stream, stride=None, t0: float = 0.0):
+    """Per-window flows over an EventStream (stream.slice_stream windows, the
+    window start as each slice's time origin), all windows in one pipelined
+    host batch.  Returns [(t_start, (n_i, 2) float64)]."""
+    from .stream import predict_stream
+    return predict_stream(self, stream, stride, t0)
+
+
+NormalFlowRegressor.predict_stream = _stream_predict
+
+
 def _pinned_pair(n: int):
     """Page-locked (n, 3) f64 event and (n, 2) f32 flow buffers (torch's host
     allocator; plain numpy memory when torch is unavailable)."""

@@ -1,0 +1,296 @@
+"""Event streams: loading, slicing into windows, and streaming prediction.
+
+Host-side restatement of the reference's stream ingestion (events.py:66-387):
+the EVN1 binary format (12-byte header `EVN1` + u32 width + u32 height, then
+packed 17-byte little-endian records f64 t, i32 x, i32 y, i8 polarity), the
+CSV format, and `slice_stream`'s windowing semantics (half-open windows
+[t0 + i·stride, t0 + i·stride + 2δt), overlapping strides, interior gaps kept
+as empty slices, trailing empty windows dropped).  Same checks, messages and
+exception types.
+
+`predict_stream` is the B200 streaming path: every window becomes one slice
+of one `vkm_predict_batch_host` call (copy-in / kernels / copy-out overlap,
+up to 64 windows per launch sequence), with the window start as the slice's
+time origin — exactly what `predict_flows` sees for a `slice_stream` slice.
+"""
+
+from __future__ import annotations
+
+import os
+import struct
+from dataclasses import dataclass
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from .errors import EventParseError, GeometryError
+
+BINARY_MAGIC = b"EVN1"
+BINARY_RECORD_DTYPE = np.dtype([("t", "<f8"), ("x", "<i4"), ("y", "<i4"), ("p", "<i1")])   # 17 bytes, packed
+
+
+@dataclass(frozen=True)
+class CameraGeometry:
+    width: int
+    height: int
+
+    def __post_init__(self) -> None:
+        if self.width < 1 or self.height < 1:
+            raise ValueError(f"geometry must be at least 1x1, got {self.width}x{self.height}")
+
+    def contains(self, x: np.ndarray, y: np.ndarray) -> np.ndarray:
+        return (x >= 0) & (x < self.width) & (y >= 0) & (y < self.height)
+
+
+@dataclass
+class EventStream:
+    """Parallel arrays t (f64 s), x, y (int32), optional polarity (int8) (events.py:66-87)."""
+
+    t: np.ndarray
+    x: np.ndarray
+    y: np.ndarray
+    geometry: CameraGeometry
+    polarity: Optional[np.ndarray] = None
+
+    def __post_init__(self) -> None:
+        self.t = np.asarray(self.t, dtype=np.float64)
+        self.x = np.asarray(self.x, dtype=np.int32)
+        self.y = np.asarray(self.y, dtype=np.int32)
+        if self.polarity is not None:
+            self.polarity = np.asarray(self.polarity, dtype=np.int8)
+            if len(self.polarity) != len(self.t):
+                raise ValueError("polarity length mismatch")
+        t, x, y = self.t, self.x, self.y
+        if not (len(t) == len(x) == len(y)):
+            raise ValueError("t, x, y must have equal length")
+        if len(t):
+            if not np.all(np.isfinite(t)) or np.any(t < 0):
+                bad = int(np.flatnonzero(~np.isfinite(t) | (t < 0))[0])
+                raise ValueError(f"event {bad}: timestamp {t[bad]} must be finite and non-negative")
+            inside = self.geometry.contains(x, y)
+            if not np.all(inside):
+                bad = int(np.flatnonzero(~inside)[0])
+                raise GeometryError(f"event {bad}: ({x[bad]}, {y[bad]}) outside geometry "
+                                    f"{self.geometry.width}x{self.geometry.height}")
+
+    def __len__(self) -> int:
+        return len(self.t)
+
+
+@dataclass
+class StreamSlice:
+    """One window of a stream: rows [lo, hi) of the time-sorted stream."""
+
+    t: np.ndarray
+    x: np.ndarray
+    y: np.ndarray
+    t_start: float
+    window: float
+    polarity: Optional[np.ndarray] = None
+
+    def __len__(self) -> int:
+        return len(self.t)
+
+    def events(self) -> np.ndarray:
+        """(n, 3) float64 [t, x, y] rows, the estimator's input layout."""
+        return np.stack([self.t, self.x.astype(np.float64), self.y.astype(np.float64)], axis=1)
+
+
+def _parse_binary(path: str) -> EventStream:
+    """events.py:238-266."""
+    with open(path, "rb") as fh:
+        header = fh.read(12)
+        if len(header) < 12 or header[:4] != BINARY_MAGIC:
+            raise EventParseError(f"{path}: missing {BINARY_MAGIC!r} header")
+        width, height = struct.unpack("<II", header[4:12])
+        payload = fh.read()
+    if len(payload) % BINARY_RECORD_DTYPE.itemsize != 0:
+        raise EventParseError(f"{path}: truncated record at offset {12 + len(payload)} "
+                              f"(payload not a multiple of {BINARY_RECORD_DTYPE.itemsize} bytes)")
+    geometry = CameraGeometry(width, height)
+    records = np.frombuffer(payload, dtype=BINARY_RECORD_DTYPE)
+    x = records["x"].astype(np.int32)
+    y = records["y"].astype(np.int32)
+    inside = geometry.contains(x, y)
+    if not np.all(inside):
+        bad = int(np.flatnonzero(~inside)[0])
+        raise GeometryError(f"{path}: record {bad} at ({x[bad]}, {y[bad]}) outside geometry {width}x{height}")
+    return EventStream(records["t"].astype(np.float64), x, y, geometry, records["p"].astype(np.int8))
+
+
+def _parse_csv(path: str, geometry: CameraGeometry) -> EventStream:
+    """events.py:177-236: optional header line, 3 or 4 fields, polarity in {0, 1, -1}."""
+    ts, xs, ys, ps = [], [], [], []
+    saw_polarity = False
+    with open(path, "r", encoding="utf-8") as fh:
+        for lineno, line in enumerate(fh, start=1):
+            line = line.strip()
+            if not line:
+                continue
+            fields = line.split(",")
+            if lineno == 1:
+                try:
+                    float(fields[0])
+                except ValueError:
+                    continue
+            if len(fields) not in (3, 4):
+                raise EventParseError(f"{path}:{lineno}: expected 3 or 4 fields, got {len(fields)}")
+            try:
+                t = float(fields[0])
+                x = int(fields[1])
+                y = int(fields[2])
+            except ValueError as exc:
+                raise EventParseError(f"{path}:{lineno}: {exc}") from exc
+            if not np.isfinite(t) or t < 0:
+                raise EventParseError(f"{path}:{lineno}: timestamp {t} not finite and non-negative")
+            if not (0 <= x < geometry.width):
+                raise GeometryError(f"{path}:{lineno}: x={x} violates 0 <= x < {geometry.width}")
+            if not (0 <= y < geometry.height):
+                raise GeometryError(f"{path}:{lineno}: y={y} violates 0 <= y < {geometry.height}")
+            if len(fields) == 4:
+                try:
+                    p = int(fields[3])
+                except ValueError as exc:
+                    raise EventParseError(f"{path}:{lineno}: bad polarity {fields[3]!r}") from exc
+                if p not in (0, 1, -1):
+                    raise EventParseError(f"{path}:{lineno}: polarity must be 0, 1 or -1, got {p}")
+                saw_polarity = True
+                ps.append(p)
+            else:
+                ps.append(0)
+            ts.append(t)
+            xs.append(x)
+            ys.append(y)
+    return EventStream(np.array(ts, dtype=np.float64), np.array(xs, dtype=np.int32),
+                       np.array(ys, dtype=np.int32), geometry,
+                       np.array(ps, dtype=np.int8) if saw_polarity else None)
+
+
+def load_events(path: str, fmt: str = "csv", geometry: Optional[CameraGeometry] = None) -> EventStream:
+    """events.py:269-291."""
+    if not os.path.exists(path):
+        raise EventParseError(f"{path}: no such file")
+    if fmt == "csv":
+        if geometry is None:
+            raise ValueError("CSV event files require an explicit geometry")
+        return _parse_csv(path, geometry)
+    if fmt == "binary":
+        stream = _parse_binary(path)
+        if geometry is not None and geometry != stream.geometry:
+            raise GeometryError(f"{path}: file geometry {stream.geometry.width}x{stream.geometry.height} "
+                                f"does not match declared {geometry.width}x{geometry.height}")
+        return stream
+    raise ValueError(f"unknown event format {fmt!r}")
+
+
+def write_events_binary(stream: EventStream, path: str) -> None:
+    records = np.empty(len(stream), dtype=BINARY_RECORD_DTYPE)
+    records["t"] = stream.t
+    records["x"] = stream.x
+    records["y"] = stream.y
+    records["p"] = stream.polarity if stream.polarity is not None else 0
+    with open(path, "wb") as fh:
+        fh.write(BINARY_MAGIC)
+        fh.write(struct.pack("<II", stream.geometry.width, stream.geometry.height))
+        fh.write(records.tobytes())
+
+
+def write_events_csv(stream: EventStream, path: str) -> None:
+    with open(path, "w", encoding="utf-8") as fh:
+        if stream.polarity is not None:
+            for t, x, y, p in zip(stream.t, stream.x, stream.y, stream.polarity):
+                fh.write(f"{float(t)!r},{x},{y},{p}\n")
+        else:
+            for t, x, y in zip(stream.t, stream.x, stream.y):
+                fh.write(f"{float(t)!r},{x},{y}\n")
+
+
+def filter_polarity(stream: EventStream, keep: str) -> EventStream:
+    """events.py:314-328."""
+    if keep not in ("pos", "neg"):
+        raise ValueError("keep must be 'pos' or 'neg'")
+    if stream.polarity is None:
+        return stream
+    mask = stream.polarity > 0 if keep == "pos" else stream.polarity <= 0
+    return EventStream(stream.t[mask], stream.x[mask], stream.y[mask], stream.geometry, stream.polarity[mask])
+
+
+def window_bounds(t: np.ndarray, delta_t: float, stride: float, t0: float = 0.0) -> List[Tuple[int, int, float]]:
+    """(lo, hi, t_start) of every window of slice_stream over sorted times t
+    (events.py:331-387): searchsorted with side='left' at both edges, so the
+    windows are half-open; trailing empty windows are dropped."""
+    if delta_t <= 0:
+        raise ValueError("delta_t must be positive")
+    if stride <= 0:
+        raise ValueError("stride must be positive")
+    window = 2.0 * delta_t
+    if len(t) == 0:
+        return []
+    t_last = float(t[-1])
+    count = 0
+    while t0 + count * stride <= t_last:   # same float sequence as the reference's loop
+        count += 1
+    starts = np.array([t0 + i * stride for i in range(count)], dtype=np.float64)
+    lo = np.searchsorted(t, starts, side="left")
+    hi = np.searchsorted(t, starts + window, side="left")
+    out = [(int(a), int(b), float(s)) for a, b, s in zip(lo, hi, starts)]
+    while out and out[-1][1] == out[-1][0]:
+        out.pop()
+    return out
+
+
+def slice_stream(stream: EventStream, delta_t: float, stride: float, t0: float = 0.0) -> List[StreamSlice]:
+    """Cut a stream into windows of length 2·delta_t (events.py:331-387)."""
+    if delta_t <= 0:
+        raise ValueError("delta_t must be positive")
+    if stride <= 0:
+        raise ValueError("stride must be positive")
+    if len(stream) == 0:
+        return []
+    t, x, y, p = stream.t, stream.x, stream.y, stream.polarity
+    if np.any(np.diff(t) < 0):
+        order = np.argsort(t, kind="stable")
+        t, x, y = t[order], x[order], y[order]
+        p = p[order] if p is not None else None
+    return [StreamSlice(t[lo:hi], x[lo:hi], y[lo:hi], start, 2.0 * delta_t, p[lo:hi] if p is not None else None)
+            for lo, hi, start in window_bounds(t, delta_t, stride, t0)]
+
+
+def predict_stream(regressor, stream: EventStream, stride: Optional[float] = None, t0: float = 0.0):
+    """Per-window normal flow over a whole stream on the B200 path.
+
+    Returns a list of (t_start, flows) with flows (n_window, 2) float64, one
+    entry per slice_stream window (empty windows give (0, 2) arrays).  The
+    window start is each slice's time origin, like predict_flows on a
+    slice_stream slice.  stride defaults to the window (2·delta_t)."""
+    from .estimators import _pinned_pair
+    dt = float(regressor.delta_t)
+    if stride is None:
+        stride = 2.0 * dt
+    g = stream.geometry
+    if (g.width, g.height) != (regressor.width, regressor.height):
+        raise GeometryError(f"stream geometry {g.width}x{g.height} does not match the estimator's "
+                            f"{regressor.width}x{regressor.height}")
+    eng = regressor.engine()
+    t, x, y = stream.t, stream.x, stream.y
+    if len(t) and np.any(np.diff(t) < 0):
+        order = np.argsort(t, kind="stable")
+        t, x, y = t[order], x[order], y[order]
+    wins = window_bounds(t, dt, stride, t0)
+    if not wins:
+        return []
+    sizes = np.array([hi - lo for lo, hi, _ in wins], dtype=np.int64)
+    offsets = np.zeros(len(wins) + 1, dtype=np.int64)
+    np.cumsum(sizes, out=offsets[1:])
+    total = int(offsets[-1])
+    if total == 0:
+        return [(s, np.empty((0, 2))) for _, _, s in wins]
+    ev, out = _pinned_pair(total)
+    for (lo, hi, _), o in zip(wins, offsets[:-1]):
+        if hi > lo:   # overlapping windows duplicate their shared events
+            ev[o:o + hi - lo, 0] = t[lo:hi]
+            ev[o:o + hi - lo, 1] = x[lo:hi]
+            ev[o:o + hi - lo, 2] = y[lo:hi]
+    t_starts = np.array([s for _, _, s in wins], dtype=np.float64)
+    eng.predict_batch_host(ev, offsets, t_starts, flows=out)
+    return [(s, out[a:b].astype(np.float64)) for (_, _, s), a, b in zip(wins, offsets[:-1], offsets[1:])]

@@ -1,0 +1,113 @@
+"""Stream ingestion and slicing (events.py:238-387) against fixtures frozen from
+the reference (tests/golden/make_golden_stream.py); streaming prediction on
+the GPU against per-window predictions."""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, has_cuda
+from oracle import veckm_oracle as vo
+
+
+def _S():
+    from paper_2504_19417_b200 import stream as S
+    return S
+
+
+@pytest.mark.parametrize("name", ["overlap", "disjoint", "gap", "edges", "unsorted"])
+def test_slice_stream_matches_reference(name):
+    S = _S()
+    with np.load(os.path.join(GOLDEN, "stream_slices.npz")) as z:
+        g = {k: z[k] for k in z.files}
+    delta_t, stride, t0 = g[f"{name}_params"]
+    st = S.EventStream(g[f"{name}_t"], g[f"{name}_x"], g[f"{name}_y"], S.CameraGeometry(64, 48))
+    sl = S.slice_stream(st, float(delta_t), float(stride), float(t0))
+    np.testing.assert_array_equal([s.t_start for s in sl], g[f"{name}_starts"])
+    np.testing.assert_array_equal([len(s) for s in sl], g[f"{name}_lens"])
+    np.testing.assert_array_equal([s.t[0] if len(s) else -1.0 for s in sl], g[f"{name}_first"])
+    np.testing.assert_array_equal([int(s.x.sum()) for s in sl], g[f"{name}_xsum"])
+
+
+def test_slice_stream_errors_and_empty():
+    S = _S()
+    st = S.EventStream(np.zeros(0), np.zeros(0, int), np.zeros(0, int), S.CameraGeometry(4, 4))
+    assert S.slice_stream(st, 0.016, 0.01) == []
+    with pytest.raises(ValueError, match="delta_t"):
+        S.slice_stream(st, 0.0, 0.01)
+    with pytest.raises(ValueError, match="stride"):
+        S.slice_stream(st, 0.016, 0.0)
+
+
+def test_evn1_reads_reference_file_and_round_trips(tmp_path):
+    S = _S()
+    st = S.load_events(os.path.join(GOLDEN, "events_small.evn1"), "binary")
+    with np.load(os.path.join(GOLDEN, "events_small.npz")) as z:
+        np.testing.assert_array_equal(st.t, z["t"])
+        np.testing.assert_array_equal(st.x, z["x"])
+        np.testing.assert_array_equal(st.y, z["y"])
+        np.testing.assert_array_equal(st.polarity, z["p"])
+    assert (st.geometry.width, st.geometry.height) == (346, 260)
+    out = tmp_path / "rt.evn1"
+    S.write_events_binary(st, str(out))
+    assert out.read_bytes() == open(os.path.join(GOLDEN, "events_small.evn1"), "rb").read()
+    assert len(out.read_bytes()) == 12 + 17 * len(st)   # packed 17-byte records
+
+
+def test_event_file_errors(tmp_path):
+    S = _S()
+    from paper_2504_19417_b200.errors import EventParseError, GeometryError
+    bad = tmp_path / "bad.evn1"
+    bad.write_bytes(b"EVN1" + (4).to_bytes(4, "little") + (4).to_bytes(4, "little") + b"\x00" * 5)
+    with pytest.raises(EventParseError, match="truncated"):
+        S.load_events(str(bad), "binary")
+    with pytest.raises(EventParseError, match="header"):
+        (tmp_path / "nohdr.evn1").write_bytes(b"XXXX")
+        S.load_events(str(tmp_path / "nohdr.evn1"), "binary")
+    csv = tmp_path / "ev.csv"
+    csv.write_text("t,x,y\n0.001,1,2\n0.002,3,1,1\n")
+    st = S.load_events(str(csv), "csv", S.CameraGeometry(4, 4))
+    assert len(st) == 2 and st.polarity is not None
+    csv.write_text("0.001,9,2\n")
+    with pytest.raises(GeometryError, match="x=9"):
+        S.load_events(str(csv), "csv", S.CameraGeometry(4, 4))
+    with pytest.raises(ValueError, match="explicit geometry"):
+        S.load_events(str(csv), "csv")
+
+
+@pytest.mark.gpu
+def test_predict_stream_matches_per_window_predictions():
+    """Overlapping windows (stride < window) through one pipelined host batch:
+    each window equals its own single-slice run with the window start as time
+    origin (counts exact, flows to f32 rounding), and one window matches the
+    CPU oracle."""
+    if not has_cuda():
+        pytest.fail("GPU test needs a CUDA device")
+    import paper_2504_19417_b200 as pkg
+    S = _S()
+    W, H = 120, 90
+    rng = np.random.default_rng(12)
+    n = 60000
+    st = S.EventStream(np.sort(rng.uniform(0.0, 0.4, n)), rng.integers(0, W, n), rng.integers(0, H, n),
+                       S.CameraGeometry(W, H))
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    reg = pkg.NormalFlowRegressor(width=W, height=H, weights=w)
+    res = S.predict_stream(reg, st, stride=0.01, t0=0.0)
+    sl = S.slice_stream(st, 0.016, 0.01, 0.0)
+    assert len(res) == len(sl)
+    eng = reg.engine()
+    for (t_start, flows), s in zip(res, sl):
+        assert t_start == s.t_start and flows.shape == (len(s), 2)
+        if len(s):
+            np.testing.assert_allclose(flows, eng.predict_host(s.events(), s.t_start), rtol=0, atol=1e-5)
+    s = sl[7]
+    fr = vo.Freqs(b.time_freqs, b.x_freqs, b.y_freqs, 25.0)
+    ev = s.events()
+    g = vo.accumulate(ev[:, 0] - s.t_start, s.x.astype(np.int64), s.y.astype(np.int64), W, H, 10, 10, fr, 0.016)
+    q = np.arange(0, len(s), 37)
+    emb, _ = vo.pool(g, vo.spatial_table(fr, 10, 10), ev[q, 0] - s.t_start, s.x[q].astype(np.int64),
+                     s.y[q].astype(np.int64), fr, 0.016)
+    np.testing.assert_allclose(res[7][1][q], vo.mlp(w.w1, w.b1, w.w2, w.b2, vo.to_features(emb)), rtol=0, atol=1e-4)
