@@ -35,7 +35,8 @@ constexpr unsigned kFullMask = 0xffffffffu;
 
 __global__ void __launch_bounds__(256) k_prep(const double* __restrict__ ev, const SliceTab st, double delta_t,
                                               int W, int H, int32_t* __restrict__ pix_out,
-                                              uint64_t* __restrict__ val_out, int* __restrict__ cnt,
+                                              uint64_t* __restrict__ val_out, int32_t* __restrict__ rank_out,
+                                              int* __restrict__ cnt,
                                               float* __restrict__ flows_invalid,
                                               int32_t* __restrict__ counts_invalid) {
   const int P = W * H;
@@ -50,7 +51,7 @@ __global__ void __launch_bounds__(256) k_prep(const double* __restrict__ ev, con
     int pix = st.nb * P;   // out-of-sensor events sort after every pixel run
     if (xi >= 0 && xi < W && yi >= 0 && yi < H && x == double(xi) && y == double(yi)) {
       pix = b * P + yi * W + xi;
-      atomicAdd(cnt + pix, 1);
+      rank_out[e] = atomicAdd(cnt + pix, 1);   // arrival rank: the counting scatter's offset
     } else {
       if (flows_invalid)
         reinterpret_cast<float2*>(flows_invalid)[e] = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
@@ -65,7 +66,8 @@ __global__ void __launch_bounds__(256) k_prep(const double* __restrict__ ev, con
 // precomputed, pixels as 16-bit coordinates.
 __global__ void __launch_bounds__(256) k_prep_packed(const uint2* __restrict__ evp, const SliceTab st, int W, int H,
                                                      int32_t* __restrict__ pix_out, uint64_t* __restrict__ val_out,
-                                                     int* __restrict__ cnt, float* __restrict__ flows_invalid,
+                                                     int32_t* __restrict__ rank_out, int* __restrict__ cnt,
+                                                     float* __restrict__ flows_invalid,
                                                      int32_t* __restrict__ counts_invalid) {
   const int P = W * H;
   const int64_t n = st.off[st.nb];
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(256) k_prep_packed(const uint2* __restrict__ e
     int pix = st.nb * P;
     if (xi < W && yi < H) {
       pix = b * P + yi * W + xi;
-      atomicAdd(cnt + pix, 1);
+      rank_out[e] = atomicAdd(cnt + pix, 1);   // arrival rank: the counting scatter's offset
     } else {
       if (flows_invalid)
         reinterpret_cast<float2*>(flows_invalid)[e] = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
@@ -320,8 +322,9 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
 
 // ---------------------------------------------------------------------------
 // Counting sort (default): the histogram and run starts exist already
-// (k_prep + scan), so each event's slot is start[pixel] + a per-pixel atomic
-// cursor.  That scatter is stable only up to the order of the atomics; the
+// (k_prep + scan), so each event's slot is start[pixel] + its arrival rank
+// (the value k_prep's histogram atomic returned).  That scatter is stable only
+// up to the order of the atomics; the
 // runs are then put back into event (= time) order, which is exactly the
 // stable pixel-major order of np.argsort(kind="stable") (encoder.py:255-257):
 //   k_runsort   one thread per pixel, insertion sort of runs <= 32 events;
@@ -331,14 +334,14 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
 //               runs <= 4096, in global memory beyond (pathological hot pixels)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_scatter(const int32_t* __restrict__ pix, const uint64_t* __restrict__ val,
-                                                 int64_t n, int64_t P, const int* __restrict__ start,
-                                                 int* __restrict__ cursor, uint64_t* __restrict__ val_s,
+                                                 const int32_t* __restrict__ rank, int64_t n, int64_t P,
+                                                 const int* __restrict__ start, uint64_t* __restrict__ val_s,
                                                  int32_t* __restrict__ pix_s) {
   pdl_wait();
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
     const int p = __ldg(pix + e);
     if (p >= P) continue;   // outside the sensor: no slot (slots [start[P], n) are never read)
-    const int slot = __ldg(start + p) + atomicAdd(cursor + p, 1);
+    const int slot = __ldg(start + p) + __ldg(rank + e);
     val_s[slot] = __ldg(val + e);
     pix_s[slot] = p;
   }
@@ -356,7 +359,7 @@ constexpr int kRunsortStage = 3072;   // slots staged per block (24 KB)
 
 __global__ void __launch_bounds__(256) k_runsort(const int* __restrict__ start, int64_t P, int ppb,
                                                  uint64_t* __restrict__ val_s, int* __restrict__ longlist,
-                                                 int* __restrict__ longcount, int* __restrict__ cursor) {
+                                                 int* __restrict__ longcount) {
   pdl_wait();
   __shared__ uint64_t stage[kRunsortStage];
   for (int64_t p0 = int64_t(blockIdx.x) * ppb; p0 < P; p0 += int64_t(gridDim.x) * ppb) {
@@ -368,7 +371,6 @@ __global__ void __launch_bounds__(256) k_runsort(const int* __restrict__ start, 
       for (int i = threadIdx.x; i < b1 - b0; i += blockDim.x) stage[i] = val_s[b0 + i];
     __syncthreads();
     if (threadIdx.x < ppb && p < P) {
-      cursor[p] = 0;   // ready for the next call's scatter (saves a memset)
       const int s = __ldg(start + p), L = __ldg(start + p + 1) - s;
       if (L > kShortRun) {
         longlist[atomicAdd(longcount, 1)] = int(p);
@@ -589,9 +591,11 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
   if (n > 0) {
     const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
     if (packed)
-      k_prep_packed<<<blocks, 256, 0, s>>>(packed, st, W, H, sb.pix, sb.val, g.C, flows_invalid, counts_invalid);
+      k_prep_packed<<<blocks, 256, 0, s>>>(packed, st, W, H, sb.pix, sb.val, sb.rank, g.C, flows_invalid,
+                                           counts_invalid);
     else
-      k_prep<<<blocks, 256, 0, s>>>(ev, st, delta_t, W, H, sb.pix, sb.val, g.C, flows_invalid, counts_invalid);
+      k_prep<<<blocks, 256, 0, s>>>(ev, st, delta_t, W, H, sb.pix, sb.val, sb.rank, g.C, flows_invalid,
+                                    counts_invalid);
     ++launches;
   }
   size_t scan_bytes = sb.temp_bytes;
@@ -606,15 +610,16 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
   // bandwidth-bound onesweep passes (cfg5 K1 3.7 ms vs 6.0 ms).
   const bool counting = !use_cub && double(n) <= 8.0 * double(P);
   if (n > 0 && counting) {
-    cudaMemsetAsync(sb.longcount, 0, sizeof(int), s);   // sb.cursor is zero (allocation, then k_runsort)
+    cudaMemsetAsync(sb.longcount, 0, sizeof(int), s);
     const int eb = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
-    launch_pdl(k_scatter, eb, 256, 0, s, sb.pix, sb.val, n, P, sb.start, sb.cursor, sb.val_s, sb.pix_s);
+    launch_pdl(k_scatter, eb, 256, 0, s, static_cast<const int32_t*>(sb.pix), static_cast<const uint64_t*>(sb.val),
+               static_cast<const int32_t*>(sb.rank), n, P, static_cast<const int*>(sb.start), sb.val_s, sb.pix_s);
     // pixels per runsort block step: ~2000 expected slots (fits the stage), 16..256 pixels
     const double mean_run = double(n) / double(std::max<int64_t>(P, 1));
     int ppb = 256;
     while (ppb > 16 && ppb * mean_run > 2000.0) ppb >>= 1;
     const int pb = int(std::min<int64_t>((P + ppb - 1) / ppb, 148 * 16));
-    launch_pdl(k_runsort, pb, 256, 0, s, sb.start, P, ppb, sb.val_s, sb.longlist, sb.longcount, sb.cursor);
+    launch_pdl(k_runsort, pb, 256, 0, s, static_cast<const int*>(sb.start), P, ppb, sb.val_s, sb.longlist, sb.longcount);
     launch_pdl(k_longsort, 148, 512, 0, s, sb.start, sb.val_s, sb.longlist, sb.longcount);
     launches += 3;
   } else if (n > 0) {

@@ -218,14 +218,15 @@ int ensure_sort(vkm_handle* h, int64_t n, int64_t Pv) {
   const size_t cap = size_t(std::max<int64_t>(n, 1));
   const size_t temp = vkm::sort_pairs_temp_bytes(int64_t(cap), Pv);
   if (h->sort_cap >= cap && h->sb.sort_temp_bytes >= temp) return VKM_OK;
-  void* arrs[] = {h->sb.pix, h->sb.val, h->sb.val_s, h->sb.pix_s, h->sb.sort_temp};
+  void* arrs[] = {h->sb.pix, h->sb.val, h->sb.val_s, h->sb.pix_s, h->sb.sort_temp, h->sb.rank};
   for (void* p : arrs)
     if (p) cudaFree(p);
-  h->sb.pix = nullptr; h->sb.val = nullptr; h->sb.val_s = nullptr; h->sb.pix_s = nullptr;
+  h->sb.pix = nullptr; h->sb.val = nullptr; h->sb.val_s = nullptr; h->sb.pix_s = nullptr; h->sb.rank = nullptr;
   h->sb.sort_temp = nullptr;
   h->sort_cap = 0;
   h->sb.sort_temp_bytes = 0;
   VKM_CK(cudaMalloc(&h->sb.pix, 4 * cap));
+  VKM_CK(cudaMalloc(&h->sb.rank, 4 * cap));
   VKM_CK(cudaMalloc(&h->sb.val, 8 * cap));
   VKM_CK(cudaMalloc(&h->sb.val_s, 8 * cap));
   VKM_CK(cudaMalloc(&h->sb.pix_s, 4 * cap));
@@ -239,11 +240,11 @@ int ensure_sort(vkm_handle* h, int64_t n, int64_t Pv) {
 // counts, pooled counts, run starts and the scan scratch.
 int ensure_grid(vkm_handle* h, int64_t Pv) {
   if (h->grid_cap >= Pv) return VKM_OK;
-  void* arrs[] = {h->G, h->Q, h->C, h->NQ, h->sb.start, h->sb.temp, h->sb.cursor, h->sb.longlist, h->sb.longcount};
+  void* arrs[] = {h->G, h->Q, h->C, h->NQ, h->sb.start, h->sb.temp, h->sb.longlist, h->sb.longcount};
   for (void* p : arrs)
     if (p) cudaFree(p);
   h->G = h->Q = nullptr;
-  h->C = h->NQ = h->sb.start = h->sb.cursor = h->sb.longlist = h->sb.longcount = nullptr;
+  h->C = h->NQ = h->sb.start = h->sb.longlist = h->sb.longcount = nullptr;
   h->sb.temp = nullptr;
   h->grid_cap = 0;
   VKM_CK(cudaMalloc(&h->G, sizeof(float2) * 8 * h->planes * Pv));
@@ -251,8 +252,6 @@ int ensure_grid(vkm_handle* h, int64_t Pv) {
   VKM_CK(cudaMalloc(&h->C, sizeof(int) * (Pv + 1)));
   VKM_CK(cudaMalloc(&h->NQ, sizeof(int) * Pv));
   VKM_CK(cudaMalloc(&h->sb.start, sizeof(int) * (Pv + 1)));
-  VKM_CK(cudaMalloc(&h->sb.cursor, sizeof(int) * (Pv + 1)));
-  VKM_CK(cudaMemset(h->sb.cursor, 0, sizeof(int) * (Pv + 1)));   // k_runsort re-zeroes it after each use
   VKM_CK(cudaMalloc(&h->sb.longlist, sizeof(int) * Pv));
   VKM_CK(cudaMalloc(&h->sb.longcount, sizeof(int)));
   h->sb.temp_bytes = vkm::sort_scan_temp_bytes(Pv);
@@ -630,7 +629,7 @@ void vkm_destroy(vkm_handle* h) {
   void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->myp, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
                   h->G, h->C, h->Q, h->NQ, h->feats, h->cnt_scratch, h->ev_stage, h->out_stage, h->cnt_stage,
                   h->sb.pix, h->sb.val, h->sb.start, h->sb.val_s, h->sb.pix_s, h->sb.temp, h->sb.sort_temp,
-                  h->sb.cursor, h->sb.longlist, h->sb.longcount};
+                  h->sb.rank, h->sb.longlist, h->sb.longcount};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->evt)

@@ -51,7 +51,7 @@ struct SortBufs {
   size_t temp_bytes;
   void* sort_temp;   // CUB radix-sort scratch (grown with n)
   size_t sort_temp_bytes;
-  int* cursor;       // [P+1] per-pixel fill cursors of the counting scatter
+  int32_t* rank;     // [n]   event's arrival rank inside its pixel (k_prep's histogram atomic)
   int* longlist;     // [P]   pixels whose run is longer than one warp sort
   int* longcount;    // [1]
 };
