@@ -344,6 +344,7 @@ def run_b200(args):
         return
 
     hbm_peak, tc_peak, peak_kind = load_peaks()
+    clk_mhz = clk.summary().get("sm_mhz")
     k1b, k2b, k3b = algorithmic_bytes(len(host[0]), P, p_occ[0])
     kernels = None
     roofline = None
@@ -369,6 +370,20 @@ def run_b200(args):
         roofline = {"bound": "hbm", "kernel": names[dom], "achieved": a, "peak": hbm_peak, "unit": "GB/s",
                     "frac": a / hbm_peak, "traffic": traffic, "alg_bytes_per_launch": int(byts[dom]),
                     "peak_kind": peak_kind}
+        # The encoder groups are instruction-issue bound (64 complex phases per
+        # event, twice): warp instructions per launch from the committed ncu
+        # capture of the same step (profiles/ncu_instr.json) over the group's
+        # live CUDA-event time, against 148 SMs x 4 schedulers x the SM clock.
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_instr.json")) as fh:
+                ins = json.load(fh).get(args.workload, {})
+            clk = clk_mhz or 1965.0
+            peak_issue = 148 * 4 * clk * 1e6
+            roofline["issue"] = {g: {"warp_instr_per_launch": ins[g], "achieved": ins[g] / (kernels[g]["ms"] * 1e-3),
+                                     "peak": peak_issue, "frac": ins[g] / (kernels[g]["ms"] * 1e-3) / peak_issue}
+                                 for g in names if g in ins}
+        except Exception:
+            pass
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
