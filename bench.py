@@ -377,8 +377,7 @@ def run_b200(args):
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_instr.json")) as fh:
                 ins = json.load(fh).get(args.workload, {})
-            clk = clk_mhz or 1965.0
-            peak_issue = 148 * 4 * clk * 1e6
+            peak_issue = 148 * 4 * (clk_mhz or 1965.0) * 1e6
             roofline["issue"] = {g: {"warp_instr_per_launch": ins[g], "achieved": ins[g] / (kernels[g]["ms"] * 1e-3),
                                      "peak": peak_issue, "frac": ins[g] / (kernels[g]["ms"] * 1e-3) / peak_issue}
                                  for g in names if g in ins}
