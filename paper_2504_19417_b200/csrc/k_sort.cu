@@ -258,16 +258,16 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
     float av0 = ld_a(jb + lane), av1 = ld_a(jb + 32 + lane);
 
     int k = 0;                                      // sweep index of the pixel being summed
-    int je = ends[0];
+    int je = ends[0], je_n = ends[1];               // run end of pixel k, and of k+1 (loaded a pixel early)
     float4 mc = __ldg(mxl + int64_t(min(max(xs, 0), W - 1)) * 32);
     uint64_t gr = 0, gi = 0, ar = 0, ai = 0;
     ulonglong2* pn = ring0;                          // ring slot of pixel k
     ulonglong2* po = ring0 + 32;                     // ring slot of pixel k - 2δx
+    ulonglong2 old = *po;                            // its value, read a pixel early (0 here)
     auto finish = [&]() {
       const uint64_t mre = f2pack(mc.x, mc.y), mim = f2pack(mc.z, mc.w);
       const uint64_t mr = fsub2(fmul2(gr, mre), fmul2(gi, mim));
       const uint64_t mi = ffma2(gr, mim, fmul2(gi, mre));
-      const ulonglong2 old = *po;
       *pn = make_ulonglong2(mr, mi);
       ar = fadd2(ar, mr);
       ai = fadd2(ai, mi);
@@ -283,8 +283,10 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
       gi = 0;
       pn = po;
       po = (po + 32 == ring_end) ? ring0 : po + 32;
+      old = *po;                                     // next trailing value: its slot is not written again before use
       ++k;
-      je = ends[k];
+      je = je_n;
+      je_n = ends[min(k + 1, nx)];                   // shared-memory latency off the per-pixel chain
       mc = __ldg(mxl + int64_t(min(max(xs + k, 0), W - 1)) * 32);   // next pixel's factor, in flight early
     };
 
