@@ -23,6 +23,9 @@
  *   vkm_predict_batch_host  the same loop over host buffers, with the H2D of
  *                     slice s+1 and the D2H of slice s-1 overlapping the kernels of
  *                     slice s (NormalFlowRegressor.predict_slices)
+ *   vkm_select_rows / vkm_scatter_rows  the device side of the multi-GPU
+ *                     row-strip split of one slice: strip
+ *                     partition with event halo, and the owned-flow gather
  *   vkm_last_error    exception text of the reference's error hierarchy (errors.py:4-29)
  *
  * Event layout: the reference's (n, 3) float64 array [t, x, y], row-major,
@@ -135,6 +138,21 @@ int vkm_predict_batch(vkm_handle* h, const double* events_dev, const int64_t* of
 int vkm_predict_batch_host(vkm_handle* h, const double* events_host, const int64_t* offsets_host,
                            int32_t n_slices, const double* t_starts_host, float* flows_host,
                            int32_t* counts_host);
+
+/* Spatial split, partition side: stable (time-order preserving) selection of
+ * the events of rows [y_lo, y_hi) of events_dev (n rows [t, x, y]) into
+ * out_events_dev (rows rebased by -y_lo), their row indices into
+ * out_index_dev and owned flags (row in [own_lo, own_hi)) into out_owned_dev;
+ * *count_host receives the number selected (the call synchronizes the
+ * handle's stream).  Outputs must hold n rows. */
+int vkm_select_rows(vkm_handle* h, const double* events_dev, int64_t n, int32_t y_lo, int32_t y_hi, int32_t own_lo,
+                    int32_t own_hi, double* out_events_dev, int64_t* out_index_dev, uint8_t* out_owned_dev,
+                    int64_t* count_host);
+
+/* Spatial split, gather side: dst_dev[index[i]] = src_dev[i] (rows of
+ * row_floats floats) for every i < m with mask_dev[i] != 0 (mask may be NULL). */
+int vkm_scatter_rows(vkm_handle* h, const float* src_dev, const int64_t* index_dev, const uint8_t* mask_dev,
+                     int64_t m, int32_t row_floats, float* dst_dev, void* stream);
 
 /* Parity hook: the per-pixel grid in the reference's PixelGrid layout.
  * grid_dev: (width, height, D) complex64 as interleaved f32 pairs, [x][y][d];

@@ -52,6 +52,8 @@ SIGNATURES = {
     "vkm_predict_batch": (C.c_int, [_P, _P, _I64, C.c_int32, _D, _P, _P, _P]),
     "vkm_predict_batch_host": (C.c_int, [_P, _P, _I64, C.c_int32, _D, _P, _P]),
     "vkm_grid": (C.c_int, [_P, _P, C.c_int64, C.c_double, C.c_int32, _P, _P, _P]),
+    "vkm_select_rows": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _I64]),
+    "vkm_scatter_rows": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int32, _P, _P]),
     "vkm_set_profiling": (C.c_int, [_P, C.c_int32]),
     "vkm_last_timings": (C.c_int, [_P, _F, _I32]),
 }

@@ -183,6 +183,8 @@ struct vkm_handle {
   uint2* hpack[2] = {nullptr, nullptr};   // page-locked packed-event staging (host)
   size_t hpack_cap[2] = {0, 0};
   HostPool* pool = nullptr;
+  uint8_t* sel_temp = nullptr;   // vkm_select_rows: count + CUB scratch
+  size_t sel_temp_cap = 0;
   // timing
   bool profiling = false;
   cudaEvent_t evt[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -643,6 +645,7 @@ void vkm_destroy(vkm_handle* h) {
   for (int i = 0; i < 2; ++i)
     if (h->hpack[i]) cudaFreeHost(h->hpack[i]);
   delete h->pool;
+  if (h->sel_temp) cudaFree(h->sel_temp);
   if (h->s_in) cudaStreamSynchronize(h->s_in), cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamSynchronize(h->s_out), cudaStreamDestroy(h->s_out);
   if (h->s_side) cudaStreamSynchronize(h->s_side), cudaStreamDestroy(h->s_side);
@@ -873,6 +876,37 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
   VKM_CK(cudaStreamSynchronize(sc));
   h->have_timing = false;
   h->last_launches = launches;
+  return VKM_OK;
+}
+
+int vkm_select_rows(vkm_handle* h, const double* ev, int64_t n, int32_t y_lo, int32_t y_hi, int32_t own_lo,
+                    int32_t own_hi, double* out_ev, int64_t* out_index, uint8_t* out_owned, int64_t* count_host) {
+  if (int rc = check_handle(h)) return rc;
+  if (n < 0 || !count_host) return fail(VKM_EINVAL, "bad arguments");
+  *count_host = 0;
+  if (n == 0) return VKM_OK;
+  if (!ev || !out_ev || !out_index || !out_owned) return fail(VKM_EINVAL, "null device buffer");
+  DeviceGuard dg(h->p.device);
+  const size_t temp_bytes = vkm::select_rows_temp_bytes(n);
+  int rc = grow(&h->sel_temp, &h->sel_temp_cap, std::max<size_t>(temp_bytes, 16) + 64);
+  if (rc) return rc;
+  int64_t* count_dev = reinterpret_cast<int64_t*>(h->sel_temp);   // first 8 bytes; CUB scratch after 64
+  vkm::launch_select_rows(ev, n, y_lo, y_hi, own_lo, own_hi, h->sel_temp + 64, temp_bytes, out_index, count_dev,
+                          out_ev, out_owned, h->stream);
+  VKM_CK(cudaGetLastError());
+  VKM_CK(cudaMemcpyAsync(count_host, count_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  VKM_CK(cudaStreamSynchronize(h->stream));
+  return VKM_OK;
+}
+
+int vkm_scatter_rows(vkm_handle* h, const float* src, const int64_t* index, const uint8_t* mask, int64_t m,
+                     int32_t row_floats, float* dst, void* stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (m < 0 || row_floats < 1) return fail(VKM_EINVAL, "bad arguments");
+  if (m > 0 && (!src || !index || !dst)) return fail(VKM_EINVAL, "null device buffer");
+  DeviceGuard dg(h->p.device);
+  vkm::launch_scatter_rows(src, index, mask, m, row_floats, dst, static_cast<cudaStream_t>(stream));
+  VKM_CK(cudaGetLastError());
   return VKM_OK;
 }
 

@@ -134,6 +134,17 @@ struct TcWeights {
 void launch_gather_mlp_tc(int64_t n, const DevTables& tb, int W, int H, const GridBufs& g, const SortBufs& sb,
                           const TcWeights& w, int mode, float* flows, int32_t* counts_out, int num_sms,
                           cudaStream_t s);
+// Spatial split (k_split.cu): stable selection of the events of rows
+// [y_lo, y_hi) with rows rebased by -y_lo, their global indices and an owned
+// flag for rows [own_lo, own_hi); count_dev receives the number selected.
+size_t select_rows_temp_bytes(int64_t n);
+void launch_select_rows(const double* ev, int64_t n, int y_lo, int y_hi, int own_lo, int own_hi, void* temp,
+                        size_t temp_bytes, int64_t* sel, int64_t* count_dev, double* out, uint8_t* owned,
+                        cudaStream_t s);
+// dst[index[i]] = src[i] (rows of row_floats floats) where mask[i] != 0 (mask may be null).
+void launch_scatter_rows(const float* src, const int64_t* index, const uint8_t* mask, int64_t m, int row_floats,
+                         float* dst, cudaStream_t s);
+
 // Host helper: build the UMMA smem image (K-major, 128B swizzle) of a 128x128 fp16/bf16 matrix.
 void build_umma_image_kmajor_128x128(const uint16_t* rowmajor, uint16_t* image);
 

@@ -144,3 +144,111 @@ def predict_spatial(engine_factory, events: np.ndarray, t_start: float, width: i
         return (flows, counts) if return_counts else flows
     out = assemble(len(events), parts, fl, ct)
     return out if return_counts else out[0]
+
+
+def _is_gloo(group=None) -> bool:
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
+def _send(t, dst, group=None):
+    import torch.distributed as dist
+    dist.send(t.cpu() if _is_gloo(group) else t, dst, group=group)
+
+
+def _recv(shape, dtype, src, device, group=None):
+    import torch
+    import torch.distributed as dist
+    if _is_gloo(group):
+        buf = torch.empty(shape, dtype=dtype)
+        dist.recv(buf, src, group=group)
+        return buf.to(device)
+    buf = torch.empty(shape, dtype=dtype, device=device)
+    dist.recv(buf, src, group=group)
+    return buf
+
+
+def predict_spatial_device(make_engine, events, t_start: float, width: int, height: int, delta_y: int,
+                           world: int = 1, rank: int = 0, group=None, device=None):
+    """Device-resident row-strip split of one oversized slice (SURVEY.md §8e,
+    config 5): the data path never leaves the GPUs.
+
+    Rank 0 holds the slice as a CUDA (n, 3) float64 tensor (other ranks pass
+    None).  Rank 0 builds the row histogram on its GPU and the strips on the
+    host (a few hundred integers, broadcast); for every rank it selects the
+    strip's events plus the δy-row halo with vkm_select_rows (stable, rows
+    rebased, owned flags) and sends them over NCCL (NVLink peer-to-peer on an
+    NVSwitch box).  Each rank runs its strip through `make_engine(strip_height)`
+    (a FlowEngine) on its own GPU with the global t_start, so every phase is
+    bit-identical to the unsplit slice; only the flows travel back (rank 0
+    kept the indices and owned flags) and vkm_scatter_rows puts the owned
+    rows into slice order on GPU 0.  Returns the (n, 2) float32 flows tensor
+    on rank 0, None elsewhere.  (gloo groups stage the messages through host
+    memory, for CPU-only plumbing tests.)"""
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from . import _lib
+
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    distributed = world > 1
+    if rank == 0:
+        n = int(events.shape[0])
+        rows = torch.bincount(events[:, 2].to(torch.int64), minlength=height).cpu().numpy()
+        strips = row_strips(rows, world, delta_y)
+        hdr = [strips, n]
+    else:
+        hdr = [None, None]
+    if distributed:
+        dist.broadcast_object_list(hdr, src=0, group=group)
+    strips, n = hdr
+    mine = strips[rank]
+    eng = make_engine(mine.height)
+    lib = _lib.load()
+    stream = torch.cuda.current_stream(device)
+
+    def select(r):
+        s = strips[r]
+        m = C.c_int64()
+        out = torch.empty((n, 3), dtype=torch.float64, device=device)
+        idx = torch.empty(n, dtype=torch.int64, device=device)
+        own = torch.empty(n, dtype=torch.uint8, device=device)
+        stream.synchronize()
+        _lib.check(lib.vkm_select_rows(eng._h, C.c_void_p(events.data_ptr()), n, s.in_lo, s.in_hi, s.lo, s.hi,
+                                       C.c_void_p(out.data_ptr()), C.c_void_p(idx.data_ptr()),
+                                       C.c_void_p(own.data_ptr()), C.byref(m)))
+        k = int(m.value)
+        return out[:k].contiguous(), idx[:k], own[:k]
+
+    parts = {}
+    if rank == 0:
+        for r in range(world):
+            ev_r, idx_r, own_r = select(r)
+            parts[r] = (idx_r, own_r)
+            if r == 0:
+                my_ev = ev_r
+            else:
+                _send(torch.tensor([ev_r.shape[0]], dtype=torch.int64, device=device), r, group)
+                if ev_r.shape[0]:
+                    _send(ev_r, r, group)
+    else:
+        k = int(_recv((1,), torch.int64, 0, device, group).item())
+        my_ev = _recv((k, 3), torch.float64, 0, device, group) if k else torch.empty((0, 3), dtype=torch.float64,
+                                                                                        device=device)
+    flows_mine = eng.predict_device(my_ev, t_start) if my_ev.shape[0] else torch.empty((0, 2), dtype=torch.float32,
+                                                                                        device=device)
+    if rank != 0:
+        if flows_mine.shape[0]:
+            _send(flows_mine, 0, group)
+        return None
+    out = torch.full((n, 2), float("nan"), dtype=torch.float32, device=device)
+    for r in range(world):
+        idx_r, own_r = parts[r]
+        f_r = flows_mine if r == 0 else (_recv((idx_r.shape[0], 2), torch.float32, r, device, group)
+                                         if idx_r.shape[0] else None)
+        if f_r is not None and idx_r.shape[0]:
+            _lib.check(lib.vkm_scatter_rows(eng._h, C.c_void_p(f_r.data_ptr()), C.c_void_p(idx_r.data_ptr()),
+                                            C.c_void_p(own_r.data_ptr()), idx_r.shape[0], 2,
+                                            C.c_void_p(out.data_ptr()), C.c_void_p(stream.cuda_stream)))
+    return out

@@ -454,3 +454,47 @@ def test_host_batch_packing_edge_cases():
         assert out.returncode == 0, out.stderr[-2000:]
         np.testing.assert_array_equal(np.load(os.path.join(td, "c.npy")), counts)
         np.testing.assert_array_equal(np.load(os.path.join(td, "f.npy")), flows)
+
+
+def _spatial_worker(rank, world, port, W, H, d, path, out_path):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_2504_19417_b200 as pkg
+    from paper_2504_19417_b200 import sharding
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    X = np.load(path)
+    ev = torch.from_numpy(X).cuda() if rank == 0 else None
+    out = sharding.predict_spatial_device(lambda h: pkg.FlowEngine(W, h, d, d, 0.016, b, w), ev, float(X[0, 0]),
+                                          W, H, d, world, rank)
+    if rank == 0:
+        np.save(out_path, out.cpu().numpy())
+    dist.destroy_process_group()
+
+
+def test_spatial_split_device_path_two_ranks(tmp_path):
+    """Device-resident row-strip split (vkm_select_rows partition, strip runs,
+    vkm_scatter_rows gather) with two ranks sharing this GPU (gloo stages the
+    messages through host memory): equal to the unsplit slice (flows within
+    f32 rounding of the different x/y segmentations)."""
+    import socket
+    import torch.multiprocessing as mp
+    pkg = _pkg()
+    W, H, d, n = 200, 160, 10, 120_000
+    X = vo.synth_uniform_noise(n, W, H, seed=21)
+    path, out_path = str(tmp_path / "X.npy"), str(tmp_path / "f.npy")
+    np.save(path, X)
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    mp.spawn(_spatial_worker, args=(2, port, W, H, d, path, out_path), nprocs=2, join=True)
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    full = pkg.FlowEngine(W, H, d, d, 0.016, b, w).predict_host(X, float(X[0, 0]))
+    got = np.load(out_path)
+    assert np.isfinite(got).all()
+    np.testing.assert_allclose(got, full, rtol=0, atol=1e-5)
