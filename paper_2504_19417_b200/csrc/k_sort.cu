@@ -674,12 +674,8 @@ void launch_reduce_x(const DevTables& tb, int W, int H, int nb, int dx, const So
   const int variant = variant_env >= 0 ? variant_env : (dx >= 16 ? 1 : 0);
   if (variant == 1) {   // one channel per lane, two warps per item
     const size_t smem = reduce_x1_smem(dx);
-    static bool attr1 = false;
-    if (!attr1) {
-      cudaFuncSetAttribute(k_reduce_x1, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(reduce_x1_smem(kMaxFusedDx)));
-      attr1 = true;
-    }
+    // per call: the attribute is per device, and one process may drive several
+    cudaFuncSetAttribute(k_reduce_x1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(reduce_x1_smem(kMaxFusedDx)));
     int per = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reduce_x1, kRx1Warps * 32, smem);
     const int64_t res_items = int64_t(std::max(1, per)) * num_sms * (kRx1Warps / 2);
@@ -693,11 +689,7 @@ void launch_reduce_x(const DevTables& tb, int W, int H, int nb, int dx, const So
     return;
   }
   const size_t smem = reduce_x_smem(dx);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_reduce_x, cudaFuncAttributeMaxDynamicSharedMemorySize, int(reduce_x_smem(kMaxFusedDx)));
-    attr = true;
-  }
+  cudaFuncSetAttribute(k_reduce_x, cudaFuncAttributeMaxDynamicSharedMemorySize, int(reduce_x_smem(kMaxFusedDx)));
   int per = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reduce_x, kRxWarps * 32, smem);
   const int64_t res_warps = int64_t(std::max(1, per)) * num_sms * kRxWarps;
