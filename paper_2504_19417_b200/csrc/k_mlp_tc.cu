@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float rs = __shfl_sync(0xffffffffu, rs_reg, u);
         const uint32_t m = warp * kRows + u;
         uint64_t sn, cs;
-        VKM_SINCOS_HOT(fmul2(f2pack(aj, aj), T01), sn, cs);
+        VKM_SINCOS_K3(fmul2(f2pack(aj, aj), T01), sn, cs);
         // conj(phase) * acc / cnt for channels (c0, c0+1), packed
         const uint64_t ar = f2pack(src_u.x, src_u.y), ai = f2pack(src_u.z, src_u.w);   // packed pairs
         const uint64_t rs2 = f2pack(rs, rs);

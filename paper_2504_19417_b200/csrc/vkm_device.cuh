@@ -181,6 +181,13 @@ __device__ __forceinline__ void sincos2p_f32(uint64_t theta, uint64_t& s01, uint
 #define VKM_SINCOS_HOT sincos2p_f32
 #endif
 #define VKM_SINCOS_CS sincos2_cs
+// K3 de-phase: the pi-reduced variant by default (K3 is issue-bound since the
+// metadata pipeline; -DVKM_K3_ACCURATE_SINCOS restores the accurate one).
+#ifdef VKM_K3_ACCURATE_SINCOS
+#define VKM_SINCOS_K3 sincos2p_f32
+#else
+#define VKM_SINCOS_K3 sincos2p_pi
+#endif
 
 // a = f32((t - t0) / delta_t): f64 rebase and divide, then one rounding to f32,
 // exactly as rebase_slice (events.py:390-407) + _temporal_phases
