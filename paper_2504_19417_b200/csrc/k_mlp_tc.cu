@@ -269,12 +269,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float rs = __shfl_sync(0xffffffffu, rs_reg, u);
         const uint32_t m = warp * kRows + u;
         uint64_t sn, cs;
-        VKM_SINCOS_K3(fmul2(f2pack(aj, aj), T01), sn, cs);
-        // conj(phase) * acc / cnt for channels (c0, c0+1), packed
+        // conj(phase) * acc / cnt for channels (c0, c0+1), packed; the ÷count
+        // (and fp16 pre-scale) rides on the sin/cos sign fix-up
+        VKM_SINCOS_K3_SCALED(fmul2(f2pack(aj, aj), T01), f2pack(rs, rs), sn, cs);
         const uint64_t ar = f2pack(src_u.x, src_u.y), ai = f2pack(src_u.z, src_u.w);   // packed pairs
-        const uint64_t rs2 = f2pack(rs, rs);
-        const uint64_t re = fmul2(ffma2(sn, ai, fmul2(cs, ar)), rs2);
-        const uint64_t im = fmul2(ffma2(fneg2(sn), ar, fmul2(cs, ai)), rs2);
+        const uint64_t re = ffma2(sn, ai, fmul2(cs, ar));
+        const uint64_t im = fsub2(fmul2(cs, ai), fmul2(sn, ar));
         // umma_off(m, c0) and umma_off(m, 64 + c0) with the lane parts hoisted
         const uint32_t ore = (m >> 3) * 1024 + (m & 7) * 128 + ((lane_chunk ^ (m & 7)) << 4) + lane_byte;
         const uint32_t oim = ore + kAtomBytes;

@@ -161,6 +161,35 @@ __device__ __forceinline__ void sincos2_cs(uint64_t theta, uint64_t& cs0, uint64
   cs1 = f2pack(c1, s1);
 }
 
+// sincos2p_pi with a per-pair scale folded into the sign fix-up:
+// s01 = scale·sin, c01 = scale·cos (scale01 = (k0, k1)).  The quadrant sign
+// rides on the scale (one 64-bit XOR), so scaling costs two mul.f32x2 in
+// place of the four sign XORs.
+__device__ __forceinline__ void sincos2p_pi_scaled(uint64_t x, uint64_t scale01, uint64_t& s01, uint64_t& c01) {
+  const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
+  const uint64_t qb = ffma2(x, f2pack(0.318309886f, 0.318309886f), magic);
+  const uint64_t q = fsub2(qb, magic);
+  uint64_t r = ffma2(q, f2pack(-3.14159203e+00f, -3.14159203e+00f), x);
+  r = ffma2(q, f2pack(-6.27832946e-07f, -6.27832946e-07f), r);
+  r = ffma2(q, f2pack(-1.07806051e-14f, -1.07806051e-14f), r);
+  const uint64_t u = fmul2(r, r);
+  uint64_t ps = ffma2(f2pack(-2.384669173e-08f, -2.384669173e-08f), u, f2pack(2.752261935e-06f, 2.752261935e-06f));
+  ps = ffma2(ps, u, f2pack(-1.984080445e-04f, -1.984080445e-04f));
+  ps = ffma2(ps, u, f2pack(8.333330043e-03f, 8.333330043e-03f));
+  ps = ffma2(ps, u, f2pack(-1.666666716e-01f, -1.666666716e-01f));
+  ps = fmul2(ps, u);
+  const uint64_t sr = ffma2(ps, r, r);
+  uint64_t pc = ffma2(f2pack(1.991995235e-09f, 1.991995235e-09f), u, f2pack(-2.752566104e-07f, -2.752566104e-07f));
+  pc = ffma2(pc, u, f2pack(2.480107105e-05f, 2.480107105e-05f));
+  pc = ffma2(pc, u, f2pack(-1.388888457e-03f, -1.388888457e-03f));
+  pc = ffma2(pc, u, f2pack(4.166666791e-02f, 4.166666791e-02f));
+  pc = ffma2(pc, u, f2pack(-5.000000000e-01f, -5.000000000e-01f));
+  const uint64_t cr = ffma2(pc, u, f2pack(1.0f, 1.0f));
+  const uint64_t f = scale01 ^ ((qb << 31) & 0x8000000080000000ull);
+  s01 = fmul2(sr, f);
+  c01 = fmul2(cr, f);
+}
+
 // Packed-in/packed-out variant: theta = (x0, x1), returns (s0, s1), (c0, c1).
 __device__ __forceinline__ void sincos2p_f32(uint64_t theta, uint64_t& s01, uint64_t& c01) {
   float x0, x1, s0, c0, s1, c1;
@@ -184,9 +213,14 @@ __device__ __forceinline__ void sincos2p_f32(uint64_t theta, uint64_t& s01, uint
 // K3 de-phase: the pi-reduced variant by default (K3 is issue-bound since the
 // metadata pipeline; -DVKM_K3_ACCURATE_SINCOS restores the accurate one).
 #ifdef VKM_K3_ACCURATE_SINCOS
-#define VKM_SINCOS_K3 sincos2p_f32
+#define VKM_SINCOS_K3_SCALED(x, k, s, c) \
+  do {                                    \
+    sincos2p_f32((x), (s), (c));          \
+    (s) = fmul2((s), (k));                \
+    (c) = fmul2((c), (k));                \
+  } while (0)
 #else
-#define VKM_SINCOS_K3 sincos2p_pi
+#define VKM_SINCOS_K3_SCALED sincos2p_pi_scaled
 #endif
 
 // a = f32((t - t0) / delta_t): f64 rebase and divide, then one rounding to f32,
