@@ -210,7 +210,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float4* Q4 = reinterpret_cast<const float4*>(Q);
     const int plane = lane >> 2, q4 = lane & 3;
     constexpr int kRows = kM / kProdWarps;        // 8
-    const uint32_t lane_chunk = uint32_t(lane >> 2), lane_byte = uint32_t(lane & 3) * 4;
+    // K position of this lane's values: 4·lane (see feature_kpos)
+    const uint32_t lane_atom = uint32_t(lane >> 4) * kAtomBytes;
+    const uint32_t lane_chunk = uint32_t(lane & 15) >> 1, lane_byte = uint32_t(lane & 1) * 8;
     // lanes 0..7 hold the metadata of the warp's 8 rows
     // Slot metadata is pipelined over three tiles so no load is consumed right
     // after it issues: (pixel, time argument) two tiles ahead, the pooled count
@@ -275,9 +277,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t ar = f2pack(src_u.x, src_u.y), ai = f2pack(src_u.z, src_u.w);   // packed pairs
         const uint64_t re = ffma2(sn, ai, fmul2(cs, ar));
         const uint64_t im = fsub2(fmul2(cs, ai), fmul2(sn, ar));
-        // umma_off(m, c0) and umma_off(m, 64 + c0) with the lane parts hoisted
-        const uint32_t ore = (m >> 3) * 1024 + (m & 7) * 128 + ((lane_chunk ^ (m & 7)) << 4) + lane_byte;
-        const uint32_t oim = ore + kAtomBytes;
+        // Feature order on the K axis is (Re c, Re c+1, Im c, Im c+1) per
+        // channel pair (W1's columns are permuted to match on the host), so a
+        // lane's four values are 8 contiguous bytes: one 64-bit store per image.
+        const uint32_t off = lane_atom + (m >> 3) * 1024 + (m & 7) * 128 + ((lane_chunk ^ (m & 7)) << 4) + lane_byte;
         float re0, re1, im0, im1;
         f2unpack(re, re0, re1);
         f2unpack(im, im0, im1);
@@ -288,15 +291,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           float l0, l1, l2, l3;
           f2unpack(fsub2(re, f2pack(fre.x, fre.y)), l0, l1);
           f2unpack(fsub2(im, f2pack(fim.x, fim.y)), l2, l3);
-          *reinterpret_cast<__half2*>(ah + ore) = hre;
-          *reinterpret_cast<__half2*>(ah + oim) = him;
-          *reinterpret_cast<__half2*>(al + ore) = __floats2half2_rn(l0, l1);
-          *reinterpret_cast<__half2*>(al + oim) = __floats2half2_rn(l2, l3);
+          const __half2 lre = __floats2half2_rn(l0, l1), lim = __floats2half2_rn(l2, l3);
+          *reinterpret_cast<uint2*>(ah + off) =
+              make_uint2(*reinterpret_cast<const uint32_t*>(&hre), *reinterpret_cast<const uint32_t*>(&him));
+          *reinterpret_cast<uint2*>(al + off) =
+              make_uint2(*reinterpret_cast<const uint32_t*>(&lre), *reinterpret_cast<const uint32_t*>(&lim));
         } else {
-          *reinterpret_cast<__nv_bfloat162*>(ah + ore) = __floats2bfloat162_rn(re0, re1);
-          *reinterpret_cast<__nv_bfloat162*>(ah + oim) = __floats2bfloat162_rn(im0, im1);
-        }
-      }
+          const __nv_bfloat162 bre = __floats2bfloat162_rn(re0, re1), bim = __floats2bfloat162_rn(im0, im1);
+          *reinterpret_cast<uint2*>(ah + off) =
+              make_uint2(*reinterpret_cast<const uint32_t*>(&bre), *reinterpret_cast<const uint32_t*>(&bim));
+        }      }
     };
 
     const int64_t G = gridDim.x;
@@ -428,6 +432,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 }  // namespace tc
+
+int feature_kpos(int f) {   // [Re(0..63) | Im(0..63)] -> per channel pair (Re c, Re c+1, Im c, Im c+1)
+  const int c = f & 63, im = f >> 6;
+  return 4 * (c >> 1) + 2 * im + (c & 1);
+}
 
 void build_umma_image_kmajor_128x128(const uint16_t* rowmajor, uint16_t* image) {
   for (uint32_t m = 0; m < 128; ++m)

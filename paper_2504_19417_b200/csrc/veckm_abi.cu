@@ -599,13 +599,16 @@ int vkm_create(vkm_handle** out, const vkm_params* params, const double* T, cons
       h->w_scale_f16 = std::ldexp(1.0f, e);
       std::vector<uint16_t> hi(128 * 128), lo(128 * 128), bf(128 * 128);
       for (int i = 0; i < 128 * 128; ++i) {
+        // column f of W1 goes to K position feature_kpos(f) of the operand image
+        const int r = i >> 7, f = i & 127;
+        const int j = r * 128 + vkm::feature_kpos(f);
         const float v = w1p[i] * h->w_scale_f16;
         const __half vh = __float2half_rn(v);
         const __half vl = __float2half_rn(v - __half2float(vh));
-        std::memcpy(&hi[i], &vh, 2);
-        std::memcpy(&lo[i], &vl, 2);
+        std::memcpy(&hi[j], &vh, 2);
+        std::memcpy(&lo[j], &vl, 2);
         const __nv_bfloat16 vb = __float2bfloat16_rn(w1p[i]);
-        std::memcpy(&bf[i], &vb, 2);
+        std::memcpy(&bf[j], &vb, 2);
       }
       std::vector<uint16_t> img(128 * 128);
       VKM_CKH(cudaMalloc(&h->w1_f16_hi, 2 * 128 * 128));

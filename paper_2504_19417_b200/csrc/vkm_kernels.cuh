@@ -145,6 +145,9 @@ void launch_select_rows(const double* ev, int64_t n, int y_lo, int y_hi, int own
 void launch_scatter_rows(const float* src, const int64_t* index, const uint8_t* mask, int64_t m, int row_floats,
                          float* dst, cudaStream_t s);
 
+// K position of feature f ([Re(0..63) | Im(0..63)]) in the tensor-core head's
+// operand images: channel pairs (Re c, Re c+1, Im c, Im c+1) are contiguous.
+int feature_kpos(int f);
 // Host helper: build the UMMA smem image (K-major, 128B swizzle) of a 128x128 fp16/bf16 matrix.
 void build_umma_image_kmajor_128x128(const uint16_t* rowmajor, uint16_t* image);
 
