@@ -14,7 +14,7 @@ import threading
 from .errors import DimensionMismatchError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libveckm.so")
+LIB_PATH = os.environ.get("VKM_LIB") or os.path.join(HERE, "libveckm.so")   # VKM_LIB: A/B of builds (tools)
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "veckm.h")
 
 VKM_OK, VKM_EINVAL, VKM_EDIM, VKM_ECUDA, VKM_EOOM, VKM_EUNSUPPORTED = range(6)

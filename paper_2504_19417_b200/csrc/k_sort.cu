@@ -207,7 +207,10 @@ __global__ void __launch_bounds__(256) k_reduce_small(const int* __restrict__ st
 // boundaries are tracked from start[] (32 run ends per coalesced load).
 // ---------------------------------------------------------------------------
 constexpr int kMaxFusedDx = 24;
-constexpr int kRxWarps = 2;
+#ifndef VKM_RX_WARPS
+#define VKM_RX_WARPS 1   // one-warp CTAs spread the items over the SMs most evenly (cfg2 K1 -4.6 % vs 2)
+#endif
+constexpr int kRxWarps = VKM_RX_WARPS;   // warps (items) per CTA
 constexpr int kRxMaxSeg = 128;
 constexpr int kRxEnds = kRxMaxSeg + 2 * kMaxFusedDx + 4 + 64;   // run ends of one sweep (+ sentinel) + 64-float stage
 #ifndef VKM_RX_GROUP
