@@ -250,10 +250,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (cp.async, 16 B per lane, zero-filled for empty slots), so the
     // L2/HBM latency of the gathers overlaps the de-phase/split work.
     float4* const ring = &S.qring[warp][0][lane];
+    // lane-constant parts of the gather (global plane base, shared ring slot 0)
+    // hoisted: per row only the pixel offset and the slot offset are added
+    const float4* const qlane = Q4 + ((int64_t(plane) * P) << 2) + q4;
+    const uint32_t ring_s = smem_u32(ring);
     auto issue_row = [&](int pj, int slot) {
-      const float4* src = Q4 + ((int64_t(plane) * P + (pj >= 0 ? pj : 0)) << 2) + q4;
+      const float4* src = qlane + (int64_t(pj >= 0 ? pj : 0) << 2);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n\tcp.async.commit_group;" ::"r"(
-                       smem_u32(ring + slot * 32)),
+                       ring_s + uint32_t(slot) * 512u),
                    "l"(src), "r"(pj >= 0 ? 16 : 0)
                    : "memory");
     };
@@ -285,12 +289,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         f2unpack(re, re0, re1);
         f2unpack(im, im0, im1);
         if (kSplit) {
-          const __half2 hre = __floats2half2_rn(re0, re1);
-          const __half2 him = __floats2half2_rn(im0, im1);
-          const float2 fre = __half22float2(hre), fim = __half22float2(him);
-          float l0, l1, l2, l3;
-          f2unpack(fsub2(re, f2pack(fre.x, fre.y)), l0, l1);
-          f2unpack(fsub2(im, f2pack(fim.x, fim.y)), l2, l3);
+          // hi = the value truncated to fp16's 11 significant bits (clearing
+          // 13 mantissa bits: ALU LOP3s instead of fp16->f32 conversions on
+          // the FMA pipe); exact in fp16 for |x| >= 2^-14, and below that its
+          // rounding is < 2^-25 absolute.  lo = x - hi is exact in f32.
+          const uint64_t tmask = 0xFFFFE000FFFFE000ull;
+          const uint64_t tre = re & tmask, tim = im & tmask;
+          float h0, h1, h2, h3, l0, l1, l2, l3;
+          f2unpack(tre, h0, h1);
+          f2unpack(tim, h2, h3);
+          f2unpack(fsub2(re, tre), l0, l1);
+          f2unpack(fsub2(im, tim), l2, l3);
+          const __half2 hre = __floats2half2_rn(h0, h1), him = __floats2half2_rn(h2, h3);
           const __half2 lre = __floats2half2_rn(l0, l1), lim = __floats2half2_rn(l2, l3);
           *reinterpret_cast<uint2*>(ah + off) =
               make_uint2(*reinterpret_cast<const uint32_t*>(&hre), *reinterpret_cast<const uint32_t*>(&him));
