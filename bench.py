@@ -273,14 +273,25 @@ def run_b200(args):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    if slices == 1:
-        eng.set_profiling(True)
-        for _ in range(max(5, min(20, args.steps))):
-            flush.zero_()
+    # Per-kernel times: one launch sequence per profiled step.  Batched
+    # slices: the first chunk's worth (the slices one launch sequence takes,
+    # pixel budget VKM_BATCH_PIXELS, default 4 Mpx, at most 64 slices).
+    kslices = 1
+    if slices > 1:
+        kslices = int(max(1, min(64, slices, int(os.environ.get("VKM_BATCH_PIXELS", 1 << 22)) // P)))
+    eng.set_profiling(True)
+    for _ in range(max(5, min(20, args.steps))):
+        flush.zero_()
+        if slices > 1:
+            eng.predict_batch_device(ev_all[: int(offs_all[kslices])], offs_all[: kslices + 1], t0s[:kslices],
+                                     flows=fl_all, stream=stream)
+        else:
             step()
-            kern.append(eng.last_timings()[0])
-        eng.set_profiling(False)
-        torch.cuda.synchronize()
+        t = eng.last_timings()[0]
+        if len(t) >= 3 and min(t[:3]) > 0:   # -1: no per-kernel events for this call
+            kern.append(t)
+    eng.set_profiling(False)
+    torch.cuda.synchronize()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(sum(step_ms))
     if world > 1:
@@ -345,7 +356,11 @@ def run_b200(args):
 
     hbm_peak, tc_peak, peak_kind = load_peaks()
     clk_mhz = clk.summary().get("sm_mhz")
-    k1b, k2b, k3b = algorithmic_bytes(len(host[0]), P, p_occ[0])
+    k1b = k2b = k3b = 0
+    n_prof = 0
+    for i in range(kslices):   # the slices of one profiled launch sequence
+        b1, b2, b3 = algorithmic_bytes(len(host[i]), P, p_occ[i])
+        k1b, k2b, k3b, n_prof = k1b + b1, k2b + b2, k3b + b3, n_prof + len(host[i])
     kernels = None
     roofline = None
     if kern:
@@ -356,7 +371,7 @@ def run_b200(args):
         for i, nm in enumerate(names):
             gbs = byts[i] / (avg[i] * 1e-3) / 1e9
             kernels[nm] = {"ms": float(avg[i]), "alg_bytes": int(byts[i]), "gbs": gbs, "frac_hbm": gbs / hbm_peak}
-        mlp_tflops = 33280.0 * n / (avg[2] * 1e-3) / 1e12
+        mlp_tflops = 33280.0 * n_prof / (avg[2] * 1e-3) / 1e12
         kernels["gather_mlp"]["mlp_tflops"] = mlp_tflops
         kernels["gather_mlp"]["frac_tensor_bf16"] = mlp_tflops / tc_peak
         dom = int(np.argmax(avg[:3]))

@@ -770,6 +770,7 @@ int vkm_predict_batch(vkm_handle* h, const double* ev, const int64_t* offsets, i
   int launches = 0;
   rec(h, 0, sm);
   // chunks of up to kMaxBatch slices (pixel budget batch_pixels) share one launch sequence
+  int chunks = 0;
   for (int s = 0; s < n_slices;) {
     vkm::SliceTab st;
     const int s1 = next_chunk(h, offsets, n_slices, t_starts, s, st);
@@ -777,11 +778,13 @@ int vkm_predict_batch(vkm_handle* h, const double* ev, const int64_t* offsets, i
     if (st.nb > 0) {
       int rc = predict_chunk(h, ev + 3 * lo, st, flows + 2 * lo, counts ? counts + lo : nullptr, sm, &launches);
       if (rc) return rc;
+      ++chunks;
     }
     s = s1;
   }
   rec(h, 3, sm);
-  h->have_timing = false;  // per-chunk events are overwritten; only the total is meaningful
+  // per-kernel events are overwritten per chunk: meaningful for a one-chunk call
+  h->have_timing = h->profiling && chunks == 1;
   h->last_launches = launches;
   return VKM_OK;
 }
