@@ -74,6 +74,12 @@ __global__ void __launch_bounds__(256) k_box_y(const float2* __restrict__ M, flo
 #define VKM_YU 4
 #endif
 constexpr int kYU = VKM_YU;   // rows per batched step of the packed y pass
+//
+// Odd segments sweep upwards (d = -1), even ones downwards, so the two
+// segments on either side of a boundary read the rows around it at the same
+// time (both at their start, or both at their end): the 2δy-row warm-up of one
+// segment is the other's lead rows, served by one DRAM read instead of two.
+// The window update is acc += R[y + dδ] (lead), out(y), acc -= R[y - dδ].
 __global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ Rin, float4* __restrict__ Q, int W,
                                                      int H, int segs, int dy, int RS, int64_t P,
                                                      const float4* __restrict__ mxp,
@@ -81,8 +87,10 @@ __global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ 
   pdl_wait();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= W * 4) return;
-  const int slice = blockIdx.y / segs;
-  const int y0 = (blockIdx.y - slice * segs) * RS, y1 = min(H, y0 + RS);
+  const int slice = blockIdx.y / segs, seg = blockIdx.y - slice * segs;
+  const int y0 = seg * RS, y1 = min(H, y0 + RS);
+  const int d = (seg & 1) ? -1 : 1;
+  const int ys = d > 0 ? y0 : y1 - 1, ny = y1 - y0;   // rows ys, ys + d, ... (ny of them)
   const int pair = int(blockIdx.z) * 4 + (idx & 3);
   const int64_t base = (int64_t(blockIdx.z) * P + int64_t(slice) * H * W) * 4 + idx;
   const ulonglong2* Rp = reinterpret_cast<const ulonglong2*>(Rin) + base;
@@ -94,33 +102,35 @@ __global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ 
   // lead rows stay in L2 (evict_last) until the trailing edge re-reads them
   // 2δy+1 rows later (evict_first)
   const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
-  auto ld = [&](const ulonglong2* p, uint64_t pol) {
-    ulonglong2 v;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
-        : "=l"(v.x), "=l"(v.y)
-        : "l"(p), "l"(pol));
+  auto ld = [&](int y, uint64_t pol) {   // row y of the column, zero outside the image
+    ulonglong2 v = make_ulonglong2(0ull, 0ull);
+    if (y >= 0 && y < H)
+      asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+          : "=l"(v.x), "=l"(v.y)
+          : "l"(Rp + int64_t(y) * rs), "l"(pol));
     return v;
   };
   uint64_t ar = 0, ai = 0;
-  for (int y = max(0, y0 - dy); y < min(H, y0 + dy); ++y) {
-    const ulonglong2 v = ld(Rp + int64_t(y) * rs, keep);
+  for (int j = -dy; j < dy; ++j) {   // window of ys without its lead row
+    const ulonglong2 v = ld(ys + d * j, keep);
     ar = fadd2(ar, v.x);
     ai = fadd2(ai, v.y);
   }
-  for (int y = y0; y < y1; y += kYU) {
+  for (int i = 0; i < ny; i += kYU) {
     ulonglong2 lv[kYU], tv[kYU];
     float4 fm[kYU];
 #pragma unroll
     for (int u = 0; u < kYU; ++u) {
-      const int yy = y + u;
-      const bool ok = yy < y1;
-      lv[u] = (ok && yy + dy < H) ? ld(Rp + int64_t(yy + dy) * rs, keep) : make_ulonglong2(0ull, 0ull);
-      tv[u] = (ok && yy - dy >= 0) ? ld(Rp + int64_t(yy - dy) * rs, drop) : make_ulonglong2(0ull, 0ull);
-      fm[u] = ok ? __ldg(myc + int64_t(yy) * D2) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const bool ok = i + u < ny;
+      const int y = ys + d * (i + u);
+      lv[u] = ok ? ld(y + d * dy, keep) : make_ulonglong2(0ull, 0ull);
+      tv[u] = ok ? ld(y - d * dy, drop) : make_ulonglong2(0ull, 0ull);
+      fm[u] = ok ? __ldg(myc + int64_t(y) * D2) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < kYU; ++u) {
-      if (y + u < y1) {
+      if (i + u < ny) {
+        const int y = ys + d * (i + u);
         ar = fadd2(ar, lv[u].x);
         ai = fadd2(ai, lv[u].y);
         const uint64_t fyr = f2pack(fm[u].x, fm[u].y), fyi = f2pack(fm[u].z, fm[u].w);
@@ -129,7 +139,7 @@ __global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ 
         const uint64_t fi = ffma2(fxr, fyi, fmul2(fxi, fyr));
         const uint64_t orr = ffma2(ar, fr, fmul2(ai, fi));
         const uint64_t oi = fsub2(fmul2(ai, fr), fmul2(ar, fi));
-        Qp[int64_t(y + u) * rs] = make_ulonglong2(orr, oi);
+        Qp[int64_t(y) * rs] = make_ulonglong2(orr, oi);
         ar = fsub2(ar, tv[u].x);
         ai = fsub2(ai, tv[u].y);
       }
