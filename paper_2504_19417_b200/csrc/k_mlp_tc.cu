@@ -24,6 +24,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "../../include/veckm.h"
 #include "vkm_device.cuh"
@@ -228,7 +229,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     auto load_cnt = [&](int pix) { return pix >= 0 ? __ldg(NQ + pix) : 0; };
     auto recip = [&](int cnt) {   // ÷count folded with the fp16 pre-scale
-      return cnt > 0 ? __frcp_rn(float(cnt)) * f_scale : 0.f;
+      // MUFU.RCP (<= 1 ulp; the IEEE-rounded __frcp_rn cost ~2 instructions
+      // per event in its fix-up sequence).  The reference divides by f32(cnt)
+      // (encoder.py:345); either reciprocal differs from that by <= 1 ulp.
+      float r;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(float(cnt)));
+      return cnt > 0 ? r * f_scale : 0.f;
     };
     // One thread prefetches the pooled-grid rows of a future tile into L2
     // with bulk (TMA-engine) prefetches: the tile's pixel range x 8 planes.
@@ -261,7 +267,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                    "l"(src), "r"(pj >= 0 ? 16 : 0)
                    : "memory");
     };
-    auto compute = [&](float a_reg, float rs_reg, int pix_c, int pix_n, uint8_t* ah, uint8_t* al) {
+    // Shared address of this lane's 8 bytes in row u of stage 0's hi image
+    // (m = 8·warp + u; the swizzle chunk is lane_chunk ^ u); the stage and the
+    // lo image are compile-time offsets, so each store is STS [reg + imm].
+    uint32_t sah[kRows];
+#pragma unroll
+    for (int u = 0; u < kRows; ++u)
+      sah[u] = smem_u32(S.ah[0]) + lane_atom + uint32_t(warp) * 1024u + uint32_t(u) * 128u +
+               ((lane_chunk ^ uint32_t(u)) << 4) + lane_byte;
+    auto sts64 = [](uint32_t addr, uint32_t lo, uint32_t hi, auto imm) {
+      asm volatile("st.shared.v2.b32 [%0+%3], {%1, %2};" ::"r"(addr), "r"(lo), "r"(hi), "n"(decltype(imm)::value)
+                   : "memory");
+    };
+    auto compute = [&](float a_reg, float rs_reg, int pix_c, int pix_n, auto stage) {
+      constexpr int kS = decltype(stage)::value;
+      constexpr int kHiOff = kS * kTileBytes;                          // S.ah[kS] - S.ah[0]
+      constexpr int kLoOff = kStages * kTileBytes + kS * kTileBytes;   // S.al[kS] - S.ah[0]
 #pragma unroll
       for (int u = 0; u < kRows; ++u) {
         asm volatile("cp.async.wait_group %0;" ::"n"(kQD - 2) : "memory");
@@ -273,7 +294,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const float aj = __shfl_sync(0xffffffffu, a_reg, u);
         const float rs = __shfl_sync(0xffffffffu, rs_reg, u);
-        const uint32_t m = warp * kRows + u;
         uint64_t sn, cs;
         // conj(phase) * acc / cnt for channels (c0, c0+1), packed; the ÷count
         // (and fp16 pre-scale) rides on the sin/cos sign fix-up
@@ -284,7 +304,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Feature order on the K axis is (Re c, Re c+1, Im c, Im c+1) per
         // channel pair (W1's columns are permuted to match on the host), so a
         // lane's four values are 8 contiguous bytes: one 64-bit store per image.
-        const uint32_t off = lane_atom + (m >> 3) * 1024 + (m & 7) * 128 + ((lane_chunk ^ (m & 7)) << 4) + lane_byte;
         float re0, re1, im0, im1;
         f2unpack(re, re0, re1);
         f2unpack(im, im0, im1);
@@ -302,15 +321,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           f2unpack(fsub2(im, tim), l2, l3);
           const __half2 hre = __floats2half2_rn(h0, h1), him = __floats2half2_rn(h2, h3);
           const __half2 lre = __floats2half2_rn(l0, l1), lim = __floats2half2_rn(l2, l3);
-          *reinterpret_cast<uint2*>(ah + off) =
-              make_uint2(*reinterpret_cast<const uint32_t*>(&hre), *reinterpret_cast<const uint32_t*>(&him));
-          *reinterpret_cast<uint2*>(al + off) =
-              make_uint2(*reinterpret_cast<const uint32_t*>(&lre), *reinterpret_cast<const uint32_t*>(&lim));
+          sts64(sah[u], *reinterpret_cast<const uint32_t*>(&hre), *reinterpret_cast<const uint32_t*>(&him),
+                std::integral_constant<int, kHiOff>{});
+          sts64(sah[u], *reinterpret_cast<const uint32_t*>(&lre), *reinterpret_cast<const uint32_t*>(&lim),
+                std::integral_constant<int, kLoOff>{});
         } else {
           const __nv_bfloat162 bre = __floats2bfloat162_rn(re0, re1), bim = __floats2bfloat162_rn(im0, im1);
-          *reinterpret_cast<uint2*>(ah + off) =
-              make_uint2(*reinterpret_cast<const uint32_t*>(&bre), *reinterpret_cast<const uint32_t*>(&bim));
-        }      }
+          sts64(sah[u], *reinterpret_cast<const uint32_t*>(&bre), *reinterpret_cast<const uint32_t*>(&bim),
+                std::integral_constant<int, kHiOff>{});
+        }
+      }
     };
 
     const int64_t G = gridDim.x;
@@ -325,15 +345,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_l2(int64_t(blockIdx.x) + G);
 #pragma unroll
     for (int u = 0; u < kQD - 1; ++u) issue_row(__shfl_sync(0xffffffffu, pix_c, u), u);
-    int it = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++it) {
-      const int s = it & 1;
+    // one tile on stage kS (compile-time: the tile loop is unrolled by the
+    // two stages, it & 1 == kS)
+    auto tile_step = [&](int64_t tile, int it, auto stage) {
+      constexpr int kS = decltype(stage)::value;
       const uint32_t ph = (it >> 1) & 1;
       prefetch_l2(tile + 2 * G);
-      mbar_wait(&S.empty[s], ph ^ 1);
-      compute(a_c, rs_c, pix_c, pix_n, S.ah[s], S.al[s]);
+      mbar_wait(&S.empty[kS], ph ^ 1);
+      compute(a_c, rs_c, pix_c, pix_n, stage);
       fence_proxy_async();
-      mbar_arrive(&S.full[s]);
+      mbar_arrive(&S.full[kS]);
       a_c = a_n;
       pix_c = pix_n;
       rs_c = recip(cnt_n);
@@ -341,6 +362,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       pix_n = pix_nn;
       cnt_n = load_cnt(pix_nn);
       load_slot(tile + 3 * G, a_nn, pix_nn);
+    };
+    static_assert(kStages == 2, "the producer loop is unrolled by the two stages");
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += 2 * G, it += 2) {
+      tile_step(tile, it, std::integral_constant<int, 0>{});
+      if (tile + G >= ntiles) break;
+      tile_step(tile + G, it + 1, std::integral_constant<int, 1>{});
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp < kProdWarps + 4) {
