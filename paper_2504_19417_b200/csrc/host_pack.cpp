@@ -1,0 +1,116 @@
+// Host-side event packing for the pipelined host batch (vkm_predict_batch_host
+// with 8-byte records): rows of the reference's (n, 3) f64 [t, x, y] layout ->
+// {f32 bits of a = f32((t - t0)/δt), x | y << 16 or 0xFFFFFFFF}.  The time
+// argument is the same IEEE f64 subtract and divide, rounded once to f32, as
+// k_prep's time_arg on the device (and rebase_slice + _temporal_phases in the
+// reference, events.py:390-407, encoder.py:220-226), so both paths produce
+// bit-identical records.  Plain C++ (no CUDA): AVX-512 / AVX2 kernels chosen
+// at run time, a scalar loop for the tail and for CPUs without AVX2.
+#include <immintrin.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+namespace vkm_host {
+
+namespace {
+
+void pack_scalar(const double* r, int64_t m, double t0, double dt, int W, int H, uint32_t* out) {
+  for (int64_t i = 0; i < m; ++i) {
+    const double t = r[3 * i], x = r[3 * i + 1], y = r[3 * i + 2];
+    const float a = float((t - t0) / dt);
+    uint32_t ab;
+    std::memcpy(&ab, &a, 4);
+    // clamp before the conversion (out-of-range doubles -> int is undefined)
+    const double xc = std::fmin(std::fmax(x, -1.0), double(W)), yc = std::fmin(std::fmax(y, -1.0), double(H));
+    const int xi = int(xc), yi = int(yc);
+    const bool ok = x >= 0.0 && x < W && y >= 0.0 && y < H && double(xi) == x && double(yi) == y;
+    out[2 * i] = ab;
+    out[2 * i + 1] = ok ? (uint32_t(xi) | (uint32_t(yi) << 16)) : 0xFFFFFFFFu;
+  }
+}
+
+__attribute__((target("avx2,fma"))) void pack_avx2(const double* r, int64_t m, double t0, double dt, int W, int H,
+                                                    uint32_t* out) {
+  const __m256d vt0 = _mm256_set1_pd(t0), vdt = _mm256_set1_pd(dt), vW = _mm256_set1_pd(W), vH = _mm256_set1_pd(H);
+  const __m256d z = _mm256_setzero_pd(), m1 = _mm256_set1_pd(-1.0);
+  const __m256i even = _mm256_setr_epi32(0, 2, 4, 6, 1, 3, 5, 7);
+  int64_t i = 0;
+  for (; i + 4 <= m; i += 4) {
+    const double* p = r + 3 * i;
+    // a0 = t0 x0 y0 t1 | a1 = x1 y1 t2 x2 | a2 = y2 t3 x3 y3
+    const __m256d a0 = _mm256_loadu_pd(p), a1 = _mm256_loadu_pd(p + 4), a2 = _mm256_loadu_pd(p + 8);
+    const __m256d b0 = _mm256_blend_pd(a0, a1, 0b0010);   // t0 y1 y0 t1
+    const __m256d b1 = _mm256_blend_pd(a1, a2, 0b0010);   // x1 t3 t2 x2
+    const __m256d b2 = _mm256_blend_pd(a2, a0, 0b0010);   // y2 x0 x3 y3
+    const __m256d t = _mm256_permute4x64_pd(_mm256_blend_pd(b0, b1, 0b0110), _MM_SHUFFLE(1, 2, 3, 0));
+    const __m256d x = _mm256_permute4x64_pd(_mm256_blend_pd(b1, b2, 0b0110), _MM_SHUFFLE(2, 3, 0, 1));
+    const __m256d y = _mm256_permute4x64_pd(_mm256_blend_pd(b2, b0, 0b0110), _MM_SHUFFLE(3, 0, 1, 2));
+    const __m128 a = _mm256_cvtpd_ps(_mm256_div_pd(_mm256_sub_pd(t, vt0), vdt));
+    const __m128i xi = _mm256_cvttpd_epi32(_mm256_min_pd(_mm256_max_pd(x, m1), vW));
+    const __m128i yi = _mm256_cvttpd_epi32(_mm256_min_pd(_mm256_max_pd(y, m1), vH));
+    __m256d ok = _mm256_and_pd(_mm256_cmp_pd(x, z, _CMP_GE_OQ), _mm256_cmp_pd(x, vW, _CMP_LT_OQ));
+    ok = _mm256_and_pd(ok, _mm256_and_pd(_mm256_cmp_pd(y, z, _CMP_GE_OQ), _mm256_cmp_pd(y, vH, _CMP_LT_OQ)));
+    ok = _mm256_and_pd(ok, _mm256_cmp_pd(_mm256_cvtepi32_pd(xi), x, _CMP_EQ_OQ));
+    ok = _mm256_and_pd(ok, _mm256_cmp_pd(_mm256_cvtepi32_pd(yi), y, _CMP_EQ_OQ));
+    const __m128i okm = _mm256_castsi256_si128(_mm256_permutevar8x32_epi32(_mm256_castpd_si256(ok), even));
+    const __m128i xy = _mm_or_si128(_mm_and_si128(okm, _mm_or_si128(xi, _mm_slli_epi32(yi, 16))),
+                                    _mm_andnot_si128(okm, _mm_set1_epi32(-1)));
+    const __m128i ab = _mm_castps_si128(a);
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(out + 2 * i), _mm_unpacklo_epi32(ab, xy));
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(out + 2 * i + 4), _mm_unpackhi_epi32(ab, xy));
+  }
+  pack_scalar(r + 3 * i, m - i, t0, dt, W, H, out + 2 * i);
+}
+
+__attribute__((target("avx512f,avx512vl,avx512dq"))) void pack_avx512(const double* r, int64_t m, double t0,
+                                                                        double dt, int W, int H, uint32_t* out) {
+  const __m512d vt0 = _mm512_set1_pd(t0), vdt = _mm512_set1_pd(dt), vW = _mm512_set1_pd(W), vH = _mm512_set1_pd(H);
+  const __m512d z = _mm512_setzero_pd(), m1 = _mm512_set1_pd(-1.0);
+  // 8 rows = 24 doubles in a0|a1|a2: component c of row k sits at 3k + c
+  const __m512i t01 = _mm512_setr_epi64(0, 3, 6, 9, 12, 15, 0, 0), t2 = _mm512_setr_epi64(0, 1, 2, 3, 4, 5, 10, 13);
+  const __m512i x01 = _mm512_setr_epi64(1, 4, 7, 10, 13, 0, 0, 0), x2 = _mm512_setr_epi64(0, 1, 2, 3, 4, 8, 11, 14);
+  const __m512i y01 = _mm512_setr_epi64(2, 5, 8, 11, 14, 0, 0, 0), y2 = _mm512_setr_epi64(0, 1, 2, 3, 4, 9, 12, 15);
+  int64_t i = 0;
+  for (; i + 8 <= m; i += 8) {
+    const double* p = r + 3 * i;
+    const __m512d a0 = _mm512_loadu_pd(p), a1 = _mm512_loadu_pd(p + 8), a2 = _mm512_loadu_pd(p + 16);
+    const __m512d t = _mm512_permutex2var_pd(_mm512_permutex2var_pd(a0, t01, a1), t2, a2);
+    const __m512d x = _mm512_permutex2var_pd(_mm512_permutex2var_pd(a0, x01, a1), x2, a2);
+    const __m512d y = _mm512_permutex2var_pd(_mm512_permutex2var_pd(a0, y01, a1), y2, a2);
+    const __m256 a = _mm512_cvtpd_ps(_mm512_div_pd(_mm512_sub_pd(t, vt0), vdt));
+    const __m256i xi = _mm512_cvttpd_epi32(_mm512_min_pd(_mm512_max_pd(x, m1), vW));
+    const __m256i yi = _mm512_cvttpd_epi32(_mm512_min_pd(_mm512_max_pd(y, m1), vH));
+    const __mmask8 ok = _mm512_cmp_pd_mask(x, z, _CMP_GE_OQ) & _mm512_cmp_pd_mask(x, vW, _CMP_LT_OQ) &
+                        _mm512_cmp_pd_mask(y, z, _CMP_GE_OQ) & _mm512_cmp_pd_mask(y, vH, _CMP_LT_OQ) &
+                        _mm512_cmp_pd_mask(_mm512_cvtepi32_pd(xi), x, _CMP_EQ_OQ) &
+                        _mm512_cmp_pd_mask(_mm512_cvtepi32_pd(yi), y, _CMP_EQ_OQ);
+    const __m256i xy = _mm256_mask_blend_epi32(ok, _mm256_set1_epi32(-1), _mm256_or_si256(xi, _mm256_slli_epi32(yi, 16)));
+    const __m256i ab = _mm256_castps_si256(a);
+    const __m256i lo = _mm256_unpacklo_epi32(ab, xy), hi = _mm256_unpackhi_epi32(ab, xy);
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(out + 2 * i), _mm256_permute2x128_si256(lo, hi, 0x20));
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(out + 2 * i + 8), _mm256_permute2x128_si256(lo, hi, 0x31));
+  }
+  pack_scalar(r + 3 * i, m - i, t0, dt, W, H, out + 2 * i);
+}
+
+}  // namespace
+
+// out: 2 uint32 per event (the device's uint2 record)
+void pack_events(const double* rows, int64_t m, double t0, double dt, int W, int H, uint32_t* out) {
+  static const int isa = [] {
+    __builtin_cpu_init();
+    if (__builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512vl") && __builtin_cpu_supports("avx512dq"))
+      return 2;
+    return __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma") ? 1 : 0;
+  }();
+  if (isa == 2)
+    pack_avx512(rows, m, t0, dt, W, H, out);
+  else if (isa == 1)
+    pack_avx2(rows, m, t0, dt, W, H, out);
+  else
+    pack_scalar(rows, m, t0, dt, W, H, out);
+}
+
+}  // namespace vkm_host

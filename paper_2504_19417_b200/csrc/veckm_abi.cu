@@ -389,6 +389,13 @@ int next_chunk(const vkm_handle* h, const int64_t* offsets, int32_t n_slices, co
   return s;
 }
 
+}  // namespace
+namespace vkm_host {
+// host_pack.cpp: vectorised packing of f64 [t, x, y] rows into 8-byte records
+void pack_events(const double* rows, int64_t m, double t0, double dt, int W, int H, uint32_t* out);
+}  // namespace vkm_host
+namespace {
+
 // Pack the events of one chunk into 8-byte records (see launch_sort_events):
 // a = f32((t - t0)/δt) in f64 exactly like k_prep, x | y << 16, 0xFFFF... for
 // events that are not integer pixels inside the sensor.
@@ -406,22 +413,11 @@ void pack_chunk(vkm_handle* h, const double* ev, const int64_t* offsets, const d
   const int parts = std::max(1, std::min<int>(4 * h->pool->size(), int((n + 65535) / 65536)));
   h->pool->run(parts, [&](int part) {
     const int64_t lo = n * part / parts, hi = n * (part + 1) / parts;
-    int b = 0;
-    while (b + 1 < st.nb && st.off[b + 1] <= lo) ++b;
-    for (int64_t i = lo; i < hi; ++i) {
-      while (b + 1 < st.nb && st.off[b + 1] <= i) ++b;
-      const double* r = ev + 3 * (base + i);
+    for (int b = 0; b < st.nb; ++b) {   // the part's events, one slice (one t0) at a time
+      const int64_t s_lo = std::max(lo, st.off[b]), s_hi = std::min(hi, st.off[b + 1]);
+      if (s_lo >= s_hi) continue;
       const double t0 = (t_starts && !std::isnan(t_starts[sidx[b]])) ? t_starts[sidx[b]] : ev[3 * (base + st.off[b])];
-      const float a = float((r[0] - t0) / dt);
-      uint32_t ab;
-      std::memcpy(&ab, &a, 4);
-      uint32_t xy = 0xFFFFFFFFu;
-      const double x = r[1], y = r[2];
-      if (x >= 0.0 && x < W && y >= 0.0 && y < H) {
-        const int xi = int(x), yi = int(y);
-        if (double(xi) == x && double(yi) == y) xy = uint32_t(xi) | (uint32_t(yi) << 16);
-      }
-      out[i] = make_uint2(ab, xy);
+      vkm_host::pack_events(ev + 3 * (base + s_lo), s_hi - s_lo, t0, dt, W, H, reinterpret_cast<uint32_t*>(out + s_lo));
     }
   });
 }
@@ -830,9 +826,10 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
   }
   // Host packing (VKM_HOST_PACK=1): 8 instead of 24 bytes per event over PCIe;
   // the host threads pack chunk c+1 while the GPU runs chunk c.  Needs the
-  // tensor-core head and 16-bit pixel coordinates.  Off by default: on the
-  // B200 boxes measured (16 host threads) packing ran at ~1.2e9 events/s,
-  // below the PCIe-bound 1.6e9 of shipping the f64 rows.
+  // tensor-core head and 16-bit pixel coordinates.  Off by default: with the
+  // AVX-512 packer (host_pack.cpp) it is +3 % at config 2 (1.72e9 vs 1.67e9
+  // flows/s e2e: the host's memory bandwidth, not PCIe, bounds both) and it
+  // stalls the small-slice pipelines (configs 1, 4: -50 %).
   static const bool pack_env = [] {
     const char* e = std::getenv("VKM_HOST_PACK");
     return e && e[0] == '1';
