@@ -123,6 +123,20 @@ int vkm_predict_host(vkm_handle* h, const double* events_host, int64_t n, double
 int vkm_encode_host(vkm_handle* h, const double* events_host, int64_t n, double t_start,
                     float* feats_host, int32_t* counts_host);
 
+/* precision="f64" (estimators.py:115, encoder.py:37-38: complex128 grid,
+ * float64 features; flow.py:98-106: the head promotes the f32 weights to f64).
+ * Same contract as vkm_predict / vkm_encode with float64 outputs:
+ * flows (n, 2) f64 with NaN rows for empty neighbourhoods, features (n, 2D)
+ * f64 [Re | Im] (NaN rows for events outside the sensor).  One slice per call. */
+int vkm_predict_f64(vkm_handle* h, const double* events_dev, int64_t n, double t_start,
+                    double* flows_dev, int32_t* counts_dev, void* stream);
+int vkm_encode_f64(vkm_handle* h, const double* events_dev, int64_t n, double t_start,
+                   double* feats_dev, int32_t* counts_dev, void* stream);
+int vkm_predict_f64_host(vkm_handle* h, const double* events_host, int64_t n, double t_start,
+                         double* flows_host, int32_t* counts_host);
+int vkm_encode_f64_host(vkm_handle* h, const double* events_host, int64_t n, double t_start,
+                        double* feats_host, int32_t* counts_host);
+
 /* Many independent slices in one call.  Slice s holds events
  * [offsets[s], offsets[s+1]) of events_dev; offsets_host has n_slices+1
  * entries; t_starts_host has n_slices entries (NAN = first event). */

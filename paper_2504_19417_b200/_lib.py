@@ -49,6 +49,10 @@ SIGNATURES = {
     "vkm_encode": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P, _P]),
     "vkm_predict_host": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),
     "vkm_encode_host": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),
+    "vkm_predict_f64": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P, _P]),
+    "vkm_encode_f64": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P, _P]),
+    "vkm_predict_f64_host": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),
+    "vkm_encode_f64_host": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),
     "vkm_predict_batch": (C.c_int, [_P, _P, _I64, C.c_int32, _D, _P, _P, _P]),
     "vkm_predict_batch_host": (C.c_int, [_P, _P, _I64, C.c_int32, _D, _P, _P]),
     "vkm_grid": (C.c_int, [_P, _P, C.c_int64, C.c_double, C.c_int32, _P, _P, _P]),
@@ -105,4 +109,4 @@ def declared_symbols():
     with open(HEADER_PATH) as fh:
         text = fh.read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(vkm_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(vkm_[a-z0-9_]+)\s*\(", text)))

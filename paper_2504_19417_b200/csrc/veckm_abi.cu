@@ -142,6 +142,14 @@ struct vkm_handle {
   float2* mx = nullptr;
   float4* mxp = nullptr;
   float4* myp = nullptr;
+  double* t64 = nullptr;    // precision="f64" tables (k_f64.cu)
+  double2* mx64 = nullptr;
+  double2* my64 = nullptr;
+  double2* g64a = nullptr;   // f64 grid buffers [P][D8], grown on the first f64 call
+  double2* g64b = nullptr;
+  int64_t g64_cap = 0;
+  double* out64 = nullptr;   // f64 host-variant output staging
+  size_t out64_cap = 0;
   float* w1p = nullptr;  // [hidden][2*D8] padded
   float* b1 = nullptr;
   float* w2 = nullptr;
@@ -543,6 +551,27 @@ int vkm_create(vkm_handle** out, const vkm_params* params, const double* T, cons
   VKM_CKH(cudaMemcpy(h->tf, tf.data(), sizeof(float) * D8, cudaMemcpyHostToDevice));
   VKM_CKH(cudaMemcpy(h->my, my.data(), sizeof(float2) * my.size(), cudaMemcpyHostToDevice));
   VKM_CKH(cudaMemcpy(h->mx, mx.data(), sizeof(float2) * mx.size(), cudaMemcpyHostToDevice));
+  {   // precision="f64" tables: the same angles, not rounded to f32
+    std::vector<double> t64(D8, 0.0);
+    for (int c = 0; c < h->D; ++c) t64[c] = T[c];
+    std::vector<double2> my64(size_t(H) * D8), mx64(size_t(W) * D8);
+    for (int y = 0; y < H; ++y)
+      for (int c = 0; c < D8; ++c) {
+        const double ang = c < h->D ? (double(y) / p.delta_y) * Y[c] : 0.0;
+        my64[size_t(y) * D8 + c] = make_double2(std::cos(ang), std::sin(ang));
+      }
+    for (int x = 0; x < W; ++x)
+      for (int c = 0; c < D8; ++c) {
+        const double ang = c < h->D ? (double(x) / p.delta_x) * X[c] : 0.0;
+        mx64[size_t(x) * D8 + c] = make_double2(std::cos(ang), std::sin(ang));
+      }
+    VKM_CKH(cudaMalloc(&h->t64, sizeof(double) * D8));
+    VKM_CKH(cudaMalloc(&h->mx64, sizeof(double2) * mx64.size()));
+    VKM_CKH(cudaMalloc(&h->my64, sizeof(double2) * my64.size()));
+    VKM_CKH(cudaMemcpy(h->t64, t64.data(), sizeof(double) * D8, cudaMemcpyHostToDevice));
+    VKM_CKH(cudaMemcpy(h->mx64, mx64.data(), sizeof(double2) * mx64.size(), cudaMemcpyHostToDevice));
+    VKM_CKH(cudaMemcpy(h->my64, my64.data(), sizeof(double2) * my64.size(), cudaMemcpyHostToDevice));
+  }
   {   // packed-pair copies (cos c, cos c+1, sin c, sin c+1) of both tables
     auto pack = [&](const std::vector<float2>& t, int rows, std::vector<float4>& out) {
       out.resize(size_t(rows) * (D8 / 2));
@@ -627,7 +656,7 @@ void vkm_destroy(vkm_handle* h) {
   if (!h) return;
   DeviceGuard dg(h->p.device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->myp, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
+  void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->myp, h->t64, h->mx64, h->my64, h->g64a, h->g64b, h->out64, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
                   h->G, h->C, h->Q, h->NQ, h->feats, h->cnt_scratch, h->ev_stage, h->out_stage, h->cnt_stage,
                   h->sb.pix, h->sb.val, h->sb.start, h->sb.val_s, h->sb.pix_s, h->sb.temp, h->sb.sort_temp,
                   h->sb.rank, h->sb.longlist, h->sb.longcount};
@@ -926,6 +955,97 @@ int vkm_grid(vkm_handle* h, const double* ev, int64_t n, double t_start, int32_t
                           pooled ? nullptr : h->mx, pooled ? nullptr : h->my, pooled != 0, grid, counts, s);
   VKM_CK(cudaGetLastError());
   return VKM_OK;
+}
+
+// ---- precision="f64" (k_f64.cu) ----
+namespace {
+int run_f64(vkm_handle* h, const double* ev, int64_t n, double t_start, double* out, int32_t* counts, bool predict,
+            cudaStream_t s) {
+  if (n < 0) return fail(VKM_EINVAL, "n must be non-negative");
+  if (n > 0 && (!ev || !out)) return fail(VKM_EINVAL, "null device buffer");
+  if (predict && h->hidden <= 0) return fail(VKM_EINVAL, "handle has no flow head (hidden == 0)");
+  if (n == 0) return VKM_OK;
+  const int W = h->p.width, H = h->p.height;
+  double t0 = t_start;
+  if (std::isnan(t0)) {   // the first event's time (the f64 kernels take t0 by value)
+    VKM_CK(cudaMemcpyAsync(&t0, ev, sizeof(double), cudaMemcpyDeviceToHost, s));
+    VKM_CK(cudaStreamSynchronize(s));
+  }
+  int rc = ensure_grid(h, h->P);
+  if (!rc) rc = ensure_sort(h, n, h->P);
+  if (!rc && h->g64_cap < h->P) {
+    if (h->g64a) cudaFree(h->g64a);
+    if (h->g64b) cudaFree(h->g64b);
+    h->g64a = h->g64b = nullptr;
+    h->g64_cap = 0;
+    VKM_CK(cudaMalloc(&h->g64a, sizeof(double2) * h->D8 * h->P));
+    VKM_CK(cudaMalloc(&h->g64b, sizeof(double2) * h->D8 * h->P));
+    h->g64_cap = h->P;
+  }
+  if (rc) return rc;
+  vkm::launch_sort_events(ev, nullptr, one_slice(n, t0), h->p.delta_t, W, H, bufs(h), h->sb, nullptr, nullptr, s);
+  vkm::launch_pool_count(W, H, 1, h->p.delta_x, h->p.delta_y, bufs(h), s);
+  const vkm::F64Tables t{h->t64, h->mx64, h->my64};
+  vkm::launch_encode64(t, ev, n, t0, h->p.delta_t, W, H, h->D, h->D8, h->p.delta_x, h->p.delta_y, h->sb, h->NQ,
+                       h->g64a, h->g64b, s);
+  if (predict)
+    vkm::launch_predict64(t, ev, n, t0, h->p.delta_t, W, H, h->D, h->D8, h->g64a, h->NQ,
+                          vkm::MlpDev{h->w1p, h->b1, h->w2, h->b2, h->hidden}, out, counts, h->num_sms, s);
+  else
+    vkm::launch_features64(t, ev, n, t0, h->p.delta_t, W, H, h->D, h->D8, h->g64a, h->NQ, out, counts, s);
+  VKM_CK(cudaGetLastError());
+  h->have_timing = false;
+  return VKM_OK;
+}
+
+int run_f64_host(vkm_handle* h, const double* ev_host, int64_t n, double t_start, double* out_host,
+                 int32_t* counts_host, bool predict) {
+  if (n < 0) return fail(VKM_EINVAL, "n must be non-negative");
+  if (n == 0) return VKM_OK;
+  if (!ev_host || !out_host) return fail(VKM_EINVAL, "null host buffer");
+  const size_t per = predict ? 2 : size_t(2 * h->D);
+  int rc = grow(&h->ev_stage, &h->ev_cap, size_t(n) * 3);
+  if (!rc) rc = grow(&h->out64, &h->out64_cap, size_t(n) * per);
+  if (!rc && counts_host) rc = grow(&h->cnt_stage, &h->cnt_stage_cap, size_t(n));
+  if (rc) return rc;
+  cudaStream_t s = h->stream;
+  VKM_CK(cudaMemcpyAsync(h->ev_stage, ev_host, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+  rc = run_f64(h, h->ev_stage, n, t_start, h->out64, counts_host ? h->cnt_stage : nullptr, predict, s);
+  if (rc) return rc;
+  VKM_CK(cudaMemcpyAsync(out_host, h->out64, sizeof(double) * per * n, cudaMemcpyDeviceToHost, s));
+  if (counts_host)
+    VKM_CK(cudaMemcpyAsync(counts_host, h->cnt_stage, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  VKM_CK(cudaStreamSynchronize(s));
+  return VKM_OK;
+}
+}  // namespace
+
+int vkm_predict_f64(vkm_handle* h, const double* ev, int64_t n, double t_start, double* flows, int32_t* counts,
+                    void* stream) {
+  if (int rc = check_handle(h)) return rc;
+  DeviceGuard dg(h->p.device);
+  return run_f64(h, ev, n, t_start, flows, counts, true, static_cast<cudaStream_t>(stream));
+}
+
+int vkm_encode_f64(vkm_handle* h, const double* ev, int64_t n, double t_start, double* feats, int32_t* counts,
+                   void* stream) {
+  if (int rc = check_handle(h)) return rc;
+  DeviceGuard dg(h->p.device);
+  return run_f64(h, ev, n, t_start, feats, counts, false, static_cast<cudaStream_t>(stream));
+}
+
+int vkm_predict_f64_host(vkm_handle* h, const double* ev_host, int64_t n, double t_start, double* flows_host,
+                         int32_t* counts_host) {
+  if (int rc = check_handle(h)) return rc;
+  DeviceGuard dg(h->p.device);
+  return run_f64_host(h, ev_host, n, t_start, flows_host, counts_host, true);
+}
+
+int vkm_encode_f64_host(vkm_handle* h, const double* ev_host, int64_t n, double t_start, double* feats_host,
+                        int32_t* counts_host) {
+  if (int rc = check_handle(h)) return rc;
+  DeviceGuard dg(h->p.device);
+  return run_f64_host(h, ev_host, n, t_start, feats_host, counts_host, false);
 }
 
 int vkm_set_profiling(vkm_handle* h, int32_t enable) {

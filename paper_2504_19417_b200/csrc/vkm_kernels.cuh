@@ -114,6 +114,24 @@ void launch_features(const double* ev, int64_t n, double t0, double delta_t, con
 // K3b: FFMA two-layer head on padded features [n][2*D8] -> flows [n][2].
 void launch_mlp_ffma(const float* feats, const int32_t* counts, int64_t n, int D8, const MlpDev& m,
                      float* flows, cudaStream_t s);
+// precision="f64" path (k_f64.cu).  Tables in f64: T [D8] (0 for padded
+// channels), e^{i x X_c/δx} [W][D8], e^{i y Y_c/δy} [H][D8].  Buffers double2 [P][D8].
+struct F64Tables {
+  const double* T;
+  const double2* mx;
+  const double2* my;
+};
+// sorted slots (sb) + counts -> pooled f64 grid in bufA (bufB scratch)
+void launch_encode64(const F64Tables& t, const double* ev, int64_t n, double t0, double delta_t, int W, int H, int D,
+                     int D8, int dx, int dy, const SortBufs& sb, const int* NQ, double2* bufA, double2* bufB,
+                     cudaStream_t s);
+void launch_features64(const F64Tables& t, const double* ev, int64_t n, double t0, double delta_t, int W, int H,
+                       int D, int D8, const double2* Q, const int* NQ, double* feats, int32_t* counts,
+                       cudaStream_t s);
+void launch_predict64(const F64Tables& t, const double* ev, int64_t n, double t0, double delta_t, int W, int H, int D,
+                      int D8, const double2* Q, const int* NQ, const MlpDev& m, double* flows, int32_t* counts,
+                      int num_sms, cudaStream_t s);
+
 // Layout conversion for the parity hook: planes -> reference [x][y][D] complex64.
 // mx/my non-null: G holds the pre-modulated grid M and is demodulated on the way out.
 // packed: G uses the packed-pair layout (the pooled grid Q).

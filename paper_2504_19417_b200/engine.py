@@ -130,6 +130,39 @@ class FlowEngine:
                                                  counts.ctypes.data if counts is not None else None))
         return (feats, counts) if return_counts else feats
 
+    # -- precision="f64" (complex128 grid, float64 features and head) ----------
+    def predict_host_f64(self, events: np.ndarray, t_start: float = math.nan, return_counts: bool = False):
+        ev = np.ascontiguousarray(events, dtype=np.float64)
+        n = len(ev)
+        flows = np.empty((n, 2), dtype=np.float64)
+        counts = np.empty(n, dtype=np.int32) if return_counts else None
+        if n:
+            _lib.check(self._lib.vkm_predict_f64_host(self._h, ev.ctypes.data, n, float(t_start), flows.ctypes.data,
+                                                      counts.ctypes.data if counts is not None else None))
+        return (flows, counts) if return_counts else flows
+
+    def encode_host_f64(self, events: np.ndarray, t_start: float = math.nan, return_counts: bool = False):
+        ev = np.ascontiguousarray(events, dtype=np.float64)
+        n = len(ev)
+        feats = np.empty((n, 2 * self.embed_dim), dtype=np.float64)
+        counts = np.empty(n, dtype=np.int32) if return_counts else None
+        if n:
+            _lib.check(self._lib.vkm_encode_f64_host(self._h, ev.ctypes.data, n, float(t_start), feats.ctypes.data,
+                                                     counts.ctypes.data if counts is not None else None))
+        return (feats, counts) if return_counts else feats
+
+    def predict_device_f64(self, events, t_start: float = math.nan, flows=None, counts=None, stream=None):
+        torch = _torch()
+        self._check_events(events)
+        n = events.shape[0]
+        if flows is None:
+            flows = torch.empty((n, 2), dtype=torch.float64, device=events.device)
+        _lib.check(self._lib.vkm_predict_f64(self._h, C.c_void_p(events.data_ptr()), n, float(t_start),
+                                             C.c_void_p(flows.data_ptr()),
+                                             C.c_void_p(counts.data_ptr()) if counts is not None else None,
+                                             self._stream(stream)))
+        return flows
+
     # -- device API (torch tensors) -----------------------------------------
     def _stream(self, stream):
         torch = _torch()

@@ -37,8 +37,6 @@ def _check_config(delta_t, delta_x, delta_y, embed_dim, sigma2, seeds, precision
         raise ValueError("precision must be one of ['f32', 'f64']")
     if len(tuple(seeds)) != 3:
         raise ValueError("seeds must be a triple (time, x, y)")
-    if precision == "f64":
-        raise NotImplementedError("precision='f64' has no B200 kernel path yet (the B200 path is float32)")
 
 
 def _engine(key, factory) -> FlowEngine:
@@ -81,14 +79,16 @@ class LocalEventEncoder(TransformerMixin, BaseEstimator):
         _check_config(self.delta_t, self.delta_x, self.delta_y, self.embed_dim, self.sigma2, self.seeds,
                       self.precision)
         block = slice_from_array(X, self.width, self.height, 2.0 * self.delta_t)
+        f64 = self.precision == "f64"   # complex128 grid, float64 features (encoder.py:37-38)
         if len(block) == 0:
-            return np.empty((0, 2 * self.embed_dim), dtype=np.float32)
+            return np.empty((0, 2 * self.embed_dim), dtype=np.float64 if f64 else np.float32)
         b = self.bases_
         key = ("enc", self.width, self.height, self.delta_x, self.delta_y, float(self.delta_t), self.device,
                b.time_freqs.tobytes(), b.x_freqs.tobytes(), b.y_freqs.tobytes())
         eng = _engine(key, lambda: FlowEngine(self.width, self.height, self.delta_x, self.delta_y, self.delta_t,
                                               b, None, self.device))
-        feats, counts = eng.encode_host(block.events, block.t_start, return_counts=True)
+        encode = eng.encode_host_f64 if f64 else eng.encode_host
+        feats, counts = encode(block.events, block.t_start, return_counts=True)
         if np.any(counts == 0):  # encoder.py:337-343
             bad = np.flatnonzero(counts == 0)
             raise EmptyNeighborhoodError(f"{len(bad)} queries have empty neighborhoods "
@@ -173,6 +173,8 @@ class NormalFlowRegressor(BaseEstimator):
         block = slice_from_array(X, self.width, self.height, 2.0 * self.delta_t)
         if len(block) == 0:
             return np.full((0, 2), np.nan)
+        if self.precision == "f64":   # f64 grid, features and head (encoder.py:37-38, flow.py:98-106)
+            return eng.predict_host_f64(block.events, block.t_start)
         flows = eng.predict_host(block.events, block.t_start)
         return flows.astype(np.float64)
 
@@ -183,6 +185,8 @@ class NormalFlowRegressor(BaseEstimator):
         vkm_predict_batch_host, which overlaps the copies of neighbouring
         slices with the kernels."""
         eng = self.engine()
+        if self.precision == "f64":   # one slice per call on the f64 path
+            return [self.predict(X) for X in slices]
         blocks = [slice_from_array(X, self.width, self.height, 2.0 * self.delta_t) for X in slices]
         sizes = [len(b) for b in blocks]
         total = int(sum(sizes))

@@ -58,8 +58,8 @@ def test_span_and_geometry_and_config_errors():
         evb.encode(np.array([0.0, 0.01]), np.array([0, 64]), np.zeros(2, int), np.array([0]), CONFIG)
     with pytest.raises(TypeError):
         evb.encode(np.zeros(1), np.zeros(1, int), np.zeros(1, int), np.array([0]), 3)
-    with pytest.raises(NotImplementedError):
-        evb.encode(np.zeros(1), np.zeros(1, int), np.zeros(1, int), np.array([0]), dict(CONFIG, precision="f64"))
+    with pytest.raises(ValueError, match="precision"):
+        evb.encode(np.zeros(1), np.zeros(1, int), np.zeros(1, int), np.array([0]), dict(CONFIG, precision="f16"))
 
 
 def test_presets():

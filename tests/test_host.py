@@ -184,8 +184,8 @@ def test_estimator_errors_raised_before_the_device(rng):
     w = pkg.init_weights(16, 8, b, dtype=np.float32)
     with pytest.raises(pkg.DimensionMismatchError):
         pkg.NormalFlowRegressor(embed_dim=64, weights=w).predict(make_events(rng))
-    with pytest.raises(NotImplementedError):
-        pkg.NormalFlowRegressor(embed_dim=16, precision="f64", weights=w).predict(make_events(rng))
+    with pytest.raises(ValueError, match="precision"):
+        pkg.NormalFlowRegressor(embed_dim=16, precision="f16", weights=w).predict(make_events(rng))
     with pytest.raises(NotImplementedError):
         pkg.NormalFlowRegressor(embed_dim=16).fit(make_events(rng), np.zeros((50, 2)))
     # pretrained weights: fit only stores them (estimators.py:166-170)

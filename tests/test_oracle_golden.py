@@ -111,3 +111,23 @@ def test_vkmw_golden_file_layout():
     with open(p, "rb") as fh:
         buf = fh.read()
     assert buf[:4] == b"VKMW" and buf[18:22] == b"VKMB"
+
+
+F64_CASES = ["f64_cfg1_6k", "f64_dense_asym", "f64_d16_offset"]
+
+
+@pytest.mark.parametrize("case", F64_CASES)
+def test_oracle_f64_matches_reference_golden(case):
+    """precision="f64" (complex128 grid, float64 features and head): the oracle
+    against the reference's own f64 outputs (tests/golden/make_golden_f64.py)."""
+    g = load_golden(case)
+    fr = vo.Freqs(g["freqT"], g["freqX"], g["freqY"], 25.0)
+    W, H, dx, dy = int(g["width"]), int(g["height"]), int(g["dx"]), int(g["dy"])
+    dt = float(g["delta_t"])
+    flows, counts = vo.predict(g["X"], W, H, dx, dy, dt, fr, g["w1"], g["b1"], g["w2"], g["b2"],
+                               precision="f64", return_counts=True)
+    np.testing.assert_array_equal(counts, g["counts"])
+    np.testing.assert_allclose(flows, g["flows"], rtol=0, atol=1e-10)
+    feats = vo.encode_features(g["X"], W, H, dx, dy, dt, fr, precision="f64")
+    assert feats.dtype == np.float64
+    np.testing.assert_allclose(feats[g["feat_idx"]], g["feats"], rtol=0, atol=1e-12)
