@@ -137,6 +137,15 @@ int vkm_predict_f64_host(vkm_handle* h, const double* events_host, int64_t n, do
 int vkm_encode_f64_host(vkm_handle* h, const double* events_host, int64_t n, double t_start,
                         double* feats_host, int32_t* counts_host);
 
+/* Direct summation (oracle_encode, encoder.py:413-440): for each query index
+ * q into the time-sorted events_host rows, the f64 mean of
+ * exp(i[(t_e-t_q)/δt·T + (x_e-x_q)/δx·X + (y_e-y_q)/δy·Y]) over the events
+ * within (δx, δy) of it, emb_host (nq, D) complex128 as (re, im) pairs, and
+ * the neighbourhood size.  Quadratic in the window population; a validation
+ * path independent of the pooled grid (test_acceptance.py:49-86). */
+int vkm_direct_encode_host(vkm_handle* h, const double* events_host, int64_t n, const int64_t* queries_host,
+                           int64_t nq, double* emb_host, int32_t* counts_host);
+
 /* Many independent slices in one call.  Slice s holds events
  * [offsets[s], offsets[s+1]) of events_dev; offsets_host has n_slices+1
  * entries; t_starts_host has n_slices entries (NAN = first event). */

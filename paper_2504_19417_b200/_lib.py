@@ -53,6 +53,7 @@ SIGNATURES = {
     "vkm_encode_f64": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P, _P]),
     "vkm_predict_f64_host": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),
     "vkm_encode_f64_host": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),
+    "vkm_direct_encode_host": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, _P, _P]),
     "vkm_predict_batch": (C.c_int, [_P, _P, _I64, C.c_int32, _D, _P, _P, _P]),
     "vkm_predict_batch_host": (C.c_int, [_P, _P, _I64, C.c_int32, _D, _P, _P]),
     "vkm_grid": (C.c_int, [_P, _P, C.c_int64, C.c_double, C.c_int32, _P, _P, _P]),

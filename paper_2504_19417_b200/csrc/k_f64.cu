@@ -245,7 +245,55 @@ __global__ void k64_predict(const double* __restrict__ ev, int64_t n, double t0,
   }
 }
 
+// Direct summation over the query's window in f64 (oracle_encode,
+// encoder.py:413-440): mean over the events e with |x_e - x_q| <= δx and
+// |y_e - y_q| <= δy of exp(i[(t_e - t_q)/δt·T + (x_e - x_q)/δx·X + (y_e - y_q)/δy·Y]).
+// Independent of the grid / modulation formulation (it walks the events of the
+// window's pixel runs), so it validates the pooled paths at scale.  Threads =
+// (query, channel < D).  emb: (nq, D) complex128; NaN and count 0 for an
+// empty window.
+__global__ void __launch_bounds__(256) k64_direct(const double* __restrict__ ev, const int64_t* __restrict__ queries,
+                                                  int64_t nq, const int* __restrict__ start,
+                                                  const uint64_t* __restrict__ val_s, int W, int H, int dx, int dy,
+                                                  double delta_t, const double* __restrict__ T,
+                                                  const double* __restrict__ X, const double* __restrict__ Y, int D,
+                                                  double2* __restrict__ emb, int32_t* __restrict__ counts) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nq * D) return;
+  const int64_t qi = i / D;
+  const int c = int(i - qi * D);
+  const int64_t q = queries[qi];
+  const double tq = ev[3 * q];
+  const int xq = int(ev[3 * q + 1]), yq = int(ev[3 * q + 2]);
+  const double Tc = T[c], Xc = X[c], Yc = Y[c];
+  double2 acc = make_double2(0.0, 0.0);
+  int cnt = 0;
+  for (int y = max(0, yq - dy); y <= min(H - 1, yq + dy); ++y)
+    for (int x = max(0, xq - dx); x <= min(W - 1, xq + dx); ++x) {
+      const int64_t p = int64_t(y) * W + x;
+      const double sp = (double(x - xq) / dx) * Xc + (double(y - yq) / dy) * Yc;
+      for (int j = start[p]; j < start[p + 1]; ++j) {
+        const double arg = ((ev[3 * int64_t(slot_event(val_s[j]))] - tq) / delta_t) * Tc + sp;
+        double sn, cs;
+        sincos(arg, &sn, &cs);
+        acc.x += cs;
+        acc.y += sn;
+        ++cnt;
+      }
+    }
+  emb[qi * D + c] = cnt > 0 ? make_double2(acc.x / cnt, acc.y / cnt) : make_double2(nan(""), nan(""));
+  if (counts && c == 0) counts[qi] = cnt;
+}
+
 }  // namespace
+
+void launch_direct64(const double* ev, const int64_t* queries, int64_t nq, const SortBufs& sb, int W, int H, int dx,
+                     int dy, double delta_t, const double* T, const double* X, const double* Y, int D, double2* emb,
+                     int32_t* counts, cudaStream_t s) {
+  if (nq <= 0) return;
+  k64_direct<<<int((nq * D + 255) / 256), 256, 0, s>>>(ev, queries, nq, sb.start, sb.val_s, W, H, dx, dy, delta_t, T,
+                                                       X, Y, D, emb, counts);
+}
 
 size_t predict64_smem(int D, int hidden) {
   return ((size_t(2 * D) * hidden * 4 + 15) / 16) * 16 + size_t(kEvPerStep) * 2 * D * 8 + 32 * kEvPerStep * 2 * 8 +

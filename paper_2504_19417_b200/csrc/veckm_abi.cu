@@ -142,6 +142,7 @@ struct vkm_handle {
   float2* mx = nullptr;
   float4* mxp = nullptr;
   float4* myp = nullptr;
+  double* xyz64 = nullptr;  // raw f64 bases T | X | Y [3][D] (direct summation)
   double* t64 = nullptr;    // precision="f64" tables (k_f64.cu)
   double2* mx64 = nullptr;
   double2* my64 = nullptr;
@@ -565,6 +566,14 @@ int vkm_create(vkm_handle** out, const vkm_params* params, const double* T, cons
         const double ang = c < h->D ? (double(x) / p.delta_x) * X[c] : 0.0;
         mx64[size_t(x) * D8 + c] = make_double2(std::cos(ang), std::sin(ang));
       }
+    std::vector<double> xyz(3 * size_t(h->D));
+    for (int c = 0; c < h->D; ++c) {
+      xyz[c] = T[c];
+      xyz[h->D + c] = X[c];
+      xyz[2 * h->D + c] = Y[c];
+    }
+    VKM_CKH(cudaMalloc(&h->xyz64, sizeof(double) * xyz.size()));
+    VKM_CKH(cudaMemcpy(h->xyz64, xyz.data(), sizeof(double) * xyz.size(), cudaMemcpyHostToDevice));
     VKM_CKH(cudaMalloc(&h->t64, sizeof(double) * D8));
     VKM_CKH(cudaMalloc(&h->mx64, sizeof(double2) * mx64.size()));
     VKM_CKH(cudaMalloc(&h->my64, sizeof(double2) * my64.size()));
@@ -656,7 +665,7 @@ void vkm_destroy(vkm_handle* h) {
   if (!h) return;
   DeviceGuard dg(h->p.device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->myp, h->t64, h->mx64, h->my64, h->g64a, h->g64b, h->out64, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
+  void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->myp, h->xyz64, h->t64, h->mx64, h->my64, h->g64a, h->g64b, h->out64, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
                   h->G, h->C, h->Q, h->NQ, h->feats, h->cnt_scratch, h->ev_stage, h->out_stage, h->cnt_stage,
                   h->sb.pix, h->sb.val, h->sb.start, h->sb.val_s, h->sb.pix_s, h->sb.temp, h->sb.sort_temp,
                   h->sb.rank, h->sb.longlist, h->sb.longcount};
@@ -1046,6 +1055,39 @@ int vkm_encode_f64_host(vkm_handle* h, const double* ev_host, int64_t n, double 
   if (int rc = check_handle(h)) return rc;
   DeviceGuard dg(h->p.device);
   return run_f64_host(h, ev_host, n, t_start, feats_host, counts_host, false);
+}
+
+int vkm_direct_encode_host(vkm_handle* h, const double* ev_host, int64_t n, const int64_t* queries_host, int64_t nq,
+                           double* emb_host, int32_t* counts_host) {
+  if (int rc = check_handle(h)) return rc;
+  if (n < 0 || nq < 0) return fail(VKM_EINVAL, "n and nq must be non-negative");
+  if (nq == 0) return VKM_OK;
+  if (!ev_host || !queries_host || !emb_host) return fail(VKM_EINVAL, "null host buffer");
+  for (int64_t i = 0; i < nq; ++i)
+    if (queries_host[i] < 0 || queries_host[i] >= n) return fail(VKM_EINVAL, "query index out of range");
+  DeviceGuard dg(h->p.device);
+  const int W = h->p.width, H = h->p.height, D = h->D;
+  int rc = ensure_grid(h, h->P);
+  if (!rc) rc = ensure_sort(h, n, h->P);
+  if (!rc) rc = grow(&h->ev_stage, &h->ev_cap, size_t(n) * 3);
+  if (!rc) rc = grow(&h->out64, &h->out64_cap, size_t(nq) * 2 * D + size_t(nq));   // + the query indices
+  if (!rc) rc = grow(&h->cnt_stage, &h->cnt_stage_cap, size_t(nq));
+  if (rc) return rc;
+  cudaStream_t s = h->stream;
+  int64_t* q_dev = reinterpret_cast<int64_t*>(h->out64 + size_t(nq) * 2 * D);   // queries after the outputs
+  VKM_CK(cudaMemcpyAsync(h->ev_stage, ev_host, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+  VKM_CK(cudaMemcpyAsync(q_dev, queries_host, sizeof(int64_t) * nq, cudaMemcpyHostToDevice, s));
+  vkm::launch_sort_events(h->ev_stage, nullptr, one_slice(n, ev_host[0]), h->p.delta_t, W, H, bufs(h), h->sb,
+                          nullptr, nullptr, s);
+  vkm::launch_direct64(h->ev_stage, q_dev, nq, h->sb, W, H, h->p.delta_x, h->p.delta_y, h->p.delta_t, h->xyz64,
+                       h->xyz64 + D, h->xyz64 + 2 * D, D, reinterpret_cast<double2*>(h->out64), h->cnt_stage, s);
+  VKM_CK(cudaGetLastError());
+  VKM_CK(cudaMemcpyAsync(emb_host, h->out64, sizeof(double) * 2 * D * nq, cudaMemcpyDeviceToHost, s));
+  if (counts_host)
+    VKM_CK(cudaMemcpyAsync(counts_host, h->cnt_stage, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, s));
+  VKM_CK(cudaStreamSynchronize(s));
+  h->have_timing = false;
+  return VKM_OK;
 }
 
 int vkm_set_profiling(vkm_handle* h, int32_t enable) {

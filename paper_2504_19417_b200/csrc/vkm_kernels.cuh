@@ -132,6 +132,12 @@ void launch_predict64(const F64Tables& t, const double* ev, int64_t n, double t0
                       int D8, const double2* Q, const int* NQ, const MlpDev& m, double* flows, int32_t* counts,
                       int num_sms, cudaStream_t s);
 
+// Direct f64 summation per query (oracle_encode, encoder.py:413-440) over the
+// sorted pixel runs of sb; X, Y, T: the raw f64 bases [D].
+void launch_direct64(const double* ev, const int64_t* queries, int64_t nq, const SortBufs& sb, int W, int H, int dx,
+                     int dy, double delta_t, const double* T, const double* X, const double* Y, int D, double2* emb,
+                     int32_t* counts, cudaStream_t s);
+
 // Layout conversion for the parity hook: planes -> reference [x][y][D] complex64.
 // mx/my non-null: G holds the pre-modulated grid M and is demodulated on the way out.
 // packed: G uses the packed-pair layout (the pooled grid Q).

@@ -163,6 +163,19 @@ class FlowEngine:
                                              self._stream(stream)))
         return flows
 
+    def direct_encode_host(self, events: np.ndarray, queries, return_counts: bool = False):
+        """oracle_encode (encoder.py:413-440) on the GPU: f64 direct summation
+        over each query's window; `events` time-sorted (n, 3) rows, `queries`
+        indices into them.  Returns (nq, D) complex128 (+ int32 counts)."""
+        ev = np.ascontiguousarray(events, dtype=np.float64)
+        q = np.ascontiguousarray(queries, dtype=np.int64)
+        emb = np.empty((len(q), self.embed_dim), dtype=np.complex128)
+        counts = np.empty(len(q), dtype=np.int32)
+        if len(q):
+            _lib.check(self._lib.vkm_direct_encode_host(self._h, ev.ctypes.data, len(ev), q.ctypes.data, len(q),
+                                                        emb.ctypes.data, counts.ctypes.data))
+        return (emb, counts) if return_counts else emb
+
     # -- device API (torch tensors) -----------------------------------------
     def _stream(self, stream):
         torch = _torch()

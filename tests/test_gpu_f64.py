@@ -104,3 +104,54 @@ def test_f64_agrees_with_f32_path_at_config2_size():
     np.testing.assert_array_equal(cnt, c64[q])
     want = vo.mlp(w.w1, w.b1, w.w2, w.b2, vo.to_features(emb))
     np.testing.assert_allclose(f64[q], want, rtol=0, atol=FLOW_TOL64)
+
+
+def _fuzz_slice(rng, n, width, height, window=0.032):
+    """pkg/tests/conftest.py:18-25: sorted uniform times, uniform pixels, t_start = 0."""
+    t = np.sort(rng.uniform(0.0, window, size=n))
+    return np.stack([t, rng.integers(0, width, size=n), rng.integers(0, height, size=n)], 1).astype(np.float64)
+
+
+def test_direct_encode_matches_cpu_direct_sum():
+    """The GPU oracle_encode against the CPU oracle's direct summation (both f64)."""
+    pkg = _pkg()
+    rng = np.random.default_rng(3)
+    X = _fuzz_slice(rng, 4000, 50, 40)
+    b = pkg.generate_bases(64)
+    eng = pkg.FlowEngine(50, 40, 8, 6, 0.016, b)
+    q = rng.integers(0, len(X), 40)
+    emb, cnt = eng.direct_encode_host(X, q, return_counts=True)
+    fr = vo.Freqs(b.time_freqs, b.x_freqs, b.y_freqs, 25.0)
+    for i, qi in enumerate(q):
+        want, n = vo.direct_encode(X[:, 0], X[:, 1], X[:, 2], int(qi), 8, 6, fr, 0.016)
+        assert cnt[i] == n
+        np.testing.assert_allclose(emb[i], want, rtol=1e-12, atol=1e-13)
+
+
+def test_acceptance_oracle_equivalence_fuzz():
+    """test_acceptance.py:49-86 on the GPU: 1000 fuzzed slices (n <= 5000,
+    geometry <= 64x64, radii 8 and 10, two queries each); the pooled
+    embeddings of both precisions against the direct summation: f64 < 1e-6
+    and f32 < 1e-3 relative (floors 1e-9 / 1e-6), counts equal."""
+    pkg = _pkg()
+    rng = np.random.default_rng(7)
+    b = pkg.generate_bases(64)
+    # one 64x64 handle per radius: pixels beyond a slice's own geometry are empty,
+    # so its encodings equal those on its own sensor size
+    engines = {r: pkg.FlowEngine(64, 64, r, r, 0.016, b) for r in (8, 10)}
+    worst = {"f64": 0.0, "f32": 0.0}
+    for i in range(1000):
+        r = 8 if i % 2 == 0 else 10
+        n = int(rng.integers(1, 5001))
+        X = _fuzz_slice(rng, n, int(rng.integers(16, 65)), int(rng.integers(16, 65)))
+        q = rng.integers(0, n, size=min(2, n)).astype(np.int64)
+        eng = engines[r]
+        want, wcnt = eng.direct_encode_host(X, q, return_counts=True)
+        for prec, fn, floor in (("f64", eng.encode_host_f64, 1e-9), ("f32", eng.encode_host, 1e-6)):
+            feats, cnt = fn(X, 0.0, return_counts=True)
+            np.testing.assert_array_equal(cnt[q], wcnt)
+            got = feats[q, :64].astype(np.float64) + 1j * feats[q, 64:].astype(np.float64)
+            err = float(np.max(np.abs(got - want) / np.maximum(np.abs(want), floor)))
+            worst[prec] = max(worst[prec], err)
+    print(f"acceptance fuzz: max rel err f64={worst['f64']:.2e} f32={worst['f32']:.2e}")
+    assert worst["f64"] < 1e-6 and worst["f32"] < 1e-3, worst
