@@ -146,6 +146,29 @@ int vkm_encode_f64_host(vkm_handle* h, const double* events_host, int64_t n, dou
 int vkm_direct_encode_host(vkm_handle* h, const double* events_host, int64_t n, const int64_t* queries_host,
                            int64_t nq, double* emb_host, int32_t* counts_host);
 
+/* Head training on the GPU (train_head / flow_loss_grads, flow.py:234-402):
+ * float64 mini-batch Adam on the constraint loss with the data set resident in
+ * HBM.  The host keeps the reference's control flow (RNG permutations, the
+ * validation split, best-epoch selection); the device holds the features
+ * (n, F) f64, the targets (n, 2) f64, the parameters W1 (H, F), b1 (H),
+ * W2 (2, H), b2 (2) and the Adam moments.  All index arrays are host int64. */
+typedef struct vkm_trainer vkm_trainer;
+int vkm_train_create(vkm_trainer** out, int32_t device, const double* feats_host, const double* u_host, int64_t n,
+                     int32_t n_features, int32_t hidden, const double* w1, const double* b1, const double* w2,
+                     const double* b2, double margin, double margin_weight, double constraint_eps,
+                     double learning_rate);
+void vkm_train_destroy(vkm_trainer* t);
+/* One epoch: mini-batches of batch_size consecutive entries of order_host, one
+ * Adam step each (flow.py:364-385). */
+int vkm_train_epoch(vkm_trainer* t, const int64_t* order_host, int64_t m, int32_t batch_size);
+/* flow_loss (flow.py:234-248) of the current parameters on samples idx_host;
+ * bad_step_out: the first Adam step whose mini-batch loss was not finite, or -1. */
+int vkm_train_loss(vkm_trainer* t, const int64_t* idx_host, int64_t m, double* loss_out, int64_t* bad_step_out);
+/* Keep the current parameters as the best so far. */
+int vkm_train_keep(vkm_trainer* t);
+/* Copy out the current (best = 0) or the kept (best = 1) parameters. */
+int vkm_train_get(vkm_trainer* t, int32_t best, double* w1, double* b1, double* w2, double* b2);
+
 /* Many independent slices in one call.  Slice s holds events
  * [offsets[s], offsets[s+1]) of events_dev; offsets_host has n_slices+1
  * entries; t_starts_host has n_slices entries (NAN = first event). */

@@ -26,6 +26,7 @@ from .errors import (
     GeometryError,
 )
 from .estimators import LocalEventEncoder, NormalFlowRegressor
+from .training import TrainConfig, TrainingDivergedError, train_head
 from .validation import check_event_array, check_flow_array, slice_from_array
 from .weights import (
     Bases,
@@ -41,5 +42,5 @@ __all__ = [
     "FlowEngine", "NormalFlowRegressor", "LocalEventEncoder", "Bases", "MlpWeights", "generate_bases",
     "init_weights", "load_weights", "save_weights", "standard_normals", "check_event_array",
     "check_flow_array", "slice_from_array", "EvflowError", "EventParseError", "GeometryError",
-    "DimensionMismatchError", "EmptyNeighborhoodError",
+    "DimensionMismatchError", "EmptyNeighborhoodError", "TrainConfig", "TrainingDivergedError", "train_head",
 ]

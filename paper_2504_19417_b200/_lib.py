@@ -54,6 +54,13 @@ SIGNATURES = {
     "vkm_predict_f64_host": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),
     "vkm_encode_f64_host": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),
     "vkm_direct_encode_host": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, _P, _P]),
+    "vkm_train_create": (C.c_int, [C.POINTER(_P), C.c_int32, _D, _D, C.c_int64, C.c_int32, C.c_int32, _D, _D, _D,
+                                   _D, C.c_double, C.c_double, C.c_double, C.c_double]),
+    "vkm_train_destroy": (None, [_P]),
+    "vkm_train_epoch": (C.c_int, [_P, _P, C.c_int64, C.c_int32]),
+    "vkm_train_loss": (C.c_int, [_P, _P, C.c_int64, C.POINTER(C.c_double), _I64]),
+    "vkm_train_keep": (C.c_int, [_P]),
+    "vkm_train_get": (C.c_int, [_P, C.c_int32, _D, _D, _D, _D]),
     "vkm_predict_batch": (C.c_int, [_P, _P, _I64, C.c_int32, _D, _P, _P, _P]),
     "vkm_predict_batch_host": (C.c_int, [_P, _P, _I64, C.c_int32, _D, _P, _P]),
     "vkm_grid": (C.c_int, [_P, _P, C.c_int64, C.c_double, C.c_int32, _P, _P, _P]),

@@ -1090,6 +1090,202 @@ int vkm_direct_encode_host(vkm_handle* h, const double* ev_host, int64_t n, cons
   return VKM_OK;
 }
 
+}  // extern "C"
+
+// ---- head training (k_train.cu) ----
+struct vkm_trainer {
+  int device = 0;
+  int F = 0, H = 0;
+  int64_t n = 0;
+  double margin = 0, mw = 0, eps = 0, lr = 0;
+  int64_t step = 0;
+  cudaStream_t s = nullptr;
+  double *feats = nullptr, *u = nullptr, *prm = nullptr, *m = nullptr, *v = nullptr, *best = nullptr;
+  double *loss_part = nullptr, *g_part = nullptr;
+  int64_t *idx = nullptr, *bad = nullptr;
+  int64_t idx_cap = 0, part_rows = 0;
+  int64_t G() const { return int64_t(F) * H + 3 * int64_t(H) + 2; }
+};
+
+namespace {
+// parameters <-> packed device layout W1ᵀ [F][H] | b1 | W2 | b2
+void pack_params(int F, int H, const double* w1, const double* b1, const double* w2, const double* b2,
+                 std::vector<double>& out) {
+  out.assign(size_t(F) * H + 3 * size_t(H) + 2, 0.0);
+  for (int k = 0; k < H; ++k)
+    for (int j = 0; j < F; ++j) out[size_t(j) * H + k] = w1[size_t(k) * F + j];
+  const size_t FH = size_t(F) * H;
+  for (int k = 0; k < H; ++k) {
+    out[FH + k] = b1[k];
+    out[FH + H + k] = w2[k];
+    out[FH + 2 * H + k] = w2[H + k];
+  }
+  out[FH + 3 * H] = b2[0];
+  out[FH + 3 * H + 1] = b2[1];
+}
+
+int train_idx(vkm_trainer* t, const int64_t* idx_host, int64_t m) {
+  for (int64_t i = 0; i < m; ++i)
+    if (idx_host[i] < 0 || idx_host[i] >= t->n) return fail(VKM_EINVAL, "sample index out of range");
+  if (t->idx_cap < m) {
+    if (t->idx) cudaFree(t->idx);
+    t->idx = nullptr;
+    t->idx_cap = 0;
+    VKM_CK(cudaMalloc(&t->idx, sizeof(int64_t) * std::max<int64_t>(m, 1)));
+    t->idx_cap = m;
+  }
+  const int64_t rows = (m + vkm::train_rows_per_cta() - 1) / vkm::train_rows_per_cta();
+  if (t->part_rows < rows) {
+    if (t->loss_part) cudaFree(t->loss_part);
+    if (t->g_part) cudaFree(t->g_part);
+    t->loss_part = t->g_part = nullptr;
+    t->part_rows = 0;
+    VKM_CK(cudaMalloc(&t->loss_part, sizeof(double) * 2 * rows));
+    VKM_CK(cudaMalloc(&t->g_part, sizeof(double) * rows * t->G()));
+    t->part_rows = rows;
+  }
+  VKM_CK(cudaMemcpyAsync(t->idx, idx_host, sizeof(int64_t) * m, cudaMemcpyHostToDevice, t->s));
+  return VKM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int vkm_train_create(vkm_trainer** out, int32_t device, const double* feats_host, const double* u_host, int64_t n,
+                     int32_t n_features, int32_t hidden, const double* w1, const double* b1, const double* w2,
+                     const double* b2, double margin, double margin_weight, double constraint_eps,
+                     double learning_rate) {
+  if (!out) return fail(VKM_EINVAL, "null output pointer");
+  *out = nullptr;
+  if (n <= 0) return fail(VKM_EINVAL, "training dataset is empty");
+  if (n_features < 1 || n_features > 128 || hidden < 1 || hidden > 256)
+    return fail(VKM_EINVAL, "head training supports 2D <= 128 features and hidden <= 256");
+  if (!feats_host || !u_host || !w1 || !b1 || !w2 || !b2) return fail(VKM_EINVAL, "null host buffer");
+  DeviceGuard dg(device);
+  auto* t = new vkm_trainer();
+  t->device = device;
+  t->F = n_features;
+  t->H = hidden;
+  t->n = n;
+  t->margin = margin;
+  t->mw = margin_weight;
+  t->eps = constraint_eps;
+  t->lr = learning_rate;
+  std::vector<double> packed;
+  pack_params(t->F, t->H, w1, b1, w2, b2, packed);
+  const size_t G = packed.size();
+  auto bail = [&](cudaError_t e) {
+    vkm_train_destroy(t);
+    return fail(VKM_ECUDA, std::string("cuda: ") + cudaGetErrorString(e));
+  };
+#define VKM_CKT(x)                  \
+  do {                              \
+    cudaError_t e_ = (x);           \
+    if (e_ != cudaSuccess) return bail(e_); \
+  } while (0)
+  VKM_CKT(cudaStreamCreateWithFlags(&t->s, cudaStreamNonBlocking));
+  VKM_CKT(cudaMalloc(&t->feats, sizeof(double) * n * n_features));
+  VKM_CKT(cudaMalloc(&t->u, sizeof(double) * n * 2));
+  for (double** p : {&t->prm, &t->m, &t->v, &t->best}) VKM_CKT(cudaMalloc(p, sizeof(double) * G));
+  VKM_CKT(cudaMalloc(&t->bad, sizeof(int64_t)));
+  VKM_CKT(cudaMemcpy(t->feats, feats_host, sizeof(double) * n * n_features, cudaMemcpyHostToDevice));
+  VKM_CKT(cudaMemcpy(t->u, u_host, sizeof(double) * n * 2, cudaMemcpyHostToDevice));
+  VKM_CKT(cudaMemcpy(t->prm, packed.data(), sizeof(double) * G, cudaMemcpyHostToDevice));
+  VKM_CKT(cudaMemcpy(t->best, packed.data(), sizeof(double) * G, cudaMemcpyHostToDevice));
+  VKM_CKT(cudaMemset(t->m, 0, sizeof(double) * G));
+  VKM_CKT(cudaMemset(t->v, 0, sizeof(double) * G));
+  const int64_t none = -1;
+  VKM_CKT(cudaMemcpy(t->bad, &none, sizeof(int64_t), cudaMemcpyHostToDevice));
+#undef VKM_CKT
+  *out = t;
+  return VKM_OK;
+}
+
+void vkm_train_destroy(vkm_trainer* t) {
+  if (!t) return;
+  DeviceGuard dg(t->device);
+  if (t->s) cudaStreamSynchronize(t->s);
+  for (void* p : {static_cast<void*>(t->feats), static_cast<void*>(t->u), static_cast<void*>(t->prm),
+                  static_cast<void*>(t->m), static_cast<void*>(t->v), static_cast<void*>(t->best),
+                  static_cast<void*>(t->loss_part), static_cast<void*>(t->g_part), static_cast<void*>(t->idx),
+                  static_cast<void*>(t->bad)})
+    if (p) cudaFree(p);
+  if (t->s) cudaStreamDestroy(t->s);
+  delete t;
+}
+
+int vkm_train_epoch(vkm_trainer* t, const int64_t* order_host, int64_t m, int32_t batch_size) {
+  if (!t) return fail(VKM_EINVAL, "null vkm_trainer");
+  if (m < 0 || batch_size < 1) return fail(VKM_EINVAL, "bad epoch arguments");
+  if (m == 0) return VKM_OK;
+  if (!order_host) return fail(VKM_EINVAL, "null host buffer");
+  DeviceGuard dg(t->device);
+  if (int rc = train_idx(t, order_host, m)) return rc;
+  for (int64_t lo = 0; lo < m; lo += batch_size) {
+    const int64_t nb = std::min<int64_t>(batch_size, m - lo);
+    ++t->step;
+    vkm::launch_train_batch(t->feats, t->u, t->idx + lo, nb, t->F, t->H, t->prm, t->m, t->v, t->margin, t->mw,
+                            t->eps, 1, t->lr, t->step, t->loss_part, t->g_part, t->bad, t->s);
+  }
+  VKM_CK(cudaGetLastError());
+  VKM_CK(cudaStreamSynchronize(t->s));   // the index buffer is reused by the next call
+  return VKM_OK;
+}
+
+int vkm_train_loss(vkm_trainer* t, const int64_t* idx_host, int64_t m, double* loss_out, int64_t* bad_step_out) {
+  if (!t) return fail(VKM_EINVAL, "null vkm_trainer");
+  if (m <= 0 || !idx_host || !loss_out) return fail(VKM_EINVAL, "bad loss arguments");
+  DeviceGuard dg(t->device);
+  if (int rc = train_idx(t, idx_host, m)) return rc;
+  vkm::launch_train_batch(t->feats, t->u, t->idx, m, t->F, t->H, t->prm, nullptr, nullptr, t->margin, t->mw,
+                          t->eps, 0, 0.0, 0, t->loss_part, nullptr, nullptr, t->s);
+  VKM_CK(cudaGetLastError());
+  const int64_t rows = (m + vkm::train_rows_per_cta() - 1) / vkm::train_rows_per_cta();
+  std::vector<double> part(2 * rows);
+  int64_t bad = -1;
+  VKM_CK(cudaMemcpyAsync(part.data(), t->loss_part, sizeof(double) * 2 * rows, cudaMemcpyDeviceToHost, t->s));
+  VKM_CK(cudaMemcpyAsync(&bad, t->bad, sizeof(int64_t), cudaMemcpyDeviceToHost, t->s));
+  VKM_CK(cudaStreamSynchronize(t->s));
+  double l1 = 0.0, l2 = 0.0;
+  for (int64_t b = 0; b < rows; ++b) {
+    l1 += part[2 * b];
+    l2 += part[2 * b + 1];
+  }
+  *loss_out = l1 / double(m) + t->mw * (l2 / double(m));   // flow.py:246-248
+  if (bad_step_out) *bad_step_out = bad;
+  return VKM_OK;
+}
+
+int vkm_train_keep(vkm_trainer* t) {
+  if (!t) return fail(VKM_EINVAL, "null vkm_trainer");
+  DeviceGuard dg(t->device);
+  VKM_CK(cudaMemcpyAsync(t->best, t->prm, sizeof(double) * t->G(), cudaMemcpyDeviceToDevice, t->s));
+  VKM_CK(cudaStreamSynchronize(t->s));
+  return VKM_OK;
+}
+
+int vkm_train_get(vkm_trainer* t, int32_t best, double* w1, double* b1, double* w2, double* b2) {
+  if (!t) return fail(VKM_EINVAL, "null vkm_trainer");
+  if (!w1 || !b1 || !w2 || !b2) return fail(VKM_EINVAL, "null host buffer");
+  DeviceGuard dg(t->device);
+  std::vector<double> packed(size_t(t->G()));
+  VKM_CK(cudaMemcpyAsync(packed.data(), best ? t->best : t->prm, sizeof(double) * packed.size(),
+                         cudaMemcpyDeviceToHost, t->s));
+  VKM_CK(cudaStreamSynchronize(t->s));
+  const int F = t->F, H = t->H;
+  const size_t FH = size_t(F) * H;
+  for (int k = 0; k < H; ++k)
+    for (int j = 0; j < F; ++j) w1[size_t(k) * F + j] = packed[size_t(j) * H + k];
+  for (int k = 0; k < H; ++k) {
+    b1[k] = packed[FH + k];
+    w2[k] = packed[FH + H + k];
+    w2[H + k] = packed[FH + 2 * H + k];
+  }
+  b2[0] = packed[FH + 3 * H];
+  b2[1] = packed[FH + 3 * H + 1];
+  return VKM_OK;
+}
+
 int vkm_set_profiling(vkm_handle* h, int32_t enable) {
   if (int rc = check_handle(h)) return rc;
   h->profiling = enable != 0;

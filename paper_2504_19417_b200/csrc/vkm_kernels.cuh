@@ -138,6 +138,14 @@ void launch_direct64(const double* ev, const int64_t* queries, int64_t nq, const
                      int dy, double delta_t, const double* T, const double* X, const double* Y, int D, double2* emb,
                      int32_t* counts, cudaStream_t s);
 
+// Head training (k_train.cu).  prm/m/v: packed W1ᵀ [F][H] | b1 | W2 [2][H] | b2.
+size_t train_batch_smem(int F, int H);
+int train_rows_per_cta();
+void launch_train_batch(const double* feats, const double* u, const int64_t* idx, int64_t nb, int F, int H,
+                        double* prm, double* m, double* v, double margin, double mw, double eps, int with_grads,
+                        double lr, int64_t step, double* loss_part, double* g_part, int64_t* bad_step,
+                        cudaStream_t s);
+
 // Layout conversion for the parity hook: planes -> reference [x][y][D] complex64.
 // mx/my non-null: G holds the pre-modulated grid M and is demodulated on the way out.
 // packed: G uses the packed-pair layout (the pooled grid Q).

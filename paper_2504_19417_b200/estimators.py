@@ -136,9 +136,25 @@ class NormalFlowRegressor(BaseEstimator):
         if pretrained is not None:
             self.weights_ = pretrained
             return self
-        raise NotImplementedError(
-            "training the flow head is outside the B200 inference path; train with the reference "
-            "(evflow.train_head / evflow.NormalFlowRegressor.fit) and pass weights=")
+        # estimators.py:171-190: train the head on the GPU (training.train_head)
+        from .training import TrainConfig, train_head
+        from .validation import check_flow_array
+        _check_config(self.delta_t, self.delta_x, self.delta_y, self.embed_dim, self.sigma2, self.seeds,
+                      self.precision)
+        slices = X if isinstance(X, (list, tuple)) else [X]
+        targets = y if isinstance(y, (list, tuple)) else [y]
+        if len(slices) != len(targets):
+            raise ValueError("X and y must pair one flow array per slice")
+        dataset = []
+        for arr, flows in zip(slices, targets):
+            blk = slice_from_array(arr, self.width, self.height, 2.0 * self.delta_t)
+            dataset.append((arr, check_flow_array(flows, len(blk))))
+        tc = TrainConfig(hidden=self.hidden, epochs=self.epochs, batch_size=self.batch_size,
+                         learning_rate=self.learning_rate, margin_weight=self.margin_weight, seed=self.random_state)
+        bases = generate_bases(self.embed_dim, self.sigma2, tuple(self.seeds))
+        self.weights_ = train_head(dataset, self.width, self.height, self.delta_x, self.delta_y, self.delta_t,
+                                   self.embed_dim, tc, bases, self.precision, self.device)
+        return self
 
     def _ready(self) -> MlpWeights:
         if not hasattr(self, "weights_"):

@@ -186,8 +186,11 @@ def test_estimator_errors_raised_before_the_device(rng):
         pkg.NormalFlowRegressor(embed_dim=64, weights=w).predict(make_events(rng))
     with pytest.raises(ValueError, match="precision"):
         pkg.NormalFlowRegressor(embed_dim=16, precision="f16", weights=w).predict(make_events(rng))
-    with pytest.raises(NotImplementedError):
-        pkg.NormalFlowRegressor(embed_dim=16).fit(make_events(rng), np.zeros((50, 2)))
+    # training (GPU) validates its targets on the host first (estimators.py:171-181)
+    with pytest.raises(ValueError, match="flow targets"):
+        pkg.NormalFlowRegressor(embed_dim=16).fit(make_events(rng), np.zeros((3, 2)))
+    with pytest.raises(ValueError, match="pair one flow array"):
+        pkg.NormalFlowRegressor(embed_dim=16).fit([make_events(rng)], [np.zeros((3, 2)), np.zeros((3, 2))])
     # pretrained weights: fit only stores them (estimators.py:166-170)
     reg = pkg.NormalFlowRegressor(embed_dim=16, weights=w).fit(None, None)
     assert reg.weights_ is w
