@@ -120,9 +120,10 @@ __device__ __forceinline__ void sincos2_f32(float x0, float x1, float& s0, float
 
 // Two sin/cos pairs with the reduction by pi (r in [-pi/2, pi/2]): the only
 // quadrant fix-up is a common sign (-1)^k, applied with one shift and one
-// LOP3 per value, so the whole evaluation is 17 packed FMA-pipe instructions
-// plus 6 integer ones (31 for sincos2p_f32).  Degree-11 sin / degree-12 cos
-// minimax polynomials (tools/fit_sincos.py); max abs error 1.5e-7 over
+// LOP3 per value, so the whole evaluation is 15 packed FMA-pipe instructions
+// plus 6 integer ones (31 for sincos2p_f32).  Degree-9 sin / degree-10 cos
+// minimax polynomials (tools/fit_sincos.py; degrees 11/12 measured the same
+// f32 error, the evaluation rounding dominates): max abs error 1.4e-7 over
 // |x| < 60 (sincos2p_f32: 7.3e-8), i.e. ~2.5 ulp of 1.0.
 __device__ __forceinline__ void sincos2p_pi(uint64_t x, uint64_t& s01, uint64_t& c01) {
   const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
@@ -132,16 +133,14 @@ __device__ __forceinline__ void sincos2p_pi(uint64_t x, uint64_t& s01, uint64_t&
   r = ffma2(q, f2pack(-6.27832946e-07f, -6.27832946e-07f), r);
   r = ffma2(q, f2pack(-1.07806051e-14f, -1.07806051e-14f), r);
   const uint64_t u = fmul2(r, r);
-  uint64_t ps = ffma2(f2pack(-2.384669173e-08f, -2.384669173e-08f), u, f2pack(2.752261935e-06f, 2.752261935e-06f));
-  ps = ffma2(ps, u, f2pack(-1.984080445e-04f, -1.984080445e-04f));
-  ps = ffma2(ps, u, f2pack(8.333330043e-03f, 8.333330043e-03f));
-  ps = ffma2(ps, u, f2pack(-1.666666716e-01f, -1.666666716e-01f));
+  uint64_t ps = ffma2(f2pack(2.600054358e-06f, 2.600054358e-06f), u, f2pack(-1.980661473e-04f, -1.980661473e-04f));
+  ps = ffma2(ps, u, f2pack(8.333017118e-03f, 8.333017118e-03f));
+  ps = ffma2(ps, u, f2pack(-1.666665673e-01f, -1.666665673e-01f));
   ps = fmul2(ps, u);
   const uint64_t sr = ffma2(ps, r, r);
-  uint64_t pc = ffma2(f2pack(1.991995235e-09f, 1.991995235e-09f), u, f2pack(-2.752566104e-07f, -2.752566104e-07f));
-  pc = ffma2(pc, u, f2pack(2.480107105e-05f, 2.480107105e-05f));
-  pc = ffma2(pc, u, f2pack(-1.388888457e-03f, -1.388888457e-03f));
-  pc = ffma2(pc, u, f2pack(4.166666791e-02f, 4.166666791e-02f));
+  uint64_t pc = ffma2(f2pack(-2.607710599e-07f, -2.607710599e-07f), u, f2pack(2.476188638e-05f, 2.476188638e-05f));
+  pc = ffma2(pc, u, f2pack(-1.388840377e-03f, -1.388840377e-03f));
+  pc = ffma2(pc, u, f2pack(4.166664183e-02f, 4.166664183e-02f));
   pc = ffma2(pc, u, f2pack(-5.000000000e-01f, -5.000000000e-01f));
   const uint64_t cr = ffma2(pc, u, f2pack(1.0f, 1.0f));
   // (-1)^k: the parity of k sits in bit 0 of each f32 lane of qb
@@ -173,16 +172,14 @@ __device__ __forceinline__ void sincos2p_pi_scaled(uint64_t x, uint64_t scale01,
   r = ffma2(q, f2pack(-6.27832946e-07f, -6.27832946e-07f), r);
   r = ffma2(q, f2pack(-1.07806051e-14f, -1.07806051e-14f), r);
   const uint64_t u = fmul2(r, r);
-  uint64_t ps = ffma2(f2pack(-2.384669173e-08f, -2.384669173e-08f), u, f2pack(2.752261935e-06f, 2.752261935e-06f));
-  ps = ffma2(ps, u, f2pack(-1.984080445e-04f, -1.984080445e-04f));
-  ps = ffma2(ps, u, f2pack(8.333330043e-03f, 8.333330043e-03f));
-  ps = ffma2(ps, u, f2pack(-1.666666716e-01f, -1.666666716e-01f));
+  uint64_t ps = ffma2(f2pack(2.600054358e-06f, 2.600054358e-06f), u, f2pack(-1.980661473e-04f, -1.980661473e-04f));
+  ps = ffma2(ps, u, f2pack(8.333017118e-03f, 8.333017118e-03f));
+  ps = ffma2(ps, u, f2pack(-1.666665673e-01f, -1.666665673e-01f));
   ps = fmul2(ps, u);
   const uint64_t sr = ffma2(ps, r, r);
-  uint64_t pc = ffma2(f2pack(1.991995235e-09f, 1.991995235e-09f), u, f2pack(-2.752566104e-07f, -2.752566104e-07f));
-  pc = ffma2(pc, u, f2pack(2.480107105e-05f, 2.480107105e-05f));
-  pc = ffma2(pc, u, f2pack(-1.388888457e-03f, -1.388888457e-03f));
-  pc = ffma2(pc, u, f2pack(4.166666791e-02f, 4.166666791e-02f));
+  uint64_t pc = ffma2(f2pack(-2.607710599e-07f, -2.607710599e-07f), u, f2pack(2.476188638e-05f, 2.476188638e-05f));
+  pc = ffma2(pc, u, f2pack(-1.388840377e-03f, -1.388840377e-03f));
+  pc = ffma2(pc, u, f2pack(4.166664183e-02f, 4.166664183e-02f));
   pc = ffma2(pc, u, f2pack(-5.000000000e-01f, -5.000000000e-01f));
   const uint64_t cr = ffma2(pc, u, f2pack(1.0f, 1.0f));
   const uint64_t f = scale01 ^ ((qb << 31) & 0x8000000080000000ull);
