@@ -60,19 +60,21 @@ __global__ void __launch_bounds__(256) k64_reduce(const int* __restrict__ start,
   }
 }
 
-// Sliding (2δy+1)-row window down each (column, channel).
+// Sliding (2δy+1)-row window down each (column, channel) over one row
+// segment [y0, y0 + RS) (blockIdx.y): warm-up from the δy rows above.
 __global__ void __launch_bounds__(256) k64_box_y(const double2* __restrict__ M, double2* __restrict__ R, int W, int H,
-                                                 int D8, int dy) {
+                                                 int D8, int dy, int RS) {
   const int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;   // x * D8 + c
   if (col >= int64_t(W) * D8) return;
   const int64_t rs = int64_t(W) * D8;
+  const int y0 = blockIdx.y * RS, y1 = min(H, y0 + RS);
   double2 acc = make_double2(0.0, 0.0);
-  for (int y = 0; y < min(H, dy); ++y) {
+  for (int y = max(0, y0 - dy); y < min(H, y0 + dy); ++y) {
     const double2 v = M[y * rs + col];
     acc.x += v.x;
     acc.y += v.y;
   }
-  for (int y = 0; y < H; ++y) {
+  for (int y = y0; y < y1; ++y) {
     if (y + dy < H) {
       const double2 v = M[(y + dy) * rs + col];
       acc.x += v.x;
@@ -87,23 +89,25 @@ __global__ void __launch_bounds__(256) k64_box_y(const double2* __restrict__ M, 
   }
 }
 
-// Sliding (2δx+1)-column window along each (row, channel), then demodulation.
+// Sliding (2δx+1)-column window along each (row, channel) over one column
+// segment [x0, x0 + CS) (blockIdx.y), then demodulation.
 __global__ void __launch_bounds__(256) k64_box_x(const double2* __restrict__ R, double2* __restrict__ Q, int W, int H,
-                                                 int D8, int dx, const double2* __restrict__ mx,
+                                                 int D8, int dx, int CS, const double2* __restrict__ mx,
                                                  const double2* __restrict__ my) {
   const int64_t rc = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;   // y * D8 + c
   if (rc >= int64_t(H) * D8) return;
   const int y = int(rc / D8), c = int(rc - int64_t(y) * D8);
+  const int x0 = blockIdx.y * CS, x1 = min(W, x0 + CS);
   const double2* Rr = R + int64_t(y) * W * D8 + c;
   double2* Qr = Q + int64_t(y) * W * D8 + c;
   const double2 fy = my[int64_t(y) * D8 + c];
   double2 acc = make_double2(0.0, 0.0);
-  for (int x = 0; x < min(W, dx); ++x) {
+  for (int x = max(0, x0 - dx); x < min(W, x0 + dx); ++x) {
     const double2 v = Rr[int64_t(x) * D8];
     acc.x += v.x;
     acc.y += v.y;
   }
-  for (int x = 0; x < W; ++x) {
+  for (int x = x0; x < x1; ++x) {
     if (x + dx < W) {
       const double2 v = Rr[int64_t(x + dx) * D8];
       acc.x += v.x;
@@ -156,13 +160,16 @@ __global__ void __launch_bounds__(256) k64_features(const double* __restrict__ e
   if (counts && c == 0) counts[e] = cnt;
 }
 
-constexpr int kEvPerStep = 8;   // events per block step of k64_predict
+constexpr int kEvPerStep = 16;   // events per block step of k64_predict
 
 // Fused features + head.  Block = hidden threads (<= 256, rounded to a warp):
 // per step the block builds the features of kEvPerStep events in shared
 // memory (f64), then thread k forms hidden unit k for each of them with W1ᵀ
 // column k (f32 in shared memory, promoted), ReLU, and the two outputs are
 // block-reduced.  NaN rows for empty neighbourhoods (flow.py:188-196).
+// WT: the type W1ᵀ is kept in shared memory as — double when it fits (no
+// f32 -> f64 conversion in the inner loop), else float (promoted on use).
+template <typename WT>
 __global__ void k64_predict(const double* __restrict__ ev, int64_t n, double t0, double delta_t,
                             const double* __restrict__ T, const double2* __restrict__ Q, const int* __restrict__ NQ,
                             int W, int H, int D, int D8, const float* __restrict__ w1p, const float* __restrict__ b1,
@@ -170,15 +177,15 @@ __global__ void k64_predict(const double* __restrict__ ev, int64_t n, double t0,
                             double* __restrict__ flows, int32_t* __restrict__ counts) {
   extern __shared__ __align__(16) uint8_t sm64[];
   const int F = 2 * D;                                          // features per event
-  float* w1t = reinterpret_cast<float*>(sm64);                  // [F][hidden]
-  double* fs = reinterpret_cast<double*>(sm64 + ((size_t(F) * hidden * 4 + 15) / 16) * 16);   // [kEv][F]
+  WT* w1t = reinterpret_cast<WT*>(sm64);                        // [F][hidden]
+  double* fs = reinterpret_cast<double*>(sm64 + ((size_t(F) * hidden * sizeof(WT) + 15) / 16) * 16);   // [kEv][F]
   double* red = fs + kEvPerStep * F;                            // [32 warps][kEv][2]
   int* cnts = reinterpret_cast<int*>(red + 32 * kEvPerStep * 2);
   const int k = threadIdx.x;
   for (int i = threadIdx.x; i < F * hidden; i += blockDim.x) {   // W1 row r, feature j -> w1t[j][r]
     const int r = i / F, j = i - r * F;
     const int src = j < D ? j : D8 + (j - D);                   // w1p is [hidden][2·D8] (Re | Im padded)
-    w1t[j * hidden + r] = w1p[int64_t(r) * 2 * D8 + src];
+    w1t[j * hidden + r] = WT(w1p[int64_t(r) * 2 * D8 + src]);
   }
   const double bk = k < hidden ? double(b1[k]) : 0.0;
   const double wa = k < hidden ? double(w2[k]) : 0.0, wb = k < hidden ? double(w2[hidden + k]) : 0.0;
@@ -295,9 +302,9 @@ void launch_direct64(const double* ev, const int64_t* queries, int64_t nq, const
                                                        X, Y, D, emb, counts);
 }
 
-size_t predict64_smem(int D, int hidden) {
-  return ((size_t(2 * D) * hidden * 4 + 15) / 16) * 16 + size_t(kEvPerStep) * 2 * D * 8 + 32 * kEvPerStep * 2 * 8 +
-         kEvPerStep * 4;
+size_t predict64_smem(int D, int hidden, size_t wbytes) {
+  return ((size_t(2 * D) * hidden * wbytes + 15) / 16) * 16 + size_t(kEvPerStep) * 2 * D * 8 +
+         32 * kEvPerStep * 2 * 8 + kEvPerStep * 4;
 }
 
 void launch_encode64(const F64Tables& t, const double* ev, int64_t n, double t0, double delta_t, int W, int H, int D,
@@ -307,8 +314,13 @@ void launch_encode64(const F64Tables& t, const double* ev, int64_t n, double t0,
   const int ppb = 256 / D8;
   k64_reduce<<<int(std::min<int64_t>((P + ppb - 1) / ppb, 148 * 32)), ppb * D8, 0, s>>>(
       sb.start, sb.val_s, ev, t0, delta_t, t.T, t.mx, t.my, W, P, D8, bufA);
-  k64_box_y<<<int((int64_t(W) * D8 + 255) / 256), 256, 0, s>>>(bufA, bufB, W, H, D8, dy);
-  k64_box_x<<<int((int64_t(H) * D8 + 255) / 256), 256, 0, s>>>(bufB, bufA, W, H, D8, dx, t.mx, t.my);
+  // segments so each pass runs ~8 threads per (column|row, channel) pair of the
+  // grid (a ≥ 4δ-long segment keeps the 2δ warm-up re-reads below half)
+  const int RS = std::max(4 * dy, (H + 7) / 8), CS = std::max(4 * dx, (W + 7) / 8);
+  k64_box_y<<<dim3(unsigned((int64_t(W) * D8 + 255) / 256), unsigned((H + RS - 1) / RS)), 256, 0, s>>>(
+      bufA, bufB, W, H, D8, dy, RS);
+  k64_box_x<<<dim3(unsigned((int64_t(H) * D8 + 255) / 256), unsigned((W + CS - 1) / CS)), 256, 0, s>>>(
+      bufB, bufA, W, H, D8, dx, CS, t.mx, t.my);
   (void)n;
   (void)NQ;
 }
@@ -325,11 +337,20 @@ void launch_predict64(const F64Tables& t, const double* ev, int64_t n, double t0
                       int num_sms, cudaStream_t s) {
   if (n <= 0) return;
   const int threads = std::max(32, (m.hidden + 31) / 32 * 32);
-  const size_t smem = predict64_smem(D, m.hidden);
-  cudaFuncSetAttribute(k64_predict, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   const int blocks = int(std::min<int64_t>((n + kEvPerStep - 1) / kEvPerStep, int64_t(num_sms) * 4));
-  k64_predict<<<blocks, threads, smem, s>>>(ev, n, t0, delta_t, t.T, Q, NQ, W, H, D, D8, m.w1, m.b1, m.w2, m.b2,
-                                            m.hidden, flows, counts);
+  // f32 W1ᵀ in shared memory (promoted per use): twice the resident blocks of
+  // an f64 copy, which measured 1.5x slower (4 warps per SM at 128 KB)
+  const size_t smem64 = predict64_smem(D, m.hidden, 8);
+  if (smem64 <= 64 * 1024) {   // f64 copy only for small heads
+    cudaFuncSetAttribute(k64_predict<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem64));
+    k64_predict<double><<<blocks, threads, smem64, s>>>(ev, n, t0, delta_t, t.T, Q, NQ, W, H, D, D8, m.w1, m.b1,
+                                                        m.w2, m.b2, m.hidden, flows, counts);
+  } else {
+    const size_t smem = predict64_smem(D, m.hidden, 4);
+    cudaFuncSetAttribute(k64_predict<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k64_predict<float><<<blocks, threads, smem, s>>>(ev, n, t0, delta_t, t.T, Q, NQ, W, H, D, D8, m.w1, m.b1, m.w2,
+                                                     m.b2, m.hidden, flows, counts);
+  }
 }
 
 }  // namespace vkm
