@@ -169,6 +169,23 @@ int vkm_train_keep(vkm_trainer* t);
 /* Copy out the current (best = 0) or the kept (best = 1) parameters. */
 int vkm_train_get(vkm_trainer* t, int32_t best, double* w1, double* b1, double* w2, double* b2);
 
+/* Host-only (no device): one-pass check of an (n, >=3) f64 [t, x, y] array
+ * with row stride ld doubles against the estimator's input contract
+ * (validation.py:10-37, 49-65).  Returns 0 and fills *out; the caller raises
+ * the reference's errors in its order (non-finite, negative t, non-integer
+ * pixels, first pixel outside W x H) and sorts when !sorted. */
+typedef struct vkm_event_check {
+  int32_t nonfinite;
+  int32_t negative_t;
+  int32_t nonint;
+  int32_t sorted;
+  int64_t first_outside;
+  int32_t outside_x, outside_y;
+  double t_first, t_last;
+} vkm_event_check;
+int vkm_check_events(const double* events_host, int64_t n, int64_t ld, int32_t width, int32_t height,
+                     vkm_event_check* out);
+
 /* Many independent slices in one call.  Slice s holds events
  * [offsets[s], offsets[s+1]) of events_dev; offsets_host has n_slices+1
  * entries; t_starts_host has n_slices entries (NAN = first event). */

@@ -207,3 +207,55 @@ def test_reference_weights_object_is_accepted():
     d.bases = b
     reg = pkg.NormalFlowRegressor(embed_dim=8, weights=d)
     assert reg._resolve_pretrained().hidden == 4
+
+
+def test_native_event_check_matches_numpy_semantics():
+    """vkm_check_events (one pass, AVX-512 body + scalar tail) against the
+    numpy predicates of validation.py:10-37 on adversarial arrays."""
+    import ctypes
+    from paper_2504_19417_b200 import _lib, validation as v
+    lib = _lib.load()
+    rng = np.random.default_rng(11)
+    W, H = 40, 30
+    for trial in range(300):
+        n = int(rng.integers(0, 70))
+        cols = 3 if trial % 3 else 4                       # (n, 4) rows: the strided scalar path
+        X = np.stack([np.sort(rng.uniform(0, 0.03, n)), rng.integers(-2, W + 2, n), rng.integers(-2, H + 2, n)]
+                     + ([rng.uniform(size=n)] if cols == 4 else []), 1).astype(np.float64)
+        for _ in range(int(rng.integers(0, 3))):           # sprinkle defects
+            if n == 0:
+                break
+            i, kind = int(rng.integers(0, n)), int(rng.integers(0, 7))
+            if kind == 0:
+                X[i, int(rng.integers(0, 3))] = np.nan
+            elif kind == 1:
+                X[i, int(rng.integers(0, 3))] = -np.inf
+            elif kind == 2:
+                X[i, 0] = -1e-3
+            elif kind == 3:
+                X[i, 1 + int(rng.integers(0, 2))] += 0.5
+            elif kind == 4:
+                X[i, 1] = 3e9                              # out of int32 range
+            elif kind == 5:
+                X[i, 0] = 0.05 * rng.uniform()             # breaks the order
+            else:
+                X[i, 2] = 2.0 ** 60                        # huge but integer-valued
+        c = v._EventCheck()
+        assert lib.vkm_check_events(X.ctypes.data, n, cols, W, H, ctypes.byref(c)) == 0
+        X3 = X[:, :3]
+        t, x, y = X3[:, 0], X3[:, 1], X3[:, 2]
+        fin = np.isfinite(X3).all(axis=1)
+        assert bool(c.nonfinite) == (not fin.all())
+        assert bool(c.negative_t) == bool(np.any(t < 0))
+        with np.errstate(invalid="ignore"):
+            nonint = bool(np.any(fin & ((x != np.round(x)) | (y != np.round(y)))))
+            xi, yi = x.astype(np.int32), y.astype(np.int32)
+        assert bool(c.nonint) == nonint
+        with np.errstate(invalid="ignore"):
+            assert bool(c.sorted) == (not np.any(np.diff(t) < 0))
+        outside = fin & ~((xi >= 0) & (xi < W) & (yi >= 0) & (yi < H))
+        if outside.any():
+            k = int(np.flatnonzero(outside)[0])
+            assert (c.first_outside, c.outside_x, c.outside_y) == (k, xi[k], yi[k])
+        else:
+            assert c.first_outside == -1

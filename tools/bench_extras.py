@@ -36,6 +36,19 @@ f64 = torch.empty((n, 2), dtype=torch.float64, device="cuda")
 ms32 = timed(lambda: eng.predict_device(ev, t0, flows=f32), 20)
 ms64 = timed(lambda: eng.predict_device_f64(ev, t0, flows=f64), 5)
 
+# the drop-in call: NormalFlowRegressor.predict(X) on a pageable numpy slice
+# (host validation, copies, kernels, float64 result), wall clock
+reg = pkg.NormalFlowRegressor(width=W, height=H, weights=w)
+reg.predict(X)
+t = time.perf_counter()
+for _ in range(5):
+    reg.predict(X)
+predict_ms = (time.perf_counter() - t) / 5 * 1e3
+t = time.perf_counter()
+for _ in range(5):
+    pkg.slice_from_array(X, W, H, 0.032)
+validate_ms = (time.perf_counter() - t) / 5 * 1e3
+
 # trainer: 200k samples, D = 64 (128 features), hidden 128, batch 512
 m = 200_000
 rng = np.random.default_rng(0)
@@ -49,6 +62,7 @@ torch.cuda.synchronize()
 tr_s = time.perf_counter() - t
 train_samples = 5 * (m - int(m * 0.2))
 print(json.dumps({"cfg2_f32_flows_per_s": n / (ms32 / 1e3), "cfg2_f64_flows_per_s": n / (ms64 / 1e3),
+                  "dropin_predict_ms_1M": predict_ms, "dropin_validate_ms_1M": validate_ms,
                   "f64_ms": ms64, "f32_ms": ms32,
                   "train_samples_per_s": train_samples / tr_s, "train_wall_s": tr_s,
                   "train_config": "200k samples (160k train), 128 features, hidden 128, batch 512, 5 epochs, wall clock incl. per-epoch validation"}))
