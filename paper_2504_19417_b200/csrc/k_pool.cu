@@ -139,7 +139,11 @@ __global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ 
         const uint64_t fi = ffma2(fxr, fyi, fmul2(fxi, fyr));
         const uint64_t orr = ffma2(ar, fr, fmul2(ai, fi));
         const uint64_t oi = fsub2(fmul2(ai, fr), fmul2(ar, fi));
-        Qp[int64_t(y) * rs] = make_ulonglong2(orr, oi);
+        // Q with evict_first: its 158 MB (cfg 2) must not push out the lead
+        // rows of R kept for the trailing re-read (pool -7 % at cfg 3 and 4)
+        asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(Qp + int64_t(y) * rs),
+                     "l"(orr), "l"(oi), "l"(drop)
+                     : "memory");
         ar = fsub2(ar, tv[u].x);
         ai = fsub2(ai, tv[u].y);
       }
