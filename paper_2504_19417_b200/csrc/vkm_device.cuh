@@ -18,11 +18,13 @@ struct SliceGeom {
 };
 
 // ---------------------------------------------------------------------------
-// sin/cos of an f32 argument.  3-part Cody-Waite reduction by pi/2 and
-// minimax polynomials on [-pi/4, pi/4] (coefficients fitted for this project,
-// tools in DESIGN.md).  Max error 1.42 ulp / 7.3e-8 abs over |x| < 60; agrees
-// bit-for-bit with numpy's float32 sin/cos on 98.9% of arguments and within
-// 1 ulp elsewhere.  Valid for |x| < ~1e5 (phase arguments here are < 100).
+// sin/cos of an f32 argument.  2-part Cody-Waite reduction by pi/2 (the
+// third part, q·5.4e-15, stays below 1e-12 for |x| < 1e3 — far under f32
+// resolution — and is left out) and minimax polynomials on [-pi/4, pi/4]
+// (coefficients fitted for this project, tools in DESIGN.md).  Max error
+// 1.42 ulp / 7.3e-8 abs over |x| < 60; agrees bit-for-bit with numpy's
+// float32 sin/cos on 98.9% of arguments and within 1 ulp elsewhere.  Valid
+// for |x| < ~1e3 (phase arguments here are < 100).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void sincos_f32(float x, float& s, float& c) {
   // q = rint(x·2/π) via the 1.5·2^23 magic constant (exact for |x·2/π| < 2^22):
@@ -31,7 +33,6 @@ __device__ __forceinline__ void sincos_f32(float x, float& s, float& c) {
   const float q = __fsub_rn(qb, 12582912.0f);
   float r = fmaf(q, -1.57079601e+00f, x);
   r = fmaf(q, -3.13916473e-07f, r);
-  r = fmaf(q, -5.39030253e-15f, r);
   const float u = r * r;
   float ps = 2.718123369e-06f;
   ps = fmaf(ps, u, -1.983931288e-04f);
@@ -93,7 +94,6 @@ __device__ __forceinline__ void sincos2_f32(float x0, float x1, float& s0, float
   const uint64_t q = fsub2(qb, magic);
   uint64_t r = ffma2(q, f2pack(-1.57079601e+00f, -1.57079601e+00f), x);
   r = ffma2(q, f2pack(-3.13916473e-07f, -3.13916473e-07f), r);
-  r = ffma2(q, f2pack(-5.39030253e-15f, -5.39030253e-15f), r);
   const uint64_t u = fmul2(r, r);
   uint64_t ps = ffma2(f2pack(2.718123369e-06f, 2.718123369e-06f), u, f2pack(-1.983931288e-04f, -1.983931288e-04f));
   ps = ffma2(ps, u, f2pack(8.333329111e-03f, 8.333329111e-03f));
@@ -131,7 +131,6 @@ __device__ __forceinline__ void sincos2p_pi(uint64_t x, uint64_t& s01, uint64_t&
   const uint64_t q = fsub2(qb, magic);
   uint64_t r = ffma2(q, f2pack(-3.14159203e+00f, -3.14159203e+00f), x);
   r = ffma2(q, f2pack(-6.27832946e-07f, -6.27832946e-07f), r);
-  r = ffma2(q, f2pack(-1.07806051e-14f, -1.07806051e-14f), r);
   const uint64_t u = fmul2(r, r);
   uint64_t ps = ffma2(f2pack(2.600054358e-06f, 2.600054358e-06f), u, f2pack(-1.980661473e-04f, -1.980661473e-04f));
   ps = ffma2(ps, u, f2pack(8.333017118e-03f, 8.333017118e-03f));
@@ -170,7 +169,6 @@ __device__ __forceinline__ void sincos2p_pi_scaled(uint64_t x, uint64_t scale01,
   const uint64_t q = fsub2(qb, magic);
   uint64_t r = ffma2(q, f2pack(-3.14159203e+00f, -3.14159203e+00f), x);
   r = ffma2(q, f2pack(-6.27832946e-07f, -6.27832946e-07f), r);
-  r = ffma2(q, f2pack(-1.07806051e-14f, -1.07806051e-14f), r);
   const uint64_t u = fmul2(r, r);
   uint64_t ps = ffma2(f2pack(2.600054358e-06f, 2.600054358e-06f), u, f2pack(-1.980661473e-04f, -1.980661473e-04f));
   ps = ffma2(ps, u, f2pack(8.333017118e-03f, 8.333017118e-03f));
