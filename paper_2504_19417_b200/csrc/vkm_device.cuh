@@ -29,7 +29,7 @@ struct SliceGeom {
 __device__ __forceinline__ void sincos_f32(float x, float& s, float& c) {
   // q = rint(x·2/π) via the 1.5·2^23 magic constant (exact for |x·2/π| < 2^22):
   // stays on the FMA/ALU pipes; the low mantissa bits carry the quadrant.
-  const float qb = __fadd_rn(__fmul_rn(x, 0.636619772f), 12582912.0f);
+  const float qb = fmaf(x, 0.636619772f, 12582912.0f);
   const float q = __fsub_rn(qb, 12582912.0f);
   float r = fmaf(q, -1.57079601e+00f, x);
   r = fmaf(q, -3.13916473e-07f, r);
@@ -90,7 +90,7 @@ __device__ __forceinline__ uint64_t fneg2(uint64_t a) { return a ^ 0x80000000800
 __device__ __forceinline__ void sincos2_f32(float x0, float x1, float& s0, float& c0, float& s1, float& c1) {
   const uint64_t x = f2pack(x0, x1);
   const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
-  const uint64_t qb = fadd2(fmul2(x, f2pack(0.636619772f, 0.636619772f)), magic);
+  const uint64_t qb = ffma2(x, f2pack(0.636619772f, 0.636619772f), magic);   // rint(x·2/π) in the low bits
   const uint64_t q = fsub2(qb, magic);
   uint64_t r = ffma2(q, f2pack(-1.57079601e+00f, -1.57079601e+00f), x);
   r = ffma2(q, f2pack(-3.13916473e-07f, -3.13916473e-07f), r);
