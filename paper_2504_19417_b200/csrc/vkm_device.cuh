@@ -195,7 +195,7 @@ __device__ __forceinline__ void sincos2p_f32(uint64_t theta, uint64_t& s01, uint
 }
 
 // sin/cos used by the two hot kernels (k_reduce_x, k_gather_mlp_tc).  The
-// pi-reduced variant issues 23 instead of 31 instructions per pair but
+// pi-reduced variant issues fewer instructions per pair but
 // measured no faster on B200 (both kernels are dependency-latency bound:
 // k_reduce_x 128 -> 132 us, K3 ~equal, ncu cfg2) and is 2x less accurate, so
 // the pi/2-reduced version is the default; -DVKM_SINCOS_PI selects the other.
