@@ -44,6 +44,10 @@ constexpr int kProdWarps = 16;                // producer warps (8 tile rows eac
 constexpr int kThreads = (kProdWarps + 5) * 32; // + 4 epilogue warps + 1 MMA warp
 constexpr uint32_t kTmemCols = kAcc * kN;
 constexpr int kQD = 4;                          // per-warp cp.async ring of pooled rows (3 in flight)
+#ifndef VKM_K3_PHB
+#define VKM_K3_PHB 2   // 1, 2, 4, 8 measured within 0.5 % (2 best at cfg2 and cfg3)
+#endif
+constexpr int kPhB = VKM_K3_PHB;                // rows whose phases are computed back to back (divides 8)
 
 struct Smem {
   // operand images, each 1024-byte aligned (SWIZZLE_128B atoms)
@@ -283,8 +287,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr int kS = decltype(stage)::value;
       constexpr int kHiOff = kS * kTileBytes;                          // S.ah[kS] - S.ah[0]
       constexpr int kLoOff = kStages * kTileBytes + kS * kTileBytes;   // S.al[kS] - S.ah[0]
+      // The phases of kPhB rows are computed back to back before their pooled
+      // rows are consumed: independent sin/cos chains for ILP, and the first
+      // ring wait of the batch overlaps them.
+      uint64_t snb[kPhB], csb[kPhB];
 #pragma unroll
       for (int u = 0; u < kRows; ++u) {
+        if (u % kPhB == 0) {
+#pragma unroll
+          for (int v = 0; v < kPhB; ++v) {
+            const float aj = __shfl_sync(0xffffffffu, a_reg, u + v);
+            const float rs = __shfl_sync(0xffffffffu, rs_reg, u + v);
+            // conj(phase) * acc / cnt for channels (c0, c0+1), packed; the ÷count
+            // (and fp16 pre-scale) rides on the sin/cos sign fix-up
+            VKM_SINCOS_K3_SCALED(fmul2(f2pack(aj, aj), T01), f2pack(rs, rs), snb[v], csb[v]);
+          }
+        }
+        const uint64_t sn = snb[u % kPhB], cs = csb[u % kPhB];
         asm volatile("cp.async.wait_group %0;" ::"n"(kQD - 2) : "memory");
         const float4 src_u = ring[(u & (kQD - 1)) * 32];
         {   // refill the slot read one row ago with the row kQD-1 ahead
@@ -292,12 +311,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int pj = un < kRows ? __shfl_sync(0xffffffffu, pix_c, un) : __shfl_sync(0xffffffffu, pix_n, un - kRows);
           issue_row(pj, un & (kQD - 1));
         }
-        const float aj = __shfl_sync(0xffffffffu, a_reg, u);
-        const float rs = __shfl_sync(0xffffffffu, rs_reg, u);
-        uint64_t sn, cs;
-        // conj(phase) * acc / cnt for channels (c0, c0+1), packed; the ÷count
-        // (and fp16 pre-scale) rides on the sin/cos sign fix-up
-        VKM_SINCOS_K3_SCALED(fmul2(f2pack(aj, aj), T01), f2pack(rs, rs), sn, cs);
         const uint64_t ar = f2pack(src_u.x, src_u.y), ai = f2pack(src_u.z, src_u.w);   // packed pairs
         const uint64_t re = ffma2(sn, ai, fmul2(cs, ar));
         const uint64_t im = fsub2(fmul2(cs, ai), fmul2(sn, ar));
