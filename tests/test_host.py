@@ -259,3 +259,17 @@ def test_native_event_check_matches_numpy_semantics():
             assert (c.first_outside, c.outside_x, c.outside_y) == (k, xi[k], yi[k])
         else:
             assert c.first_outside == -1
+
+
+def test_product_path_does_not_import_the_oracle():
+    """oracle/ is test infrastructure only: importing the package and building
+    an estimator pulls in nothing from it (run in a fresh interpreter)."""
+    import subprocess, sys, os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r); import paper_2504_19417_b200 as p; "
+            "import paper_2504_19417_b200.bindings, paper_2504_19417_b200.stream, paper_2504_19417_b200.sharding, "
+            "paper_2504_19417_b200.training; p.NormalFlowRegressor(); "
+            "bad = [m for m in sys.modules if m == 'oracle' or m.startswith('oracle.')]; "
+            "assert not bad, bad") % root
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr[-2000:]
