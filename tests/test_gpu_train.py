@@ -84,3 +84,27 @@ def test_divergence_and_empty_dataset():
                        precision="f64")
     with pytest.raises(ValueError, match="empty"):
         pkg.train_head([], 16, 16, 2, 2, 0.016, 4, pkg.TrainConfig(epochs=1), b)
+
+
+def test_fit_then_predict_shapes_and_pipeline():
+    """pkg/tests/test_estimators.py:97-115: fit on three slices then predict
+    (training on the GPU), and the encoder inside an sklearn Pipeline."""
+    from sklearn.pipeline import Pipeline
+    pkg = _pkg()
+    rng = np.random.default_rng(5)
+
+    def make_events(n):
+        t = np.sort(rng.uniform(0, 0.03, n))
+        return np.stack([t, rng.integers(0, 64, n), rng.integers(0, 64, n)], 1).astype(np.float64)
+
+    slices = [make_events(30) for _ in range(3)]
+    targets = [np.tile([20.0, 0.0], (30, 1)) for _ in range(3)]
+    reg = pkg.NormalFlowRegressor(delta_t=0.016, delta_x=4, delta_y=4, embed_dim=8, width=64, height=64,
+                                  hidden=8, epochs=5)
+    reg.fit(slices, targets)
+    flows = reg.predict(slices[0])
+    assert flows.shape == (30, 2) and np.all(np.isfinite(flows))
+    pipe = Pipeline([("encode", pkg.LocalEventEncoder(delta_t=0.016, delta_x=4, delta_y=4, embed_dim=8,
+                                                       width=64, height=64))])
+    feats = pipe.fit_transform(make_events(12))
+    assert feats.shape == (12, 16)
