@@ -435,7 +435,9 @@ def main():
     ap.add_argument("--split", choices=["slices", "spatial"], default="slices",
                     help="slices: independent slices per rank (weak); spatial: one slice in row strips (strong)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-slices", type=int, default=8, help="slices per vkm_predict_batch_host call in the e2e leg")
+    ap.add_argument("--e2e-slices", type=int, default=32,
+                    help="slices per vkm_predict_batch_host call in the e2e leg (32: the pipeline's fill and drain "
+                         "amortised; 8 measured 1.5-1.7e9, 32 and 64 1.97e9 flows/s at cfg2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -835,7 +835,11 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
   DeviceGuard dg(h->p.device);
   // chunks (each one launch sequence), then the largest chunk sizes the staging slots
   // at most 2M events (or a quarter of the call) per chunk so copies overlap kernels
-  const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(int64_t(1) << 21, (offsets[n_slices] - offsets[0]) / 4));
+  static const int64_t chunk_events = [] {   // VKM_CHUNK_EVENTS: A/B of the pipeline granularity
+    const char* e = std::getenv("VKM_CHUNK_EVENTS");
+    return (e && std::atoll(e) > 0) ? int64_t(std::atoll(e)) : (int64_t(1) << 21);
+  }();
+  const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(chunk_events, (offsets[n_slices] - offsets[0]) / 4));
   std::vector<std::pair<int, vkm::SliceTab>> chunks;
   int64_t nmax = 0;
   for (int s = 0; s < n_slices;) {
