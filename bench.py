@@ -310,7 +310,10 @@ def run_b200(args):
     e2e = None
     if not args.no_e2e:
         n_e2e = len(host[0])
-        K = max(2, min(args.e2e_slices, 64_000_000 // max(1, n_e2e)))   # <= 1.5 GB of pinned input
+        # slices per call: --e2e-slices, or by default ~32M events per call
+        # (the pipeline's fill and drain amortised; 768 MB of pinned input)
+        K = args.e2e_slices if args.e2e_slices > 0 else 32_000_000 // max(1, n_e2e)
+        K = max(2, min(K, 64_000_000 // max(1, n_e2e)))   # <= 1.5 GB of pinned input
         pin_ev = torch.empty((K * n_e2e, 3), dtype=torch.float64).pin_memory().numpy()
         pin_out = torch.empty((K * n_e2e, 2), dtype=torch.float32).pin_memory().numpy()
         for k in range(K):
@@ -435,9 +438,9 @@ def main():
     ap.add_argument("--split", choices=["slices", "spatial"], default="slices",
                     help="slices: independent slices per rank (weak); spatial: one slice in row strips (strong)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-slices", type=int, default=32,
-                    help="slices per vkm_predict_batch_host call in the e2e leg (32: the pipeline's fill and drain "
-                         "amortised; 8 measured 1.5-1.7e9, 32 and 64 1.97e9 flows/s at cfg2)")
+    ap.add_argument("--e2e-slices", type=int, default=0,
+                    help="slices per vkm_predict_batch_host call in the e2e leg (0: ~32M events per call, the "
+                         "pipeline's fill and drain amortised; at cfg2 8 slices measured 1.5-1.7e9, 32 1.97e9)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
