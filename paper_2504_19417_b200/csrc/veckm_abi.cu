@@ -866,17 +866,22 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
     if (!rc && counts_host) rc = grow(&h->pcnt[i], &h->pcnt_cap[i], size_t(nmax));
     if (rc) return rc;
   }
-  // Host packing (VKM_HOST_PACK=1): 8 instead of 24 bytes per event over PCIe;
-  // the host threads pack chunk c+1 while the GPU runs chunk c.  Needs the
-  // tensor-core head and 16-bit pixel coordinates.  Off by default: with the
-  // AVX-512 packer (host_pack.cpp) it is +3 % at config 2 (1.72e9 vs 1.67e9
-  // flows/s e2e: the host's memory bandwidth, not PCIe, bounds both) and it
-  // stalls the small-slice pipelines (configs 1, 4: -50 %).
-  static const bool pack_env = [] {
+  // Host packing: 8 instead of 24 bytes per event over PCIe (f32 time
+  // argument computed on the host in f64 exactly like k_prep, 16-bit pixel
+  // coordinates; host_pack.cpp's AVX-512 packer on a host thread pool packs
+  // chunk c+1 while the GPU runs chunk c).  Needs the tensor-core head and
+  // 16-bit coordinates.  Default: on for calls of >= 8M events, where it
+  // measured +4.5 % (cfg2), +9 % (cfg4), +18 % (cfg3), +8 % (cfg5) e2e and
+  // equal at cfg1; small calls stall on the synchronous packing of their
+  // first chunks (cfg1/cfg4 at 8 slices per call: -50 %).  VKM_HOST_PACK=0/1
+  // forces it.
+  static const int pack_env = [] {
     const char* e = std::getenv("VKM_HOST_PACK");
-    return e && e[0] == '1';
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
-  const bool pack = pack_env && batchable(h) && h->p.width < 65535 && h->p.height < 65535;
+  const int64_t total_events = offsets[n_slices] - offsets[0];
+  const bool pack_wanted = pack_env >= 0 ? pack_env == 1 : total_events >= (int64_t(8) << 20);
+  const bool pack = pack_wanted && batchable(h) && h->p.width < 65535 && h->p.height < 65535;
   if (pack)
     for (int i = 0; i < 2; ++i)
       if (h->hpack_cap[i] < size_t(nmax)) {
