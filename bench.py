@@ -346,9 +346,16 @@ def run_b200(args):
         per_slice = n if spatial else world * n_e2e
         e2e_s = timed(call_batch, reps)
         single_s = timed(call_single, max(5, args.steps // 4))
-        e2e = {"value": per_slice * K * reps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 24 * n_e2e,
-               "d2h_bytes_per_step": 8 * n_e2e, "steps": K * reps, "slices_per_call": K,
-               "api": "vkm_predict_batch_host (C-ABI, pinned host buffers, copy/compute overlap)",
+        # the C-ABI packs the f64 rows into 8-byte records on the host for
+        # calls of >= 8M events (VKM_HOST_PACK forces it on/off): PCIe bytes
+        pk = os.environ.get("VKM_HOST_PACK")
+        packed = (pk == "1") if pk is not None else K * n_e2e >= (8 << 20)
+        e2e = {"value": per_slice * K * reps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": (8 if packed else 24) * n_e2e, "d2h_bytes_per_step": 8 * n_e2e,
+               "input_bytes_per_step": 24 * n_e2e, "host_packed": bool(packed),
+               "steps": K * reps, "slices_per_call": K,
+               "api": "vkm_predict_batch_host (C-ABI, pinned host buffers of (n,3) f64 rows, copy/compute "
+                      "overlap" + ("; rows packed to 8-byte records by host threads" if packed else "") + ")",
                "single_slice": {"value": per_slice * max(5, args.steps // 4) / single_s,
                                 "api": "vkm_predict_host (synchronous, one slice per call)"}}
 
