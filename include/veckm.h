@@ -186,6 +186,21 @@ typedef struct vkm_event_check {
 int vkm_check_events(const double* events_host, int64_t n, int64_t ld, int32_t width, int32_t height,
                      vkm_event_check* out);
 
+/* Stream windowing on the device (slice_stream, events.py:331-387):
+ * vkm_window_bounds: for a time-sorted device stream (n, 3), the bounds
+ *   [lo, hi) of windows [starts[i], starts[i] + window) by binary search
+ *   (np.searchsorted side="left" at both edges), written to bounds_host
+ *   (n_windows, 2) int64.
+ * vkm_predict_windows: per-window flows for those bounds, each window with its
+ *   start as time origin; the windows' rows are gathered on the device
+ *   (overlapping windows share one upload of the stream), flows_dev (sum of
+ *   window sizes, 2) f32 in window order.  Synchronous on `stream`. */
+int vkm_window_bounds(vkm_handle* h, const double* events_dev, int64_t n, const double* starts_host,
+                      int32_t n_windows, double window, int64_t* bounds_host);
+int vkm_predict_windows(vkm_handle* h, const double* events_dev, int64_t n, const double* starts_host,
+                        const int64_t* bounds_host, int32_t n_windows, float* flows_dev, int32_t* counts_dev,
+                        void* stream);
+
 /* Many independent slices in one call.  Slice s holds events
  * [offsets[s], offsets[s+1]) of events_dev; offsets_host has n_slices+1
  * entries; t_starts_host has n_slices entries (NAN = first event). */

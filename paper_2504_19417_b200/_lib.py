@@ -62,6 +62,8 @@ SIGNATURES = {
     "vkm_train_keep": (C.c_int, [_P]),
     "vkm_train_get": (C.c_int, [_P, C.c_int32, _D, _D, _D, _D]),
     "vkm_check_events": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.c_int32, _P]),
+    "vkm_window_bounds": (C.c_int, [_P, _P, C.c_int64, _D, C.c_int32, C.c_double, _I64]),
+    "vkm_predict_windows": (C.c_int, [_P, _P, C.c_int64, _D, _I64, C.c_int32, _P, _P, _P]),
     "vkm_predict_batch": (C.c_int, [_P, _P, _I64, C.c_int32, _D, _P, _P, _P]),
     "vkm_predict_batch_host": (C.c_int, [_P, _P, _I64, C.c_int32, _D, _P, _P]),
     "vkm_grid": (C.c_int, [_P, _P, C.c_int64, C.c_double, C.c_int32, _P, _P, _P]),

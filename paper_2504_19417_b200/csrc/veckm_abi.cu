@@ -151,6 +151,10 @@ struct vkm_handle {
   int64_t g64_cap = 0;
   double* out64 = nullptr;   // f64 host-variant output staging
   size_t out64_cap = 0;
+  double* win_ev = nullptr;     // stream windowing: gathered window rows (n, 3)
+  size_t win_ev_cap = 0;
+  int64_t* win_aux = nullptr;   // window starts (as doubles), bounds, offsets, lows
+  size_t win_aux_cap = 0;
   float* w1p = nullptr;  // [hidden][2*D8] padded
   float* b1 = nullptr;
   float* w2 = nullptr;
@@ -665,7 +669,7 @@ void vkm_destroy(vkm_handle* h) {
   if (!h) return;
   DeviceGuard dg(h->p.device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->myp, h->xyz64, h->t64, h->mx64, h->my64, h->g64a, h->g64b, h->out64, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
+  void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->myp, h->xyz64, h->t64, h->mx64, h->my64, h->g64a, h->g64b, h->out64, h->win_ev, h->win_aux, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
                   h->G, h->C, h->Q, h->NQ, h->feats, h->cnt_scratch, h->ev_stage, h->out_stage, h->cnt_stage,
                   h->sb.pix, h->sb.val, h->sb.start, h->sb.val_s, h->sb.pix_s, h->sb.temp, h->sb.sort_temp,
                   h->sb.rank, h->sb.longlist, h->sb.longcount};
@@ -1293,6 +1297,61 @@ int vkm_train_get(vkm_trainer* t, int32_t best, double* w1, double* b1, double* 
   b2[0] = packed[FH + 3 * H];
   b2[1] = packed[FH + 3 * H + 1];
   return VKM_OK;
+}
+
+int vkm_window_bounds(vkm_handle* h, const double* ev, int64_t n, const double* starts_host, int32_t n_windows,
+                      double window, int64_t* bounds_host) {
+  if (int rc = check_handle(h)) return rc;
+  if (n < 0 || n_windows < 0) return fail(VKM_EINVAL, "n and n_windows must be non-negative");
+  if (n_windows == 0) return VKM_OK;
+  if ((n > 0 && !ev) || !starts_host || !bounds_host) return fail(VKM_EINVAL, "null buffer");
+  if (!(window > 0.0)) return fail(VKM_EINVAL, "window must be positive");
+  DeviceGuard dg(h->p.device);
+  int rc = grow(&h->win_aux, &h->win_aux_cap, 3 * size_t(n_windows));
+  if (rc) return rc;
+  cudaStream_t s = h->stream;
+  double* starts_dev = reinterpret_cast<double*>(h->win_aux);
+  int64_t* bounds_dev = h->win_aux + n_windows;
+  VKM_CK(cudaMemcpyAsync(starts_dev, starts_host, sizeof(double) * n_windows, cudaMemcpyHostToDevice, s));
+  vkm::launch_window_bounds(ev, n, starts_dev, n_windows, window, bounds_dev, s);
+  VKM_CK(cudaGetLastError());
+  VKM_CK(cudaMemcpyAsync(bounds_host, bounds_dev, sizeof(int64_t) * 2 * n_windows, cudaMemcpyDeviceToHost, s));
+  VKM_CK(cudaStreamSynchronize(s));
+  return VKM_OK;
+}
+
+int vkm_predict_windows(vkm_handle* h, const double* ev, int64_t n, const double* starts_host,
+                        const int64_t* bounds_host, int32_t n_windows, float* flows, int32_t* counts, void* stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (n_windows < 0) return fail(VKM_EINVAL, "n_windows must be non-negative");
+  if (n_windows == 0) return VKM_OK;
+  if (!starts_host || !bounds_host) return fail(VKM_EINVAL, "null host buffer");
+  std::vector<int64_t> off(size_t(n_windows) + 1, 0);
+  std::vector<int64_t> lo(static_cast<size_t>(n_windows), 0);
+  for (int32_t w = 0; w < n_windows; ++w) {
+    const int64_t a = bounds_host[2 * w], b = bounds_host[2 * w + 1];
+    if (a < 0 || b < a || b > n) return fail(VKM_EINVAL, "window bounds outside the stream");
+    lo[w] = a;
+    off[w + 1] = off[w] + (b - a);
+  }
+  const int64_t total = off[n_windows];
+  if (total == 0) return VKM_OK;
+  if (!ev || !flows) return fail(VKM_EINVAL, "null device buffer");
+  DeviceGuard dg(h->p.device);
+  int rc = grow(&h->win_ev, &h->win_ev_cap, size_t(total) * 3);
+  if (!rc) rc = grow(&h->win_aux, &h->win_aux_cap, 3 * size_t(n_windows) + 1);
+  if (rc) return rc;
+  cudaStream_t sm = static_cast<cudaStream_t>(stream);
+  int64_t* off_dev = h->win_aux;
+  int64_t* lo_dev = h->win_aux + n_windows + 1;
+  VKM_CK(cudaMemcpyAsync(off_dev, off.data(), sizeof(int64_t) * (n_windows + 1), cudaMemcpyHostToDevice, sm));
+  VKM_CK(cudaMemcpyAsync(lo_dev, lo.data(), sizeof(int64_t) * n_windows, cudaMemcpyHostToDevice, sm));
+  vkm::launch_gather_windows(ev, off_dev, lo_dev, n_windows, total, h->win_ev, sm);
+  VKM_CK(cudaGetLastError());
+  rc = vkm_predict_batch(h, h->win_ev, off.data(), n_windows, starts_host, flows, counts, stream);
+  // the host arrays above are read by the async copies: finish them before returning
+  VKM_CK(cudaStreamSynchronize(sm));
+  return rc;
 }
 
 int vkm_set_profiling(vkm_handle* h, int32_t enable) {

@@ -146,6 +146,14 @@ void launch_train_batch(const double* feats, const double* u, const int64_t* idx
                         double lr, int64_t step, double* loss_part, double* g_part, int64_t* bad_step,
                         cudaStream_t s);
 
+// Stream windowing (k_window.cu): bounds [lo, hi) of windows [start, start +
+// window) in a time-sorted device stream (searchsorted side="left"), and the
+// gather of the windows' rows into one batch buffer (off: exclusive offsets).
+void launch_window_bounds(const double* ev, int64_t n, const double* starts_dev, int32_t nw, double window,
+                          int64_t* bounds_dev, cudaStream_t s);
+void launch_gather_windows(const double* ev, const int64_t* off_dev, const int64_t* lo_dev, int32_t nw,
+                           int64_t total, double* out, cudaStream_t s);
+
 // Layout conversion for the parity hook: planes -> reference [x][y][D] complex64.
 // mx/my non-null: G holds the pre-modulated grid M and is demodulated on the way out.
 // packed: G uses the packed-pair layout (the pooled grid Q).

@@ -256,13 +256,65 @@ def slice_stream(stream: EventStream, delta_t: float, stride: float, t0: float =
             for lo, hi, start in window_bounds(t, delta_t, stride, t0)]
 
 
-def predict_stream(regressor, stream: EventStream, stride: Optional[float] = None, t0: float = 0.0):
+def _window_starts(t: np.ndarray, stride: float, t0: float) -> np.ndarray:
+    """The reference loop's window starts t0 + i·stride while <= t[-1] (events.py:363-368)."""
+    t_last = float(t[-1])
+    count = 0
+    while t0 + count * stride <= t_last:
+        count += 1
+    return np.array([t0 + i * stride for i in range(count)], dtype=np.float64)
+
+
+def _predict_stream_device(eng, t, x, y, dt: float, stride: float, t0: float):
+    """The windows searched and gathered on the GPU (vkm_window_bounds /
+    vkm_predict_windows): the stream crosses PCIe once however much the
+    windows overlap."""
+    import ctypes as C
+    import torch
+    from . import _lib
+    n = len(t)
+    host = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    hv = host.numpy()
+    hv[:, 0], hv[:, 1], hv[:, 2] = t, x, y
+    ev = host.to(torch.device("cuda", eng.device), non_blocking=True)
+    starts = _window_starts(t, stride, t0)
+    nw = len(starts)
+    bounds = np.empty((nw, 2), dtype=np.int64)
+    torch.cuda.current_stream(eng.device).synchronize()
+    _lib.check(eng._lib.vkm_window_bounds(eng._h, C.c_void_p(ev.data_ptr()), n,
+                                          starts.ctypes.data_as(C.POINTER(C.c_double)), nw, 2.0 * dt,
+                                          bounds.ctypes.data_as(C.POINTER(C.c_int64))))
+    while nw and bounds[nw - 1, 1] == bounds[nw - 1, 0]:   # trailing empty windows are dropped
+        nw -= 1
+    starts, bounds = np.ascontiguousarray(starts[:nw]), np.ascontiguousarray(bounds[:nw])
+    sizes = bounds[:, 1] - bounds[:, 0]
+    offsets = np.zeros(nw + 1, dtype=np.int64)
+    np.cumsum(sizes, out=offsets[1:])
+    total = int(offsets[-1])
+    if total == 0:
+        return [(float(s), np.empty((0, 2))) for s in starts]
+    flows = torch.empty((total, 2), dtype=torch.float32, device=ev.device)
+    _lib.check(eng._lib.vkm_predict_windows(eng._h, C.c_void_p(ev.data_ptr()), n,
+                                            starts.ctypes.data_as(C.POINTER(C.c_double)),
+                                            bounds.ctypes.data_as(C.POINTER(C.c_int64)), nw,
+                                            C.c_void_p(flows.data_ptr()), None,
+                                            C.c_void_p(torch.cuda.current_stream(eng.device).cuda_stream)))
+    out = flows.cpu().numpy().astype(np.float64)
+    return [(float(s), out[a:b]) for s, a, b in zip(starts, offsets[:-1], offsets[1:])]
+
+
+def predict_stream(regressor, stream: EventStream, stride: Optional[float] = None, t0: float = 0.0,
+                   device_windows: Optional[bool] = None):
     """Per-window normal flow over a whole stream on the B200 path.
 
     Returns a list of (t_start, flows) with flows (n_window, 2) float64, one
     entry per slice_stream window (empty windows give (0, 2) arrays).  The
     window start is each slice's time origin, like predict_flows on a
-    slice_stream slice.  stride defaults to the window (2·delta_t)."""
+    slice_stream slice.  stride defaults to the window (2·delta_t).
+
+    device_windows: search and gather the windows on the GPU (the stream is
+    uploaded once); default when the windows overlap (stride < window),
+    where the host path would copy shared events once per window."""
     from .estimators import _pinned_pair
     dt = float(regressor.delta_t)
     if stride is None:
@@ -271,11 +323,21 @@ def predict_stream(regressor, stream: EventStream, stride: Optional[float] = Non
     if (g.width, g.height) != (regressor.width, regressor.height):
         raise GeometryError(f"stream geometry {g.width}x{g.height} does not match the estimator's "
                             f"{regressor.width}x{regressor.height}")
+    if dt <= 0:
+        raise ValueError("delta_t must be positive")
+    if stride <= 0:
+        raise ValueError("stride must be positive")
     eng = regressor.engine()
     t, x, y = stream.t, stream.x, stream.y
     if len(t) and np.any(np.diff(t) < 0):
         order = np.argsort(t, kind="stable")
         t, x, y = t[order], x[order], y[order]
+    if len(t) == 0:
+        return []
+    if device_windows is None:
+        device_windows = stride < 2.0 * dt
+    if device_windows:
+        return _predict_stream_device(eng, t, x, y, dt, stride, t0)
     wins = window_bounds(t, dt, stride, t0)
     if not wins:
         return []

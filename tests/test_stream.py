@@ -111,3 +111,31 @@ def test_predict_stream_matches_per_window_predictions():
     emb, _ = vo.pool(g, vo.spatial_table(fr, 10, 10), ev[q, 0] - s.t_start, s.x[q].astype(np.int64),
                      s.y[q].astype(np.int64), fr, 0.016)
     np.testing.assert_allclose(res[7][1][q], vo.mlp(w.w1, w.b1, w.w2, w.b2, vo.to_features(emb)), rtol=0, atol=1e-4)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("stride", [0.004, 0.01, 0.032, 0.05])
+def test_device_windowing_matches_host_windowing(stride):
+    """vkm_window_bounds / vkm_predict_windows (windows searched and gathered on
+    the GPU from one upload of the stream) equal the host-windowed batch: same
+    windows and starts, flows within 1e-6 (the two paths group the windows
+    into different launch batches, which moves f32 roundings)."""
+    if not has_cuda():
+        pytest.fail("GPU test needs a CUDA device")
+    import paper_2504_19417_b200 as pkg
+    S = _S()
+    W, H = 100, 80
+    rng = np.random.default_rng(31)
+    n = 40000
+    t = np.sort(np.concatenate([rng.uniform(0.0, 0.15, n // 2), rng.uniform(0.25, 0.4, n - n // 2)]))  # a gap
+    st = S.EventStream(t, rng.integers(0, W, n), rng.integers(0, H, n), S.CameraGeometry(W, H))
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    reg = pkg.NormalFlowRegressor(width=W, height=H, weights=w)
+    dev = S.predict_stream(reg, st, stride=stride, t0=0.0, device_windows=True)
+    host = S.predict_stream(reg, st, stride=stride, t0=0.0, device_windows=False)
+    ref = S.slice_stream(st, 0.016, stride, 0.0)
+    assert len(dev) == len(host) == len(ref)
+    for (sd, fd), (sh, fh), r in zip(dev, host, ref):
+        assert sd == sh == r.t_start and fd.shape == fh.shape == (len(r), 2)
+        np.testing.assert_allclose(fd, fh, rtol=0, atol=1e-6)
