@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import os
 import struct
+import threading
 from dataclasses import dataclass
 from typing import List, Optional, Tuple
 
@@ -265,6 +266,20 @@ def _window_starts(t: np.ndarray, stride: float, t0: float) -> np.ndarray:
     return np.array([t0 + i * stride for i in range(count)], dtype=np.float64)
 
 
+_staging = threading.local()
+
+
+def _pinned(name: str, n: int, dtype):
+    """A grow-only page-locked host buffer per thread (reused across calls:
+    pinning hundreds of MB costs more than the copies it speeds up)."""
+    import torch
+    buf = getattr(_staging, name, None)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(max(n, 1 << 20), dtype=dtype).pin_memory()
+        setattr(_staging, name, buf)
+    return buf[:n]
+
+
 def _predict_stream_device(eng, t, x, y, dt: float, stride: float, t0: float):
     """The windows searched and gathered on the GPU (vkm_window_bounds /
     vkm_predict_windows): the stream crosses PCIe once however much the
@@ -273,10 +288,11 @@ def _predict_stream_device(eng, t, x, y, dt: float, stride: float, t0: float):
     import torch
     from . import _lib
     n = len(t)
-    host = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    dev = torch.device("cuda", eng.device)
+    host = _pinned("ev", 3 * n, torch.float64)
     hv = host.numpy()
-    hv[:, 0], hv[:, 1], hv[:, 2] = t, x, y
-    ev = host.to(torch.device("cuda", eng.device), non_blocking=True)
+    hv[:n], hv[n:2 * n], hv[2 * n:] = t, x, y        # column blocks: contiguous host writes
+    ev = host.to(dev, non_blocking=True).view(3, n).t().contiguous()   # rows [t, x, y] on the device
     starts = _window_starts(t, stride, t0)
     nw = len(starts)
     bounds = np.empty((nw, 2), dtype=np.int64)
@@ -293,13 +309,15 @@ def _predict_stream_device(eng, t, x, y, dt: float, stride: float, t0: float):
     total = int(offsets[-1])
     if total == 0:
         return [(float(s), np.empty((0, 2))) for s in starts]
-    flows = torch.empty((total, 2), dtype=torch.float32, device=ev.device)
+    flows = torch.empty((total, 2), dtype=torch.float32, device=dev)
     _lib.check(eng._lib.vkm_predict_windows(eng._h, C.c_void_p(ev.data_ptr()), n,
                                             starts.ctypes.data_as(C.POINTER(C.c_double)),
                                             bounds.ctypes.data_as(C.POINTER(C.c_int64)), nw,
                                             C.c_void_p(flows.data_ptr()), None,
                                             C.c_void_p(torch.cuda.current_stream(eng.device).cuda_stream)))
-    out = flows.cpu().numpy().astype(np.float64)
+    fh = _pinned("flows", 2 * total, torch.float32)
+    fh.copy_(flows.view(-1))                          # pinned D2H
+    out = fh.numpy().astype(np.float64).reshape(total, 2)   # one widening pass into the result
     return [(float(s), out[a:b]) for s, a, b in zip(starts, offsets[:-1], offsets[1:])]
 
 
@@ -313,8 +331,10 @@ def predict_stream(regressor, stream: EventStream, stride: Optional[float] = Non
     slice_stream slice.  stride defaults to the window (2·delta_t).
 
     device_windows: search and gather the windows on the GPU (the stream is
-    uploaded once); default when the windows overlap (stride < window),
-    where the host path would copy shared events once per window."""
+    uploaded once, results come back through a pinned buffer); the default
+    unless the stream and its windows would take more than
+    VKM_STREAM_DEVICE_BYTES (default 16 GiB) of HBM, where the windows go
+    through the pipelined host batch instead."""
     from .estimators import _pinned_pair
     dt = float(regressor.delta_t)
     if stride is None:
@@ -335,7 +355,9 @@ def predict_stream(regressor, stream: EventStream, stride: Optional[float] = Non
     if len(t) == 0:
         return []
     if device_windows is None:
-        device_windows = stride < 2.0 * dt
+        overlap = max(1.0, 2.0 * dt / stride)     # events per window set ≈ overlap · n
+        need = len(t) * (24 + overlap * (24 + 8))  # stream + gathered rows + f32 flows
+        device_windows = need <= float(os.environ.get("VKM_STREAM_DEVICE_BYTES", 16 << 30))
     if device_windows:
         return _predict_stream_device(eng, t, x, y, dt, stride, t0)
     wins = window_bounds(t, dt, stride, t0)

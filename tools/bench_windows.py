@@ -31,4 +31,9 @@ for stride in (0.032, 0.008):
         rows = sum(len(f) for _, f in r)
         out[f"stride{stride}_{'device' if dev else 'host'}"] = {"s": min(ts), "windows": len(r), "flows": rows,
                                                                 "flows_per_s": rows / min(ts)}
+import cProfile, pstats, io
+pr = cProfile.Profile(); pr.enable()
+S.predict_stream(reg, st, stride=0.008, device_windows=True)
+pr.disable(); b = io.StringIO(); pstats.Stats(pr, stream=b).sort_stats("tottime").print_stats(8)
+out["profile_device_stride0.008"] = b.getvalue().splitlines()[-14:]
 print(json.dumps(out))
