@@ -1,0 +1,30 @@
+"""Reused page-locked host staging for the host-memory batch APIs.
+
+Pinning hundreds of MB per call costs more than the asynchronous copies it
+enables, so each host thread keeps grow-only pinned buffers (torch's host
+allocator) and the calls copy their results out of them before returning."""
+
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+
+_local = threading.local()
+
+
+def pinned(name: str, n: int, dtype=np.float64) -> np.ndarray:
+    """A length-n page-locked array of `dtype`, valid until this thread's next
+    request under the same name."""
+    dt = np.dtype(dtype)
+    key = (name, dt.str)
+    bufs = getattr(_local, "bufs", None)
+    if bufs is None:
+        bufs = _local.bufs = {}
+    buf = bufs.get(key)
+    if buf is None or len(buf) < n:
+        import torch
+        tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32}[dt]
+        buf = torch.empty(max(int(n), 1 << 20), dtype=tdt).pin_memory().numpy()
+        bufs[key] = buf
+    return buf[:n]

@@ -15,6 +15,7 @@ import numpy as np
 from sklearn.base import BaseEstimator, TransformerMixin
 from sklearn.exceptions import NotFittedError
 
+from ._staging import pinned
 from .engine import FlowEngine
 from .errors import DimensionMismatchError, EmptyNeighborhoodError
 from .validation import check_event_array, slice_from_array
@@ -208,7 +209,8 @@ class NormalFlowRegressor(BaseEstimator):
         total = int(sum(sizes))
         if total == 0:
             return [np.full((0, 2), np.nan) for _ in blocks]
-        ev, out = _pinned_pair(total)
+        ev = pinned("batch_events", 3 * total, np.float64).reshape(total, 3)
+        out = pinned("batch_flows", 2 * total, np.float32).reshape(total, 2)
         offsets = np.zeros(len(blocks) + 1, dtype=np.int64)
         np.cumsum(sizes, out=offsets[1:])
         for b, lo in zip(blocks, offsets[:-1]):
@@ -216,7 +218,8 @@ class NormalFlowRegressor(BaseEstimator):
                 ev[lo:lo + len(b)] = b.events
         t_starts = np.array([b.t_start if len(b) else 0.0 for b in blocks], dtype=np.float64)
         eng.predict_batch_host(ev, offsets, t_starts, flows=out)
-        return [out[lo:hi].astype(np.float64) for lo, hi in zip(offsets[:-1], offsets[1:])]
+        res = out.astype(np.float64)   # results leave the reused staging buffer
+        return [res[lo:hi] for lo, hi in zip(offsets[:-1], offsets[1:])]
 
 
 def _stream_predict(self, stream, stride=None, t0: float = 0.0):
@@ -228,15 +231,3 @@ def _stream_predict(self, stream, stride=None, t0: float = 0.0):
 
 
 NormalFlowRegressor.predict_stream = _stream_predict
-
-
-def _pinned_pair(n: int):
-    """Page-locked (n, 3) f64 event and (n, 2) f32 flow buffers (torch's host
-    allocator; plain numpy memory when torch is unavailable)."""
-    try:
-        import torch
-        ev = torch.empty((n, 3), dtype=torch.float64).pin_memory().numpy()
-        out = torch.empty((n, 2), dtype=torch.float32).pin_memory().numpy()
-        return ev, out
-    except Exception:
-        return np.empty((n, 3), dtype=np.float64), np.empty((n, 2), dtype=np.float32)

@@ -18,7 +18,6 @@ from __future__ import annotations
 
 import os
 import struct
-import threading
 from dataclasses import dataclass
 from typing import List, Optional, Tuple
 
@@ -266,20 +265,6 @@ def _window_starts(t: np.ndarray, stride: float, t0: float) -> np.ndarray:
     return np.array([t0 + i * stride for i in range(count)], dtype=np.float64)
 
 
-_staging = threading.local()
-
-
-def _pinned(name: str, n: int, dtype):
-    """A grow-only page-locked host buffer per thread (reused across calls:
-    pinning hundreds of MB costs more than the copies it speeds up)."""
-    import torch
-    buf = getattr(_staging, name, None)
-    if buf is None or buf.numel() < n:
-        buf = torch.empty(max(n, 1 << 20), dtype=dtype).pin_memory()
-        setattr(_staging, name, buf)
-    return buf[:n]
-
-
 def _predict_stream_device(eng, t, x, y, dt: float, stride: float, t0: float):
     """The windows searched and gathered on the GPU (vkm_window_bounds /
     vkm_predict_windows): the stream crosses PCIe once however much the
@@ -287,12 +272,12 @@ def _predict_stream_device(eng, t, x, y, dt: float, stride: float, t0: float):
     import ctypes as C
     import torch
     from . import _lib
+    from ._staging import pinned
     n = len(t)
     dev = torch.device("cuda", eng.device)
-    host = _pinned("ev", 3 * n, torch.float64)
-    hv = host.numpy()
+    hv = pinned("stream_cols", 3 * n, np.float64)
     hv[:n], hv[n:2 * n], hv[2 * n:] = t, x, y        # column blocks: contiguous host writes
-    ev = host.to(dev, non_blocking=True).view(3, n).t().contiguous()   # rows [t, x, y] on the device
+    ev = torch.from_numpy(hv).to(dev, non_blocking=True).view(3, n).t().contiguous()   # rows [t, x, y]
     starts = _window_starts(t, stride, t0)
     nw = len(starts)
     bounds = np.empty((nw, 2), dtype=np.int64)
@@ -315,9 +300,9 @@ def _predict_stream_device(eng, t, x, y, dt: float, stride: float, t0: float):
                                             bounds.ctypes.data_as(C.POINTER(C.c_int64)), nw,
                                             C.c_void_p(flows.data_ptr()), None,
                                             C.c_void_p(torch.cuda.current_stream(eng.device).cuda_stream)))
-    fh = _pinned("flows", 2 * total, torch.float32)
-    fh.copy_(flows.view(-1))                          # pinned D2H
-    out = fh.numpy().astype(np.float64).reshape(total, 2)   # one widening pass into the result
+    fh = pinned("flows", 2 * total, np.float32)
+    torch.from_numpy(fh).copy_(flows.view(-1))        # pinned D2H
+    out = fh.astype(np.float64).reshape(total, 2)     # one widening pass into the result
     return [(float(s), out[a:b]) for s, a, b in zip(starts, offsets[:-1], offsets[1:])]
 
 
@@ -335,7 +320,7 @@ def predict_stream(regressor, stream: EventStream, stride: Optional[float] = Non
     unless the stream and its windows would take more than
     VKM_STREAM_DEVICE_BYTES (default 16 GiB) of HBM, where the windows go
     through the pipelined host batch instead."""
-    from .estimators import _pinned_pair
+    from ._staging import pinned
     dt = float(regressor.delta_t)
     if stride is None:
         stride = 2.0 * dt
@@ -369,7 +354,8 @@ def predict_stream(regressor, stream: EventStream, stride: Optional[float] = Non
     total = int(offsets[-1])
     if total == 0:
         return [(s, np.empty((0, 2))) for _, _, s in wins]
-    ev, out = _pinned_pair(total)
+    ev = pinned("batch_events", 3 * total, np.float64).reshape(total, 3)
+    out = pinned("batch_flows", 2 * total, np.float32).reshape(total, 2)
     for (lo, hi, _), o in zip(wins, offsets[:-1]):
         if hi > lo:   # overlapping windows duplicate their shared events
             ev[o:o + hi - lo, 0] = t[lo:hi]
@@ -377,4 +363,5 @@ def predict_stream(regressor, stream: EventStream, stride: Optional[float] = Non
             ev[o:o + hi - lo, 2] = y[lo:hi]
     t_starts = np.array([s for _, _, s in wins], dtype=np.float64)
     eng.predict_batch_host(ev, offsets, t_starts, flows=out)
-    return [(s, out[a:b].astype(np.float64)) for (_, _, s), a, b in zip(wins, offsets[:-1], offsets[1:])]
+    res = out.astype(np.float64)
+    return [(s, res[a:b]) for (_, _, s), a, b in zip(wins, offsets[:-1], offsets[1:])]
