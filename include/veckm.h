@@ -122,6 +122,12 @@ int vkm_predict_host(vkm_handle* h, const double* events_host, int64_t n, double
                      float* flows_host, int32_t* counts_host);
 int vkm_encode_host(vkm_handle* h, const double* events_host, int64_t n, double t_start,
                     float* feats_host, int32_t* counts_host);
+/* vkm_predict_host with the flows widened to float64 on the host (the type
+ * NormalFlowRegressor.predict returns, estimators.py:203-206): the f32 rows
+ * come back through page-locked staging in pieces and the host pool widens
+ * piece i while piece i+1 is in flight. */
+int vkm_predict_host_wide(vkm_handle* h, const double* events_host, int64_t n, double t_start,
+                          double* flows_host, int32_t* counts_host);
 
 /* precision="f64" (estimators.py:115, encoder.py:37-38: complex128 grid,
  * float64 features; flow.py:98-106: the head promotes the f32 weights to f64).

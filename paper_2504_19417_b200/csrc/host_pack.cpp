@@ -11,6 +11,10 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "host_pool.h"
 
 namespace vkm_host {
 
@@ -185,12 +189,9 @@ __attribute__((target("avx512f,avx512vl,avx512dq"))) int64_t check_avx512(const 
   if (bad_ord) c.sorted = 0;
   return i;
 }
-}  // namespace
-
-extern "C" {
-
-int vkm_check_events(const double* X, int64_t n, int64_t ld, int32_t W, int32_t H, vkm_event_check* out) {
-  if (!out || n < 0 || (n > 0 && (!X || ld < 3))) return 1;
+// One serial pass over rows [0, n) (X already offset): the flags, the
+// first outside pixel (index relative to X), t of the first and last rows.
+void check_range(const double* X, int64_t n, int64_t ld, int32_t W, int32_t H, vkm_event_check& out) {
   vkm_event_check c{0, 0, 0, 1, -1, 0, 0, 0.0, 0.0};
   double prev = n ? X[0] : 0.0;
   static const bool avx512 = [] {
@@ -229,7 +230,49 @@ int vkm_check_events(const double* X, int64_t n, int64_t ld, int32_t W, int32_t 
     c.t_first = X[0];
     c.t_last = X[(n - 1) * ld];
   }
-  *out = c;
+  out = c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vkm_check_events(const double* X, int64_t n, int64_t ld, int32_t W, int32_t H, vkm_event_check* out) {
+  if (!out || n < 0 || (n > 0 && (!X || ld < 3))) return 1;
+  // large inputs: contiguous parts on the shared host pool, merged in part
+  // order (the first outside pixel is the first part's first; sortedness also
+  // checks each part boundary with the same comparison)
+  const int64_t kPart = int64_t(1) << 16;
+  static std::mutex pool_m;
+  std::unique_lock<std::mutex> lock(pool_m, std::defer_lock);
+  if (n >= 4 * kPart && lock.try_lock()) {   // busy (another thread validating): serial pass
+    static vkm_host::HostPool* pool =
+        new vkm_host::HostPool(std::max(0, std::min(15, int(std::thread::hardware_concurrency()) - 1)));   // never torn down
+    const int parts = int(std::min<int64_t>(4 * pool->size(), n / kPart));
+    std::vector<vkm_event_check> pc(parts);
+    pool->run(parts, [&](int p) {
+      const int64_t lo = n * p / parts, hi = n * (p + 1) / parts;
+      check_range(X + lo * ld, hi - lo, ld, W, H, pc[p]);
+      if (pc[p].first_outside >= 0) pc[p].first_outside += lo;
+    });
+    vkm_event_check c = pc[0];
+    for (int p = 1; p < parts; ++p) {
+      const vkm_event_check& q = pc[p];
+      c.nonfinite |= q.nonfinite;
+      c.negative_t |= q.negative_t;
+      c.nonint |= q.nonint;
+      c.sorted &= q.sorted & !(q.t_first < c.t_last);
+      if (c.first_outside < 0 && q.first_outside >= 0) {
+        c.first_outside = q.first_outside;
+        c.outside_x = q.outside_x;
+        c.outside_y = q.outside_y;
+      }
+      c.t_last = q.t_last;
+    }
+    *out = c;
+    return 0;
+  }
+  check_range(X, n, ld, W, H, *out);
   return 0;
 }
 

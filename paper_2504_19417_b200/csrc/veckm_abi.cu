@@ -22,6 +22,7 @@
 
 #include "../../include/veckm.h"
 #include "vkm_kernels.cuh"
+#include "host_pool.h"
 
 namespace {
 
@@ -60,74 +61,6 @@ int round_d8(int D) {
   return d;
 }
 
-// Persistent host worker pool: packs host events into 8-byte records for the
-// pipelined host batch (the calling thread works too).
-class HostPool {
- public:
-  explicit HostPool(int n) {
-    for (int i = 0; i < n; ++i) threads_.emplace_back([this] { loop(); });
-  }
-  ~HostPool() {
-    {
-      std::lock_guard<std::mutex> l(m_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    for (auto& t : threads_) t.join();
-  }
-  int size() const { return int(threads_.size()) + 1; }
-  void run(int parts, const std::function<void(int)>& fn) {
-    {
-      std::lock_guard<std::mutex> l(m_);
-      task_ = &fn;
-      total_ = parts;
-      next_ = 0;
-      done_ = 0;
-      ++gen_;
-    }
-    cv_.notify_all();
-    work();
-    std::unique_lock<std::mutex> l(m_);
-    done_cv_.wait(l, [&] { return done_ == total_; });
-    task_ = nullptr;
-  }
-
- private:
-  void work() {
-    for (;;) {
-      int i;
-      const std::function<void(int)>* fn;
-      {
-        std::lock_guard<std::mutex> l(m_);
-        if (!task_ || next_ >= total_) return;
-        i = next_++;
-        fn = task_;
-      }
-      (*fn)(i);
-      std::lock_guard<std::mutex> l(m_);
-      if (++done_ == total_) done_cv_.notify_all();
-    }
-  }
-  void loop() {
-    uint64_t seen = 0;
-    for (;;) {
-      {
-        std::unique_lock<std::mutex> l(m_);
-        cv_.wait(l, [&] { return stop_ || gen_ != seen; });
-        if (stop_) return;
-        seen = gen_;
-      }
-      work();
-    }
-  }
-  std::vector<std::thread> threads_;
-  std::mutex m_;
-  std::condition_variable cv_, done_cv_;
-  const std::function<void(int)>* task_ = nullptr;
-  int total_ = 0, next_ = 0, done_ = 0;
-  uint64_t gen_ = 0;
-  bool stop_ = false;
-};
 
 }  // namespace
 
@@ -194,8 +127,11 @@ struct vkm_handle {
   int32_t* pcnt[2] = {nullptr, nullptr};
   size_t pcnt_cap[2] = {0, 0};
   uint2* hpack[2] = {nullptr, nullptr};   // page-locked packed-event staging (host)
+  float* hout = nullptr;                  // page-locked flow staging of the single-slice host calls
+  size_t hout_cap = 0;
+  cudaEvent_t dl_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // download pieces
   size_t hpack_cap[2] = {0, 0};
-  HostPool* pool = nullptr;
+  vkm_host::HostPool* pool = nullptr;
   uint8_t* sel_temp = nullptr;   // vkm_select_rows: count + CUB scratch
   size_t sel_temp_cap = 0;
   // timing
@@ -422,7 +358,7 @@ void pack_chunk(vkm_handle* h, const double* ev, const int64_t* offsets, const d
   for (int s = s0, b = 0; b < st.nb; ++s)
     if (offsets[s + 1] > offsets[s] && offsets[s] - base == st.off[b]) sidx[b++] = s;
   const int64_t n = st.off[st.nb];
-  if (!h->pool) h->pool = new HostPool(std::max(0, std::min(15, int(std::thread::hardware_concurrency()) - 1)));
+  if (!h->pool) h->pool = new vkm_host::HostPool(std::max(0, std::min(15, int(std::thread::hardware_concurrency()) - 1)));
   const int parts = std::max(1, std::min<int>(4 * h->pool->size(), int((n + 65535) / 65536)));
   h->pool->run(parts, [&](int part) {
     const int64_t lo = n * part / parts, hi = n * (part + 1) / parts;
@@ -433,6 +369,89 @@ void pack_chunk(vkm_handle* h, const double* ev, const int64_t* offsets, const d
       vkm_host::pack_events(ev + 3 * (base + s_lo), s_hi - s_lo, t0, dt, W, H, reinterpret_cast<uint32_t*>(out + s_lo));
     }
   });
+}
+
+// Pack events [lo, hi) of one slice (time origin t0) on the host pool.
+void pack_range(vkm_handle* h, const double* ev, int64_t lo, int64_t hi, double t0, uint2* out) {
+  if (!h->pool) h->pool = new vkm_host::HostPool(std::max(0, std::min(15, int(std::thread::hardware_concurrency()) - 1)));
+  const int64_t m = hi - lo;
+  const int parts = std::max(1, std::min<int>(h->pool->size(), int((m + 32767) / 32768)));
+  h->pool->run(parts, [&](int part) {
+    const int64_t a = lo + m * part / parts, b = lo + m * (part + 1) / parts;
+    if (b > a)
+      vkm_host::pack_events(ev + 3 * a, b - a, t0, h->p.delta_t, h->p.width, h->p.height,
+                            reinterpret_cast<uint32_t*>(out + a));
+  });
+}
+
+// Single-slice host calls: pageable rows -> 8-byte records in page-locked
+// staging (host pool), copied in pieces so packing piece i+1 overlaps the
+// copy of piece i.  A pageable 24-byte-per-event copy runs at ~20 GB/s; the
+// packed one moves a third of the bytes at the pinned rate.
+bool single_pack(const vkm_handle* h, int64_t n) {
+  static const int64_t min_events = [] {   // VKM_HOST_PACK_SINGLE: minimum events (0 = off)
+    const char* e = std::getenv("VKM_HOST_PACK_SINGLE");
+    return e ? int64_t(std::atoll(e)) : int64_t(1) << 17;
+  }();
+  return min_events > 0 && n >= min_events && batchable(h) && h->p.width < 65535 && h->p.height < 65535;
+}
+
+int upload_packed(vkm_handle* h, const double* ev_host, int64_t n, double t0, cudaStream_t s, uint2** dev) {
+  if (h->hpack_cap[0] < size_t(n)) {
+    if (h->hpack[0]) cudaFreeHost(h->hpack[0]);
+    h->hpack[0] = nullptr;
+    h->hpack_cap[0] = 0;
+    VKM_CK(cudaHostAlloc(&h->hpack[0], sizeof(uint2) * size_t(n), cudaHostAllocDefault));
+    h->hpack_cap[0] = size_t(n);
+  }
+  int rc = grow(&h->ev_stage, &h->ev_cap, size_t(n) * 3);   // n uint2 fit in 3n doubles
+  if (rc) return rc;
+  uint2* d = reinterpret_cast<uint2*>(h->ev_stage);
+  const int pieces = int(std::min<int64_t>(4, (n + (1 << 17) - 1) >> 17));
+  for (int i = 0; i < pieces; ++i) {
+    const int64_t lo = n * i / pieces, hi = n * (i + 1) / pieces;
+    pack_range(h, ev_host, lo, hi, t0, h->hpack[0]);
+    VKM_CK(cudaMemcpyAsync(d + lo, h->hpack[0] + lo, sizeof(uint2) * (hi - lo), cudaMemcpyHostToDevice, s));
+  }
+  *dev = d;
+  return VKM_OK;
+}
+
+// D2H of n flow rows (f32 on the device) into the caller's f32 or f64 buffer
+// through page-locked staging, in pieces: the host pool copies / widens piece
+// i while piece i+1 is in flight.  Ends with the stream drained up to the
+// last piece.
+int download_flows(vkm_handle* h, const float* dev, int64_t n, cudaStream_t s, float* out32, double* out64) {
+  if (h->hout_cap < size_t(2 * n)) {
+    if (h->hout) cudaFreeHost(h->hout);
+    h->hout = nullptr;
+    h->hout_cap = 0;
+    VKM_CK(cudaHostAlloc(&h->hout, sizeof(float) * size_t(2 * n), cudaHostAllocDefault));
+    h->hout_cap = size_t(2 * n);
+  }
+  for (auto& e : h->dl_ev)
+    if (!e) VKM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const int pieces = int(std::max<int64_t>(1, std::min<int64_t>(4, (n + (1 << 17) - 1) >> 17)));
+  for (int i = 0; i < pieces; ++i) {
+    const int64_t lo = n * i / pieces, hi = n * (i + 1) / pieces;
+    VKM_CK(cudaMemcpyAsync(h->hout + 2 * lo, dev + 2 * lo, sizeof(float) * 2 * (hi - lo), cudaMemcpyDeviceToHost, s));
+    VKM_CK(cudaEventRecord(h->dl_ev[i], s));
+  }
+  if (!h->pool) h->pool = new vkm_host::HostPool(std::max(0, std::min(15, int(std::thread::hardware_concurrency()) - 1)));
+  for (int i = 0; i < pieces; ++i) {
+    const int64_t lo = 2 * (n * i / pieces), hi = 2 * (n * (i + 1) / pieces);
+    VKM_CK(cudaEventSynchronize(h->dl_ev[i]));
+    const int64_t m = hi - lo;
+    const int parts = std::max(1, std::min<int>(h->pool->size(), int((m + 65535) / 65536)));
+    h->pool->run(parts, [&](int part) {
+      const int64_t a = lo + m * part / parts, b = lo + m * (part + 1) / parts;
+      if (out64)
+        for (int64_t k = a; k < b; ++k) out64[k] = double(h->hout[k]);
+      else
+        std::memcpy(out32 + a, h->hout + a, sizeof(float) * size_t(b - a));
+    });
+  }
+  return VKM_OK;
 }
 
 int check_handle(const vkm_handle* h) {
@@ -683,6 +702,9 @@ void vkm_destroy(vkm_handle* h) {
     for (cudaEvent_t e : {h->in_ready[i], h->computed[i], h->out_done[i]})
       if (e) cudaEventDestroy(e);
   }
+  if (h->hout) cudaFreeHost(h->hout);
+  for (auto& e : h->dl_ev)
+    if (e) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i)
     if (h->hpack[i]) cudaFreeHost(h->hpack[i]);
   delete h->pool;
@@ -746,32 +768,63 @@ int vkm_encode(vkm_handle* h, const double* ev, int64_t n, double t_start, float
   return VKM_OK;
 }
 
-int vkm_predict_host(vkm_handle* h, const double* ev_host, int64_t n, double t_start, float* flows_host,
-                     int32_t* counts_host) {
+}  // extern "C"
+
+namespace {
+int predict_host_impl(vkm_handle* h, const double* ev_host, int64_t n, double t_start, float* flows_host,
+                      double* flows64_host, int32_t* counts_host) {
   if (int rc = check_handle(h)) return rc;
   if (h->hidden <= 0) return fail(VKM_EINVAL, "handle has no flow head (hidden == 0)");
   if (n < 0) return fail(VKM_EINVAL, "n must be non-negative");
   if (n == 0) return VKM_OK;
-  if (!ev_host || !flows_host) return fail(VKM_EINVAL, "null host buffer");
+  if (!ev_host || (!flows_host && !flows64_host)) return fail(VKM_EINVAL, "null host buffer");
   DeviceGuard dg(h->p.device);
   int rc = grow(&h->ev_stage, &h->ev_cap, size_t(n) * 3);
   if (!rc) rc = grow(&h->out_stage, &h->out_cap, size_t(n) * 2);
   if (!rc && counts_host) rc = grow(&h->cnt_stage, &h->cnt_stage_cap, size_t(n));
   if (rc) return rc;
   cudaStream_t s = h->stream;
-  VKM_CK(cudaMemcpyAsync(h->ev_stage, ev_host, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
   int launches = 0;
-  rec(h, 0, s);
-  rc = predict_one(h, h->ev_stage, n, t_start, h->out_stage, counts_host ? h->cnt_stage : nullptr, s, &launches);
+  if (single_pack(h, n)) {
+    // the host stages the next call's records into hpack: the previous call has synchronised
+    const double t0 = std::isnan(t_start) ? ev_host[0] : t_start;
+    uint2* packed = nullptr;
+    rc = upload_packed(h, ev_host, n, t0, s, &packed);
+    rec(h, 0, s);
+    if (!rc) rc = predict_chunk(h, h->ev_stage, one_slice(n, t0), h->out_stage, counts_host ? h->cnt_stage : nullptr,
+                                s, &launches, packed);
+  } else {
+    VKM_CK(cudaMemcpyAsync(h->ev_stage, ev_host, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    rec(h, 0, s);
+    rc = predict_one(h, h->ev_stage, n, t_start, h->out_stage, counts_host ? h->cnt_stage : nullptr, s, &launches);
+  }
   if (rc) return rc;
   rec(h, 3, s);
-  VKM_CK(cudaMemcpyAsync(flows_host, h->out_stage, sizeof(float) * 2 * n, cudaMemcpyDeviceToHost, s));
   if (counts_host)
     VKM_CK(cudaMemcpyAsync(counts_host, h->cnt_stage, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  if (flows64_host || single_pack(h, n)) {
+    rc = download_flows(h, h->out_stage, n, s, flows_host, flows64_host);
+    if (rc) return rc;
+  } else {
+    VKM_CK(cudaMemcpyAsync(flows_host, h->out_stage, sizeof(float) * 2 * n, cudaMemcpyDeviceToHost, s));
+  }
   VKM_CK(cudaStreamSynchronize(s));
   h->have_timing = h->profiling;
   h->last_launches = launches;
   return VKM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int vkm_predict_host(vkm_handle* h, const double* ev_host, int64_t n, double t_start, float* flows_host,
+                     int32_t* counts_host) {
+  return predict_host_impl(h, ev_host, n, t_start, flows_host, nullptr, counts_host);
+}
+
+int vkm_predict_host_wide(vkm_handle* h, const double* ev_host, int64_t n, double t_start, double* flows_host,
+                          int32_t* counts_host) {
+  return predict_host_impl(h, ev_host, n, t_start, nullptr, flows_host, counts_host);
 }
 
 int vkm_encode_host(vkm_handle* h, const double* ev_host, int64_t n, double t_start, float* feats_host,

@@ -98,6 +98,17 @@ class FlowEngine:
                                                   counts.ctypes.data if counts is not None else None))
         return (flows, counts) if return_counts else flows
 
+    def predict_host_wide(self, events: np.ndarray, t_start: float = math.nan, return_counts: bool = False):
+        """predict_host with (n, 2) float64 flows (vkm_predict_host_wide)."""
+        ev = np.ascontiguousarray(events, dtype=np.float64)
+        n = len(ev)
+        flows = np.empty((n, 2), dtype=np.float64)
+        counts = np.empty(n, dtype=np.int32) if return_counts else None
+        if n:
+            _lib.check(self._lib.vkm_predict_host_wide(self._h, ev.ctypes.data, n, float(t_start), flows.ctypes.data,
+                                                       counts.ctypes.data if counts is not None else None))
+        return (flows, counts) if return_counts else flows
+
     def predict_batch_host(self, events: np.ndarray, offsets: Sequence[int], t_starts=None,
                            flows: Optional[np.ndarray] = None, return_counts: bool = False):
         """Many slices from host memory in one pipelined call (copy-in of slice

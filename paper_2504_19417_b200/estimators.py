@@ -192,8 +192,7 @@ class NormalFlowRegressor(BaseEstimator):
             return np.full((0, 2), np.nan)
         if self.precision == "f64":   # f64 grid, features and head (encoder.py:37-38, flow.py:98-106)
             return eng.predict_host_f64(block.events, block.t_start)
-        flows = eng.predict_host(block.events, block.t_start)
-        return flows.astype(np.float64)
+        return eng.predict_host_wide(block.events, block.t_start)
 
     def predict_slices(self, slices: Sequence) -> List[np.ndarray]:
         """Additive API: many independent slices, one result

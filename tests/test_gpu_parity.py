@@ -498,3 +498,54 @@ def test_spatial_split_device_path_two_ranks(tmp_path):
     got = np.load(out_path)
     assert np.isfinite(got).all()
     np.testing.assert_allclose(got, full, rtol=0, atol=1e-5)
+
+
+def test_single_slice_host_packing_and_wide_output():
+    """vkm_predict_host on large single slices packs the rows on host threads
+    into page-locked staging (n >= VKM_HOST_PACK_SINGLE) and brings the flows
+    back in pinned pieces; vkm_predict_host_wide widens them to float64 on the
+    host pool.  Both equal the unpacked f64-row path bitwise (fresh process,
+    VKM_HOST_PACK_SINGLE=0), out-of-sensor / non-integer pixels included, with
+    an explicit and a NaN t_start."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    pkg = _pkg()
+    W, H = 320, 240
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    eng = pkg.FlowEngine(W, H, 10, 10, 0.016, b, w)
+    ev = np.ascontiguousarray(vo.synth_uniform_noise(300_000, W, H, seed=77))
+    ev[1000, 1] = W          # outside
+    ev[2000, 2] = 7.25       # not an integer pixel
+    res = {}
+    for ts in (float(ev[0, 0]) - 1e-3, math.nan):
+        f, c = eng.predict_host(ev, ts, return_counts=True)
+        fw, cw = eng.predict_host_wide(ev, ts, return_counts=True)
+        assert fw.dtype == np.float64
+        np.testing.assert_array_equal(fw, f.astype(np.float64))
+        np.testing.assert_array_equal(cw, c)
+        assert np.isnan(f[[1000, 2000]]).all() and (c[[1000, 2000]] == 0).all()
+        res[str(ts)] = (f, c)
+    small, sc = eng.predict_host_wide(ev[:5000], math.nan, return_counts=True)   # below the packing threshold
+    np.testing.assert_array_equal(small, eng.predict_host(ev[:5000], math.nan).astype(np.float64))
+    with tempfile.TemporaryDirectory() as td:
+        np.save(os.path.join(td, "ev.npy"), ev)
+        code = (
+            "import sys, math, numpy as np; sys.path.insert(0, %r); import paper_2504_19417_b200 as pkg;"
+            "ev = np.load(%r); b = pkg.generate_bases(64); w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32);"
+            "e = pkg.FlowEngine(%d, %d, 10, 10, 0.016, b, w);"
+            "r = [e.predict_host(ev, t, return_counts=True) for t in (%r, math.nan)];"
+            "np.savez(%r, f0=r[0][0], c0=r[0][1], f1=r[1][0], c1=r[1][1])"
+        ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.join(td, "ev.npy"), W, H,
+             float(ev[0, 0]) - 1e-3, os.path.join(td, "r.npz"))
+        out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, VKM_HOST_PACK_SINGLE="0"),
+                             capture_output=True, text=True, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        r = np.load(os.path.join(td, "r.npz"))
+        (f0, c0), (f1, c1) = res[str(float(ev[0, 0]) - 1e-3)], res["nan"]
+        np.testing.assert_array_equal(r["c0"], c0)
+        np.testing.assert_array_equal(r["f0"], f0)
+        np.testing.assert_array_equal(r["c1"], c1)
+        np.testing.assert_array_equal(r["f1"], f1)

@@ -240,25 +240,64 @@ def test_native_event_check_matches_numpy_semantics():
                 X[i, 0] = 0.05 * rng.uniform()             # breaks the order
             else:
                 X[i, 2] = 2.0 ** 60                        # huge but integer-valued
-        c = v._EventCheck()
-        assert lib.vkm_check_events(X.ctypes.data, n, cols, W, H, ctypes.byref(c)) == 0
-        X3 = X[:, :3]
-        t, x, y = X3[:, 0], X3[:, 1], X3[:, 2]
-        fin = np.isfinite(X3).all(axis=1)
-        assert bool(c.nonfinite) == (not fin.all())
-        assert bool(c.negative_t) == bool(np.any(t < 0))
-        with np.errstate(invalid="ignore"):
-            nonint = bool(np.any(fin & ((x != np.round(x)) | (y != np.round(y)))))
-            xi, yi = x.astype(np.int32), y.astype(np.int32)
-        assert bool(c.nonint) == nonint
-        with np.errstate(invalid="ignore"):
-            assert bool(c.sorted) == (not np.any(np.diff(t) < 0))
-        outside = fin & ~((xi >= 0) & (xi < W) & (yi >= 0) & (yi < H))
-        if outside.any():
-            k = int(np.flatnonzero(outside)[0])
-            assert (c.first_outside, c.outside_x, c.outside_y) == (k, xi[k], yi[k])
-        else:
-            assert c.first_outside == -1
+        _assert_check_matches(lib, X, W, H)
+
+
+def _assert_check_matches(lib, X, W, H):
+    import ctypes
+    from paper_2504_19417_b200 import validation as v
+    n, cols = X.shape
+    c = v._EventCheck()
+    assert lib.vkm_check_events(X.ctypes.data, n, cols, W, H, ctypes.byref(c)) == 0
+    X3 = X[:, :3]
+    t, x, y = X3[:, 0], X3[:, 1], X3[:, 2]
+    fin = np.isfinite(X3).all(axis=1)
+    assert bool(c.nonfinite) == (not fin.all())
+    assert bool(c.negative_t) == bool(np.any(t < 0))
+    with np.errstate(invalid="ignore"):
+        nonint = bool(np.any(fin & ((x != np.round(x)) | (y != np.round(y)))))
+        xi, yi = x.astype(np.int32), y.astype(np.int32)
+    assert bool(c.nonint) == nonint
+    with np.errstate(invalid="ignore"):
+        assert bool(c.sorted) == (not np.any(np.diff(t) < 0))
+    outside = fin & ~((xi >= 0) & (xi < W) & (yi >= 0) & (yi < H))
+    if outside.any():
+        k = int(np.flatnonzero(outside)[0])
+        assert (c.first_outside, c.outside_x, c.outside_y) == (k, xi[k], yi[k])
+    else:
+        assert c.first_outside == -1
+    if n:
+        assert (c.t_first, c.t_last) == (X[0, 0], X[-1, 0]) or np.isnan(X[[0, -1], 0]).any()
+
+
+def test_native_event_check_parallel_parts():
+    """Large inputs are checked in contiguous parts on the host pool and
+    merged: defects placed on and around part boundaries (order breaks
+    across a boundary, the first outside pixel in a late part while an
+    earlier part is clean) give the serial pass's answer."""
+    from paper_2504_19417_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(12)
+    W, H = 64, 48
+    for trial in range(12):
+        n = int(rng.integers(1 << 18, 1 << 20))
+        X = np.stack([np.sort(rng.uniform(0, 0.03, n)), rng.integers(0, W, n), rng.integers(0, H, n)],
+                     1).astype(np.float64)
+        cuts = [n * k // 16 for k in range(1, 16)] + [n * k // 64 for k in range(1, 64, 7)]
+        for _ in range(int(rng.integers(0, 4))):
+            i = int(np.clip(rng.choice(cuts) + int(rng.integers(-2, 2)), 1, n - 1))
+            kind = int(rng.integers(0, 5))
+            if kind == 0:
+                X[i, 0] = X[i - 1, 0] - 1e-9                # order break at / near a boundary
+            elif kind == 1:
+                X[i, 1] = W + int(rng.integers(0, 3))       # outside
+            elif kind == 2:
+                X[i, 2] = np.nan
+            elif kind == 3:
+                X[i, 1] += 0.25
+            else:
+                X[i, 0] = -1.0
+        _assert_check_matches(lib, X, W, H)
 
 
 def test_product_path_does_not_import_the_oracle():
