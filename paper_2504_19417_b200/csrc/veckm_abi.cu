@@ -388,12 +388,15 @@ void pack_range(vkm_handle* h, const double* ev, int64_t lo, int64_t hi, double 
 // staging (host pool), copied in pieces so packing piece i+1 overlaps the
 // copy of piece i.  A pageable 24-byte-per-event copy runs at ~20 GB/s; the
 // packed one moves a third of the bytes at the pinned rate.
-bool single_pack(const vkm_handle* h, int64_t n) {
+bool host_staged(int64_t n) {
   static const int64_t min_events = [] {   // VKM_HOST_PACK_SINGLE: minimum events (0 = off)
     const char* e = std::getenv("VKM_HOST_PACK_SINGLE");
     return e ? int64_t(std::atoll(e)) : int64_t(1) << 17;
   }();
-  return min_events > 0 && n >= min_events && batchable(h) && h->p.width < 65535 && h->p.height < 65535;
+  return min_events > 0 && n >= min_events;
+}
+bool single_pack(const vkm_handle* h, int64_t n) {
+  return host_staged(n) && batchable(h) && h->p.width < 65535 && h->p.height < 65535;
 }
 
 int upload_packed(vkm_handle* h, const double* ev_host, int64_t n, double t0, cudaStream_t s, uint2** dev) {
@@ -417,34 +420,32 @@ int upload_packed(vkm_handle* h, const double* ev_host, int64_t n, double t0, cu
   return VKM_OK;
 }
 
-// D2H of n flow rows (f32 on the device) into the caller's f32 or f64 buffer
-// through page-locked staging, in pieces: the host pool copies / widens piece
-// i while piece i+1 is in flight.  Ends with the stream drained up to the
-// last piece.
-int download_flows(vkm_handle* h, const float* dev, int64_t n, cudaStream_t s, float* out32, double* out64) {
-  if (h->hout_cap < size_t(2 * n)) {
+// D2H of m f32 values into the caller's f32 or f64 buffer through page-locked
+// staging, in pieces: the host pool copies / widens piece i while piece i+1
+// is in flight.  Returns with every piece consumed.
+int download_f32(vkm_handle* h, const float* dev, int64_t m, cudaStream_t s, float* out32, double* out64) {
+  if (h->hout_cap < size_t(m)) {
     if (h->hout) cudaFreeHost(h->hout);
     h->hout = nullptr;
     h->hout_cap = 0;
-    VKM_CK(cudaHostAlloc(&h->hout, sizeof(float) * size_t(2 * n), cudaHostAllocDefault));
-    h->hout_cap = size_t(2 * n);
+    VKM_CK(cudaHostAlloc(&h->hout, sizeof(float) * size_t(m), cudaHostAllocDefault));
+    h->hout_cap = size_t(m);
   }
   for (auto& e : h->dl_ev)
     if (!e) VKM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  const int pieces = int(std::max<int64_t>(1, std::min<int64_t>(4, (n + (1 << 17) - 1) >> 17)));
+  const int pieces = int(std::max<int64_t>(1, std::min<int64_t>(4, (m + (1 << 18) - 1) >> 18)));
   for (int i = 0; i < pieces; ++i) {
-    const int64_t lo = n * i / pieces, hi = n * (i + 1) / pieces;
-    VKM_CK(cudaMemcpyAsync(h->hout + 2 * lo, dev + 2 * lo, sizeof(float) * 2 * (hi - lo), cudaMemcpyDeviceToHost, s));
+    const int64_t lo = m * i / pieces, hi = m * (i + 1) / pieces;
+    VKM_CK(cudaMemcpyAsync(h->hout + lo, dev + lo, sizeof(float) * (hi - lo), cudaMemcpyDeviceToHost, s));
     VKM_CK(cudaEventRecord(h->dl_ev[i], s));
   }
   if (!h->pool) h->pool = new vkm_host::HostPool(std::max(0, std::min(15, int(std::thread::hardware_concurrency()) - 1)));
   for (int i = 0; i < pieces; ++i) {
-    const int64_t lo = 2 * (n * i / pieces), hi = 2 * (n * (i + 1) / pieces);
+    const int64_t lo = m * i / pieces, hi = m * (i + 1) / pieces, len = hi - lo;
     VKM_CK(cudaEventSynchronize(h->dl_ev[i]));
-    const int64_t m = hi - lo;
-    const int parts = std::max(1, std::min<int>(h->pool->size(), int((m + 65535) / 65536)));
+    const int parts = std::max(1, std::min<int>(h->pool->size(), int((len + 65535) / 65536)));
     h->pool->run(parts, [&](int part) {
-      const int64_t a = lo + m * part / parts, b = lo + m * (part + 1) / parts;
+      const int64_t a = lo + len * part / parts, b = lo + len * (part + 1) / parts;
       if (out64)
         for (int64_t k = a; k < b; ++k) out64[k] = double(h->hout[k]);
       else
@@ -802,8 +803,8 @@ int predict_host_impl(vkm_handle* h, const double* ev_host, int64_t n, double t_
   rec(h, 3, s);
   if (counts_host)
     VKM_CK(cudaMemcpyAsync(counts_host, h->cnt_stage, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
-  if (flows64_host || single_pack(h, n)) {
-    rc = download_flows(h, h->out_stage, n, s, flows_host, flows64_host);
+  if (flows64_host || host_staged(n)) {
+    rc = download_f32(h, h->out_stage, 2 * n, s, flows_host, flows64_host);
     if (rc) return rc;
   } else {
     VKM_CK(cudaMemcpyAsync(flows_host, h->out_stage, sizeof(float) * 2 * n, cudaMemcpyDeviceToHost, s));
@@ -842,9 +843,14 @@ int vkm_encode_host(vkm_handle* h, const double* ev_host, int64_t n, double t_st
   VKM_CK(cudaMemcpyAsync(h->ev_stage, ev_host, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
   rc = vkm_encode(h, h->ev_stage, n, t_start, h->out_stage, counts_host ? h->cnt_stage : nullptr, s);
   if (rc) return rc;
-  VKM_CK(cudaMemcpyAsync(feats_host, h->out_stage, sizeof(float) * 2 * h->D * n, cudaMemcpyDeviceToHost, s));
   if (counts_host)
     VKM_CK(cudaMemcpyAsync(counts_host, h->cnt_stage, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  if (host_staged(n)) {   // large feature blocks: pinned pieces, copied out by the host pool
+    rc = download_f32(h, h->out_stage, 2 * h->D * n, s, feats_host, nullptr);
+    if (rc) return rc;
+  } else {
+    VKM_CK(cudaMemcpyAsync(feats_host, h->out_stage, sizeof(float) * 2 * h->D * n, cudaMemcpyDeviceToHost, s));
+  }
   VKM_CK(cudaStreamSynchronize(s));
   return VKM_OK;
 }

@@ -24,3 +24,4 @@ print("predict_host_wide", tm(lambda: eng.predict_host_wide(blk.events, blk.t_st
 print("events contiguous?", blk.events.flags.c_contiguous, blk.events.dtype, blk.events is X)
 import os
 print("VKM_HOST_PACK_SINGLE", os.environ.get("VKM_HOST_PACK_SINGLE"))
+print("encode_host", tm(lambda: eng.encode_host(blk.events, blk.t_start), 5))
