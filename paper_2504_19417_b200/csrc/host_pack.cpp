@@ -247,7 +247,7 @@ int vkm_check_events(const double* X, int64_t n, int64_t ld, int32_t W, int32_t 
   std::unique_lock<std::mutex> lock(pool_m, std::defer_lock);
   if (n >= 4 * kPart && lock.try_lock()) {   // busy (another thread validating): serial pass
     static vkm_host::HostPool* pool =
-        new vkm_host::HostPool(std::max(0, std::min(15, int(std::thread::hardware_concurrency()) - 1)));   // never torn down
+        new vkm_host::HostPool(vkm_host::default_pool_threads());   // never torn down
     const int parts = int(std::min<int64_t>(4 * pool->size(), n / kPart));
     std::vector<vkm_event_check> pc(parts);
     pool->run(parts, [&](int p) {

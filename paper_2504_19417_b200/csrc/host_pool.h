@@ -4,7 +4,9 @@
 // all parts are done.  One run at a time per pool.
 #pragma once
 
+#include <algorithm>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstdint>
 #include <functional>
 #include <mutex>
@@ -79,5 +81,12 @@ class HostPool {
   uint64_t gen_ = 0;
   bool stop_ = false;
 };
+
+// Worker threads per pool (the caller is one more): VKM_HOST_THREADS, else
+// hardware threads - 1, at most 15.
+inline int default_pool_threads() {
+  if (const char* e = std::getenv("VKM_HOST_THREADS")) return std::max(0, std::atoi(e) - 1);
+  return std::max(0, std::min(15, int(std::thread::hardware_concurrency()) - 1));
+}
 
 }  // namespace vkm_host

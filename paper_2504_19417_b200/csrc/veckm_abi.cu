@@ -358,7 +358,7 @@ void pack_chunk(vkm_handle* h, const double* ev, const int64_t* offsets, const d
   for (int s = s0, b = 0; b < st.nb; ++s)
     if (offsets[s + 1] > offsets[s] && offsets[s] - base == st.off[b]) sidx[b++] = s;
   const int64_t n = st.off[st.nb];
-  if (!h->pool) h->pool = new vkm_host::HostPool(std::max(0, std::min(15, int(std::thread::hardware_concurrency()) - 1)));
+  if (!h->pool) h->pool = new vkm_host::HostPool(vkm_host::default_pool_threads());
   const int parts = std::max(1, std::min<int>(4 * h->pool->size(), int((n + 65535) / 65536)));
   h->pool->run(parts, [&](int part) {
     const int64_t lo = n * part / parts, hi = n * (part + 1) / parts;
@@ -373,7 +373,7 @@ void pack_chunk(vkm_handle* h, const double* ev, const int64_t* offsets, const d
 
 // Pack events [lo, hi) of one slice (time origin t0) on the host pool.
 void pack_range(vkm_handle* h, const double* ev, int64_t lo, int64_t hi, double t0, uint2* out) {
-  if (!h->pool) h->pool = new vkm_host::HostPool(std::max(0, std::min(15, int(std::thread::hardware_concurrency()) - 1)));
+  if (!h->pool) h->pool = new vkm_host::HostPool(vkm_host::default_pool_threads());
   const int64_t m = hi - lo;
   const int parts = std::max(1, std::min<int>(h->pool->size(), int((m + 32767) / 32768)));
   h->pool->run(parts, [&](int part) {
@@ -439,7 +439,7 @@ int download_f32(vkm_handle* h, const float* dev, int64_t m, cudaStream_t s, flo
     VKM_CK(cudaMemcpyAsync(h->hout + lo, dev + lo, sizeof(float) * (hi - lo), cudaMemcpyDeviceToHost, s));
     VKM_CK(cudaEventRecord(h->dl_ev[i], s));
   }
-  if (!h->pool) h->pool = new vkm_host::HostPool(std::max(0, std::min(15, int(std::thread::hardware_concurrency()) - 1)));
+  if (!h->pool) h->pool = new vkm_host::HostPool(vkm_host::default_pool_threads());
   for (int i = 0; i < pieces; ++i) {
     const int64_t lo = m * i / pieces, hi = m * (i + 1) / pieces, len = hi - lo;
     VKM_CK(cudaEventSynchronize(h->dl_ev[i]));
