@@ -127,8 +127,8 @@ struct vkm_handle {
   int32_t* pcnt[2] = {nullptr, nullptr};
   size_t pcnt_cap[2] = {0, 0};
   uint2* hpack[2] = {nullptr, nullptr};   // page-locked packed-event staging (host)
-  float* hout = nullptr;                  // page-locked flow staging of the single-slice host calls
-  size_t hout_cap = 0;
+  uint8_t* hout = nullptr;                // page-locked result staging of the single-slice host calls
+  size_t hout_cap = 0;                    // bytes
   cudaEvent_t dl_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // download pieces
   size_t hpack_cap[2] = {0, 0};
   vkm_host::HostPool* pool = nullptr;
@@ -420,39 +420,56 @@ int upload_packed(vkm_handle* h, const double* ev_host, int64_t n, double t0, cu
   return VKM_OK;
 }
 
-// D2H of m f32 values into the caller's f32 or f64 buffer through page-locked
-// staging, in pieces: the host pool copies / widens piece i while piece i+1
-// is in flight.  Returns with every piece consumed.
-int download_f32(vkm_handle* h, const float* dev, int64_t m, cudaStream_t s, float* out32, double* out64) {
-  if (h->hout_cap < size_t(m)) {
+// D2H of `bytes` bytes through page-locked staging, in up to four pieces:
+// consume(lo, hi) (on the host pool, byte range of the result) runs for
+// piece i while piece i+1 is in flight.  Returns with every piece consumed.
+template <class Consume>
+int download_staged(vkm_handle* h, const void* dev, size_t bytes, size_t align, cudaStream_t s, Consume consume) {
+  if (h->hout_cap < bytes) {
     if (h->hout) cudaFreeHost(h->hout);
     h->hout = nullptr;
     h->hout_cap = 0;
-    VKM_CK(cudaHostAlloc(&h->hout, sizeof(float) * size_t(m), cudaHostAllocDefault));
-    h->hout_cap = size_t(m);
+    VKM_CK(cudaHostAlloc(&h->hout, bytes, cudaHostAllocDefault));
+    h->hout_cap = bytes;
   }
   for (auto& e : h->dl_ev)
     if (!e) VKM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  const int pieces = int(std::max<int64_t>(1, std::min<int64_t>(4, (m + (1 << 18) - 1) >> 18)));
+  const size_t units = bytes / align;
+  const int pieces = int(std::max<size_t>(1, std::min<size_t>(4, (bytes + (size_t(1) << 20) - 1) >> 20)));
+  auto edge = [&](int i) { return units * size_t(i) / size_t(pieces) * align; };
   for (int i = 0; i < pieces; ++i) {
-    const int64_t lo = m * i / pieces, hi = m * (i + 1) / pieces;
-    VKM_CK(cudaMemcpyAsync(h->hout + lo, dev + lo, sizeof(float) * (hi - lo), cudaMemcpyDeviceToHost, s));
+    VKM_CK(cudaMemcpyAsync(h->hout + edge(i), static_cast<const uint8_t*>(dev) + edge(i), edge(i + 1) - edge(i),
+                           cudaMemcpyDeviceToHost, s));
     VKM_CK(cudaEventRecord(h->dl_ev[i], s));
   }
   if (!h->pool) h->pool = new vkm_host::HostPool(vkm_host::default_pool_threads());
   for (int i = 0; i < pieces; ++i) {
-    const int64_t lo = m * i / pieces, hi = m * (i + 1) / pieces, len = hi - lo;
+    const size_t lo = edge(i) / align, len = edge(i + 1) / align - lo;
     VKM_CK(cudaEventSynchronize(h->dl_ev[i]));
-    const int parts = std::max(1, std::min<int>(h->pool->size(), int((len + 65535) / 65536)));
+    const int parts = int(std::max<size_t>(1, std::min<size_t>(size_t(h->pool->size()), (len * align) >> 18)));
     h->pool->run(parts, [&](int part) {
-      const int64_t a = lo + len * part / parts, b = lo + len * (part + 1) / parts;
-      if (out64)
-        for (int64_t k = a; k < b; ++k) out64[k] = double(h->hout[k]);
-      else
-        std::memcpy(out32 + a, h->hout + a, sizeof(float) * size_t(b - a));
+      consume((lo + len * size_t(part) / size_t(parts)) * align, (lo + len * size_t(part + 1) / size_t(parts)) * align);
     });
   }
   return VKM_OK;
+}
+
+// m f32 values into the caller's f32 buffer (copied) or f64 buffer (widened)
+int download_f32(vkm_handle* h, const float* dev, int64_t m, cudaStream_t s, float* out32, double* out64) {
+  return download_staged(h, dev, sizeof(float) * size_t(m), sizeof(float), s, [&](size_t a, size_t b) {
+    const float* st = reinterpret_cast<const float*>(h->hout);   // (re)allocated by download_staged
+    if (out64)
+      for (size_t k = a / 4; k < b / 4; ++k) out64[k] = double(st[k]);
+    else
+      std::memcpy(reinterpret_cast<uint8_t*>(out32) + a, h->hout + a, b - a);
+  });
+}
+
+// bytes copied as they are (float64 results)
+int download_raw(vkm_handle* h, const void* dev, size_t bytes, cudaStream_t s, void* out) {
+  return download_staged(h, dev, bytes, 8, s, [&](size_t a, size_t b) {
+    std::memcpy(static_cast<uint8_t*>(out) + a, h->hout + a, b - a);
+  });
 }
 
 int check_handle(const vkm_handle* h) {
@@ -1093,9 +1110,14 @@ int run_f64_host(vkm_handle* h, const double* ev_host, int64_t n, double t_start
   VKM_CK(cudaMemcpyAsync(h->ev_stage, ev_host, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
   rc = run_f64(h, h->ev_stage, n, t_start, h->out64, counts_host ? h->cnt_stage : nullptr, predict, s);
   if (rc) return rc;
-  VKM_CK(cudaMemcpyAsync(out_host, h->out64, sizeof(double) * per * n, cudaMemcpyDeviceToHost, s));
   if (counts_host)
     VKM_CK(cudaMemcpyAsync(counts_host, h->cnt_stage, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  if (!predict && host_staged(n)) {   // feature blocks (1 KB/event); the 16 B/event flows measured no gain
+    rc = download_raw(h, h->out64, sizeof(double) * per * n, s, out_host);
+    if (rc) return rc;
+  } else {
+    VKM_CK(cudaMemcpyAsync(out_host, h->out64, sizeof(double) * per * n, cudaMemcpyDeviceToHost, s));
+  }
   VKM_CK(cudaStreamSynchronize(s));
   return VKM_OK;
 }

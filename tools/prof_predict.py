@@ -25,3 +25,5 @@ print("events contiguous?", blk.events.flags.c_contiguous, blk.events.dtype, blk
 import os
 print("VKM_HOST_PACK_SINGLE", os.environ.get("VKM_HOST_PACK_SINGLE"))
 print("encode_host", tm(lambda: eng.encode_host(blk.events, blk.t_start), 5))
+print("predict_host_f64", tm(lambda: eng.predict_host_f64(blk.events, blk.t_start), 5))
+print("encode_host_f64", tm(lambda: eng.encode_host_f64(blk.events, blk.t_start), 3))
