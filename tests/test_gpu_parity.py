@@ -549,3 +549,35 @@ def test_single_slice_host_packing_and_wide_output():
         np.testing.assert_array_equal(r["f0"], f0)
         np.testing.assert_array_equal(r["c1"], c1)
         np.testing.assert_array_equal(r["f1"], f1)
+
+
+def test_large_host_encodes_match_device_encodes():
+    """Feature blocks of large host calls come back through pinned pieces
+    copied out by the host pool (vkm_encode_host, vkm_encode_f64_host): equal
+    bitwise to the device-pointer calls on the same slice."""
+    import torch
+    pkg = _pkg()
+    W, H = 160, 120
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    eng = pkg.FlowEngine(W, H, 6, 6, 0.016, b, w)
+    ev = np.ascontiguousarray(vo.synth_uniform_noise(200_000, W, H, seed=91))
+    t0 = float(ev[0, 0])
+    fh, ch = eng.encode_host(ev, t0, return_counts=True)
+    evd = torch.from_numpy(ev).cuda()
+    fd = torch.empty((len(ev), 128), dtype=torch.float32, device="cuda")
+    cd = torch.empty(len(ev), dtype=torch.int32, device="cuda")
+    eng.encode_device(evd, t0, feats=fd, counts=cd)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(fh, fd.cpu().numpy())
+    np.testing.assert_array_equal(ch, cd.cpu().numpy())
+    import ctypes as C
+    m = 150_000
+    f64h = eng.encode_host_f64(ev[:m], t0)
+    f64d = torch.empty((m, 128), dtype=torch.float64, device="cuda")
+    rc = eng._lib.vkm_encode_f64(eng._h, C.c_void_p(evd.data_ptr()), m, t0, C.c_void_p(f64d.data_ptr()), None,
+                                 C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    np.testing.assert_array_equal(f64h, f64d.cpu().numpy())
+    fl64 = eng.predict_host_f64(ev[:m], t0)
+    np.testing.assert_array_equal(fl64, eng.predict_device_f64(evd[:m], t0).cpu().numpy())
