@@ -223,6 +223,16 @@ int vkm_predict_batch_host(vkm_handle* h, const double* events_host, const int64
                            int32_t n_slices, const double* t_starts_host, float* flows_host,
                            int32_t* counts_host);
 
+/* Multi-GPU slice sharding without a collective: the
+ * slices are split into contiguous ranges of about equal event counts, one
+ * per handle (one handle per device, all with the same geometry and head),
+ * and each range runs vkm_predict_batch_host on its own host thread.  Same
+ * buffers and offsets as vkm_predict_batch_host; results land at the slices'
+ * own rows.  Handles must be distinct. */
+int vkm_predict_multi_host(vkm_handle* const* handles, int32_t n_handles, const double* events_host,
+                           const int64_t* offsets_host, int32_t n_slices, const double* t_starts_host,
+                           float* flows_host, int32_t* counts_host);
+
 /* Spatial split, partition side: stable (time-order preserving) selection of
  * the events of rows [y_lo, y_hi) of events_dev (n rows [t, x, y]) into
  * out_events_dev (rows rebased by -y_lo), their row indices into

@@ -1009,6 +1009,49 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
   return VKM_OK;
 }
 
+int vkm_predict_multi_host(vkm_handle* const* handles, int32_t n_handles, const double* ev_host,
+                           const int64_t* offsets, int32_t n_slices, const double* t_starts, float* flows_host,
+                           int32_t* counts_host) {
+  if (n_handles < 1 || !handles) return fail(VKM_EINVAL, "need at least one handle");
+  for (int i = 0; i < n_handles; ++i) {
+    if (int rc = check_handle(handles[i])) return rc;
+    for (int j = 0; j < i; ++j)
+      if (handles[j] == handles[i]) return fail(VKM_EINVAL, "handles must be distinct (a handle is not re-entrant)");
+    if (handles[i]->p.width != handles[0]->p.width || handles[i]->p.height != handles[0]->p.height)
+      return fail(VKM_EINVAL, "handles must share the sensor geometry");
+  }
+  if (n_slices < 0 || (n_slices > 0 && !offsets)) return fail(VKM_EINVAL, "bad slice offsets");
+  for (int s = 0; s < n_slices; ++s)
+    if (offsets[s + 1] < offsets[s] || offsets[s] < 0) return fail(VKM_EINVAL, "slice offsets must be non-decreasing");
+  if (n_slices == 0 || offsets[n_slices] == offsets[0]) return VKM_OK;
+  // contiguous slice ranges of about equal event counts, one per handle (no exchange)
+  const int64_t total = offsets[n_slices] - offsets[0];
+  std::vector<int> cut(static_cast<size_t>(n_handles) + 1, n_slices);
+  cut[0] = 0;
+  for (int i = 1; i < n_handles; ++i) {
+    const int64_t target = offsets[0] + total * i / n_handles;
+    int s = cut[i - 1];
+    while (s < n_slices && offsets[s] < target) ++s;
+    cut[i] = s;
+  }
+  std::vector<int> rcs(static_cast<size_t>(n_handles), int(VKM_OK));
+  std::vector<std::string> errs(static_cast<size_t>(n_handles));
+  auto run = [&](int i) {
+    const int s0 = cut[i], s1 = cut[i + 1];
+    if (s1 > s0)
+      rcs[i] = vkm_predict_batch_host(handles[i], ev_host, offsets + s0, s1 - s0, t_starts ? t_starts + s0 : nullptr,
+                                      flows_host, counts_host);
+    if (rcs[i]) errs[i] = vkm_last_error();   // thread-local: carried back to the caller's thread
+  };
+  std::vector<std::thread> workers;
+  for (int i = 1; i < n_handles; ++i) workers.emplace_back(run, i);
+  run(0);
+  for (auto& t : workers) t.join();
+  for (int i = 0; i < n_handles; ++i)
+    if (rcs[i]) return fail(rcs[i], "handle " + std::to_string(i) + ": " + errs[i]);
+  return VKM_OK;
+}
+
 int vkm_select_rows(vkm_handle* h, const double* ev, int64_t n, int32_t y_lo, int32_t y_hi, int32_t own_lo,
                     int32_t own_hi, double* out_ev, int64_t* out_index, uint8_t* out_owned, int64_t* count_host) {
   if (int rc = check_handle(h)) return rc;

@@ -252,3 +252,26 @@ class FlowEngine:
                                       int(bool(pooled)), C.c_void_p(g.data_ptr()), C.c_void_p(c.data_ptr()),
                                       self._stream(stream)))
         return torch.view_as_complex(g), c
+
+
+def predict_multi_host(engines: Sequence["FlowEngine"], events: np.ndarray, offsets: Sequence[int], t_starts=None,
+                       flows: Optional[np.ndarray] = None) -> np.ndarray:
+    """vkm_predict_multi_host: the slices split into contiguous ranges of
+    about equal event counts, one per engine (device), each range pipelined
+    through its engine on its own host thread; no collective (SURVEY §8e,
+    config 4).  Engines must be distinct handles with the same geometry."""
+    if not engines:
+        raise ValueError("need at least one engine")
+    lib = engines[0]._lib
+    ev = np.ascontiguousarray(events, dtype=np.float64)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    if flows is None:
+        flows = np.empty((len(ev), 2), dtype=np.float32)
+    ts = None
+    if t_starts is not None:
+        ts_arr = np.ascontiguousarray(t_starts, dtype=np.float64)
+        ts = _dptr(ts_arr)
+    hs = (C.c_void_p * len(engines))(*[e._h.value for e in engines])
+    _lib.check(lib.vkm_predict_multi_host(hs, len(engines), ev.ctypes.data, off.ctypes.data_as(C.POINTER(C.c_int64)),
+                                          len(off) - 1, ts, flows.ctypes.data, None))
+    return flows

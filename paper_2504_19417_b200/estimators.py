@@ -16,7 +16,7 @@ from sklearn.base import BaseEstimator, TransformerMixin
 from sklearn.exceptions import NotFittedError
 
 from ._staging import pinned
-from .engine import FlowEngine
+from .engine import FlowEngine, predict_multi_host
 from .errors import DimensionMismatchError, EmptyNeighborhoodError
 from .validation import check_event_array, slice_from_array
 from .weights import MlpWeights, as_weights, generate_bases, load_weights
@@ -194,12 +194,32 @@ class NormalFlowRegressor(BaseEstimator):
             return eng.predict_host_f64(block.events, block.t_start)
         return eng.predict_host_wide(block.events, block.t_start)
 
-    def predict_slices(self, slices: Sequence) -> List[np.ndarray]:
+    def engines(self, devices: Sequence[int]) -> List[FlowEngine]:
+        """One cached libveckm handle per entry of `devices` (a device listed
+        twice gets two handles: two pipelines on one GPU)."""
+        w = self._ready()
+        cache = self.__dict__.setdefault("_device_engines", {})
+        out, seen = [], {}
+        for d in devices:
+            d = int(d)
+            k = seen[d] = seen.get(d, -1) + 1
+            key = (self.width, self.height, self.delta_x, self.delta_y, float(self.delta_t), d, k, self.mlp_mode)
+            hit = cache.get(key)
+            if hit is None or hit[0] is not w:
+                hit = (w, FlowEngine(self.width, self.height, self.delta_x, self.delta_y, self.delta_t, w.bases, w, d,
+                                     self.mlp_mode))
+                cache[key] = hit
+            out.append(hit[1])
+        return out
+
+    def predict_slices(self, slices: Sequence, devices: Optional[Sequence[int]] = None) -> List[np.ndarray]:
         """Additive API: many independent slices, one result
         per slice, each with `predict`'s semantics.  The slices are validated
         on the host, packed into one page-locked buffer and streamed through
         vkm_predict_batch_host, which overlaps the copies of neighbouring
-        slices with the kernels."""
+        slices with the kernels.  `devices` (e.g. [0, 1, ..., 7]) shards the
+        slices over several GPUs, contiguous ranges of equal event counts, one
+        host thread per GPU (vkm_predict_multi_host; no collective)."""
         eng = self.engine()
         if self.precision == "f64":   # one slice per call on the f64 path
             return [self.predict(X) for X in slices]
@@ -216,7 +236,10 @@ class NormalFlowRegressor(BaseEstimator):
             if len(b):
                 ev[lo:lo + len(b)] = b.events
         t_starts = np.array([b.t_start if len(b) else 0.0 for b in blocks], dtype=np.float64)
-        eng.predict_batch_host(ev, offsets, t_starts, flows=out)
+        if devices is not None and len(devices) > 1:
+            predict_multi_host(self.engines(devices), ev, offsets, t_starts, flows=out)
+        else:
+            (self.engines(devices)[0] if devices else eng).predict_batch_host(ev, offsets, t_starts, flows=out)
         res = out.astype(np.float64)   # results leave the reused staging buffer
         return [res[lo:hi] for lo, hi in zip(offsets[:-1], offsets[1:])]
 

@@ -581,3 +581,33 @@ def test_large_host_encodes_match_device_encodes():
     np.testing.assert_array_equal(f64h, f64d.cpu().numpy())
     fl64 = eng.predict_host_f64(ev[:m], t0)
     np.testing.assert_array_equal(fl64, eng.predict_device_f64(evd[:m], t0).cpu().numpy())
+
+
+def test_multi_handle_slice_sharding():
+    """vkm_predict_multi_host (config 4's sharding: contiguous slice ranges of
+    equal event counts, one handle and host thread each, no collective) with
+    several handles on this GPU equals the single-handle batch, empty slices
+    and uneven sizes included; duplicate handles are rejected.  Flows within
+    1e-6, not bitwise: a handle batches its own slices, and the y pass's
+    sliding-window segments depend on how many slices share a launch, which
+    moves f32 roundings of the window sums."""
+    from paper_2504_19417_b200.engine import predict_multi_host
+    pkg = _pkg()
+    W, H = 128, 96
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    reg = pkg.NormalFlowRegressor(width=W, height=H, delta_x=5, delta_y=5, weights=w)
+    sizes = [3000, 0, 12000, 1, 700, 25000, 0, 4000, 9000]
+    slices = [vo.synth_uniform_noise(n, W, H, seed=500 + i) if n else np.zeros((0, 3)) for i, n in enumerate(sizes)]
+    ref = reg.predict_slices(slices)
+    for devs in ([0, 0], [0, 0, 0]):
+        got = reg.predict_slices(slices, devices=devs)
+        assert len(got) == len(ref)
+        for a, r in zip(got, ref):
+            assert a.shape == r.shape
+            np.testing.assert_allclose(a, r, rtol=0, atol=1e-6)
+    e = reg.engines([0])[0]
+    ev = np.ascontiguousarray(np.concatenate([s for s in slices if len(s)]))
+    off = np.cumsum([0] + [len(s) for s in slices if len(s)])
+    with pytest.raises(ValueError, match="distinct"):
+        predict_multi_host([e, e], ev, off)
