@@ -233,6 +233,18 @@ int vkm_predict_multi_host(vkm_handle* const* handles, int32_t n_handles, const 
                            const int64_t* offsets_host, int32_t n_slices, const double* t_starts_host,
                            float* flows_host, int32_t* counts_host);
 
+/* One oversized slice over several devices: rows
+ * [row_cuts[i], row_cuts[i+1]) belong to strip i (row_cuts[0] = 0,
+ * row_cuts[n_strips] = H); handle i was created for the strip plus a
+ * delta_y-row event halo clipped to the sensor (height = min(H, cut[i+1] +
+ * δy) - max(0, cut[i] - δy)), on its own device.  Each strip's events (rows
+ * shifted to the strip) run on their handle's host thread with the slice's
+ * single time origin; owned rows are written back at their input positions
+ * (events outside every strip: NaN flows, count 0).  No grid exchange. */
+int vkm_predict_strips_host(vkm_handle* const* handles, int32_t n_strips, const int32_t* row_cuts,
+                            const double* events_host, int64_t n, double t_start, float* flows_host,
+                            int32_t* counts_host);
+
 /* Spatial split, partition side: stable (time-order preserving) selection of
  * the events of rows [y_lo, y_hi) of events_dev (n rows [t, x, y]) into
  * out_events_dev (rows rebased by -y_lo), their row indices into

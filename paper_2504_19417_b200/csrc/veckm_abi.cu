@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <condition_variable>
 #include <functional>
+#include <limits>
 #include <mutex>
 #include <thread>
 #include <cstdint>
@@ -1049,6 +1050,74 @@ int vkm_predict_multi_host(vkm_handle* const* handles, int32_t n_handles, const 
   for (auto& t : workers) t.join();
   for (int i = 0; i < n_handles; ++i)
     if (rcs[i]) return fail(rcs[i], "handle " + std::to_string(i) + ": " + errs[i]);
+  return VKM_OK;
+}
+
+int vkm_predict_strips_host(vkm_handle* const* handles, int32_t n_strips, const int32_t* row_cuts,
+                            const double* ev_host, int64_t n, double t_start, float* flows_host,
+                            int32_t* counts_host) {
+  if (n_strips < 1 || !handles || !row_cuts) return fail(VKM_EINVAL, "need at least one strip");
+  if (n < 0) return fail(VKM_EINVAL, "n must be non-negative");
+  if (n == 0) return VKM_OK;
+  if (!ev_host || !flows_host) return fail(VKM_EINVAL, "null host buffer");
+  for (int i = 0; i < n_strips; ++i) {
+    if (int rc = check_handle(handles[i])) return rc;
+    for (int j = 0; j < i; ++j)
+      if (handles[j] == handles[i]) return fail(VKM_EINVAL, "handles must be distinct (a handle is not re-entrant)");
+  }
+  const int W = handles[0]->p.width, dy = handles[0]->p.delta_y;
+  if (row_cuts[0] != 0) return fail(VKM_EINVAL, "row_cuts[0] must be 0");
+  for (int i = 0; i < n_strips; ++i) {
+    if (row_cuts[i + 1] <= row_cuts[i]) return fail(VKM_EINVAL, "row_cuts must be increasing");
+    const int H = row_cuts[n_strips];
+    const int in_lo = std::max(0, row_cuts[i] - dy), in_hi = std::min(H, row_cuts[i + 1] + dy);
+    if (handles[i]->p.width != W || handles[i]->p.delta_y != dy || handles[i]->p.height != in_hi - in_lo)
+      return fail(VKM_EINVAL, "handle " + std::to_string(i) + " must have the strip's geometry (W x rows + halo)");
+  }
+  const double t0 = std::isnan(t_start) ? ev_host[0] : t_start;   // one time origin for every strip
+  const int H = row_cuts[n_strips];
+  std::vector<int> rcs(static_cast<size_t>(n_strips), int(VKM_OK));
+  std::vector<std::string> errs(static_cast<size_t>(n_strips));
+  auto run = [&](int i) {
+    const int in_lo = std::max(0, row_cuts[i] - dy), in_hi = std::min(H, row_cuts[i + 1] + dy);
+    std::vector<double> sub;
+    std::vector<int64_t> idx;
+    std::vector<uint8_t> own;
+    for (int64_t e = 0; e < n; ++e) {   // time order kept: events in input order
+      const double y = ev_host[3 * e + 2];
+      if (!(y >= in_lo && y < in_hi)) continue;
+      sub.insert(sub.end(), {ev_host[3 * e], ev_host[3 * e + 1], y - in_lo});
+      idx.push_back(e);
+      own.push_back(y >= row_cuts[i] && y < row_cuts[i + 1]);
+    }
+    const int64_t m = int64_t(idx.size());
+    if (m == 0) return;
+    std::vector<float> f(size_t(2 * m));
+    std::vector<int32_t> c(counts_host ? size_t(m) : 0);
+    rcs[i] = vkm_predict_host(handles[i], sub.data(), m, t0, f.data(), counts_host ? c.data() : nullptr);
+    if (rcs[i]) {
+      errs[i] = vkm_last_error();
+      return;
+    }
+    for (int64_t k = 0; k < m; ++k)
+      if (own[size_t(k)]) {
+        flows_host[2 * idx[size_t(k)]] = f[size_t(2 * k)];
+        flows_host[2 * idx[size_t(k)] + 1] = f[size_t(2 * k + 1)];
+        if (counts_host) counts_host[idx[size_t(k)]] = c[size_t(k)];
+      }
+  };
+  // events outside every strip (y outside [0, H) or not integer rows inside) keep the unsplit path's
+  // NaN / 0 answer: pre-fill, strips overwrite their owned rows
+  for (int64_t e = 0; e < n; ++e) {
+    flows_host[2 * e] = flows_host[2 * e + 1] = std::numeric_limits<float>::quiet_NaN();
+    if (counts_host) counts_host[e] = 0;
+  }
+  std::vector<std::thread> workers;
+  for (int i = 1; i < n_strips; ++i) workers.emplace_back(run, i);
+  run(0);
+  for (auto& t : workers) t.join();
+  for (int i = 0; i < n_strips; ++i)
+    if (rcs[i]) return fail(rcs[i], "strip " + std::to_string(i) + ": " + errs[i]);
   return VKM_OK;
 }
 

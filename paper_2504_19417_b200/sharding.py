@@ -146,6 +146,31 @@ def predict_spatial(engine_factory, events: np.ndarray, t_start: float, width: i
     return out if return_counts else out[0]
 
 
+def predict_strips_host(make_engine, events: np.ndarray, t_start: float, height: int, delta_y: int,
+                        devices: Sequence[int], return_counts: bool = False):
+    """One oversized slice over several GPUs from one process
+    (vkm_predict_strips_host): row strips of about equal event counts with a
+    δy-row event halo, strip i on a handle made by make_engine(strip_height,
+    devices[i]) and its own host thread; flows (n, 2) f32 in input order."""
+    import ctypes as C
+    from . import _lib
+    ev = np.ascontiguousarray(events, dtype=np.float64)
+    n = len(ev)
+    y = ev[:, 2]
+    rows = np.bincount(np.clip(y, 0, height - 1).astype(np.int64), minlength=height)[:height] if n else \
+        np.zeros(height, dtype=np.int64)
+    strips = row_strips(rows, len(devices), delta_y)
+    engines = [make_engine(st.in_hi - st.in_lo, d) for st, d in zip(strips, devices)]
+    cuts = np.array([st.lo for st in strips] + [strips[-1].hi], dtype=np.int32)
+    hs = (C.c_void_p * len(engines))(*[e._h.value for e in engines])
+    flows = np.empty((n, 2), dtype=np.float32)
+    counts = np.empty(n, dtype=np.int32) if return_counts else None
+    _lib.check(engines[0]._lib.vkm_predict_strips_host(hs, len(engines), cuts.ctypes.data, ev.ctypes.data, n,
+                                                       float(t_start), flows.ctypes.data,
+                                                       counts.ctypes.data if counts is not None else None))
+    return (flows, counts) if return_counts else flows
+
+
 def _is_gloo(group=None) -> bool:
     import torch.distributed as dist
     return dist.get_backend(group) == "gloo"

@@ -611,3 +611,28 @@ def test_multi_handle_slice_sharding():
     off = np.cumsum([0] + [len(s) for s in slices if len(s)])
     with pytest.raises(ValueError, match="distinct"):
         predict_multi_host([e, e], ev, off)
+
+
+def test_strips_host_matches_unsplit_slice():
+    """vkm_predict_strips_host (config 5's row-strip split from one process,
+    one handle per strip, δy event halo, one time origin) against the unsplit
+    slice: counts exact, flows within 1e-5 (the strips segment the window
+    sums differently); out-of-sensor events stay NaN / 0."""
+    from paper_2504_19417_b200.sharding import predict_strips_host
+    pkg = _pkg()
+    W, H, d = 200, 150, 7
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    eng = pkg.FlowEngine(W, H, d, d, 0.016, b, w)
+    ev = np.ascontiguousarray(vo.synth_uniform_noise(150_000, W, H, seed=17))
+    ev[5, 2] = H + 3          # outside every strip
+    ev[6, 1] = W              # outside in x, inside a strip's rows
+    t0 = float(ev[0, 0])
+    f_ref, c_ref = eng.predict_host(ev, t0, return_counts=True)
+    for k in (2, 3):
+        f, c = predict_strips_host(lambda h, dev: pkg.FlowEngine(W, h, d, d, 0.016, b, w, dev), ev, t0, H, d,
+                                   [0] * k, return_counts=True)
+        np.testing.assert_array_equal(c, c_ref)
+        assert np.isnan(f[[5, 6]]).all() and np.isnan(f_ref[[5, 6]]).all()
+        good = np.isfinite(f_ref[:, 0])
+        np.testing.assert_allclose(f[good], f_ref[good], rtol=0, atol=1e-5)
