@@ -140,3 +140,18 @@ def test_device_windowing_matches_host_windowing(stride):
     for (sd, fd), (sh, fh), r in zip(dev, host, ref):
         assert sd == sh == r.t_start and fd.shape == fh.shape == (len(r), 2)
         np.testing.assert_allclose(fd, fh, rtol=0, atol=1e-6)
+
+
+def test_device_window_starts_follow_the_reference_loop():
+    """The starts uploaded for device windowing are the reference loop's
+    float sequence (events.py:363-368), the same as the host windowing's,
+    before trailing empty windows are dropped."""
+    S = _S()
+    from paper_2504_19417_b200.stream import _window_starts
+    rng = np.random.default_rng(3)
+    for stride in (0.004, 0.01, 0.032, 0.1 / 3):
+        t = np.sort(rng.uniform(0.0, 0.4, 5000))
+        starts = _window_starts(t, stride, 0.0)
+        wins = S.window_bounds(t, 0.016, stride, 0.0)
+        assert [s for _, _, s in wins] == list(starts[:len(wins)])
+        assert starts[-1] <= t[-1] < starts[-1] + stride
