@@ -8,7 +8,9 @@
 // at run time, a scalar loop for the tail and for CPUs without AVX2.
 #include <immintrin.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -76,7 +78,20 @@ __attribute__((target("avx512f,avx512vl,avx512dq"))) void pack_avx512(const doub
   const __m512i t01 = _mm512_setr_epi64(0, 3, 6, 9, 12, 15, 0, 0), t2 = _mm512_setr_epi64(0, 1, 2, 3, 4, 5, 10, 13);
   const __m512i x01 = _mm512_setr_epi64(1, 4, 7, 10, 13, 0, 0, 0), x2 = _mm512_setr_epi64(0, 1, 2, 3, 4, 8, 11, 14);
   const __m512i y01 = _mm512_setr_epi64(2, 5, 8, 11, 14, 0, 0, 0), y2 = _mm512_setr_epi64(0, 1, 2, 3, 4, 9, 12, 15);
+  // Non-temporal stores (the records go to page-locked staging that only the
+  // DMA engine reads): no read-for-ownership of the destination lines, 8 of
+  // the ~56 host-DRAM bytes per event.  They need 32-byte alignment: the
+  // first events up to that boundary take the scalar path.
+  static const bool nt = [] {
+    const char* e = std::getenv("VKM_PACK_NT");
+    return !(e && e[0] == '0');
+  }();
   int64_t i = 0;
+  if (nt) {
+    const int64_t head = std::min<int64_t>(m, int64_t((32 - (reinterpret_cast<uintptr_t>(out) & 31)) & 31) / 8);
+    pack_scalar(r, head, t0, dt, W, H, out);
+    i = head;
+  }
   for (; i + 8 <= m; i += 8) {
     const double* p = r + 3 * i;
     const __m512d a0 = _mm512_loadu_pd(p), a1 = _mm512_loadu_pd(p + 8), a2 = _mm512_loadu_pd(p + 16);
@@ -93,9 +108,15 @@ __attribute__((target("avx512f,avx512vl,avx512dq"))) void pack_avx512(const doub
     const __m256i xy = _mm256_mask_blend_epi32(ok, _mm256_set1_epi32(-1), _mm256_or_si256(xi, _mm256_slli_epi32(yi, 16)));
     const __m256i ab = _mm256_castps_si256(a);
     const __m256i lo = _mm256_unpacklo_epi32(ab, xy), hi = _mm256_unpackhi_epi32(ab, xy);
-    _mm256_storeu_si256(reinterpret_cast<__m256i*>(out + 2 * i), _mm256_permute2x128_si256(lo, hi, 0x20));
-    _mm256_storeu_si256(reinterpret_cast<__m256i*>(out + 2 * i + 8), _mm256_permute2x128_si256(lo, hi, 0x31));
+    if (nt) {
+      _mm256_stream_si256(reinterpret_cast<__m256i*>(out + 2 * i), _mm256_permute2x128_si256(lo, hi, 0x20));
+      _mm256_stream_si256(reinterpret_cast<__m256i*>(out + 2 * i + 8), _mm256_permute2x128_si256(lo, hi, 0x31));
+    } else {
+      _mm256_storeu_si256(reinterpret_cast<__m256i*>(out + 2 * i), _mm256_permute2x128_si256(lo, hi, 0x20));
+      _mm256_storeu_si256(reinterpret_cast<__m256i*>(out + 2 * i + 8), _mm256_permute2x128_si256(lo, hi, 0x31));
+    }
   }
+  if (nt) _mm_sfence();   // streamed records visible before the copy is issued
   pack_scalar(r + 3 * i, m - i, t0, dt, W, H, out + 2 * i);
 }
 
