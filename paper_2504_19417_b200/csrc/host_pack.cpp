@@ -122,6 +122,29 @@ __attribute__((target("avx512f,avx512vl,avx512dq"))) void pack_avx512(const doub
 
 }  // namespace
 
+// f32 -> f64 widening of result rows into the caller's buffer, streamed
+// (the destination is fresh memory the caller reads later: no
+// read-for-ownership), scalar until dst is 64-byte aligned.
+__attribute__((target("avx512f"))) static void widen_avx512(const float* src, double* dst, int64_t m) {
+  int64_t i = 0;
+  for (; i < m && (reinterpret_cast<uintptr_t>(dst + i) & 63); ++i) dst[i] = double(src[i]);
+  for (; i + 8 <= m; i += 8) _mm512_stream_pd(dst + i, _mm512_cvtps_pd(_mm256_loadu_ps(src + i)));
+  _mm_sfence();
+  for (; i < m; ++i) dst[i] = double(src[i]);
+}
+
+void widen_f32(const float* src, double* dst, int64_t m) {
+  static const bool avx512 = [] {
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx512f");
+  }();
+  if (avx512) {
+    widen_avx512(src, dst, m);
+    return;
+  }
+  for (int64_t i = 0; i < m; ++i) dst[i] = double(src[i]);
+}
+
 // out: 2 uint32 per event (the device's uint2 record)
 void pack_events(const double* rows, int64_t m, double t0, double dt, int W, int H, uint32_t* out) {
   static const int isa = [] {

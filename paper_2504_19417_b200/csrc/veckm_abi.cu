@@ -343,6 +343,7 @@ int next_chunk(const vkm_handle* h, const int64_t* offsets, int32_t n_slices, co
 namespace vkm_host {
 // host_pack.cpp: vectorised packing of f64 [t, x, y] rows into 8-byte records
 void pack_events(const double* rows, int64_t m, double t0, double dt, int W, int H, uint32_t* out);
+void widen_f32(const float* src, double* dst, int64_t m);
 }  // namespace vkm_host
 namespace {
 
@@ -460,7 +461,7 @@ int download_f32(vkm_handle* h, const float* dev, int64_t m, cudaStream_t s, flo
   return download_staged(h, dev, sizeof(float) * size_t(m), sizeof(float), s, [&](size_t a, size_t b) {
     const float* st = reinterpret_cast<const float*>(h->hout);   // (re)allocated by download_staged
     if (out64)
-      for (size_t k = a / 4; k < b / 4; ++k) out64[k] = double(st[k]);
+      vkm_host::widen_f32(st + a / 4, out64 + a / 4, int64_t((b - a) / 4));
     else
       std::memcpy(reinterpret_cast<uint8_t*>(out32) + a, h->hout + a, b - a);
   });
