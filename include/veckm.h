@@ -192,6 +192,10 @@ typedef struct vkm_event_check {
 int vkm_check_events(const double* events_host, int64_t n, int64_t ld, int32_t width, int32_t height,
                      vkm_event_check* out);
 
+/* Host utility: dst[i] = (double)src[i] for n values, split over the host
+ * pool with streaming stores (the float64 results of the batch APIs). */
+int vkm_widen_f32(const float* src, double* dst, int64_t n);
+
 /* Stream windowing on the device (slice_stream, events.py:331-387):
  * vkm_window_bounds: for a time-sorted device stream (n, 3), the bounds
  *   [lo, hi) of windows [starts[i], starts[i] + window) by binary search

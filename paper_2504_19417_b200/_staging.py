@@ -28,3 +28,15 @@ def pinned(name: str, n: int, dtype=np.float64) -> np.ndarray:
         buf = torch.empty(max(int(n), 1 << 20), dtype=tdt).pin_memory().numpy()
         bufs[key] = buf
     return buf[:n]
+
+
+def widen(src: np.ndarray) -> np.ndarray:
+    """float64 copy of a float32 array through libveckm's pooled, streaming
+    widening (vkm_widen_f32): the host side of the batch APIs' float64
+    results."""
+    from . import _lib
+    a = np.ascontiguousarray(src, dtype=np.float32)
+    out = np.empty(a.shape, dtype=np.float64)
+    if a.size:
+        _lib.check(_lib.load().vkm_widen_f32(a.ctypes.data, out.ctypes.data, a.size))
+    return out

@@ -279,6 +279,18 @@ void check_range(const double* X, int64_t n, int64_t ld, int32_t W, int32_t H, v
 
 }  // namespace
 
+// The host pool of the handle-free host utilities (validation, widening):
+// created on first use, never torn down; one user at a time (try_lock, else
+// the caller works alone).
+static vkm_host::HostPool* shared_pool() {
+  static vkm_host::HostPool* pool = new vkm_host::HostPool(vkm_host::default_pool_threads());
+  return pool;
+}
+static std::mutex& shared_pool_mutex() {
+  static std::mutex m;
+  return m;
+}
+
 extern "C" {
 
 int vkm_check_events(const double* X, int64_t n, int64_t ld, int32_t W, int32_t H, vkm_event_check* out) {
@@ -287,11 +299,9 @@ int vkm_check_events(const double* X, int64_t n, int64_t ld, int32_t W, int32_t 
   // order (the first outside pixel is the first part's first; sortedness also
   // checks each part boundary with the same comparison)
   const int64_t kPart = int64_t(1) << 16;
-  static std::mutex pool_m;
-  std::unique_lock<std::mutex> lock(pool_m, std::defer_lock);
-  if (n >= 4 * kPart && lock.try_lock()) {   // busy (another thread validating): serial pass
-    static vkm_host::HostPool* pool =
-        new vkm_host::HostPool(vkm_host::default_pool_threads());   // never torn down
+  std::unique_lock<std::mutex> lock(shared_pool_mutex(), std::defer_lock);
+  if (n >= 4 * kPart && lock.try_lock()) {   // busy (another thread using the pool): serial pass
+    vkm_host::HostPool* pool = shared_pool();
     const int parts = int(std::min<int64_t>(4 * pool->size(), n / kPart));
     std::vector<vkm_event_check> pc(parts);
     pool->run(parts, [&](int p) {
@@ -317,6 +327,23 @@ int vkm_check_events(const double* X, int64_t n, int64_t ld, int32_t W, int32_t 
     return 0;
   }
   check_range(X, n, ld, W, H, *out);
+  return 0;
+}
+
+int vkm_widen_f32(const float* src, double* dst, int64_t n) {
+  if (n < 0 || (n > 0 && (!src || !dst))) return 1;
+  const int64_t kPart = int64_t(1) << 18;
+  std::unique_lock<std::mutex> lock(shared_pool_mutex(), std::defer_lock);
+  if (n >= 2 * kPart && lock.try_lock()) {
+    vkm_host::HostPool* pool = shared_pool();
+    const int parts = int(std::min<int64_t>(pool->size(), n / kPart));
+    pool->run(parts, [&](int p) {
+      const int64_t lo = n * p / parts, hi = n * (p + 1) / parts;
+      vkm_host::widen_f32(src + lo, dst + lo, hi - lo);
+    });
+    return 0;
+  }
+  vkm_host::widen_f32(src, dst, n);
   return 0;
 }
 

@@ -15,7 +15,7 @@ import numpy as np
 from sklearn.base import BaseEstimator, TransformerMixin
 from sklearn.exceptions import NotFittedError
 
-from ._staging import pinned
+from ._staging import pinned, widen
 from .engine import FlowEngine, predict_multi_host
 from .errors import DimensionMismatchError, EmptyNeighborhoodError
 from .validation import check_event_array, slice_from_array
@@ -240,7 +240,7 @@ class NormalFlowRegressor(BaseEstimator):
             predict_multi_host(self.engines(devices), ev, offsets, t_starts, flows=out)
         else:
             (self.engines(devices)[0] if devices else eng).predict_batch_host(ev, offsets, t_starts, flows=out)
-        res = out.astype(np.float64)   # results leave the reused staging buffer
+        res = widen(out)   # results leave the reused staging buffer
         return [res[lo:hi] for lo, hi in zip(offsets[:-1], offsets[1:])]
 
 

@@ -272,7 +272,7 @@ def _predict_stream_device(eng, t, x, y, dt: float, stride: float, t0: float):
     import ctypes as C
     import torch
     from . import _lib
-    from ._staging import pinned
+    from ._staging import pinned, widen
     n = len(t)
     dev = torch.device("cuda", eng.device)
     hv = pinned("stream_cols", 3 * n, np.float64)
@@ -302,7 +302,7 @@ def _predict_stream_device(eng, t, x, y, dt: float, stride: float, t0: float):
                                             C.c_void_p(torch.cuda.current_stream(eng.device).cuda_stream)))
     fh = pinned("flows", 2 * total, np.float32)
     torch.from_numpy(fh).copy_(flows.view(-1))        # pinned D2H
-    out = fh.astype(np.float64).reshape(total, 2)     # one widening pass into the result
+    out = widen(fh).reshape(total, 2)     # one widening pass into the result
     return [(float(s), out[a:b]) for s, a, b in zip(starts, offsets[:-1], offsets[1:])]
 
 
@@ -320,7 +320,7 @@ def predict_stream(regressor, stream: EventStream, stride: Optional[float] = Non
     unless the stream and its windows would take more than
     VKM_STREAM_DEVICE_BYTES (default 16 GiB) of HBM, where the windows go
     through the pipelined host batch instead."""
-    from ._staging import pinned
+    from ._staging import pinned, widen
     dt = float(regressor.delta_t)
     if stride is None:
         stride = 2.0 * dt
@@ -363,5 +363,5 @@ def predict_stream(regressor, stream: EventStream, stride: Optional[float] = Non
             ev[o:o + hi - lo, 2] = y[lo:hi]
     t_starts = np.array([s for _, _, s in wins], dtype=np.float64)
     eng.predict_batch_host(ev, offsets, t_starts, flows=out)
-    res = out.astype(np.float64)
+    res = widen(out)
     return [(s, res[a:b]) for (_, _, s), a, b in zip(wins, offsets[:-1], offsets[1:])]

@@ -312,3 +312,23 @@ def test_product_path_does_not_import_the_oracle():
             "assert not bad, bad") % root
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_native_widening_matches_astype():
+    """vkm_widen_f32 (pooled, streaming stores, scalar head until the
+    destination is 64-byte aligned) equals numpy's astype(float64), NaN and
+    infinities included, for sizes around the pool threshold and misaligned
+    destinations."""
+    import ctypes
+    from paper_2504_19417_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(4)
+    for n in (0, 1, 7, 8, 9, 1000, (1 << 19) - 3, (1 << 19) + 5, 3_000_001):
+        src = rng.standard_normal(n).astype(np.float32)
+        if n > 10:
+            src[[1, 5, n - 1]] = [np.nan, np.inf, -np.inf]
+        buf = np.empty(n + 3, dtype=np.float64)
+        for off in (0, 1, 3):
+            dst = buf[off:off + n]
+            assert lib.vkm_widen_f32(src.ctypes.data, dst.ctypes.data, n) == 0
+            np.testing.assert_array_equal(dst, src.astype(np.float64))
