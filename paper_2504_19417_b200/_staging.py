@@ -24,7 +24,8 @@ def pinned(name: str, n: int, dtype=np.float64) -> np.ndarray:
     buf = bufs.get(key)
     if buf is None or len(buf) < n:
         import torch
-        tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32}[dt]
+        tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32,
+               np.dtype(np.int32): torch.int32}[dt]
         buf = torch.empty(max(int(n), 1 << 20), dtype=tdt).pin_memory().numpy()
         bufs[key] = buf
     return buf[:n]

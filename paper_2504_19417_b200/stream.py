@@ -275,9 +275,13 @@ def _predict_stream_device(eng, t, x, y, dt: float, stride: float, t0: float):
     from ._staging import pinned, widen
     n = len(t)
     dev = torch.device("cuda", eng.device)
-    hv = pinned("stream_cols", 3 * n, np.float64)
-    hv[:n], hv[n:2 * n], hv[2 * n:] = t, x, y        # column blocks: contiguous host writes
-    ev = torch.from_numpy(hv).to(dev, non_blocking=True).view(3, n).t().contiguous()   # rows [t, x, y]
+    ht = pinned("stream_t", n, np.float64)
+    hxy = pinned("stream_xy", 2 * n, np.int32)
+    ht[:] = t                                         # plain copies: 16 B/event, no host conversion
+    hxy[:n], hxy[n:] = x, y
+    td = torch.from_numpy(ht).to(dev, non_blocking=True)
+    xyd = torch.from_numpy(hxy).to(dev, non_blocking=True).view(2, n)
+    ev = torch.stack([td, xyd[0].double(), xyd[1].double()], 1)   # rows [t, x, y] built on the device
     starts = _window_starts(t, stride, t0)
     nw = len(starts)
     bounds = np.empty((nw, 2), dtype=np.int64)
