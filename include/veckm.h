@@ -196,6 +196,11 @@ int vkm_check_events(const double* events_host, int64_t n, int64_t ld, int32_t w
  * pool with streaming stores (the float64 results of the batch APIs). */
 int vkm_widen_f32(const float* src, double* dst, int64_t n);
 
+/* Host utility: concatenate n_arrays row blocks (rows[a] rows of ld doubles
+ * at srcs[a]) into dst, split over the host pool (the staging of the batch
+ * APIs' many-slice inputs). */
+int vkm_concat_rows(const double* const* srcs, const int64_t* rows, int32_t n_arrays, int64_t ld, double* dst);
+
 /* Stream windowing on the device (slice_stream, events.py:331-387):
  * vkm_window_bounds: for a time-sorted device stream (n, 3), the bounds
  *   [lo, hi) of windows [starts[i], starts[i] + window) by binary search

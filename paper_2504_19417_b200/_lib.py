@@ -50,6 +50,7 @@ SIGNATURES = {
     "vkm_predict_host": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),
     "vkm_predict_host_wide": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),
     "vkm_widen_f32": (C.c_int, [_P, _P, C.c_int64]),
+    "vkm_concat_rows": (C.c_int, [_P, _P, C.c_int32, C.c_int64, _P]),
     "vkm_predict_multi_host": (C.c_int, [_P, C.c_int32, _P, _I64, C.c_int32, _D, _P, _P]),
     "vkm_predict_strips_host": (C.c_int, [_P, C.c_int32, _P, _P, C.c_int64, C.c_double, _P, _P]),
     "vkm_encode_host": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),

@@ -41,3 +41,16 @@ def widen(src: np.ndarray) -> np.ndarray:
     if a.size:
         _lib.check(_lib.load().vkm_widen_f32(a.ctypes.data, out.ctypes.data, a.size))
     return out
+
+
+def concat_rows(blocks, dst: np.ndarray) -> None:
+    """dst[...] = the row blocks back to back (C-contiguous float64 arrays of
+    dst's row width), copied by libveckm's host pool (vkm_concat_rows)."""
+    import ctypes as C
+    from . import _lib
+    arrs = [np.ascontiguousarray(b, dtype=np.float64) for b in blocks]
+    ld = dst.shape[1] if dst.ndim == 2 else 1
+    ptrs = (C.c_void_p * max(1, len(arrs)))(*[a.ctypes.data for a in arrs])
+    rows = np.array([len(a) for a in arrs], dtype=np.int64)
+    assert rows.sum() == len(dst) and all(a.ndim == 2 and a.shape[1] == ld for a in arrs if len(a))
+    _lib.check(_lib.load().vkm_concat_rows(ptrs, rows.ctypes.data, len(arrs), ld, dst.ctypes.data))

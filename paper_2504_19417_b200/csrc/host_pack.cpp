@@ -330,6 +330,35 @@ int vkm_check_events(const double* X, int64_t n, int64_t ld, int32_t W, int32_t 
   return 0;
 }
 
+int vkm_concat_rows(const double* const* srcs, const int64_t* rows, int32_t n_arrays, int64_t ld, double* dst) {
+  if (n_arrays < 0 || ld < 1 || (n_arrays > 0 && (!srcs || !rows || !dst))) return 1;
+  std::vector<int64_t> off(static_cast<size_t>(n_arrays) + 1, 0);
+  for (int32_t a = 0; a < n_arrays; ++a) {
+    if (rows[a] < 0 || (rows[a] > 0 && !srcs[a])) return 1;
+    off[size_t(a) + 1] = off[size_t(a)] + rows[a];
+  }
+  const int64_t total = off[size_t(n_arrays)] * ld;   // doubles
+  auto copy = [&](int64_t lo, int64_t hi) {            // destination doubles [lo, hi)
+    int32_t a = int32_t(std::upper_bound(off.begin(), off.end(), lo / ld) - off.begin()) - 1;
+    while (lo < hi) {
+      while (off[size_t(a) + 1] * ld <= lo) ++a;
+      const int64_t end = std::min(hi, off[size_t(a) + 1] * ld);
+      std::memcpy(dst + lo, srcs[a] + (lo - off[size_t(a)] * ld), sizeof(double) * size_t(end - lo));
+      lo = end;
+    }
+  };
+  const int64_t kPart = int64_t(1) << 18;
+  std::unique_lock<std::mutex> lock(shared_pool_mutex(), std::defer_lock);
+  if (total >= 2 * kPart && lock.try_lock()) {
+    vkm_host::HostPool* pool = shared_pool();
+    const int parts = int(std::min<int64_t>(pool->size(), total / kPart));
+    pool->run(parts, [&](int p) { copy(total * p / parts, total * (p + 1) / parts); });
+    return 0;
+  }
+  copy(0, total);
+  return 0;
+}
+
 int vkm_widen_f32(const float* src, double* dst, int64_t n) {
   if (n < 0 || (n > 0 && (!src || !dst))) return 1;
   const int64_t kPart = int64_t(1) << 18;

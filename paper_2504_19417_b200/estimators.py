@@ -15,7 +15,7 @@ import numpy as np
 from sklearn.base import BaseEstimator, TransformerMixin
 from sklearn.exceptions import NotFittedError
 
-from ._staging import pinned, widen
+from ._staging import concat_rows, pinned, widen
 from .engine import FlowEngine, predict_multi_host
 from .errors import DimensionMismatchError, EmptyNeighborhoodError
 from .validation import check_event_array, slice_from_array
@@ -232,9 +232,7 @@ class NormalFlowRegressor(BaseEstimator):
         out = pinned("batch_flows", 2 * total, np.float32).reshape(total, 2)
         offsets = np.zeros(len(blocks) + 1, dtype=np.int64)
         np.cumsum(sizes, out=offsets[1:])
-        for b, lo in zip(blocks, offsets[:-1]):
-            if len(b):
-                ev[lo:lo + len(b)] = b.events
+        concat_rows([b.events for b in blocks if len(b)], ev)
         t_starts = np.array([b.t_start if len(b) else 0.0 for b in blocks], dtype=np.float64)
         if devices is not None and len(devices) > 1:
             predict_multi_host(self.engines(devices), ev, offsets, t_starts, flows=out)

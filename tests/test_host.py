@@ -332,3 +332,15 @@ def test_native_widening_matches_astype():
             dst = buf[off:off + n]
             assert lib.vkm_widen_f32(src.ctypes.data, dst.ctypes.data, n) == 0
             np.testing.assert_array_equal(dst, src.astype(np.float64))
+
+
+def test_native_concat_rows_matches_numpy():
+    """vkm_concat_rows (pooled copy of row blocks into one buffer, parts that
+    straddle block borders) equals np.concatenate, empty blocks included."""
+    from paper_2504_19417_b200._staging import concat_rows
+    rng = np.random.default_rng(6)
+    for sizes in ([0], [5], [3, 0, 7], [200_000, 1, 0, 150_000, 33], [1] * 1000, [300_001, 299_999]):
+        blocks = [rng.standard_normal((n, 3)) for n in sizes]
+        dst = np.empty((sum(sizes), 3))
+        concat_rows(blocks, dst)
+        np.testing.assert_array_equal(dst, np.concatenate(blocks) if sizes else dst)
