@@ -170,6 +170,43 @@ def accumulate(t_rel, x, y, width: int, height: int, dx: int, dy: int, fr: Freqs
     return Grid(embed.reshape(shape + (D,)), count.reshape(shape), dx, dy, width, height)
 
 
+def accumulate_near(t_rel, x, y, width: int, height: int, dx: int, dy: int, fr: Freqs,
+                    delta_t: float, qx, qy, precision: str = "f32", chunk: int = 1 << 18) -> Grid:
+    """`accumulate` restricted to the pixels inside the windows of the queries
+    (qx, qy), in bounded memory — for at-size checks of large slices on a
+    strided query subset.  A pixel's sum depends only on its own events in
+    time order (encoder.py:255-267), so every pixel a query window touches
+    gets exactly the value `accumulate` gives it; counts are complete
+    (np.bincount over all events, encoder.py:259).  Phases are evaluated in
+    chunks of whole pixel runs, so np.add.reduceat sees the same runs."""
+    stride_x = height + 2 * dy
+    n_cells = (width + 2 * dx) * stride_x
+    D = fr.dim
+    embed = np.zeros((n_cells, D), dtype=_CPLX[precision])
+    x = np.asarray(x, np.int64)
+    y = np.asarray(y, np.int64)
+    key = (x + dx) * stride_x + (y + dy)
+    count = np.bincount(key, minlength=n_cells).astype(np.int64)
+    need = np.zeros((width + 2 * dx, stride_x), dtype=bool)
+    for cx, cy in zip(np.asarray(qx, np.int64), np.asarray(qy, np.int64)):
+        need[cx:cx + 2 * dx + 1, cy:cy + 2 * dy + 1] = True
+    sel = np.flatnonzero(need.ravel()[key])               # time order kept
+    if len(sel):
+        ks_all = key[sel]
+        perm = np.argsort(ks_all, kind="stable")
+        ks = ks_all[perm]
+        tr = np.asarray(t_rel, np.float64)[sel][perm]
+        run_start = np.flatnonzero(np.concatenate(([True], ks[1:] != ks[:-1])))
+        bounds = list(run_start[::max(1, len(run_start) * chunk // max(len(ks), 1))]) + [len(ks)]
+        bounds = sorted(set(int(b) for b in bounds))
+        for lo, hi in zip(bounds[:-1], bounds[1:]):
+            rs = run_start[(run_start >= lo) & (run_start < hi)]
+            ph = temporal_phases(tr[lo:hi], fr, delta_t, precision)
+            embed[ks[rs]] = np.add.reduceat(ph, rs - lo, axis=0)
+    shape = (width + 2 * dx, stride_x)
+    return Grid(embed.reshape(shape + (D,)), count.reshape(shape), dx, dy, width, height)
+
+
 # --------------------------------------------------------------------------
 # Stage 2: windowed, phase-weighted pooling + de-phase    (encoder.py:312-346)
 # --------------------------------------------------------------------------

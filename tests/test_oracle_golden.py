@@ -131,3 +131,43 @@ def test_oracle_f64_matches_reference_golden(case):
     feats = vo.encode_features(g["X"], W, H, dx, dy, dt, fr, precision="f64")
     assert feats.dtype == np.float64
     np.testing.assert_allclose(feats[g["feat_idx"]], g["feats"], rtol=0, atol=1e-12)
+
+
+def test_accumulate_near_equals_full_accumulate():
+    """The bounded-memory restricted accumulation used by the at-size GPU
+    checks gives every pixel a query window touches exactly the full grid's
+    value (same runs, same reduceat order); counts are complete."""
+    g = load_golden("cfg1_20k")
+    fr = freqs_of(g)
+    t, x, y = g["sorted_t"] - float(g["t_start"]), g["sorted_x"].astype(np.int64), g["sorted_y"].astype(np.int64)
+    full = vo.accumulate(t, x, y, 346, 260, 10, 10, fr, 0.016)
+    q = np.arange(0, len(t), 731)
+    near = vo.accumulate_near(t, x, y, 346, 260, 10, 10, fr, 0.016, x[q], y[q], chunk=997)
+    np.testing.assert_array_equal(near.count_p, full.count_p)
+    tab = vo.spatial_table(fr, 10, 10)
+    e1, c1 = vo.pool(full, tab, t[q], x[q], y[q], fr, 0.016)
+    e2, c2 = vo.pool(near, tab, t[q], x[q], y[q], fr, 0.016)
+    np.testing.assert_array_equal(c1, c2)
+    np.testing.assert_array_equal(e1, e2)
+
+
+def test_cfg1_100k_golden_regenerates_and_matches_oracle():
+    """BASELINE configs[0] (346x260, 100k events, delta 10) frozen from the
+    real reference (tests/golden/make_golden_cfg1.py): the oracle's synthetic
+    slice is byte-identical to the reference's synth_workload, and the
+    oracle reproduces the reference's counts exactly and its flows to ulps
+    on a strided subset (the full 100k-query pool is the GPU test's job)."""
+    import hashlib
+    g = load_golden("cfg1_100k")
+    X = vo.synth_uniform_noise(int(g["n"]), 346, 260, seed=0)
+    assert hashlib.sha256(np.ascontiguousarray(X).tobytes()).hexdigest() == str(g["X_sha256"])
+    fr = freqs_of(g)
+    t = X[:, 0] - X[0, 0]
+    x, y = X[:, 1].astype(np.int64), X[:, 2].astype(np.int64)
+    q = np.arange(0, len(X), 53)
+    grid = vo.accumulate_near(t, x, y, 346, 260, 10, 10, fr, 0.016, x[q], y[q])
+    np.testing.assert_array_equal(grid.count.astype(np.int32), g["grid_count"])
+    emb, cnt = vo.pool(grid, vo.spatial_table(fr, 10, 10), t[q], x[q], y[q], fr, 0.016)
+    np.testing.assert_array_equal(cnt, g["counts"][q])
+    flows = vo.mlp(g["w1"], g["b1"], g["w2"], g["b2"], vo.to_features(emb))
+    np.testing.assert_allclose(flows, g["flows"][q], rtol=0, atol=1e-6)
