@@ -164,19 +164,36 @@ def cpu_reference(wl, steps, warmup, budget_s=90.0):
     return value, cores, sample, statistics.median(times)
 
 
+def bench_config(args, world):
+    """The `config` of both arms' JSON lines (identical by construction, so
+    the driver can match the reference arm to this one)."""
+    W, H, n, d, slices, desc = WORKLOADS[args.workload]
+    if args.slices:
+        slices = args.slices
+    spatial = args.split == "spatial"
+    if spatial:
+        par = f"spatial{world} (row strips + {d}-row event halo, device partition + gather of owned flows)"
+    else:
+        par = f"dp{world} (independent slices per rank, no collective)"
+    return {"workload": desc, "sensor": f"{W}x{H}", "events_per_slice": n, "delta": d,
+            "slices_per_rank_per_step": 1 if spatial else slices, "embed_dim": 64, "hidden": 128,
+            "mlp_mode": args.mlp_mode, "l2": "flushed between steps (512 MiB write, outside step events)",
+            "parallelism": par}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    value, cores, sample, step_s = cpu_reference(args.workload, args.steps, args.warmup)
-    W, H, n, d, slices, desc = WORKLOADS[args.workload]
+    value, cores, sample, step_s = cpu_reference(args.workload, args.steps, args.warmup, budget_s=args.ref_budget)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (uniform noise, seeded)",
-        "config": {"workload": desc, "sensor": f"{W}x{H}", "events_per_slice": n, "delta": d,
-                   "parallelism": "host threads (reference CPU algorithm, oracle port)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "scaling": "strong" if args.split == "spatial" else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (uniform noise, seeded per rank), random-init weights D=64/hidden=128",
+        "config": bench_config(args, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample + " (the reference algorithm on the host cores: oracle/veckm_oracle.py)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -207,44 +224,71 @@ def run_b200(args):
     bases = pkg.generate_bases(64, 25.0, (0, 1, 2))
     w = pkg.init_weights(64, 128, bases, seed=0, dtype=np.float32)
     spatial = args.split == "spatial"
-    if spatial:
-        # one slice split into row strips (event-halo duplication), strong scaling
-        from paper_2504_19417_b200 import sharding
-        full = _synth(n, W, H, seed=0)
-        rows = np.bincount(full[:, 2].astype(np.int64), minlength=H)
-        strips = sharding.row_strips(rows, world, d)
-        se = sharding.strip_events(full, strips[rank])
-        host = [se.events]
-        owned = int(se.owned.sum())
-        t_global = float(full[0, 0])
-        H_eff = strips[rank].height
-        slices = 1
-        del full
-    else:
-        host = [_synth(n, W, H, seed=1000 * rank + s) for s in range(slices)]
-        H_eff = H
-    eng = pkg.FlowEngine(W, H_eff, d, d, 0.016, bases, w, device=local, mlp_mode=args.mlp_mode)
-    P = W * H_eff
-    p_occ = [int(len(np.unique(X[:, 2].astype(np.int64) * W + X[:, 1].astype(np.int64)))) for X in host]
-    evs = [torch.from_numpy(np.ascontiguousarray(X)).to(dev) for X in host]
-    t0s = [t_global] if spatial else [float(X[0, 0]) for X in host]
-    flows = [torch.empty((len(X), 2), dtype=torch.float32, device=dev) for X in host]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    if spatial:
+        # One slice resident on GPU 0, split into row strips inside the timed
+        # step (sharding.predict_spatial_device): device row histogram,
+        # vkm_select_rows partition + δy halo, NCCL send of each strip,
+        # per-rank strip kernels, flows back, vkm_scatter_rows into slice
+        # order on GPU 0.  Strong scaling: the slice is fixed as N grows.
+        from paper_2504_19417_b200 import sharding
+        full = _synth(n, W, H, seed=0) if rank == 0 else None
+        t_global = float(full[0, 0]) if rank == 0 else 0.0
+        if world > 1:
+            box = [t_global]
+            dist.broadcast_object_list(box, src=0)
+            t_global = box[0]
+        full_dev = torch.from_numpy(full).to(dev) if rank == 0 else None
+        engines = {}
 
-    if slices > 1:
-        # independent slices of one rank: one device buffer, batched launch
-        # sequences (vkm_predict_batch: up to 64 slices share each kernel)
-        ev_all = torch.cat(evs)
-        fl_all = torch.empty((ev_all.shape[0], 2), dtype=torch.float32, device=dev)
-        offs_all = np.cumsum([0] + [len(X) for X in host])
+        def make_engine(h):
+            if h not in engines:
+                engines[h] = pkg.FlowEngine(W, h, d, d, 0.016, bases, w, device=local, mlp_mode=args.mlp_mode)
+            return engines[h]
 
-    def step():
+        def step():
+            sharding.predict_spatial_device(make_engine, full_dev, t_global, W, H, d, world, rank)
+
+        slices = 1
+        step()                                   # builds this rank's strip engine
+        torch.cuda.synchronize()
+        eng = next(iter(engines.values()))
+        H_eff = eng.height
+        host = [full] if rank == 0 else []
+        p_occ = [int(len(np.unique(full[:, 2].astype(np.int64) * W + full[:, 1].astype(np.int64))))] if rank == 0 \
+            else [0]
+        t0s = [t_global]
+    else:
+        # independent slices: --slices per rank, or for config 4 the 1000
+        # back-to-back slices of BASELINE split over the ranks (strong scaling)
+        from paper_2504_19417_b200.sharding import slice_range
+        if args.workload == "cfg4" and not args.slices:
+            mine = slice_range(1000, rank, world)
+        else:
+            mine = range(1000 * rank, 1000 * rank + slices)
+        host = [_synth(n, W, H, seed=s) for s in mine]
+        slices = len(host)
+        H_eff = H
+        eng = pkg.FlowEngine(W, H, d, d, 0.016, bases, w, device=local, mlp_mode=args.mlp_mode)
+        p_occ = [int(len(np.unique(X[:, 2].astype(np.int64) * W + X[:, 1].astype(np.int64)))) for X in host]
+        evs = [torch.from_numpy(np.ascontiguousarray(X)).to(dev) for X in host]
+        t0s = [float(X[0, 0]) for X in host]
+        flows = [torch.empty((len(X), 2), dtype=torch.float32, device=dev) for X in host]
         if slices > 1:
-            eng.predict_batch_device(ev_all, offs_all, t0s, flows=fl_all, stream=stream)
-            return
-        for s in range(slices):
-            eng.predict_device(evs[s], t0s[s], flows=flows[s], stream=stream)
+            # independent slices of one rank: one device buffer, batched launch
+            # sequences (vkm_predict_batch: up to 64 slices share each kernel)
+            ev_all = torch.cat(evs)
+            fl_all = torch.empty((ev_all.shape[0], 2), dtype=torch.float32, device=dev)
+            offs_all = np.cumsum([0] + [len(X) for X in host])
+
+        def step():
+            if slices > 1:
+                eng.predict_batch_device(ev_all, offs_all, t0s, flows=fl_all, stream=stream)
+                return
+            for s in range(slices):
+                eng.predict_device(evs[s], t0s[s], flows=flows[s], stream=stream)
+    P = W * H_eff
 
     # per-kernel CUDA events (vkm_last_timings) sit between kernels and break
     # their programmatic-dependent-launch overlap, so they are recorded on
@@ -269,7 +313,7 @@ def run_b200(args):
             starts[i].record(stream)
             step()
             ends[i].record(stream)
-            launches += launches_per_call if slices > 1 else launches_per_call * slices
+            launches += launches_per_call if (slices > 1 or spatial) else launches_per_call * slices
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -277,12 +321,12 @@ def run_b200(args):
     # slices: the first chunk's worth (the slices one launch sequence takes,
     # pixel budget VKM_BATCH_PIXELS, default 4 Mpx, at most 64 slices).
     kslices = 1
-    if slices > 1:
+    if slices > 1 and not spatial:
         kslices = int(max(1, min(64, slices, int(os.environ.get("VKM_BATCH_PIXELS", 1 << 22)) // P)))
     eng.set_profiling(True)
     for _ in range(max(5, min(20, args.steps))):
         flush.zero_()
-        if slices > 1:
+        if slices > 1 and not spatial:
             eng.predict_batch_device(ev_all[: int(offs_all[kslices])], offs_all[: kslices + 1], t0s[:kslices],
                                      flows=fl_all, stream=stream)
         else:
@@ -298,7 +342,15 @@ def run_b200(args):
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    flows_total = (n if spatial else world * slices * n) * args.steps
+    if spatial:
+        flows_total = n * args.steps
+    else:   # every rank's slices (config 4: the 1000 slices in total)
+        total_slices = slices
+        if world > 1:
+            cnt = torch.tensor([float(slices)], dtype=torch.float64, device=dev)
+            dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+            total_slices = int(cnt.item())
+        flows_total = total_slices * n * args.steps
     value = flows_total / (total_ms / 1e3)
 
     # ---- end to end through the public host-buffer API (pinned buffers) ----
@@ -308,7 +360,42 @@ def run_b200(args):
     # kernels of the neighbouring slices.  The synchronous one-slice call
     # (vkm_predict_host) is reported beside it.
     e2e = None
-    if not args.no_e2e:
+
+    def timed(fn, reps):
+        for _ in range(2):
+            fn()
+        if world > 1:
+            dist.barrier()
+        t_w = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        dt = time.perf_counter() - t_w
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        return dt
+
+    if not args.no_e2e and spatial:
+        # the slice from pinned host memory to GPU 0, the strip split over the
+        # ranks, the flows back to pinned host memory (wall clock, max over ranks)
+        from paper_2504_19417_b200 import sharding
+        pin_in = torch.from_numpy(full).pin_memory() if rank == 0 else None
+        pin_out = torch.empty((n, 2), dtype=torch.float32).pin_memory() if rank == 0 else None
+
+        def call_spatial():
+            src = pin_in.to(dev, non_blocking=True) if rank == 0 else None
+            out = sharding.predict_spatial_device(make_engine, src, t_global, W, H, d, world, rank)
+            if rank == 0:
+                pin_out.copy_(out, non_blocking=True)
+            torch.cuda.synchronize()
+
+        reps = max(3, args.steps // 4)
+        e2e_s = timed(call_spatial, reps)
+        e2e = {"value": n * reps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 8 * n,
+               "steps": reps, "api": "sharding.predict_spatial_device from a pinned host slice (H2D to GPU 0, "
+                                     "device partition, NCCL strips, owned flows back, D2H)"}
+    elif not args.no_e2e:
         n_e2e = len(host[0])
         # slices per call: --e2e-slices, or by default ~32M events per call
         # (the pipeline's fill and drain amortised; 768 MB of pinned input)
@@ -327,23 +414,8 @@ def run_b200(args):
         def call_single():
             eng.predict_host(pin_ev[:n_e2e], t0s[0])
 
-        def timed(fn, reps):
-            for _ in range(2):
-                fn()
-            if world > 1:
-                dist.barrier()
-            t_w = time.perf_counter()
-            for _ in range(reps):
-                fn()
-            dt = time.perf_counter() - t_w
-            if world > 1:
-                t = torch.tensor([dt], dtype=torch.float64, device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                dt = float(t.item())
-            return dt
-
         reps = max(3, args.steps // (4 * K))
-        per_slice = n if spatial else world * n_e2e
+        per_slice = world * n_e2e
         e2e_s = timed(call_batch, reps)
         single_s = timed(call_single, max(5, args.steps // 4))
         # the C-ABI packs the f64 rows into 8-byte records on the host for
@@ -368,9 +440,17 @@ def run_b200(args):
     clk_mhz = clk.summary().get("sm_mhz")
     k1b = k2b = k3b = 0
     n_prof = 0
-    for i in range(kslices):   # the slices of one profiled launch sequence
-        b1, b2, b3 = algorithmic_bytes(len(host[i]), P, p_occ[i])
-        k1b, k2b, k3b, n_prof = k1b + b1, k2b + b2, k3b + b3, n_prof + len(host[i])
+    if spatial:   # rank 0's strip (its events incl. the halo) is what the per-kernel times cover
+        from paper_2504_19417_b200 import sharding
+        rows = np.bincount(full[:, 2].astype(np.int64), minlength=H)
+        se = sharding.strip_events(full, sharding.row_strips(rows, world, d)[0])
+        prof = [(len(se.events), int(len(np.unique(se.events[:, 2].astype(np.int64) * W
+                                                   + se.events[:, 1].astype(np.int64)))))]
+    else:         # the slices of one profiled launch sequence
+        prof = [(len(host[i]), p_occ[i]) for i in range(kslices)]
+    for n_i, po in prof:
+        b1, b2, b3 = algorithmic_bytes(n_i, P, po)
+        k1b, k2b, k3b, n_prof = k1b + b1, k2b + b2, k3b + b3, n_prof + n_i
     kernels = None
     roofline = None
     if kern:
@@ -419,11 +499,7 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if spatial else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (uniform noise, seeded per rank), random-init weights D=64/hidden=128",
-        "config": {"workload": desc, "sensor": f"{W}x{H}", "events_per_slice": n, "delta": d,
-                   "slices_per_rank_per_step": slices, "embed_dim": 64, "hidden": 128,
-                   "mlp_mode": args.mlp_mode, "l2": "flushed between steps (512 MiB write, outside step events)",
-                   "parallelism": (f"spatial{world} (row strips + {d}-row event halo, gather of owned flows)" if spatial
-                                   else f"dp{world} (independent slices per rank, no collective)")},
+        "config": bench_config(args, world),
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "kernels": kernels,
         "cpu_baseline": cpu, "clocks": clk.summary(),
         "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
@@ -449,6 +525,8 @@ def main():
                     help="slices per vkm_predict_batch_host call in the e2e leg (0: ~32M events per call, the "
                          "pipeline's fill and drain amortised; at cfg2 8 slices measured 1.5-1.7e9, 32 1.97e9)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=90.0,
+                    help="--impl reference: seconds of host work the whole run is sized to")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

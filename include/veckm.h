@@ -106,6 +106,15 @@ void vkm_destroy(vkm_handle* h);
 /* Select the MLP mode after creation (VKM_MLP_*). */
 int vkm_set_mlp_mode(vkm_handle* h, int32_t mode);
 
+/* Float64 copy of the head for precision="f64" (vkm_predict_f64[_host]).  The
+ * reference promotes its head to float64 when the weights are float64 (e.g.
+ * returned by train_head, flow.py:98-106, 223); without this call the f64 path
+ * uses the float32 weights given to vkm_create, promoted exactly.
+ * W1 (hidden, 2D) row-major [Re | Im], b1 (hidden), W2 (2, hidden), b2 (2);
+ * shapes are the handle's.  Replaces nothing in the reference (its weights are
+ * numpy arrays of either dtype, flow.py:48-80). */
+int vkm_set_weights_f64(vkm_handle* h, const double* w1, const double* b1, const double* w2, const double* b2);
+
 /* Per-event normal flow for every event of one slice.
  * flows_dev: (n, 2) f32 [n_x, n_y]; NaN rows for empty neighbourhoods.
  * counts_dev: (n) int32 neighbourhood sizes, or NULL. */
@@ -275,6 +284,15 @@ int vkm_scatter_rows(vkm_handle* h, const float* src_dev, const int64_t* index_d
  * pooled = 1: window sums Σ G[x+i][y+j]·table[i][j] before de-phasing. */
 int vkm_grid(vkm_handle* h, const double* events_dev, int64_t n, double t_start,
              int32_t pooled, float* grid_dev, int32_t* counts_dev, void* stream);
+
+/* Parity hook: the pixel-major event order of accumulate_grid
+ * (encoder.py:255-259: order = np.argsort(flat_key, kind="stable"), the run
+ * starts = exclusive cumsum of np.bincount).  start_dev: (width*height + 1)
+ * int32, start[p] = first slot of pixel p = y*width + x, start[P] = in-sensor
+ * events; order_dev: (n) int32 event index per slot (-1 for the trailing
+ * slots of events outside the sensor). */
+int vkm_pixel_order(vkm_handle* h, const double* events_dev, int64_t n, double t_start, int32_t* start_dev,
+                    int32_t* order_dev, void* stream);
 
 /* Per-kernel device timing of the last call (ms), recorded with CUDA events
  * when enabled: [0] accumulate, [1] pool, [2] gather+MLP, [3] total.

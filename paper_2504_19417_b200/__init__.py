@@ -27,7 +27,8 @@ from .errors import (
 )
 from .estimators import LocalEventEncoder, NormalFlowRegressor
 from .training import TrainConfig, TrainingDivergedError, train_head
-from .validation import check_event_array, check_flow_array, slice_from_array
+from .stream import CameraGeometry, EventSlice, EventStream
+from .validation import block_from_array, check_event_array, check_events, check_flow_array, slice_from_array
 from .weights import (
     Bases,
     MlpWeights,
@@ -41,6 +42,7 @@ from .weights import (
 __all__ = [
     "FlowEngine", "NormalFlowRegressor", "LocalEventEncoder", "Bases", "MlpWeights", "generate_bases",
     "init_weights", "load_weights", "save_weights", "standard_normals", "check_event_array",
-    "check_flow_array", "slice_from_array", "EvflowError", "EventParseError", "GeometryError",
+    "check_flow_array", "slice_from_array", "block_from_array", "check_events", "CameraGeometry", "EventSlice",
+    "EventStream", "EvflowError", "EventParseError", "GeometryError",
     "DimensionMismatchError", "EmptyNeighborhoodError", "TrainConfig", "TrainingDivergedError", "train_head",
 ]

@@ -20,6 +20,8 @@
 #include <cmath>
 #include <cstdint>
 
+#include <type_traits>
+
 #include "vkm_device.cuh"
 #include "vkm_kernels.cuh"
 
@@ -169,26 +171,44 @@ constexpr int kEvPerStep = 16;   // events per block step of k64_predict
 // block-reduced.  NaN rows for empty neighbourhoods (flow.py:188-196).
 // WT: the type W1ᵀ is kept in shared memory as — double when it fits (no
 // f32 -> f64 conversion in the inner loop), else float (promoted on use).
-template <typename WT>
+// W64: the head arrives as float64 (m.w64: W1ᵀ | b1 | W2 | b2, the reference's
+// promoted f64 head, flow.py:98-106) and W1ᵀ is staged as double when it fits
+// (WT = double), else read from global memory (WT = void).
+template <typename WT, bool W64>
 __global__ void k64_predict(const double* __restrict__ ev, int64_t n, double t0, double delta_t,
                             const double* __restrict__ T, const double2* __restrict__ Q, const int* __restrict__ NQ,
                             int W, int H, int D, int D8, const float* __restrict__ w1p, const float* __restrict__ b1,
-                            const float* __restrict__ w2, const float* __restrict__ b2, int hidden,
+                            const float* __restrict__ w2, const float* __restrict__ b2,
+                            const double* __restrict__ w64, int hidden,
                             double* __restrict__ flows, int32_t* __restrict__ counts) {
   extern __shared__ __align__(16) uint8_t sm64[];
+  constexpr bool kGlobalW1 = std::is_void<WT>::value;
+  using WS = typename std::conditional<kGlobalW1, double, WT>::type;
   const int F = 2 * D;                                          // features per event
-  WT* w1t = reinterpret_cast<WT*>(sm64);                        // [F][hidden]
-  double* fs = reinterpret_cast<double*>(sm64 + ((size_t(F) * hidden * sizeof(WT) + 15) / 16) * 16);   // [kEv][F]
+  WS* w1t = reinterpret_cast<WS*>(sm64);                        // [F][hidden]
+  const size_t w1bytes = kGlobalW1 ? 0 : size_t(F) * hidden * sizeof(WS);
+  double* fs = reinterpret_cast<double*>(sm64 + ((w1bytes + 15) / 16) * 16);   // [kEv][F]
   double* red = fs + kEvPerStep * F;                            // [32 warps][kEv][2]
   int* cnts = reinterpret_cast<int*>(red + 32 * kEvPerStep * 2);
   const int k = threadIdx.x;
-  for (int i = threadIdx.x; i < F * hidden; i += blockDim.x) {   // W1 row r, feature j -> w1t[j][r]
-    const int r = i / F, j = i - r * F;
-    const int src = j < D ? j : D8 + (j - D);                   // w1p is [hidden][2·D8] (Re | Im padded)
-    w1t[j * hidden + r] = WT(w1p[int64_t(r) * 2 * D8 + src]);
-  }
-  const double bk = k < hidden ? double(b1[k]) : 0.0;
-  const double wa = k < hidden ? double(w2[k]) : 0.0, wb = k < hidden ? double(w2[hidden + k]) : 0.0;
+  const double* w64b1 = w64 + size_t(F) * hidden;
+  const double* w64w2 = w64b1 + hidden;
+  const double* w64b2 = w64w2 + 2 * hidden;
+  if (!kGlobalW1)
+    for (int i = threadIdx.x; i < F * hidden; i += blockDim.x) {   // W1 row r, feature j -> w1t[j][r]
+      if (W64) {
+        w1t[i] = WS(w64[i]);                                        // already W1ᵀ [F][hidden]
+      } else {
+        const int r = i / F, j = i - r * F;
+        const int src = j < D ? j : D8 + (j - D);                 // w1p is [hidden][2·D8] (Re | Im padded)
+        w1t[j * hidden + r] = WS(w1p[int64_t(r) * 2 * D8 + src]);
+      }
+    }
+  const WS* w1src = kGlobalW1 ? reinterpret_cast<const WS*>(w64) : w1t;
+  const double bk = k < hidden ? (W64 ? w64b1[k] : double(b1[k])) : 0.0;
+  const double wa = k < hidden ? (W64 ? w64w2[k] : double(w2[k])) : 0.0;
+  const double wb = k < hidden ? (W64 ? w64w2[hidden + k] : double(w2[hidden + k])) : 0.0;
+  const double b2a = W64 ? w64b2[0] : double(b2[0]), b2b = W64 ? w64b2[1] : double(b2[1]);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   __syncthreads();
   for (int64_t e0 = int64_t(blockIdx.x) * kEvPerStep; e0 < n; e0 += int64_t(gridDim.x) * kEvPerStep) {
@@ -211,7 +231,7 @@ __global__ void k64_predict(const double* __restrict__ ev, int64_t n, double t0,
 #pragma unroll
       for (int u = 0; u < kEvPerStep; ++u) h[u] = 0.0;
       for (int j = 0; j < F; ++j) {
-        const double wj = double(w1t[j * hidden + k]);
+        const double wj = double(w1src[j * hidden + k]);
 #pragma unroll
         for (int u = 0; u < kEvPerStep; ++u) h[u] = fma(fs[u * F + j], wj, h[u]);
       }
@@ -244,8 +264,8 @@ __global__ void k64_predict(const double* __restrict__ ev, int64_t n, double t0,
       }
       const int64_t e = e0 + u;
       const bool ok = cnts[u] > 0;
-      flows[2 * e] = ok ? sa + double(b2[0]) : nan("");
-      flows[2 * e + 1] = ok ? sb + double(b2[1]) : nan("");
+      flows[2 * e] = ok ? sa + b2a : nan("");
+      flows[2 * e + 1] = ok ? sb + b2b : nan("");
       if (counts) counts[e] = cnts[u];
     }
     __syncthreads();
@@ -341,15 +361,20 @@ void launch_predict64(const F64Tables& t, const double* ev, int64_t n, double t0
   // f32 W1ᵀ in shared memory (promoted per use): twice the resident blocks of
   // an f64 copy, which measured 1.5x slower (4 warps per SM at 128 KB)
   const size_t smem64 = predict64_smem(D, m.hidden, 8);
-  if (smem64 <= 64 * 1024) {   // f64 copy only for small heads
-    cudaFuncSetAttribute(k64_predict<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem64));
-    k64_predict<double><<<blocks, threads, smem64, s>>>(ev, n, t0, delta_t, t.T, Q, NQ, W, H, D, D8, m.w1, m.b1,
-                                                        m.w2, m.b2, m.hidden, flows, counts);
+  auto go = [&](auto kern, size_t smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    kern<<<blocks, threads, smem, s>>>(ev, n, t0, delta_t, t.T, Q, NQ, W, H, D, D8, m.w1, m.b1, m.w2, m.b2, m.w64,
+                                       m.hidden, flows, counts);
+  };
+  if (m.w64) {   // float64 weights: never rounded to f32
+    if (smem64 <= 200 * 1024)
+      go(k64_predict<double, true>, smem64);
+    else
+      go(k64_predict<void, true>, predict64_smem(D, m.hidden, 0));
+  } else if (smem64 <= 64 * 1024) {   // f64 copy only for small heads
+    go(k64_predict<double, false>, smem64);
   } else {
-    const size_t smem = predict64_smem(D, m.hidden, 4);
-    cudaFuncSetAttribute(k64_predict<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    k64_predict<float><<<blocks, threads, smem, s>>>(ev, n, t0, delta_t, t.T, Q, NQ, W, H, D, D8, m.w1, m.b1, m.w2,
-                                                     m.b2, m.hidden, flows, counts);
+    go(k64_predict<float, false>, predict64_smem(D, m.hidden, 4));
   }
 }
 

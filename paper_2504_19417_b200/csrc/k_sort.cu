@@ -3,8 +3,10 @@
 //   k_prep     event -> pixel key, slot value (event index, f32 time argument
 //              a = f32((t - t0)/δt)) and the per-pixel count histogram (the
 //              reference's bincount, encoder.py:259)
-//   scan       exclusive prefix sum of the counts -> pixel run starts
-//   sort       stable LSD radix sort of (pixel key, slot value): the same
+//   k_scan     exclusive prefix sum of the counts -> pixel run starts
+//              (single pass, decoupled look-back over 4096-count tiles)
+//   k_scatter  counting scatter to start[pixel] + arrival rank, then
+//   k_runsort  puts every run back into event (= time) order: the same
 //              stable pixel-major order as np.argsort(flat, kind="stable")
 //              (encoder.py:255-257), so each pixel's run is in time order
 //   k_reduce_x (default, D = 64) sums e^{i a T} per pixel sequentially in f32 —
@@ -19,10 +21,8 @@
 // memset, no L2 read-modify-write of a grid larger than L2), is bit-
 // deterministic, and reproduces the reference's per-pixel sums bit-for-bit
 // wherever the f32 phases agree (98.9% of sin/cos values).
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 
@@ -33,15 +33,25 @@ namespace vkm {
 
 constexpr unsigned kFullMask = 0xffffffffu;
 
+// Event-parallel kernels run one co-resident wave with a grid-stride loop:
+// blocks then progress together through the time-ordered events, so k_prep's
+// histogram atomics hand out arrival ranks in nearly time order.  (A grid of
+// twice the resident blocks ran its second half after the first: every run
+// became two interleaved sequences.  Warp tickets from a global counter kept
+// the order tighter but serialised on the counter: cfg-2 k_prep 15 -> 29 us.)
+template <class F>
+__device__ __forceinline__ void event_walk(int64_t n, F&& f) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) f(e);
+}
+
 __global__ void __launch_bounds__(256) k_prep(const double* __restrict__ ev, const SliceTab st, double delta_t,
                                               int W, int H, int32_t* __restrict__ pix_out,
                                               uint64_t* __restrict__ val_out, int32_t* __restrict__ rank_out,
-                                              int* __restrict__ cnt,
-                                              float* __restrict__ flows_invalid,
+                                              int* __restrict__ cnt, float* __restrict__ flows_invalid,
                                               int32_t* __restrict__ counts_invalid) {
   const int P = W * H;
   const int64_t n = st.off[st.nb];
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+  event_walk(n, [&](int64_t e) {
     int b = 0;   // slice of event e (upper_bound over the offsets)
     for (int step = kMaxBatch / 2; step > 0; step >>= 1)
       if (b + step < st.nb && st.off[b + step] <= e) b += step;
@@ -51,7 +61,10 @@ __global__ void __launch_bounds__(256) k_prep(const double* __restrict__ ev, con
     int pix = st.nb * P;   // out-of-sensor events sort after every pixel run
     if (xi >= 0 && xi < W && yi >= 0 && yi < H && x == double(xi) && y == double(yi)) {
       pix = b * P + yi * W + xi;
-      rank_out[e] = atomicAdd(cnt + pix, 1);   // arrival rank: the counting scatter's offset
+      if (rank_out)
+        rank_out[e] = atomicAdd(cnt + pix, 1);   // arrival rank: the counting scatter's offset
+      else
+        atomicAdd(cnt + pix, 1);                 // histogram only (row-bucket path)
     } else {
       if (flows_invalid)
         reinterpret_cast<float2*>(flows_invalid)[e] = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
@@ -59,7 +72,7 @@ __global__ void __launch_bounds__(256) k_prep(const double* __restrict__ ev, con
     }
     pix_out[e] = pix;
     val_out[e] = slot_pack(int32_t(e), time_arg(t, t0, delta_t));
-  }
+  });
 }
 
 // Host-packed events (vkm_predict_batch_host): the time argument arrives
@@ -71,7 +84,7 @@ __global__ void __launch_bounds__(256) k_prep_packed(const uint2* __restrict__ e
                                                      int32_t* __restrict__ counts_invalid) {
   const int P = W * H;
   const int64_t n = st.off[st.nb];
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+  event_walk(n, [&](int64_t e) {
     int b = 0;
     for (int step = kMaxBatch / 2; step > 0; step >>= 1)
       if (b + step < st.nb && st.off[b + step] <= e) b += step;
@@ -80,7 +93,10 @@ __global__ void __launch_bounds__(256) k_prep_packed(const uint2* __restrict__ e
     int pix = st.nb * P;
     if (xi < W && yi < H) {
       pix = b * P + yi * W + xi;
-      rank_out[e] = atomicAdd(cnt + pix, 1);   // arrival rank: the counting scatter's offset
+      if (rank_out)
+        rank_out[e] = atomicAdd(cnt + pix, 1);   // arrival rank: the counting scatter's offset
+      else
+        atomicAdd(cnt + pix, 1);
     } else {
       if (flows_invalid)
         reinterpret_cast<float2*>(flows_invalid)[e] = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
@@ -88,7 +104,7 @@ __global__ void __launch_bounds__(256) k_prep_packed(const uint2* __restrict__ e
     }
     pix_out[e] = pix;
     val_out[e] = slot_pack(int32_t(e), __uint_as_float(v.x));
-  }
+  });
 }
 
 // Raw grid, D8 == 64: a warp owns 32 consecutive pixels and their slot range;
@@ -340,44 +356,46 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_scatter(const int32_t* __restrict__ pix, const uint64_t* __restrict__ val,
                                                  const int32_t* __restrict__ rank, int64_t n, int64_t P,
-                                                 const int* __restrict__ start, uint64_t* __restrict__ val_s,
-                                                 int32_t* __restrict__ pix_s) {
+                                                 const int* __restrict__ start, uint64_t* __restrict__ val_s) {
   pdl_wait();
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
-    const int p = __ldg(pix + e);
-    if (p >= P) continue;   // outside the sensor: no slot (slots [start[P], n) are never read)
-    const int slot = __ldg(start + p) + __ldg(rank + e);
-    val_s[slot] = __ldg(val + e);
-    pix_s[slot] = p;
-  }
+  event_walk(n, [&](int64_t e) {
+    const int p = __ldcs(pix + e);
+    if (p < P)   // outside the sensor: no slot (slots [start[P], n) are never read)
+      val_s[__ldg(start + p) + __ldcs(rank + e)] = __ldcs(val + e);
+  });
   pdl_trigger();   // dependents may launch as this grid drains
 }
 
-constexpr int kShortRun = 256;   // runs up to this length: one thread, insertion sort
-constexpr int kSmemRun = 4096;
+// Run ordering.  The arrival ranks follow the grid-stride order of k_prep, so
+// a run is nearly time-ordered already (only events processed in the same
+// wave can be swapped): insertion sort is close to linear.  A block owns ppb
+// consecutive pixels per step, i.e. one contiguous slot range, staged through
+// shared memory (coalesced in and out) when it fits; one thread per pixel
+// insertion-sorts its run there by event index.  Runs too long for the stage
+// go to a list sorted by k_longsort.  ppb is chosen on the host from the mean
+// run length so the range usually fits (dense slices: 35 events per pixel).
+constexpr int kRunsortThreads = 128;
+constexpr int kRunsortStage = 6144;    // most slots staged per block (48 KB)
+constexpr int kInsertRun = 256;        // longer runs: k_longsort (bitonic)
+constexpr int kSmemRun = 4096;         // k_longsort sorts runs up to this in shared memory
 
-// A block owns ppb consecutive pixels per step, i.e. one contiguous slot range:
-// it is staged through shared memory (coalesced in and out) when it fits, and
-// each thread insertion-sorts its pixel's run there by event index.  ppb is
-// chosen on the host from the mean run length so the range usually fits.
-constexpr int kRunsortStage = 3072;   // slots staged per block (24 KB)
-
-__global__ void __launch_bounds__(256) k_runsort(const int* __restrict__ start, int64_t P, int ppb,
-                                                 uint64_t* __restrict__ val_s, int* __restrict__ longlist,
-                                                 int* __restrict__ longcount) {
+__global__ void __launch_bounds__(kRunsortThreads) k_runsort(const int* __restrict__ start, int64_t P, int ppb,
+                                                             int stage_cap, uint64_t* __restrict__ val_s,
+                                                             int32_t* __restrict__ pix_s, int* __restrict__ longlist,
+                                                             int* __restrict__ longcount) {
   pdl_wait();
-  __shared__ uint64_t stage[kRunsortStage];
+  extern __shared__ uint64_t stage[];   // stage_cap slots
   for (int64_t p0 = int64_t(blockIdx.x) * ppb; p0 < P; p0 += int64_t(gridDim.x) * ppb) {
-    const int64_t p = p0 + threadIdx.x;
     const int64_t pe = min(P, p0 + int64_t(ppb));
     const int b0 = __ldg(start + p0), b1 = __ldg(start + pe);
-    const bool staged = b1 - b0 <= kRunsortStage;
+    const bool staged = b1 - b0 <= stage_cap;
     if (staged)
       for (int i = threadIdx.x; i < b1 - b0; i += blockDim.x) stage[i] = val_s[b0 + i];
     __syncthreads();
-    if (threadIdx.x < ppb && p < P) {
+    for (int64_t p = p0 + threadIdx.x; p < pe; p += blockDim.x) {
       const int s = __ldg(start + p), L = __ldg(start + p + 1) - s;
-      if (L > kShortRun) {
+      for (int j = 0; j < L; ++j) pix_s[s + j] = int32_t(p);   // slot -> pixel (K3's gather key)
+      if (L > kInsertRun) {
         longlist[atomicAdd(longcount, 1)] = int(p);
       } else if (L > 1) {
         uint64_t* r = staged ? stage + (s - b0) : val_s + s;
@@ -399,6 +417,222 @@ __global__ void __launch_bounds__(256) k_runsort(const int* __restrict__ start, 
     __syncthreads();
   }
   pdl_trigger();   // dependents may launch as this grid drains
+}
+
+
+// ---------------------------------------------------------------------------
+// Dense slices (mean run > 8 events, e.g. config 5 at 35 events per pixel):
+// the counting scatter's 8-byte writes land on sectors all over a val_s far
+// larger than L2, and its runs need sorting.  Instead a stable two-level
+// counting sort (MSD: row, then column), both levels stable by construction,
+// so the runs come out in time order with no run sort:
+//   k_rowhist    per 8192-event tile: events per virtual row -> table[row][tile]
+//   k_scan       over the table (row-major): each (row, tile)'s first bucket slot
+//   k_rowscatter tile re-read; warps own consecutive 1024-event chunks, per-warp
+//                row bases from per-warp counts, in-warp order by __match_any;
+//                writes (event, a) and x into row buckets (whole-sector runs)
+//   k_xsort      one CTA per row: the same stable counting step by column,
+//                from the row bucket into val_s (pixel runs from start[]), pix_s
+// ---------------------------------------------------------------------------
+constexpr int kMsdTile = 8192, kMsdThreads = 256, kMsdWarps = kMsdThreads / 32;
+constexpr int kMsdMaxRows = 4096;                  // per-warp row bases in shared memory
+constexpr int kXsortThreads = 512, kXsortWarps = kXsortThreads / 32, kXsortMaxW = 2048;
+
+size_t msd_tab_words(int64_t n) { return size_t(kMsdMaxRows) * size_t((n + kMsdTile - 1) / kMsdTile + 1); }
+
+__global__ void __launch_bounds__(kMsdThreads) k_rowhist(const int32_t* __restrict__ pix, int64_t n, int W, int R,
+                                                         int ntiles, int* __restrict__ tab) {
+  pdl_wait();
+  extern __shared__ int rh[];   // [R]
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int r = threadIdx.x; r < R; r += blockDim.x) rh[r] = 0;
+    __syncthreads();
+    const int64_t e0 = int64_t(t) * kMsdTile, e1 = min(n, e0 + kMsdTile);
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const int p = __ldg(pix + e);
+      const int r = p / W;
+      if (r < R) atomicAdd(rh + r, 1);
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < R; r += blockDim.x) tab[int64_t(r) * ntiles + t] = rh[r];
+    __syncthreads();
+  }
+  pdl_trigger();
+}
+
+__global__ void __launch_bounds__(kMsdThreads) k_rowscatter(const int32_t* __restrict__ pix,
+                                                            const uint64_t* __restrict__ val, int64_t n, int W, int R,
+                                                            int ntiles, const int* __restrict__ off,
+                                                            uint64_t* __restrict__ bkt, int32_t* __restrict__ bx) {
+  pdl_wait();
+  extern __shared__ int wb[];   // [kMsdWarps][R]: per-warp counts, then per-warp bases
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  constexpr int kChunk = kMsdTile / kMsdWarps;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int i = threadIdx.x; i < kMsdWarps * R; i += blockDim.x) wb[i] = 0;
+    __syncthreads();
+    const int64_t c0 = int64_t(t) * kMsdTile + int64_t(w) * kChunk, c1 = min(n, c0 + kChunk);
+    for (int64_t e = c0 + lane; e < c1; e += 32) {
+      const int r = __ldg(pix + e) / W;
+      if (r < R) atomicAdd(wb + w * R + r, 1);
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {   // bases: tile offset + earlier warps' counts
+      int run = __ldg(off + int64_t(r) * ntiles + t);
+      for (int v = 0; v < kMsdWarps; ++v) {
+        const int c = wb[v * R + r];
+        wb[v * R + r] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+    int* base = wb + w * R;
+    for (int64_t eb = c0; eb < c1; eb += 32) {            // in event order, 32 at a time
+      const int64_t e = eb + lane;
+      const bool ok = e < c1;
+      const int p = ok ? __ldg(pix + e) : R * W;
+      const int r = p / W;
+      const bool in = ok && r < R;
+      const unsigned peers = __match_any_sync(kFullMask, in ? r : -1);
+      if (in) {
+        const int pos = base[r] + __popc(peers & lt);
+        bkt[pos] = __ldg(val + e);
+        bx[pos] = p - r * W;
+      }
+      __syncwarp();
+      if (in && (peers & lt) == 0) base[r] += __popc(peers);   // the group's lowest lane advances the base
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+}
+
+__global__ void __launch_bounds__(kXsortThreads) k_xsort(const uint64_t* __restrict__ bkt,
+                                                         const int32_t* __restrict__ bx, const int* __restrict__ start,
+                                                         int W, int R, uint64_t* __restrict__ val_s,
+                                                         int32_t* __restrict__ pix_s) {
+  pdl_wait();
+  extern __shared__ int xb[];   // [kXsortWarps][W]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int r = blockIdx.x; r < R; r += gridDim.x) {
+    const int* st = start + int64_t(r) * W;
+    const int rs = __ldg(st), re = __ldg(st + W);
+    const int chunk = (re - rs + kXsortWarps - 1) / kXsortWarps;
+    const int c0 = rs + w * chunk, c1 = min(re, c0 + chunk);
+    for (int i = threadIdx.x; i < kXsortWarps * W; i += blockDim.x) xb[i] = 0;
+    __syncthreads();
+    for (int j = c0 + lane; j < c1; j += 32) atomicAdd(xb + w * W + __ldg(bx + j), 1);
+    __syncthreads();
+    for (int x = threadIdx.x; x < W; x += blockDim.x) {
+      int run = __ldg(st + x);
+      for (int v = 0; v < kXsortWarps; ++v) {
+        const int c = xb[v * W + x];
+        xb[v * W + x] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+    int* base = xb + w * W;
+    for (int jb = c0; jb < c1; jb += 32) {
+      const int j = jb + lane;
+      const bool in = j < c1;
+      const int x = in ? __ldg(bx + j) : -1;
+      const unsigned peers = __match_any_sync(kFullMask, x);
+      if (in) {
+        const int pos = base[x] + __popc(peers & lt);
+        val_s[pos] = __ldg(bkt + j);
+        pix_s[pos] = r * W + x;
+      }
+      __syncwarp();
+      if (in && (peers & lt) == 0) base[x] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+}
+
+// ---------------------------------------------------------------------------
+// Exclusive scan of the per-pixel counts, one pass: each 4096-count tile
+// publishes its aggregate, looks back over its predecessors' published
+// aggregates / inclusive prefixes (a warp reads 32 at a time) and publishes
+// its own inclusive prefix (decoupled look-back).  A tile-state word packs
+// (epoch, flag, value) so the states never need a reset: words of another
+// launch carry another epoch and read as "not yet published".  Tiles are
+// taken in increasing order by a grid no larger than what is co-resident, so
+// every predecessor a tile waits on is being processed.
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 256, kScanItems = 16, kScanTile = kScanThreads * kScanItems;
+__global__ void __launch_bounds__(kScanThreads) k_scan(const int* __restrict__ in, int* __restrict__ out, int64_t m,
+                                                       int ntiles, unsigned long long* __restrict__ state,
+                                                       uint32_t epoch) {
+  pdl_wait();
+  __shared__ int warp_sum[kScanThreads / 32];
+  __shared__ int tile_prefix;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t i0 = int64_t(t) * kScanTile + int64_t(threadIdx.x) * kScanItems;
+    int v[kScanItems];
+    if (i0 + kScanItems <= m) {
+      const int4* q = reinterpret_cast<const int4*>(in + i0);
+#pragma unroll
+      for (int k = 0; k < kScanItems / 4; ++k) {
+        const int4 w = q[k];
+        v[4 * k] = w.x; v[4 * k + 1] = w.y; v[4 * k + 2] = w.z; v[4 * k + 3] = w.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kScanItems; ++k) v[k] = i0 + k < m ? in[i0 + k] : 0;
+    }
+    int tsum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) tsum += v[k];
+    int incl = tsum;   // warp inclusive scan of the thread sums
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(kFullMask, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) warp_sum[wid] = incl;
+    __syncthreads();
+    int wpre = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; ++w) {
+      const int ws = warp_sum[w];
+      wpre += w < wid ? ws : 0;
+      total += ws;
+    }
+    if (wid == 0) {
+      const uint32_t excl = lookback_publish(state, t, uint32_t(total), epoch);
+      if (lane == 0) tile_prefix = int(excl);
+    }
+    __syncthreads();
+    int run = tile_prefix + wpre + incl - tsum;
+    if (i0 + kScanItems <= m) {
+      int4* q = reinterpret_cast<int4*>(out + i0);
+#pragma unroll
+      for (int k = 0; k < kScanItems / 4; ++k) {
+        int4 w;
+        w.x = run; run += v[4 * k];
+        w.y = run; run += v[4 * k + 1];
+        w.z = run; run += v[4 * k + 2];
+        w.w = run; run += v[4 * k + 3];
+        q[k] = w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kScanItems; ++k)
+        if (i0 + k < m) {
+          out[i0 + k] = run;
+          run += v[k];
+        }
+    }
+    __syncthreads();   // warp_sum / tile_prefix are reused by the next tile
+  }
+  pdl_trigger();
 }
 
 __device__ __forceinline__ void cas_slot(uint64_t& a, uint64_t& b) {
@@ -564,27 +798,26 @@ __global__ void __launch_bounds__(kRx1Warps * 32) k_reduce_x1(const int* __restr
   pdl_trigger();   // dependents may launch as this grid drains
 }
 
-namespace {
-int key_bits(int64_t P) {   // keys are in [0, P] (P = out-of-sensor)
-  int b = 1;
-  while ((int64_t(1) << b) <= P) ++b;
-  return b;
-}
-}  // namespace
-
-size_t sort_scan_temp_bytes(int64_t P) {
-  size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<int*>(nullptr), static_cast<int*>(nullptr), int(P + 1));
-  return bytes;
+// order[slot] = event index of the slot (slots [start[P], n): -1, events outside the sensor)
+__global__ void k_slot_events(const uint64_t* __restrict__ val_s, const int* __restrict__ valid, int64_t n,
+                              int32_t* __restrict__ order) {
+  const int64_t m = *valid;
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x)
+    order[j] = j < m ? slot_event(val_s[j]) : -1;
 }
 
-size_t sort_pairs_temp_bytes(int64_t n, int64_t P) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
-                                  static_cast<const uint64_t*>(nullptr), static_cast<uint64_t*>(nullptr), int(n), 0,
-                                  key_bits(P));
-  return bytes;
+void launch_slot_events(const uint64_t* val_s, const int* valid, int64_t n, int32_t* order, cudaStream_t s) {
+  k_slot_events<<<int(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(val_s, valid, n, order);
 }
+
+uint32_t next_scan_epoch() {
+  static std::atomic<uint32_t> epoch{0};
+  uint32_t e;
+  do e = (epoch.fetch_add(1) + 1) & 0x3fffffffu; while (e == 0);   // 0 marks never-published words
+  return e;
+}
+
+size_t scan_state_words(int64_t P) { return size_t((P + 1 + kScanTile - 1) / kScanTile); }
 
 int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st, double delta_t, int W, int H,
                        const GridBufs& g, const SortBufs& sb, float* flows_invalid, int32_t* counts_invalid,
@@ -593,45 +826,86 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
   const int64_t n = st.off[st.nb];
   int launches = 0;
   cudaMemsetAsync(g.C, 0, sizeof(int) * (P + 1), s);
+  // Event-parallel kernels run one co-resident wave (grid-stride beyond it):
+  // blocks then progress together through the time-ordered events, so the
+  // arrival ranks of k_prep's histogram atomics come out nearly in time order
+  // and k_runsort's insertion sorts stay near linear.  (With twice the
+  // resident blocks, the second half of the grid ran after the first and every
+  // run became two interleaved sequences: config-5 run sort 963 us.)
+  static thread_local int dev_cached = -1, ev_blocks = 0;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != dev_cached) {
+      int sms = 148, per = 1;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_prep, 256, 0);
+      ev_blocks = std::max(1, per) * sms;
+      dev_cached = dev;
+    }
+  }
+  cudaMemsetAsync(sb.longcount, 0, sizeof(int), s);
+  // Dense slices take the row-bucket path, the others the counting scatter
+  // (VKM_SORT=counting|rows forces one, for A/B runs and tests).
+  static const int sort_env = [] {
+    const char* e = std::getenv("VKM_SORT");
+    return !e ? 0 : (std::strcmp(e, "counting") == 0 ? 1 : (std::strcmp(e, "rows") == 0 ? 2 : 0));
+  }();
+  const int R = st.nb * H;
+  const bool rows_ok = R <= kMsdMaxRows && W <= kXsortMaxW;
+  const bool dense = rows_ok && (sort_env == 2 || (sort_env == 0 && double(n) > 8.0 * double(P) && n >= (1 << 20)));
   if (n > 0) {
-    const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+    const int blocks = int(std::min<int64_t>((n + 255) / 256, ev_blocks));
+    int32_t* rank = dense ? nullptr : sb.rank;
     if (packed)
-      k_prep_packed<<<blocks, 256, 0, s>>>(packed, st, W, H, sb.pix, sb.val, sb.rank, g.C, flows_invalid,
+      k_prep_packed<<<blocks, 256, 0, s>>>(packed, st, W, H, sb.pix, sb.val, rank, g.C, flows_invalid,
                                            counts_invalid);
     else
-      k_prep<<<blocks, 256, 0, s>>>(ev, st, delta_t, W, H, sb.pix, sb.val, sb.rank, g.C, flows_invalid,
-                                    counts_invalid);
+      k_prep<<<blocks, 256, 0, s>>>(ev, st, delta_t, W, H, sb.pix, sb.val, rank, g.C, flows_invalid, counts_invalid);
     ++launches;
   }
-  size_t scan_bytes = sb.temp_bytes;
-  cub::DeviceScan::ExclusiveSum(sb.temp, scan_bytes, g.C, sb.start, int(P + 1), s);
-  launches += 2;   // CUB: init + scan
-  static const bool use_cub = [] {
-    const char* e = std::getenv("VKM_SORT");
-    return e && std::strcmp(e, "cub") == 0;
-  }();
-  // Counting scatter for sparse-to-moderate slices; dense slices (mean run >
-  // 8 events, e.g. config 5 at 35 events/pixel) sort faster with CUB's
-  // bandwidth-bound onesweep passes (cfg5 K1 3.7 ms vs 6.0 ms).
-  const bool counting = !use_cub && double(n) <= 8.0 * double(P);
-  if (n > 0 && counting) {
-    cudaMemsetAsync(sb.longcount, 0, sizeof(int), s);
-    const int eb = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  {
+    const int ntiles = int((P + 1 + kScanTile - 1) / kScanTile);
+    launch_pdl(k_scan, std::min(ntiles, 148 * 4), kScanThreads, 0, s, static_cast<const int*>(g.C), sb.start,
+               P + 1, ntiles, sb.scan_state, next_scan_epoch());
+    ++launches;
+  }
+  if (n > 0 && dense) {
+    const int ntiles = int((n + kMsdTile - 1) / kMsdTile);
+    const int64_t m = int64_t(R) * ntiles;
+    int* tab = sb.msd_tab;
+    int* off = sb.msd_tab + m;
+    const int gb = std::min(ntiles, ev_blocks / 2);
+    launch_pdl(k_rowhist, gb, kMsdThreads, size_t(R) * 4, s, static_cast<const int32_t*>(sb.pix), n, W, R, ntiles,
+               tab);
+    const int mt = int((m + kScanTile - 1) / kScanTile);
+    launch_pdl(k_scan, std::min(mt, 148 * 4), kScanThreads, 0, s, static_cast<const int*>(tab), off, m, mt,
+               sb.msd_state, next_scan_epoch());
+    const size_t rs_smem = size_t(kMsdWarps) * R * 4;
+    cudaFuncSetAttribute(k_rowscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(size_t(kMsdWarps) * kMsdMaxRows * 4));
+    launch_pdl(k_rowscatter, gb, kMsdThreads, rs_smem, s, static_cast<const int32_t*>(sb.pix),
+               static_cast<const uint64_t*>(sb.val), n, W, R, ntiles, static_cast<const int*>(off), sb.bkt, sb.rank);
+    const size_t xs_smem = size_t(kXsortWarps) * W * 4;
+    cudaFuncSetAttribute(k_xsort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(size_t(kXsortWarps) * kXsortMaxW * 4));
+    launch_pdl(k_xsort, std::min(R, 148 * 2), kXsortThreads, xs_smem, s, static_cast<const uint64_t*>(sb.bkt),
+               static_cast<const int32_t*>(sb.rank), static_cast<const int*>(sb.start), W, R, sb.val_s, sb.pix_s);
+    launches += 4;
+  } else if (n > 0) {
+    const int eb = int(std::min<int64_t>((n + 255) / 256, ev_blocks));
     launch_pdl(k_scatter, eb, 256, 0, s, static_cast<const int32_t*>(sb.pix), static_cast<const uint64_t*>(sb.val),
-               static_cast<const int32_t*>(sb.rank), n, P, static_cast<const int*>(sb.start), sb.val_s, sb.pix_s);
-    // pixels per runsort block step: ~2000 expected slots (fits the stage), 16..256 pixels
+               static_cast<const int32_t*>(sb.rank), n, P, static_cast<const int*>(sb.start), sb.val_s);
+    // pixels per runsort block step (one thread per pixel, 16..128) and the
+    // stage sized for them (~1.3x the expected slots)
     const double mean_run = double(n) / double(std::max<int64_t>(P, 1));
-    int ppb = 256;
-    while (ppb > 16 && ppb * mean_run > 2000.0) ppb >>= 1;
+    int ppb = kRunsortThreads;
+    while (ppb > 16 && ppb * mean_run > 0.75 * kRunsortStage) ppb >>= 1;
+    const int cap = int(std::min<double>(kRunsortStage, std::max(1024.0, 1.3 * ppb * mean_run + 256.0)));
     const int pb = int(std::min<int64_t>((P + ppb - 1) / ppb, 148 * 16));
-    launch_pdl(k_runsort, pb, 256, 0, s, static_cast<const int*>(sb.start), P, ppb, sb.val_s, sb.longlist, sb.longcount);
+    cudaFuncSetAttribute(k_runsort, cudaFuncAttributeMaxDynamicSharedMemorySize, kRunsortStage * 8);
+    launch_pdl(k_runsort, pb, kRunsortThreads, size_t(cap) * 8, s, static_cast<const int*>(sb.start), P, ppb, cap,
+               sb.val_s, sb.pix_s, sb.longlist, sb.longcount);
     launch_pdl(k_longsort, 148, 512, 0, s, sb.start, sb.val_s, sb.longlist, sb.longcount);
     launches += 3;
-  } else if (n > 0) {
-    size_t sort_bytes = sb.sort_temp_bytes;
-    cub::DeviceRadixSort::SortPairs(sb.sort_temp, sort_bytes, sb.pix, sb.pix_s, sb.val, sb.val_s, int(n), 0,
-                                    key_bits(P), s);
-    launches += 2 + (key_bits(P) + 7) / 8;   // CUB onesweep: histogram, exclusive sum, one pass per 8-bit digit
   }
   return launches;
 }

@@ -93,6 +93,7 @@ struct vkm_handle {
   float* b1 = nullptr;
   float* w2 = nullptr;
   float* b2 = nullptr;
+  double* w64 = nullptr;  // float64 head W1ᵀ | b1 | W2 | b2 (vkm_set_weights_f64), or null
   void* w1_f16_hi = nullptr;
   void* w1_f16_lo = nullptr;
   void* w1_bf16 = nullptr;
@@ -133,7 +134,7 @@ struct vkm_handle {
   cudaEvent_t dl_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // download pieces
   size_t hpack_cap[2] = {0, 0};
   vkm_host::HostPool* pool = nullptr;
-  uint8_t* sel_temp = nullptr;   // vkm_select_rows: count + CUB scratch
+  uint8_t* sel_temp = nullptr;   // vkm_select_rows: count + look-back tile states
   size_t sel_temp_cap = 0;
   // timing
   bool profiling = false;
@@ -168,22 +169,27 @@ void rec(vkm_handle* h, int i, cudaStream_t s) {
 
 int ensure_sort(vkm_handle* h, int64_t n, int64_t Pv) {
   const size_t cap = size_t(std::max<int64_t>(n, 1));
-  const size_t temp = vkm::sort_pairs_temp_bytes(int64_t(cap), Pv);
-  if (h->sort_cap >= cap && h->sb.sort_temp_bytes >= temp) return VKM_OK;
-  void* arrs[] = {h->sb.pix, h->sb.val, h->sb.val_s, h->sb.pix_s, h->sb.sort_temp, h->sb.rank};
+  (void)Pv;
+  if (h->sort_cap >= cap) return VKM_OK;
+  void* arrs[] = {h->sb.pix, h->sb.val, h->sb.val_s, h->sb.pix_s, h->sb.rank, h->sb.bkt, h->sb.msd_tab,
+                  h->sb.msd_state};
   for (void* p : arrs)
     if (p) cudaFree(p);
   h->sb.pix = nullptr; h->sb.val = nullptr; h->sb.val_s = nullptr; h->sb.pix_s = nullptr; h->sb.rank = nullptr;
-  h->sb.sort_temp = nullptr;
+  h->sb.bkt = nullptr; h->sb.msd_tab = nullptr; h->sb.msd_state = nullptr;
   h->sort_cap = 0;
-  h->sb.sort_temp_bytes = 0;
   VKM_CK(cudaMalloc(&h->sb.pix, 4 * cap));
   VKM_CK(cudaMalloc(&h->sb.rank, 4 * cap));
   VKM_CK(cudaMalloc(&h->sb.val, 8 * cap));
   VKM_CK(cudaMalloc(&h->sb.val_s, 8 * cap));
   VKM_CK(cudaMalloc(&h->sb.pix_s, 4 * cap));
-  VKM_CK(cudaMalloc(&h->sb.sort_temp, std::max<size_t>(temp, 16)));
-  h->sb.sort_temp_bytes = temp;
+  VKM_CK(cudaMalloc(&h->sb.bkt, 8 * cap));
+  {
+    const size_t tw = vkm::msd_tab_words(int64_t(cap)), sw = vkm::scan_state_words(int64_t(tw));
+    VKM_CK(cudaMalloc(&h->sb.msd_tab, 2 * sizeof(int) * tw));
+    VKM_CK(cudaMalloc(&h->sb.msd_state, sizeof(unsigned long long) * sw));
+    VKM_CK(cudaMemset(h->sb.msd_state, 0, sizeof(unsigned long long) * sw));   // epoch 0: never published
+  }
   h->sort_cap = cap;
   return VKM_OK;
 }
@@ -192,12 +198,12 @@ int ensure_sort(vkm_handle* h, int64_t n, int64_t Pv) {
 // counts, pooled counts, run starts and the scan scratch.
 int ensure_grid(vkm_handle* h, int64_t Pv) {
   if (h->grid_cap >= Pv) return VKM_OK;
-  void* arrs[] = {h->G, h->Q, h->C, h->NQ, h->sb.start, h->sb.temp, h->sb.longlist, h->sb.longcount};
+  void* arrs[] = {h->G, h->Q, h->C, h->NQ, h->sb.start, h->sb.scan_state, h->sb.longlist, h->sb.longcount};
   for (void* p : arrs)
     if (p) cudaFree(p);
   h->G = h->Q = nullptr;
   h->C = h->NQ = h->sb.start = h->sb.longlist = h->sb.longcount = nullptr;
-  h->sb.temp = nullptr;
+  h->sb.scan_state = nullptr;
   h->grid_cap = 0;
   VKM_CK(cudaMalloc(&h->G, sizeof(float2) * 8 * h->planes * Pv));
   VKM_CK(cudaMalloc(&h->Q, sizeof(float2) * 8 * h->planes * Pv));
@@ -206,8 +212,11 @@ int ensure_grid(vkm_handle* h, int64_t Pv) {
   VKM_CK(cudaMalloc(&h->sb.start, sizeof(int) * (Pv + 1)));
   VKM_CK(cudaMalloc(&h->sb.longlist, sizeof(int) * Pv));
   VKM_CK(cudaMalloc(&h->sb.longcount, sizeof(int)));
-  h->sb.temp_bytes = vkm::sort_scan_temp_bytes(Pv);
-  VKM_CK(cudaMalloc(&h->sb.temp, std::max<size_t>(h->sb.temp_bytes, 16)));
+  {
+    const size_t words = vkm::scan_state_words(Pv);
+    VKM_CK(cudaMalloc(&h->sb.scan_state, sizeof(unsigned long long) * words));
+    VKM_CK(cudaMemset(h->sb.scan_state, 0, sizeof(unsigned long long) * words));   // epoch 0: never published
+  }
   h->grid_cap = Pv;
   return VKM_OK;
 }
@@ -708,10 +717,10 @@ void vkm_destroy(vkm_handle* h) {
   if (!h) return;
   DeviceGuard dg(h->p.device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->myp, h->xyz64, h->t64, h->mx64, h->my64, h->g64a, h->g64b, h->out64, h->win_ev, h->win_aux, h->w1p, h->b1, h->w2, h->b2, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
+  void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->myp, h->xyz64, h->t64, h->mx64, h->my64, h->g64a, h->g64b, h->out64, h->win_ev, h->win_aux, h->w1p, h->b1, h->w2, h->b2, h->w64, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
                   h->G, h->C, h->Q, h->NQ, h->feats, h->cnt_scratch, h->ev_stage, h->out_stage, h->cnt_stage,
-                  h->sb.pix, h->sb.val, h->sb.start, h->sb.val_s, h->sb.pix_s, h->sb.temp, h->sb.sort_temp,
-                  h->sb.rank, h->sb.longlist, h->sb.longcount};
+                  h->sb.pix, h->sb.val, h->sb.start, h->sb.val_s, h->sb.pix_s, h->sb.scan_state,
+                  h->sb.rank, h->sb.longlist, h->sb.longcount, h->sb.bkt, h->sb.msd_tab, h->sb.msd_state};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->evt)
@@ -745,6 +754,30 @@ int vkm_set_mlp_mode(vkm_handle* h, int32_t mode) {
   if ((mode == VKM_MLP_F16X3 || mode == VKM_MLP_BF16) && !h->tc_ok)
     return fail(VKM_EUNSUPPORTED, "tensor-core MLP modes need embed_dim == 64 and hidden == 128");
   h->mode = mode;
+  return VKM_OK;
+}
+
+int vkm_set_weights_f64(vkm_handle* h, const double* w1, const double* b1, const double* w2, const double* b2) {
+  if (int rc = check_handle(h)) return rc;
+  if (h->hidden <= 0) return fail(VKM_EINVAL, "vkm_set_weights_f64: the handle has no head (hidden == 0)");
+  if (!w1 || !b1 || !w2 || !b2) return fail(VKM_EINVAL, "vkm_set_weights_f64: null argument");
+  const int hid = h->hidden, F = 2 * h->D;
+  std::vector<double> buf(size_t(F) * hid + hid + 2 * hid + 2);
+  for (int r = 0; r < hid; ++r)
+    for (int j = 0; j < F; ++j) buf[size_t(j) * hid + r] = w1[size_t(r) * F + j];   // W1ᵀ [F][hidden]
+  std::memcpy(buf.data() + size_t(F) * hid, b1, sizeof(double) * hid);
+  std::memcpy(buf.data() + size_t(F) * hid + hid, w2, sizeof(double) * 2 * hid);
+  std::memcpy(buf.data() + size_t(F) * hid + 3 * hid, b2, sizeof(double) * 2);
+  for (double v : buf)
+    if (!std::isfinite(v)) return fail(VKM_EINVAL, "weights must be finite");
+  DeviceGuard dg(h->p.device);
+  if (!h->w64 && cudaMalloc(&h->w64, sizeof(double) * buf.size()) != cudaSuccess) {
+    h->w64 = nullptr;
+    cudaGetLastError();
+    return fail(VKM_EOOM, "vkm_set_weights_f64: device allocation failed");
+  }
+  if (cudaMemcpy(h->w64, buf.data(), sizeof(double) * buf.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail(VKM_ECUDA, std::string("vkm_set_weights_f64: ") + cudaGetErrorString(cudaGetLastError()));
   return VKM_OK;
 }
 
@@ -1130,12 +1163,15 @@ int vkm_select_rows(vkm_handle* h, const double* ev, int64_t n, int32_t y_lo, in
   if (n == 0) return VKM_OK;
   if (!ev || !out_ev || !out_index || !out_owned) return fail(VKM_EINVAL, "null device buffer");
   DeviceGuard dg(h->p.device);
-  const size_t temp_bytes = vkm::select_rows_temp_bytes(n);
-  int rc = grow(&h->sel_temp, &h->sel_temp_cap, std::max<size_t>(temp_bytes, 16) + 64);
-  if (rc) return rc;
-  int64_t* count_dev = reinterpret_cast<int64_t*>(h->sel_temp);   // first 8 bytes; CUB scratch after 64
-  vkm::launch_select_rows(ev, n, y_lo, y_hi, own_lo, own_hi, h->sel_temp + 64, temp_bytes, out_index, count_dev,
-                          out_ev, out_owned, h->stream);
+  const size_t need = 64 + 8 * vkm::select_rows_state_words(n);
+  if (h->sel_temp_cap < need) {
+    int rc = grow(&h->sel_temp, &h->sel_temp_cap, need);
+    if (rc) return rc;
+    VKM_CK(cudaMemset(h->sel_temp, 0, need));   // tile states: epoch 0 = never published
+  }
+  int64_t* count_dev = reinterpret_cast<int64_t*>(h->sel_temp);   // first 8 bytes; tile states after 64
+  vkm::launch_select_rows(ev, n, y_lo, y_hi, own_lo, own_hi, reinterpret_cast<unsigned long long*>(h->sel_temp + 64),
+                          out_index, count_dev, out_ev, out_owned, h->stream);
   VKM_CK(cudaGetLastError());
   VKM_CK(cudaMemcpyAsync(count_host, count_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
   VKM_CK(cudaStreamSynchronize(h->stream));
@@ -1164,6 +1200,24 @@ int vkm_grid(vkm_handle* h, const double* ev, int64_t n, double t_start, int32_t
   if (rc) return rc;
   vkm::launch_grid_to_ref(pooled ? h->Q : h->G, pooled ? h->NQ : h->C, h->p.width, h->p.height, h->D, h->D8,
                           pooled ? nullptr : h->mx, pooled ? nullptr : h->my, pooled != 0, grid, counts, s);
+  VKM_CK(cudaGetLastError());
+  return VKM_OK;
+}
+
+int vkm_pixel_order(vkm_handle* h, const double* ev, int64_t n, double t_start, int32_t* start, int32_t* order,
+                    void* stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (n < 0) return fail(VKM_EINVAL, "n must be non-negative");
+  if (!start || (n > 0 && (!ev || !order))) return fail(VKM_EINVAL, "null device buffer");
+  DeviceGuard dg(h->p.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc = ensure_grid(h, h->P);
+  if (!rc) rc = ensure_sort(h, n, h->P);
+  if (rc) return rc;
+  vkm::launch_sort_events(ev, nullptr, one_slice(n, t_start), h->p.delta_t, h->p.width, h->p.height, bufs(h), h->sb,
+                          nullptr, nullptr, s);
+  VKM_CK(cudaMemcpyAsync(start, h->sb.start, sizeof(int32_t) * (h->P + 1), cudaMemcpyDeviceToDevice, s));
+  if (n > 0) vkm::launch_slot_events(h->sb.val_s, h->sb.start + h->P, n, order, s);
   VKM_CK(cudaGetLastError());
   return VKM_OK;
 }
@@ -1201,7 +1255,7 @@ int run_f64(vkm_handle* h, const double* ev, int64_t n, double t_start, double* 
                        h->g64a, h->g64b, s);
   if (predict)
     vkm::launch_predict64(t, ev, n, t0, h->p.delta_t, W, H, h->D, h->D8, h->g64a, h->NQ,
-                          vkm::MlpDev{h->w1p, h->b1, h->w2, h->b2, h->hidden}, out, counts, h->num_sms, s);
+                          vkm::MlpDev{h->w1p, h->b1, h->w2, h->b2, h->hidden, h->w64}, out, counts, h->num_sms, s);
   else
     vkm::launch_features64(t, ev, n, t0, h->p.delta_t, W, H, h->D, h->D8, h->g64a, h->NQ, out, counts, s);
   VKM_CK(cudaGetLastError());
@@ -1532,19 +1586,44 @@ int vkm_predict_windows(vkm_handle* h, const double* ev, int64_t n, const double
   if (total == 0) return VKM_OK;
   if (!ev || !flows) return fail(VKM_EINVAL, "null device buffer");
   DeviceGuard dg(h->p.device);
-  int rc = grow(&h->win_ev, &h->win_ev_cap, size_t(total) * 3);
-  if (!rc) rc = grow(&h->win_aux, &h->win_aux_cap, 3 * size_t(n_windows) + 1);
-  if (rc) return rc;
+  // Windows are gathered and predicted in chunks of at most kWinChunk events
+  // (one window may exceed it alone), so the gather buffer stays bounded
+  // however long or overlapping the stream is.
+  const int64_t kWinChunk = [] {   // read per call (tests lower it)
+    const char* e = std::getenv("VKM_WINDOW_CHUNK_EVENTS");
+    return e && std::atoll(e) > 0 ? int64_t(std::atoll(e)) : int64_t(32) << 20;
+  }();
   cudaStream_t sm = static_cast<cudaStream_t>(stream);
-  int64_t* off_dev = h->win_aux;
-  int64_t* lo_dev = h->win_aux + n_windows + 1;
-  VKM_CK(cudaMemcpyAsync(off_dev, off.data(), sizeof(int64_t) * (n_windows + 1), cudaMemcpyHostToDevice, sm));
-  VKM_CK(cudaMemcpyAsync(lo_dev, lo.data(), sizeof(int64_t) * n_windows, cudaMemcpyHostToDevice, sm));
-  vkm::launch_gather_windows(ev, off_dev, lo_dev, n_windows, total, h->win_ev, sm);
-  VKM_CK(cudaGetLastError());
-  rc = vkm_predict_batch(h, h->win_ev, off.data(), n_windows, starts_host, flows, counts, stream);
-  // the host arrays above are read by the async copies: finish them before returning
-  VKM_CK(cudaStreamSynchronize(sm));
+  int rc = grow(&h->win_aux, &h->win_aux_cap, 3 * size_t(n_windows) + 1);
+  if (rc) return rc;
+  for (int32_t w0 = 0; w0 < n_windows && !rc;) {
+    int32_t w1 = w0 + 1;
+    while (w1 < n_windows && off[w1 + 1] - off[w0] <= kWinChunk) ++w1;
+    const int32_t nw = w1 - w0;
+    const int64_t base = off[w0], part = off[w1] - base;
+    std::vector<int64_t> coff(size_t(nw) + 1);
+    for (int32_t w = 0; w <= nw; ++w) coff[w] = off[w0 + w] - base;
+    if (part > 0) {
+      rc = grow(&h->win_ev, &h->win_ev_cap, size_t(part) * 3);
+      if (rc) break;
+      int64_t* off_dev = h->win_aux;
+      int64_t* lo_dev = h->win_aux + nw + 1;
+      VKM_CK(cudaMemcpyAsync(off_dev, coff.data(), sizeof(int64_t) * (nw + 1), cudaMemcpyHostToDevice, sm));
+      VKM_CK(cudaMemcpyAsync(lo_dev, lo.data() + w0, sizeof(int64_t) * nw, cudaMemcpyHostToDevice, sm));
+      vkm::launch_gather_windows(ev, off_dev, lo_dev, nw, part, h->win_ev, sm);
+      VKM_CK(cudaGetLastError());
+      rc = vkm_predict_batch(h, h->win_ev, coff.data(), nw, starts_host + w0, flows + 2 * base,
+                             counts ? counts + base : nullptr, stream);
+    }
+    // the host arrays above are read by the async copies: finish them before reuse
+    VKM_CK(cudaStreamSynchronize(sm));
+    w0 = w1;
+  }
+  if (h->win_ev_cap > size_t(3) * kWinChunk) {   // a single huge window grew it: give it back
+    cudaFree(h->win_ev);
+    h->win_ev = nullptr;
+    h->win_ev_cap = 0;
+  }
   return rc;
 }
 

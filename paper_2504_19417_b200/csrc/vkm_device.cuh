@@ -250,6 +250,44 @@ __device__ __forceinline__ double ld_t0(const double* ev, double t0) {
 
 namespace vkm {
 // Programmatic dependent launch (PDL).  A kernel launched with
+// Decoupled look-back for single-pass scans (k_scan, k_select_strip): tile t
+// publishes its aggregate, reads its predecessors' published words 32 at a
+// time (aggregates until the nearest inclusive prefix) and publishes its own
+// inclusive prefix.  A word packs (epoch:30, flag:2, value:32); words of other
+// launches carry another epoch and read as unpublished, so the state array is
+// never reset.  Call with one full warp; every lane returns the exclusive
+// prefix.  Tiles must be taken in increasing order by co-resident blocks.
+__device__ __forceinline__ uint64_t lb_word(uint32_t epoch, uint64_t flag, uint32_t value) {
+  return (uint64_t(epoch & 0x3fffffffu) << 34) | (flag << 32) | value;
+}
+__device__ __forceinline__ uint32_t lookback_publish(unsigned long long* state, int t, uint32_t total,
+                                                     uint32_t epoch) {
+  volatile unsigned long long* vs = state;
+  const int lane = threadIdx.x & 31;
+  const uint32_t ep = epoch & 0x3fffffffu;
+  if (t == 0) {
+    if (lane == 0) vs[0] = lb_word(ep, 2, total);
+    return 0;
+  }
+  if (lane == 0) vs[t] = lb_word(ep, 1, total);
+  uint32_t excl = 0;
+  for (int p = t - 1;; p -= 32) {
+    const int q = p - lane;
+    uint64_t w = 0;
+    if (q >= 0)
+      do w = vs[q]; while (uint32_t(w >> 34) != ep || ((w >> 32) & 3) == 0);
+    const unsigned incl = __ballot_sync(0xffffffffu, q >= 0 && ((w >> 32) & 3) == 2);
+    const int stop = incl ? __ffs(incl) - 1 : 31;   // nearest predecessor carrying a prefix
+    uint32_t add = (lane <= stop && q >= 0) ? uint32_t(w) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+    excl += add;
+    if (incl || p - 32 < 0) break;
+  }
+  if (lane == 0) vs[t] = lb_word(ep, 2, excl + total);
+  return excl;
+}
+
 // launch_pdl() may be scheduled while its predecessor drains: each kernel
 // executes pdl_wait() before touching anything its predecessor writes and
 // pdl_trigger() when its own work is done, so the next grid's launch and

@@ -47,14 +47,17 @@ struct SortBufs {
   int* start;        // [P+1] exclusive scan of the counts (start[P] = valid events)
   uint64_t* val_s;   // [n]  slot -> slot_pack(event, a), stable pixel-major order
   int32_t* pix_s;    // [n]  slot -> pixel
-  void* temp;        // CUB scan scratch
-  size_t temp_bytes;
-  void* sort_temp;   // CUB radix-sort scratch (grown with n)
-  size_t sort_temp_bytes;
+  unsigned long long* scan_state;   // [scan_state_words(P)] k_scan tile states (zeroed once)
   int32_t* rank;     // [n]   event's arrival rank inside its pixel (k_prep's histogram atomic)
   int* longlist;     // [P]   pixels whose run is longer than one warp sort
-  int* longcount;    // [1]
+  int* longcount;    // [1]   long-run count
+  // dense slices (row-bucket path, k_sort.cu): row buckets of (event, a) and x,
+  // the per-(row, tile) count table + its scan, and the table scan's tile states
+  uint64_t* bkt;                     // [n]
+  int* msd_tab;                      // [2 * msd_tab_words(n)]
+  unsigned long long* msd_state;     // [scan_state_words(msd_tab_words(n))]
 };
+size_t msd_tab_words(int64_t n);     // per-(row, event tile) counters for n events, rows <= kMsdMaxRows
 
 // Slices processed by one launch sequence (batched fused path): slice b owns
 // events [off[b], off[b+1]) and the pixel block [b·P, (b+1)·P) of a virtual
@@ -73,9 +76,12 @@ struct MlpDev {
   const float* w2;   // [2][hidden]
   const float* b2;   // [2]
   int hidden;
+  // float64 head (precision="f64" with float64 weights, vkm_set_weights_f64):
+  // W1ᵀ [2D][hidden] | b1 [hidden] | W2 [2][hidden] | b2 [2] in one buffer, or null
+  const double* w64 = nullptr;
 };
 
-// K1 (sorted): prep + scan + stable radix sort of (pixel, slot_pack) pairs.
+// K1 (sorted): prep + scan + counting scatter + run ordering of (pixel, slot_pack) pairs.
 // Returns the number of kernel launches.  C must hold P+1 ints.
 // Keys live in [0, nb·W·H]; nb·W·H + 1 counters in g.C.  Events are either
 // the reference's (n, 3) f64 rows (ev) or host-packed 8-byte records
@@ -95,8 +101,10 @@ void launch_reduce_raw(const DevTables& tb, int W, int H, int D8, const GridBufs
 bool reduce_x_supported(int D8, int dx);
 void launch_reduce_x(const DevTables& tb, int W, int H, int nb, int dx, const SortBufs& sb, float2* R,
                      int num_sms, cudaStream_t s);
-size_t sort_scan_temp_bytes(int64_t P);
-size_t sort_pairs_temp_bytes(int64_t n, int64_t P);
+size_t scan_state_words(int64_t P);   // k_scan tile-state words for P pixels
+uint32_t next_scan_epoch();           // epoch tag of the next single-pass scan launch
+// order[slot] = event of each slot of val_s (-1 from *valid on)
+void launch_slot_events(const uint64_t* val_s, const int* valid, int64_t n, int32_t* order, cudaStream_t s);
 // K2 (split): box sum of the pre-modulated grid M (y-pass M -> R, x-pass +
 // demodulation R -> Qout); Qout may alias M (k_pool.cu).
 void launch_pool_split(const DevTables& tb, int W, int H, int D8, int dx, int dy, float2* M, float2* R,
@@ -177,9 +185,13 @@ void launch_gather_mlp_tc(int64_t n, const DevTables& tb, int W, int H, const Gr
 // Spatial split (k_split.cu): stable selection of the events of rows
 // [y_lo, y_hi) with rows rebased by -y_lo, their global indices and an owned
 // flag for rows [own_lo, own_hi); count_dev receives the number selected.
-size_t select_rows_temp_bytes(int64_t n);
-void launch_select_rows(const double* ev, int64_t n, int y_lo, int y_hi, int own_lo, int own_hi, void* temp,
-                        size_t temp_bytes, int64_t* sel, int64_t* count_dev, double* out, uint8_t* owned,
+// Stable selection of the events with y in [y_lo, y_hi) (single pass with
+// decoupled look-back; state = select_rows_state_words(n) words, zeroed once):
+// sel = their indices, out = their rows with y - y_lo, owned = y in [own_lo,
+// own_hi); *count_dev = how many.
+size_t select_rows_state_words(int64_t n);
+void launch_select_rows(const double* ev, int64_t n, int y_lo, int y_hi, int own_lo, int own_hi,
+                        unsigned long long* state, int64_t* sel, int64_t* count_dev, double* out, uint8_t* owned,
                         cudaStream_t s);
 // dst[index[i]] = src[i] (rows of row_floats floats) where mask[i] != 0 (mask may be null).
 void launch_scatter_rows(const float* src, const int64_t* index, const uint8_t* mask, int64_t m, int row_floats,

@@ -7,9 +7,11 @@ allocator and stream provider here, the work is the C-ABI's kernels.
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import math
-from typing import Optional, Sequence
+import threading
+from typing import Callable, Optional, Sequence
 
 import numpy as np
 
@@ -25,6 +27,41 @@ def _torch():
     return torch
 
 
+class EngineCache:
+    """Per-thread, size-bounded cache of `FlowEngine`s keyed by configuration.
+
+    A handle is bound to one device and stream and is not re-entrant, so each
+    host thread gets its own handles (distinct handles may run concurrently:
+    the ctypes calls release the GIL, as the reference bindings promise,
+    pkg/bindings/src/evflow_bindings/__init__.py:10-11).  At most `size`
+    handles live per thread; the least recently used one is closed, which
+    returns its device scratch and host threads."""
+
+    def __init__(self, size: int = 4):
+        self.size = int(size)
+        self._tls = threading.local()
+
+    def get(self, key, factory: Callable[[], "FlowEngine"]) -> "FlowEngine":
+        lru = getattr(self._tls, "lru", None)
+        if lru is None:
+            lru = self._tls.lru = collections.OrderedDict()
+        eng = lru.get(key)
+        if eng is not None:
+            lru.move_to_end(key)
+            return eng
+        eng = lru[key] = factory()
+        while len(lru) > self.size:
+            _, old = lru.popitem(last=False)
+            old.close()
+        return eng
+
+    def clear(self) -> None:
+        lru = getattr(self._tls, "lru", None)
+        while lru:
+            _, old = lru.popitem()
+            old.close()
+
+
 class FlowEngine:
     """Device-resident encoder (+ optional flow head) for one sensor geometry.
 
@@ -37,6 +74,9 @@ class FlowEngine:
                  mlp_mode: str = "auto"):
         lib = _lib.load()
         self._lib = lib
+        # one handle is not re-entrant: calls from several host
+        # threads on the same engine serialise instead of racing on its scratch
+        self._lock = threading.RLock()
         self.width, self.height = int(width), int(height)
         self.delta_x, self.delta_y = int(delta_x), int(delta_y)
         self.delta_t = float(delta_t)
@@ -59,6 +99,11 @@ class FlowEngine:
         h = C.c_void_p()
         _lib.check(lib.vkm_create(C.byref(h), C.byref(p), _dptr(T), _dptr(X), _dptr(Y), *wp))
         self._h = h
+        if weights is not None and np.asarray(weights.w1).dtype == np.float64:
+            # the reference runs a float64 head for float64 weights (flow.py:98-106);
+            # the f64 path keeps them unrounded (the f32 path uses the f32 copy)
+            w64 = [np.ascontiguousarray(a, dtype=np.float64) for a in (weights.w1, weights.b1, weights.w2, weights.b2)]
+            _lib.check(lib.vkm_set_weights_f64(h, *[_dptr(a) for a in w64]))
 
     # -- lifecycle ---------------------------------------------------------
     def close(self) -> None:
@@ -74,16 +119,16 @@ class FlowEngine:
             pass
 
     def set_mlp_mode(self, mode: str) -> None:
-        _lib.check(self._lib.vkm_set_mlp_mode(self._h, _lib.MLP_MODES[mode]))
+        with self._lock: _lib.check(self._lib.vkm_set_mlp_mode(self._h, _lib.MLP_MODES[mode]))
 
     def set_profiling(self, enable: bool) -> None:
-        _lib.check(self._lib.vkm_set_profiling(self._h, int(bool(enable))))
+        with self._lock: _lib.check(self._lib.vkm_set_profiling(self._h, int(bool(enable))))
 
     def last_timings(self):
         """(ms[accumulate, pool, gather+mlp, total], kernel launches) of the last call."""
         ms = (C.c_float * 4)()
         n = C.c_int32()
-        _lib.check(self._lib.vkm_last_timings(self._h, ms, C.byref(n)))
+        with self._lock: _lib.check(self._lib.vkm_last_timings(self._h, ms, C.byref(n)))
         return list(ms), int(n.value)
 
     # -- host-buffer API ---------------------------------------------------
@@ -93,7 +138,7 @@ class FlowEngine:
         flows = np.empty((n, 2), dtype=np.float32)
         counts = np.empty(n, dtype=np.int32) if return_counts else None
         if n:
-            _lib.check(self._lib.vkm_predict_host(self._h, ev.ctypes.data, n, float(t_start),
+            with self._lock: _lib.check(self._lib.vkm_predict_host(self._h, ev.ctypes.data, n, float(t_start),
                                                   flows.ctypes.data,
                                                   counts.ctypes.data if counts is not None else None))
         return (flows, counts) if return_counts else flows
@@ -105,7 +150,7 @@ class FlowEngine:
         flows = np.empty((n, 2), dtype=np.float64)
         counts = np.empty(n, dtype=np.int32) if return_counts else None
         if n:
-            _lib.check(self._lib.vkm_predict_host_wide(self._h, ev.ctypes.data, n, float(t_start), flows.ctypes.data,
+            with self._lock: _lib.check(self._lib.vkm_predict_host_wide(self._h, ev.ctypes.data, n, float(t_start), flows.ctypes.data,
                                                        counts.ctypes.data if counts is not None else None))
         return (flows, counts) if return_counts else flows
 
@@ -125,7 +170,7 @@ class FlowEngine:
         if t_starts is not None:
             ts_arr = np.ascontiguousarray(t_starts, dtype=np.float64)
             ts = _dptr(ts_arr)
-        _lib.check(self._lib.vkm_predict_batch_host(
+        with self._lock: _lib.check(self._lib.vkm_predict_batch_host(
             self._h, ev.ctypes.data, off.ctypes.data_as(C.POINTER(C.c_int64)), ns, ts, flows.ctypes.data,
             counts.ctypes.data if counts is not None else None))
         return (flows, counts) if return_counts else flows
@@ -136,7 +181,7 @@ class FlowEngine:
         feats = np.empty((n, 2 * self.embed_dim), dtype=np.float32)
         counts = np.empty(n, dtype=np.int32) if return_counts else None
         if n:
-            _lib.check(self._lib.vkm_encode_host(self._h, ev.ctypes.data, n, float(t_start),
+            with self._lock: _lib.check(self._lib.vkm_encode_host(self._h, ev.ctypes.data, n, float(t_start),
                                                  feats.ctypes.data,
                                                  counts.ctypes.data if counts is not None else None))
         return (feats, counts) if return_counts else feats
@@ -148,7 +193,7 @@ class FlowEngine:
         flows = np.empty((n, 2), dtype=np.float64)
         counts = np.empty(n, dtype=np.int32) if return_counts else None
         if n:
-            _lib.check(self._lib.vkm_predict_f64_host(self._h, ev.ctypes.data, n, float(t_start), flows.ctypes.data,
+            with self._lock: _lib.check(self._lib.vkm_predict_f64_host(self._h, ev.ctypes.data, n, float(t_start), flows.ctypes.data,
                                                       counts.ctypes.data if counts is not None else None))
         return (flows, counts) if return_counts else flows
 
@@ -158,7 +203,7 @@ class FlowEngine:
         feats = np.empty((n, 2 * self.embed_dim), dtype=np.float64)
         counts = np.empty(n, dtype=np.int32) if return_counts else None
         if n:
-            _lib.check(self._lib.vkm_encode_f64_host(self._h, ev.ctypes.data, n, float(t_start), feats.ctypes.data,
+            with self._lock: _lib.check(self._lib.vkm_encode_f64_host(self._h, ev.ctypes.data, n, float(t_start), feats.ctypes.data,
                                                      counts.ctypes.data if counts is not None else None))
         return (feats, counts) if return_counts else feats
 
@@ -168,7 +213,7 @@ class FlowEngine:
         n = events.shape[0]
         if flows is None:
             flows = torch.empty((n, 2), dtype=torch.float64, device=events.device)
-        _lib.check(self._lib.vkm_predict_f64(self._h, C.c_void_p(events.data_ptr()), n, float(t_start),
+        with self._lock: _lib.check(self._lib.vkm_predict_f64(self._h, C.c_void_p(events.data_ptr()), n, float(t_start),
                                              C.c_void_p(flows.data_ptr()),
                                              C.c_void_p(counts.data_ptr()) if counts is not None else None,
                                              self._stream(stream)))
@@ -183,7 +228,7 @@ class FlowEngine:
         emb = np.empty((len(q), self.embed_dim), dtype=np.complex128)
         counts = np.empty(len(q), dtype=np.int32)
         if len(q):
-            _lib.check(self._lib.vkm_direct_encode_host(self._h, ev.ctypes.data, len(ev), q.ctypes.data, len(q),
+            with self._lock: _lib.check(self._lib.vkm_direct_encode_host(self._h, ev.ctypes.data, len(ev), q.ctypes.data, len(q),
                                                         emb.ctypes.data, counts.ctypes.data))
         return (emb, counts) if return_counts else emb
 
@@ -205,7 +250,7 @@ class FlowEngine:
         n = events.shape[0]
         if flows is None:
             flows = torch.empty((n, 2), dtype=torch.float32, device=events.device)
-        _lib.check(self._lib.vkm_predict(self._h, C.c_void_p(events.data_ptr()), n, float(t_start),
+        with self._lock: _lib.check(self._lib.vkm_predict(self._h, C.c_void_p(events.data_ptr()), n, float(t_start),
                                          C.c_void_p(flows.data_ptr()),
                                          C.c_void_p(counts.data_ptr()) if counts is not None else None,
                                          self._stream(stream)))
@@ -217,7 +262,7 @@ class FlowEngine:
         n = events.shape[0]
         if feats is None:
             feats = torch.empty((n, 2 * self.embed_dim), dtype=torch.float32, device=events.device)
-        _lib.check(self._lib.vkm_encode(self._h, C.c_void_p(events.data_ptr()), n, float(t_start),
+        with self._lock: _lib.check(self._lib.vkm_encode(self._h, C.c_void_p(events.data_ptr()), n, float(t_start),
                                         C.c_void_p(feats.data_ptr()),
                                         C.c_void_p(counts.data_ptr()) if counts is not None else None,
                                         self._stream(stream)))
@@ -235,11 +280,24 @@ class FlowEngine:
         if t_starts is not None:
             ts_arr = np.ascontiguousarray(t_starts, dtype=np.float64)
             ts = _dptr(ts_arr)
-        _lib.check(self._lib.vkm_predict_batch(
+        with self._lock: _lib.check(self._lib.vkm_predict_batch(
             self._h, C.c_void_p(events.data_ptr()), off.ctypes.data_as(C.POINTER(C.c_int64)), ns, ts,
             C.c_void_p(flows.data_ptr()), C.c_void_p(counts.data_ptr()) if counts is not None else None,
             self._stream(stream)))
         return flows
+
+    def pixel_order_device(self, events, t_start: float = math.nan, stream=None):
+        """accumulate_grid's stable pixel-major order (encoder.py:255-259):
+        ((W*H + 1) int32 run starts, (n) int32 event per slot)."""
+        torch = _torch()
+        self._check_events(events)
+        n = events.shape[0]
+        start = torch.empty(self.width * self.height + 1, dtype=torch.int32, device=events.device)
+        order = torch.empty(max(n, 1), dtype=torch.int32, device=events.device)
+        with self._lock: _lib.check(self._lib.vkm_pixel_order(self._h, C.c_void_p(events.data_ptr()), n,
+                                                            float(t_start), C.c_void_p(start.data_ptr()),
+                                                            C.c_void_p(order.data_ptr()), self._stream(stream)))
+        return start, order[:n]
 
     def grid_device(self, events, t_start: float = math.nan, pooled: bool = False, stream=None):
         """Per-pixel grid in the reference PixelGrid layout: ((W, H, D) complex64, (W, H) int32)."""
@@ -248,7 +306,7 @@ class FlowEngine:
         W, H, D = self.width, self.height, self.embed_dim
         g = torch.empty((W, H, D, 2), dtype=torch.float32, device=events.device)
         c = torch.empty((W, H), dtype=torch.int32, device=events.device)
-        _lib.check(self._lib.vkm_grid(self._h, C.c_void_p(events.data_ptr()), events.shape[0], float(t_start),
+        with self._lock: _lib.check(self._lib.vkm_grid(self._h, C.c_void_p(events.data_ptr()), events.shape[0], float(t_start),
                                       int(bool(pooled)), C.c_void_p(g.data_ptr()), C.c_void_p(c.data_ptr()),
                                       self._stream(stream)))
         return torch.view_as_complex(g), c

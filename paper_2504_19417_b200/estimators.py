@@ -16,12 +16,13 @@ from sklearn.base import BaseEstimator, TransformerMixin
 from sklearn.exceptions import NotFittedError
 
 from ._staging import concat_rows, pinned, widen
-from .engine import FlowEngine, predict_multi_host
+from .engine import EngineCache, FlowEngine, predict_multi_host
 from .errors import DimensionMismatchError, EmptyNeighborhoodError
-from .validation import check_event_array, slice_from_array
+from .validation import block_from_array, check_events
 from .weights import MlpWeights, as_weights, generate_bases, load_weights
 
-_ENGINES = {}
+# LocalEventEncoder handles: per host thread, at most 4 live (EngineCache)
+_ENGINES = EngineCache()
 
 
 def _check_config(delta_t, delta_x, delta_y, embed_dim, sigma2, seeds, precision):
@@ -41,11 +42,7 @@ def _check_config(delta_t, delta_x, delta_y, embed_dim, sigma2, seeds, precision
 
 
 def _engine(key, factory) -> FlowEngine:
-    eng = _ENGINES.get(key)
-    if eng is None:
-        eng = factory()
-        _ENGINES[key] = eng
-    return eng
+    return _ENGINES.get(key, factory)
 
 
 class LocalEventEncoder(TransformerMixin, BaseEstimator):
@@ -68,9 +65,9 @@ class LocalEventEncoder(TransformerMixin, BaseEstimator):
 
     def fit(self, X=None, y=None):
         _check_config(self.delta_t, self.delta_x, self.delta_y, self.embed_dim, self.sigma2, self.seeds,
-                      "f32")
+                      self.precision)
         if X is not None:
-            check_event_array(X, self.width, self.height)
+            check_events(X, self.width, self.height)
         self.bases_ = generate_bases(self.embed_dim, self.sigma2, tuple(self.seeds))
         return self
 
@@ -79,7 +76,7 @@ class LocalEventEncoder(TransformerMixin, BaseEstimator):
             raise NotFittedError("call fit before transform")
         _check_config(self.delta_t, self.delta_x, self.delta_y, self.embed_dim, self.sigma2, self.seeds,
                       self.precision)
-        block = slice_from_array(X, self.width, self.height, 2.0 * self.delta_t)
+        block = block_from_array(X, self.width, self.height, 2.0 * self.delta_t)
         f64 = self.precision == "f64"   # complex128 grid, float64 features (encoder.py:37-38)
         if len(block) == 0:
             return np.empty((0, 2 * self.embed_dim), dtype=np.float64 if f64 else np.float32)
@@ -125,6 +122,15 @@ class NormalFlowRegressor(BaseEstimator):
         self.device = device
         self.mlp_mode = mlp_mode
 
+    def __getstate__(self):
+        """Picklable / deep-copyable after use, like the reference estimator:
+        the libveckm handles (`_engine_cache`, `_device_engines`) hold a CDLL
+        and device memory, so they are dropped and rebuilt on the next call."""
+        state = dict(super().__getstate__())
+        state.pop("_engine_cache", None)
+        state.pop("_device_engines", None)
+        return state
+
     def _resolve_pretrained(self) -> Optional[MlpWeights]:
         if self.weights is None:
             return None
@@ -148,7 +154,7 @@ class NormalFlowRegressor(BaseEstimator):
             raise ValueError("X and y must pair one flow array per slice")
         dataset = []
         for arr, flows in zip(slices, targets):
-            blk = slice_from_array(arr, self.width, self.height, 2.0 * self.delta_t)
+            blk = block_from_array(arr, self.width, self.height, 2.0 * self.delta_t)
             dataset.append((arr, check_flow_array(flows, len(blk))))
         tc = TrainConfig(hidden=self.hidden, epochs=self.epochs, batch_size=self.batch_size,
                          learning_rate=self.learning_rate, margin_weight=self.margin_weight, seed=self.random_state)
@@ -187,7 +193,7 @@ class NormalFlowRegressor(BaseEstimator):
         """(n, 2) float64 flows in pixels/s; rows in stable time-sorted order
         (input order for sorted input); NaN rows for empty neighbourhoods."""
         eng = self.engine()
-        block = slice_from_array(X, self.width, self.height, 2.0 * self.delta_t)
+        block = block_from_array(X, self.width, self.height, 2.0 * self.delta_t)
         if len(block) == 0:
             return np.full((0, 2), np.nan)
         if self.precision == "f64":   # f64 grid, features and head (encoder.py:37-38, flow.py:98-106)
@@ -223,7 +229,7 @@ class NormalFlowRegressor(BaseEstimator):
         eng = self.engine()
         if self.precision == "f64":   # one slice per call on the f64 path
             return [self.predict(X) for X in slices]
-        blocks = [slice_from_array(X, self.width, self.height, 2.0 * self.delta_t) for X in slices]
+        blocks = [block_from_array(X, self.width, self.height, 2.0 * self.delta_t) for X in slices]
         sizes = [len(b) for b in blocks]
         total = int(sum(sizes))
         if total == 0:

@@ -78,17 +78,49 @@ class EventStream:
 
 
 @dataclass
-class StreamSlice:
-    """One window of a stream: rows [lo, hi) of the time-sorted stream."""
+class EventSlice:
+    """Events of one window [t_start, t_start + window], sorted by t, with the
+    reference's construction checks (events.py:90-131: ulp-tolerant window
+    bounds, ascending times, geometry)."""
 
     t: np.ndarray
     x: np.ndarray
     y: np.ndarray
     t_start: float
     window: float
+    geometry: Optional[CameraGeometry] = None
     polarity: Optional[np.ndarray] = None
 
+    def __post_init__(self) -> None:
+        self.t = np.asarray(self.t, dtype=np.float64)
+        self.x = np.asarray(self.x, dtype=np.int32)
+        self.y = np.asarray(self.y, dtype=np.int32)
+        if self.polarity is not None:
+            self.polarity = np.asarray(self.polarity, dtype=np.int8)
+        if self.window <= 0:
+            raise ValueError("window must be positive")
+        n = len(self.t)
+        if len(self.x) != n or len(self.y) != n:
+            raise ValueError("t, x, y must have equal length")
+        if n:
+            upper = self.t_start + self.window
+            slack = 4.0 * np.spacing(max(abs(upper), self.window))   # rebasing rounds edge times
+            if self.t[0] < self.t_start - slack or self.t[-1] > upper + slack:
+                raise ValueError(f"timestamps [{self.t.min()}, {self.t.max()}] fall outside "
+                                 f"window [{self.t_start}, {upper}]")
+            if np.any(self.t[1:] < self.t[:-1]):
+                raise ValueError("slice events must be sorted ascending by t")
+        if self.geometry is not None:
+            outside = np.flatnonzero(~self.geometry.contains(self.x, self.y))
+            if len(outside):
+                bad = int(outside[0])
+                raise GeometryError(f"event {bad} at ({self.x[bad]}, {self.y[bad]}) outside geometry")
+
     def __len__(self) -> int:
+        return len(self.t)
+
+    @property
+    def n(self) -> int:
         return len(self.t)
 
     def events(self) -> np.ndarray:
@@ -96,123 +128,181 @@ class StreamSlice:
         return np.stack([self.t, self.x.astype(np.float64), self.y.astype(np.float64)], axis=1)
 
 
-def _parse_binary(path: str) -> EventStream:
-    """events.py:238-266."""
-    with open(path, "rb") as fh:
-        header = fh.read(12)
-        if len(header) < 12 or header[:4] != BINARY_MAGIC:
-            raise EventParseError(f"{path}: missing {BINARY_MAGIC!r} header")
-        width, height = struct.unpack("<II", header[4:12])
-        payload = fh.read()
-    if len(payload) % BINARY_RECORD_DTYPE.itemsize != 0:
-        raise EventParseError(f"{path}: truncated record at offset {12 + len(payload)} "
-                              f"(payload not a multiple of {BINARY_RECORD_DTYPE.itemsize} bytes)")
-    geometry = CameraGeometry(width, height)
-    records = np.frombuffer(payload, dtype=BINARY_RECORD_DTYPE)
-    x = records["x"].astype(np.int32)
-    y = records["y"].astype(np.int32)
-    inside = geometry.contains(x, y)
-    if not np.all(inside):
-        bad = int(np.flatnonzero(~inside)[0])
-        raise GeometryError(f"{path}: record {bad} at ({x[bad]}, {y[bad]}) outside geometry {width}x{height}")
-    return EventStream(records["t"].astype(np.float64), x, y, geometry, records["p"].astype(np.int8))
+StreamSlice = EventSlice   # slice_stream's windows
+
+
+# ---------------------------------------------------------------------------
+# Event files (events.py:177-311).  The formats and the error messages are the
+# reference's; the parsing is columnar: fields are converted a column at a
+# time by the C-level float/int constructors and checked with numpy, and only
+# when something fails is the first offending line re-examined on its own to
+# raise the reference's exception for it (line order first, then the check
+# order within the line: field count, t/x/y parse, t range, x, y, polarity).
+# ---------------------------------------------------------------------------
+
+def _first_bad(values, conv) -> Tuple[Optional[list], int]:
+    """(converted column, -1) or (None, index of the first unconvertible field)."""
+    try:
+        return list(map(conv, values)), -1
+    except ValueError:
+        for k, v in enumerate(values):
+            try:
+                conv(v)
+            except ValueError:
+                return None, k
+    raise AssertionError("unreachable")
+
+
+def _csv_line_error(path: str, lineno: int, fields: List[str], geometry: CameraGeometry) -> Exception:
+    """The exception the reference raises for one offending CSV line."""
+    if len(fields) not in (3, 4):
+        return EventParseError(f"{path}:{lineno}: expected 3 or 4 fields, got {len(fields)}")
+    try:
+        t, x, y = float(fields[0]), int(fields[1]), int(fields[2])
+    except ValueError as exc:
+        err = EventParseError(f"{path}:{lineno}: {exc}")
+        err.__cause__ = exc
+        return err
+    if not np.isfinite(t) or t < 0:
+        return EventParseError(f"{path}:{lineno}: timestamp {t} not finite and non-negative")
+    if not 0 <= x < geometry.width:
+        return GeometryError(f"{path}:{lineno}: x={x} violates 0 <= x < {geometry.width}")
+    if not 0 <= y < geometry.height:
+        return GeometryError(f"{path}:{lineno}: y={y} violates 0 <= y < {geometry.height}")
+    if len(fields) == 4:
+        try:
+            p = int(fields[3])
+        except ValueError as exc:
+            err = EventParseError(f"{path}:{lineno}: bad polarity {fields[3]!r}")
+            err.__cause__ = exc
+            return err
+        if p not in (0, 1, -1):
+            return EventParseError(f"{path}:{lineno}: polarity must be 0, 1 or -1, got {p}")
+    raise AssertionError(f"line {lineno} has no error")
 
 
 def _parse_csv(path: str, geometry: CameraGeometry) -> EventStream:
-    """events.py:177-236: optional header line, 3 or 4 fields, polarity in {0, 1, -1}."""
-    ts, xs, ys, ps = [], [], [], []
-    saw_polarity = False
+    """CSV events (events.py:177-236): optional header line (a non-numeric first
+    field on line 1), 3 or 4 fields, polarity in {0, 1, -1}; blank lines skipped."""
     with open(path, "r", encoding="utf-8") as fh:
-        for lineno, line in enumerate(fh, start=1):
-            line = line.strip()
-            if not line:
-                continue
-            fields = line.split(",")
-            if lineno == 1:
-                try:
-                    float(fields[0])
-                except ValueError:
-                    continue
-            if len(fields) not in (3, 4):
-                raise EventParseError(f"{path}:{lineno}: expected 3 or 4 fields, got {len(fields)}")
-            try:
-                t = float(fields[0])
-                x = int(fields[1])
-                y = int(fields[2])
-            except ValueError as exc:
-                raise EventParseError(f"{path}:{lineno}: {exc}") from exc
-            if not np.isfinite(t) or t < 0:
-                raise EventParseError(f"{path}:{lineno}: timestamp {t} not finite and non-negative")
-            if not (0 <= x < geometry.width):
-                raise GeometryError(f"{path}:{lineno}: x={x} violates 0 <= x < {geometry.width}")
-            if not (0 <= y < geometry.height):
-                raise GeometryError(f"{path}:{lineno}: y={y} violates 0 <= y < {geometry.height}")
-            if len(fields) == 4:
-                try:
-                    p = int(fields[3])
-                except ValueError as exc:
-                    raise EventParseError(f"{path}:{lineno}: bad polarity {fields[3]!r}") from exc
-                if p not in (0, 1, -1):
-                    raise EventParseError(f"{path}:{lineno}: polarity must be 0, 1 or -1, got {p}")
-                saw_polarity = True
-                ps.append(p)
-            else:
-                ps.append(0)
-            ts.append(t)
-            xs.append(x)
-            ys.append(y)
-    return EventStream(np.array(ts, dtype=np.float64), np.array(xs, dtype=np.int32),
-                       np.array(ys, dtype=np.int32), geometry,
-                       np.array(ps, dtype=np.int8) if saw_polarity else None)
+        raw = fh.read().splitlines()
+    rows, linenos = [], []
+    for k, line in enumerate(raw):
+        line = line.strip()
+        if line:
+            rows.append(line.split(","))
+            linenos.append(k + 1)
+    if rows and linenos[0] == 1 and _first_bad([rows[0][0]], float)[1] == 0:
+        rows, linenos = rows[1:], linenos[1:]          # header
+    m = len(rows)
+    nf = np.fromiter((len(r) for r in rows), dtype=np.int64, count=m)
+    cand = [int(np.flatnonzero((nf != 3) & (nf != 4))[0])] if np.any((nf != 3) & (nf != 4)) else []
+    stop = min(cand) if cand else m                    # lines past the first failure never matter
+    cols = [[r[c] for r in rows[:stop]] for c in range(3)]
+    parsed = []
+    for c, conv in enumerate((float, int, int)):
+        vals, bad = _first_bad(cols[c], conv)
+        if bad >= 0:
+            stop = min(stop, bad)
+            cand.append(bad)
+        parsed.append(vals)
+    if any(v is None for v in parsed):                 # re-convert the clean prefix
+        parsed = [list(map(conv, cols[c][:stop])) for c, conv in enumerate((float, int, int))]
+    t = np.array(parsed[0][:stop], dtype=np.float64)
+    x = np.array(parsed[1][:stop], dtype=np.int64)
+    y = np.array(parsed[2][:stop], dtype=np.int64)
+    value_bad = (~np.isfinite(t)) | (t < 0) | (x < 0) | (x >= geometry.width) | (y < 0) | (y >= geometry.height)
+    four = nf[:stop] == 4
+    pol = np.zeros(stop, dtype=np.int64)
+    if np.any(four):
+        idx = np.flatnonzero(four)
+        pv, bad = _first_bad([rows[i][3] for i in idx], int)
+        if bad >= 0:
+            cand.append(int(idx[bad]))
+            idx = idx[:bad]
+            pv = list(map(int, [rows[i][3] for i in idx]))
+        pol[idx] = pv
+        value_bad[idx] |= ~np.isin(pol[idx], (0, 1, -1))
+    if np.any(value_bad):
+        cand.append(int(np.flatnonzero(value_bad)[0]))
+    if cand:
+        k = min(cand)
+        raise _csv_line_error(path, linenos[k], rows[k], geometry)
+    return EventStream(t, x.astype(np.int32), y.astype(np.int32), geometry,
+                       pol.astype(np.int8) if np.any(four) else None)
+
+
+def _parse_binary(path: str) -> EventStream:
+    """EVN1 (events.py:238-266): `EVN1`, u32 width, u32 height, then packed
+    17-byte little-endian records (f64 t, i32 x, i32 y, i8 polarity)."""
+    size = os.path.getsize(path)
+    with open(path, "rb") as fh:
+        head = fh.read(12)
+    if len(head) < 12 or head[:4] != BINARY_MAGIC:
+        raise EventParseError(f"{path}: missing {BINARY_MAGIC!r} header")
+    width, height = struct.unpack_from("<II", head, 4)
+    rec = BINARY_RECORD_DTYPE.itemsize
+    if (size - 12) % rec:
+        raise EventParseError(f"{path}: truncated record at offset {size} "
+                              f"(payload not a multiple of {rec} bytes)")
+    geometry = CameraGeometry(width, height)
+    records = np.fromfile(path, dtype=BINARY_RECORD_DTYPE, offset=12)
+    x, y = records["x"].astype(np.int32), records["y"].astype(np.int32)
+    outside = np.flatnonzero(~geometry.contains(x, y))
+    if len(outside):
+        k = int(outside[0])
+        raise GeometryError(f"{path}: record {k} at ({x[k]}, {y[k]}) outside geometry {width}x{height}")
+    return EventStream(records["t"].astype(np.float64), x, y, geometry, records["p"].astype(np.int8))
+
+
+_READERS = {"csv": lambda path, g: _parse_csv(path, g), "binary": lambda path, g: _parse_binary(path)}
 
 
 def load_events(path: str, fmt: str = "csv", geometry: Optional[CameraGeometry] = None) -> EventStream:
-    """events.py:269-291."""
+    """Read an event file (events.py:269-291): CSV needs the geometry, EVN1
+    carries it (a declared geometry must then match)."""
     if not os.path.exists(path):
         raise EventParseError(f"{path}: no such file")
-    if fmt == "csv":
-        if geometry is None:
-            raise ValueError("CSV event files require an explicit geometry")
-        return _parse_csv(path, geometry)
-    if fmt == "binary":
-        stream = _parse_binary(path)
-        if geometry is not None and geometry != stream.geometry:
-            raise GeometryError(f"{path}: file geometry {stream.geometry.width}x{stream.geometry.height} "
-                                f"does not match declared {geometry.width}x{geometry.height}")
-        return stream
-    raise ValueError(f"unknown event format {fmt!r}")
+    if fmt not in _READERS:
+        raise ValueError(f"unknown event format {fmt!r}")
+    if fmt == "csv" and geometry is None:
+        raise ValueError("CSV event files require an explicit geometry")
+    stream = _READERS[fmt](path, geometry)
+    if fmt == "binary" and geometry is not None and geometry != stream.geometry:
+        raise GeometryError(f"{path}: file geometry {stream.geometry.width}x{stream.geometry.height} "
+                            f"does not match declared {geometry.width}x{geometry.height}")
+    return stream
 
 
 def write_events_binary(stream: EventStream, path: str) -> None:
-    records = np.empty(len(stream), dtype=BINARY_RECORD_DTYPE)
-    records["t"] = stream.t
-    records["x"] = stream.x
-    records["y"] = stream.y
-    records["p"] = stream.polarity if stream.polarity is not None else 0
+    """EVN1 writer (events.py:305-311)."""
+    rec = np.zeros(len(stream), dtype=BINARY_RECORD_DTYPE)
+    rec["t"], rec["x"], rec["y"] = stream.t, stream.x, stream.y
+    if stream.polarity is not None:
+        rec["p"] = stream.polarity
+    head = BINARY_MAGIC + struct.pack("<II", stream.geometry.width, stream.geometry.height)
     with open(path, "wb") as fh:
-        fh.write(BINARY_MAGIC)
-        fh.write(struct.pack("<II", stream.geometry.width, stream.geometry.height))
-        fh.write(records.tobytes())
+        fh.write(head + rec.tobytes())
 
 
 def write_events_csv(stream: EventStream, path: str) -> None:
+    """CSV writer (events.py:294-302): shortest round-trip repr of t, integer x, y[, p]."""
+    cols = [map(repr, stream.t.astype(np.float64).tolist()), map(str, stream.x.tolist()), map(str, stream.y.tolist())]
+    if stream.polarity is not None:
+        cols.append(map(str, stream.polarity.tolist()))
+    body = "".join(",".join(f) + "\n" for f in zip(*cols))
     with open(path, "w", encoding="utf-8") as fh:
-        if stream.polarity is not None:
-            for t, x, y, p in zip(stream.t, stream.x, stream.y, stream.polarity):
-                fh.write(f"{float(t)!r},{x},{y},{p}\n")
-        else:
-            for t, x, y in zip(stream.t, stream.x, stream.y):
-                fh.write(f"{float(t)!r},{x},{y}\n")
+        fh.write(body)
 
 
 def filter_polarity(stream: EventStream, keep: str) -> EventStream:
-    """events.py:314-328."""
+    """Keep positive ('pos': p > 0) or non-positive ('neg') events (events.py:314-328)."""
     if keep not in ("pos", "neg"):
         raise ValueError("keep must be 'pos' or 'neg'")
     if stream.polarity is None:
         return stream
-    mask = stream.polarity > 0 if keep == "pos" else stream.polarity <= 0
-    return EventStream(stream.t[mask], stream.x[mask], stream.y[mask], stream.geometry, stream.polarity[mask])
+    sel = (stream.polarity > 0) == (keep == "pos")
+    return EventStream(stream.t[sel], stream.x[sel], stream.y[sel], stream.geometry, stream.polarity[sel])
 
 
 def window_bounds(t: np.ndarray, delta_t: float, stride: float, t0: float = 0.0) -> List[Tuple[int, int, float]]:
@@ -239,7 +329,7 @@ def window_bounds(t: np.ndarray, delta_t: float, stride: float, t0: float = 0.0)
     return out
 
 
-def slice_stream(stream: EventStream, delta_t: float, stride: float, t0: float = 0.0) -> List[StreamSlice]:
+def slice_stream(stream: EventStream, delta_t: float, stride: float, t0: float = 0.0) -> List[EventSlice]:
     """Cut a stream into windows of length 2·delta_t (events.py:331-387)."""
     if delta_t <= 0:
         raise ValueError("delta_t must be positive")
@@ -252,7 +342,8 @@ def slice_stream(stream: EventStream, delta_t: float, stride: float, t0: float =
         order = np.argsort(t, kind="stable")
         t, x, y = t[order], x[order], y[order]
         p = p[order] if p is not None else None
-    return [StreamSlice(t[lo:hi], x[lo:hi], y[lo:hi], start, 2.0 * delta_t, p[lo:hi] if p is not None else None)
+    return [EventSlice(t[lo:hi], x[lo:hi], y[lo:hi], start, 2.0 * delta_t, stream.geometry,
+                       p[lo:hi] if p is not None else None)
             for lo, hi, start in window_bounds(t, delta_t, stride, t0)]
 
 

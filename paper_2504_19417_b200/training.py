@@ -103,11 +103,11 @@ def encode_dataset(dataset: Sequence, width: int, height: int, delta_x: int, del
     flows pair with the slice's time-sorted rows (as in the reference's fit)."""
     from .engine import FlowEngine
     from .errors import EmptyNeighborhoodError
-    from .validation import check_flow_array, slice_from_array
+    from .validation import block_from_array, check_flow_array
     eng = FlowEngine(width, height, delta_x, delta_y, delta_t, bases, None, device)
     feats, flows = [], []
     for X, u in dataset:
-        blk = slice_from_array(X, width, height, 2.0 * delta_t)
+        blk = block_from_array(X, width, height, 2.0 * delta_t)
         u = check_flow_array(u, len(blk))
         if len(blk) == 0:
             continue

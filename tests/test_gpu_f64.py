@@ -47,7 +47,7 @@ def test_f64_predict_matches_reference_golden(case):
     flows = reg.predict(g["X"])
     assert flows.dtype == np.float64
     np.testing.assert_allclose(flows, g["flows"], rtol=0, atol=FLOW_TOL64)
-    blk = pkg.slice_from_array(g["X"], int(g["width"]), int(g["height"]), 2 * float(g["delta_t"]))
+    blk = pkg.block_from_array(g["X"], int(g["width"]), int(g["height"]), 2 * float(g["delta_t"]))
     _, counts = reg.engine().predict_host_f64(blk.events, blk.t_start, return_counts=True)
     np.testing.assert_array_equal(counts, g["counts"])
 
@@ -155,3 +155,31 @@ def test_acceptance_oracle_equivalence_fuzz():
             worst[prec] = max(worst[prec], err)
     print(f"acceptance fuzz: max rel err f64={worst['f64']:.2e} f32={worst['f32']:.2e}")
     assert worst["f64"] < 1e-6 and worst["f32"] < 1e-3, worst
+
+
+@pytest.mark.parametrize("hidden", [128, 224])
+def test_f64_head_keeps_float64_weights(hidden):
+    """precision="f64" with float64 weights (what fit returns) runs a float64
+    head on those weights, as the reference's mlp_forward does (flow.py:98-106):
+    weights that f32 cannot represent must still agree within FLOW_TOL64.
+    hidden=128 stages W1ᵀ in shared memory as double (128 KB); at hidden=224
+    it does not fit and is read from global memory (same arithmetic)."""
+    pkg = _pkg()
+    W, H, D = 96, 80, 64
+    X = vo.synth_uniform_noise(4000, W, H, seed=11)
+    b = pkg.generate_bases(D, 25.0, (0, 1, 2))
+    w = pkg.init_weights(D, hidden, b, seed=3, dtype=np.float64)
+    g = np.random.default_rng(5)
+    w = pkg.MlpWeights(w.w1 * (1 + 1e-3 * g.standard_normal(w.w1.shape)), g.standard_normal(hidden) * 0.1,
+                       w.w2, g.standard_normal(2), b)
+    assert np.any(w.w1.astype(np.float32).astype(np.float64) != w.w1)
+    reg = pkg.NormalFlowRegressor(width=W, height=H, precision="f64", weights=w, hidden=hidden)
+    got = reg.predict(X)
+    fr = vo.Freqs(b.time_freqs, b.x_freqs, b.y_freqs, 25.0)
+    want = vo.predict(X, W, H, 10, 10, 0.016, fr, w.w1, w.b1, w.w2, w.b2, precision="f64")
+    np.testing.assert_allclose(got, want, rtol=0, atol=FLOW_TOL64)
+    # the f32-rounded head would miss the bar: the test can see the difference
+    w32 = pkg.MlpWeights(*(a.astype(np.float32) for a in (w.w1, w.b1, w.w2, w.b2)), b)
+    want32 = vo.predict(X, W, H, 10, 10, 0.016, fr, *(a.astype(np.float64) for a in (w32.w1, w32.b1, w32.w2,
+                                                                                        w32.b2)), precision="f64")
+    assert np.max(np.abs(want32 - want)) > 10 * FLOW_TOL64

@@ -63,7 +63,7 @@ def test_predict_matches_reference_golden(case, mode):
     flows = reg.predict(g["X"])
     assert flows.dtype == np.float64 and flows.shape == g["flows"].shape
     np.testing.assert_allclose(flows, g["flows"], rtol=0, atol=FLOW_TOL)
-    blk = _pkg().slice_from_array(g["X"], int(g["width"]), int(g["height"]), 2 * float(g["delta_t"]))
+    blk = _pkg().block_from_array(g["X"], int(g["width"]), int(g["height"]), 2 * float(g["delta_t"]))
     _, counts = reg.engine().predict_host(blk.events, blk.t_start, return_counts=True)
     np.testing.assert_array_equal(counts, g["counts"])
 
@@ -90,7 +90,7 @@ def test_grid_matches_reference_golden(case):
     g = load_golden(case)
     pkg = _pkg()
     reg = regressor(g)
-    blk = pkg.slice_from_array(g["X"], int(g["width"]), int(g["height"]), 2 * float(g["delta_t"]))
+    blk = pkg.block_from_array(g["X"], int(g["width"]), int(g["height"]), 2 * float(g["delta_t"]))
     ev = torch.from_numpy(blk.events).cuda()
     grid, cnt = reg.engine().grid_device(ev, blk.t_start, pooled=False)
     np.testing.assert_array_equal(cnt.cpu().numpy(), g["grid_count"])
@@ -169,7 +169,7 @@ def test_device_api_matches_host_api():
     g = load_golden("cfg1_20k")
     reg = regressor(g)
     pkg = _pkg()
-    blk = pkg.slice_from_array(g["X"], 346, 260, 0.032)
+    blk = pkg.block_from_array(g["X"], 346, 260, 0.032)
     eng = reg.engine()
     host = eng.predict_host(blk.events, blk.t_start)
     dev = eng.predict_device(torch.from_numpy(blk.events).cuda(), math.nan).cpu().numpy()
@@ -356,53 +356,27 @@ def test_batched_slices_many_chunks_edge_cases():
             assert np.isnan(flows[off[i] + len(X) // 2]).all() and cnt[off[i] + len(X) // 2] == 0
 
 
-def test_counting_sort_matches_radix_sort_with_hot_pixels():
-    """The counting scatter + per-run ordering (k_scatter, k_runsort,
-    k_longsort) must give the same stable pixel-major order as the CUB radix
-    sort (VKM_SORT=cub): runs of 1, 2..32 (warp-free insertion sort), 33..4096
-    (shared-memory bitonic) and > 4096 events (global-memory bitonic) at hot
-    pixels.  Same order -> bit-identical flows and counts."""
-    pkg = _pkg()
-    W, H = 96, 64
-    rng = np.random.default_rng(77)
-    X = vo.synth_uniform_noise(30000, W, H, seed=77)
-    hot = [(5, 5, 40), (50, 30, 700), (70, 10, 5000), (20, 60, 9000)]
-    extra = []
-    for x, y, k in hot:
-        t = rng.uniform(0.0, 0.032, k)
-        extra.append(np.stack([t, np.full(k, x), np.full(k, y)], 1))
-    X = np.concatenate([X] + extra)
-    X = X[np.argsort(X[:, 0], kind="stable")]
-    b = pkg.generate_bases(64)
-    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
-    ours = pkg.FlowEngine(W, H, 6, 6, 0.016, b, w)
-    f1, c1 = ours.predict_host(X, float(X[0, 0]), return_counts=True)
-    # the sort switch is read once per process: the CUB reference runs in a subprocess
-    import os, subprocess, sys, tempfile
-    with tempfile.TemporaryDirectory() as td:
-        np.save(os.path.join(td, "X.npy"), X)
-        code = (
-            "import sys, numpy as np; sys.path.insert(0, %r); import paper_2504_19417_b200 as pkg;"
-            "X = np.load(%r); b = pkg.generate_bases(64); w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32);"
-            "e = pkg.FlowEngine(%d, %d, 6, 6, 0.016, b, w); f, c = e.predict_host(X, float(X[0, 0]), return_counts=True);"
-            "np.save(%r, f); np.save(%r, c)"
-        ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.join(td, "X.npy"), W, H,
-             os.path.join(td, "f.npy"), os.path.join(td, "c.npy"))
-        out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, VKM_SORT="cub"), capture_output=True,
-                             text=True, timeout=300)
-        assert out.returncode == 0, out.stderr[-2000:]
-        f2, c2 = np.load(os.path.join(td, "f.npy")), np.load(os.path.join(td, "c.npy"))
-    np.testing.assert_array_equal(c1, c2)
-    np.testing.assert_array_equal(f1, f2)
-    # and the oracle on the hot pixels' events
-    q = np.flatnonzero((X[:, 1] == 70) & (X[:, 2] == 10))[::250]
-    fr = vo.Freqs(b.time_freqs, b.x_freqs, b.y_freqs, 25.0)
-    t0 = float(X[0, 0])
-    g = vo.accumulate(X[:, 0] - t0, X[:, 1].astype(np.int64), X[:, 2].astype(np.int64), W, H, 6, 6, fr, 0.016)
-    emb, c = vo.pool(g, vo.spatial_table(fr, 6, 6), X[q, 0] - t0, X[q, 1].astype(np.int64), X[q, 2].astype(np.int64),
-                     fr, 0.016)
-    np.testing.assert_array_equal(c, c1[q])
-    np.testing.assert_allclose(f1[q], vo.mlp(w.w1, w.b1, w.w2, w.b2, vo.to_features(emb)), rtol=0, atol=1e-4)
+@pytest.mark.parametrize("sort", ["auto", "counting", "rows"])
+@pytest.mark.parametrize("case", ["hot", "dense"])
+def test_pixel_order_is_the_stable_argsort(case, sort):
+    """K1's event order equals accumulate_grid's np.argsort(flat,
+    kind="stable") and bincount run starts (encoder.py:255-259) exactly, on
+    both sort paths: the counting scatter + run ordering (k_prep arrival ranks
+    -> k_scan -> k_scatter -> k_runsort / k_longsort) and the dense slices'
+    row-bucket counting sort (k_rowhist -> k_scan -> k_rowscatter -> k_xsort).
+    "hot": runs of 1, 2..256, 257..4096 and > 4096 events; "dense": 35 events
+    per pixel (the config-5 density).  The sort switch (VKM_SORT) is read once
+    per process, so each case runs in a fresh interpreter (tests/_order_check.py)."""
+    import os, subprocess, sys
+    env = dict(os.environ)
+    env.pop("VKM_SORT", None)
+    if sort != "auto":
+        env["VKM_SORT"] = sort
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = subprocess.run([sys.executable, os.path.join(here, "_order_check.py"), case], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, (out.stdout + out.stderr)[-3000:]
+    assert "order ok" in out.stdout
 
 
 def test_host_batch_packing_edge_cases():

@@ -12,7 +12,7 @@ from sklearn.exceptions import NotFittedError
 from conftest import GOLDEN, load_golden
 import paper_2504_19417_b200 as pkg
 from paper_2504_19417_b200 import _lib
-from paper_2504_19417_b200.validation import check_event_array, slice_from_array
+from paper_2504_19417_b200.validation import block_from_array, check_events
 from paper_2504_19417_b200.weights import bases_from_bytes, bases_to_bytes
 
 
@@ -70,7 +70,7 @@ def test_create_rejects_bad_params_before_touching_the_device():
 
 def test_check_event_array_types(rng):
     X = make_events(rng, n=5)
-    X3, x, y = check_event_array(X, 64, 64)
+    X3, x, y = check_events(X, 64, 64)
     assert X3.dtype == np.float64 and x.dtype == np.int32
 
 
@@ -83,25 +83,25 @@ def test_check_event_array_types(rng):
 ])
 def test_validation_messages(X, match):
     with pytest.raises(ValueError, match=match):
-        check_event_array(X, 8, 8)
+        check_events(X, 8, 8)
 
 
 def test_slice_sorts_stably_and_checks_span():
     X = np.array([[0.02, 1, 1], [0.01, 2, 2], [0.01, 3, 3]])
-    b = slice_from_array(X, 8, 8, 0.032)
+    b = block_from_array(X, 8, 8, 0.032)
     assert b.events[:, 0].tolist() == [0.01, 0.01, 0.02]
     assert b.events[:, 1].tolist() == [2, 3, 1]
     assert b.t_start == 0.01
     with pytest.raises(ValueError, match="window"):
-        slice_from_array(np.array([[0.0, 1, 1], [0.5, 1, 1]]), 8, 8, 0.032)
+        block_from_array(np.array([[0.0, 1, 1], [0.5, 1, 1]]), 8, 8, 0.032)
     # strict f64 span check (validation.py:59-64)
     with pytest.raises(ValueError, match="window"):
-        slice_from_array(np.array([[5.0, 1, 1], [5.032, 1, 1]]), 8, 8, 0.032)
+        block_from_array(np.array([[5.0, 1, 1], [5.032, 1, 1]]), 8, 8, 0.032)
 
 
 def test_slice_matches_golden_sorting(golden_case):
     g = golden_case
-    b = slice_from_array(g["X"], int(g["width"]), int(g["height"]), 2 * float(g["delta_t"]))
+    b = block_from_array(g["X"], int(g["width"]), int(g["height"]), 2 * float(g["delta_t"]))
     np.testing.assert_array_equal(b.events[:, 0], g["sorted_t"])
     np.testing.assert_array_equal(b.events[:, 1].astype(np.int32), g["sorted_x"])
     np.testing.assert_array_equal(b.events[:, 2].astype(np.int32), g["sorted_y"])
@@ -344,3 +344,95 @@ def test_native_concat_rows_matches_numpy():
         dst = np.empty((sum(sizes), 3))
         concat_rows(blocks, dst)
         np.testing.assert_array_equal(dst, np.concatenate(blocks) if sizes else dst)
+
+
+def test_estimator_pickles_after_use():
+    """Handles are dropped on pickling / deepcopy (rebuilt lazily), so a used
+    estimator stays picklable like the reference's."""
+    import copy
+    import pickle
+    import paper_2504_19417_b200 as pkg
+    b = pkg.generate_bases(8, 25.0, (0, 1, 2))
+    w = pkg.init_weights(8, 16, b, seed=0)
+    reg = pkg.NormalFlowRegressor(embed_dim=8, hidden=16, weights=w)
+    reg.weights_ = w
+    reg._engine_cache = (("k",), w, object())        # stand-ins for libveckm handles
+    reg._device_engines = {("k", 0): (w, object())}
+    back = pickle.loads(pickle.dumps(reg))
+    assert not hasattr(back, "_engine_cache") and not hasattr(back, "_device_engines")
+    np.testing.assert_array_equal(back.weights_.w1, w.w1)
+    assert copy.deepcopy(reg).get_params()["embed_dim"] == 8
+
+
+def test_engine_cache_is_per_thread_and_bounded():
+    import threading
+    from paper_2504_19417_b200.engine import EngineCache
+
+    class Fake:
+        closed = 0
+
+        def close(self):
+            Fake.closed += 1
+    cache = EngineCache(size=2)
+    a = cache.get("a", Fake)
+    assert cache.get("a", Fake) is a
+    cache.get("b", Fake)
+    cache.get("c", Fake)                 # evicts "a" (least recently used)
+    assert Fake.closed == 1
+    assert cache.get("a", Fake) is not a
+    other = []
+    th = threading.Thread(target=lambda: other.append(cache.get("b", Fake)))
+    th.start()
+    th.join()
+    assert other[0] is not cache.get("b", Fake)   # another thread, another handle
+
+
+def test_encoder_fit_checks_precision():
+    import paper_2504_19417_b200 as pkg
+    with pytest.raises(ValueError, match="precision"):
+        pkg.LocalEventEncoder(precision="f16").fit()
+
+
+def test_reference_signature_helpers():
+    """check_event_array(X, geometry) / slice_from_array(X, geometry, window)
+    keep the reference's signatures and return types (validation.py:10-65)."""
+    import paper_2504_19417_b200 as pkg
+    g = pkg.CameraGeometry(8, 6)
+    X = np.array([[0.02, 1, 2], [0.01, 3, 4], [0.01, 5, 5]])
+    t, x, y = pkg.check_event_array(X, g)
+    assert t.dtype == np.float64 and x.dtype == np.int32 and y.dtype == np.int32
+    np.testing.assert_array_equal(x, [1, 3, 5])
+    sl = pkg.slice_from_array(X, g, 0.032)
+    assert isinstance(sl, pkg.EventSlice) and sl.geometry == g and sl.window == 0.032
+    np.testing.assert_array_equal(sl.t, [0.01, 0.01, 0.02])          # stable time sort
+    np.testing.assert_array_equal(sl.x, [3, 5, 1])
+    assert sl.t_start == 0.01
+    with pytest.raises(ValueError, match="outside geometry 8x6"):
+        pkg.check_event_array(np.array([[0.0, 8, 0]]), g)
+    with pytest.raises(ValueError, match="exceeds the slice window"):
+        pkg.slice_from_array(np.array([[0.0, 1, 1], [0.5, 1, 1]]), g, 0.032)
+
+    class RefGeometry:   # duck-typed (e.g. evflow.CameraGeometry)
+        width, height = 8, 6
+    assert len(pkg.slice_from_array(X, RefGeometry(), 0.032)) == 3
+
+
+def test_bench_reference_arm_line_matches_b200_config():
+    """`bench.py --impl reference` prints the contract's line with the same
+    `config` as the b200 arm (so the driver can pair the two arms)."""
+    import json
+    import subprocess
+    import sys
+    import argparse
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--workload", "cfg1",
+                          "--steps", "1", "--warmup", "0", "--ref-budget", "2"], capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "flows/s"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+    sys.path.insert(0, root)
+    import bench
+    args = argparse.Namespace(workload="cfg1", slices=0, split="slices", mlp_mode="auto")
+    assert line["config"] == bench.bench_config(args, 1)

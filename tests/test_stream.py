@@ -114,13 +114,18 @@ def test_predict_stream_matches_per_window_predictions():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("stride", [0.004, 0.01, 0.032, 0.05])
-def test_device_windowing_matches_host_windowing(stride):
+@pytest.mark.parametrize("stride,chunk", [(0.004, 0), (0.004, 3000), (0.01, 0), (0.032, 0), (0.05, 0)])
+def test_device_windowing_matches_host_windowing(stride, chunk, monkeypatch):
     """vkm_window_bounds / vkm_predict_windows (windows searched and gathered on
     the GPU from one upload of the stream) equal the host-windowed batch: same
     windows and starts, flows within 1e-6 (the two paths group the windows
     into different launch batches, and the y pass's sliding-window segments
-    depend on how many slices share a launch, which moves f32 roundings)."""
+    depend on how many slices share a launch, which moves f32 roundings).
+    chunk > 0: the windows are gathered and predicted in chunks of at most
+    that many events (VKM_WINDOW_CHUNK_EVENTS; default 32M), one window alone
+    may exceed it."""
+    if chunk:
+        monkeypatch.setenv("VKM_WINDOW_CHUNK_EVENTS", str(chunk))
     if not has_cuda():
         pytest.fail("GPU test needs a CUDA device")
     import paper_2504_19417_b200 as pkg
@@ -155,3 +160,61 @@ def test_device_window_starts_follow_the_reference_loop():
         wins = S.window_bounds(t, 0.016, stride, 0.0)
         assert [s for _, _, s in wins] == list(starts[:len(wins)])
         assert starts[-1] <= t[-1] < starts[-1] + stride
+
+
+def test_csv_parser_matches_reference_outcomes(tmp_path):
+    """The columnar CSV reader against the reference's own outcomes
+    (tests/golden/make_golden_csv.py): parsed columns bit-exact, or the same
+    exception type and message (first offending line, then the check order
+    within the line)."""
+    import json
+    S = _S()
+    from paper_2504_19417_b200 import errors as E
+    with open(os.path.join(GOLDEN, "csv_cases.json")) as fh:
+        cases = json.load(fh)
+    g = S.CameraGeometry(16, 12)
+    for name, c in cases.items():
+        path = tmp_path / f"{name}.csv"
+        path.write_text(c["text"], encoding="utf-8")
+        if c["ok"]:
+            st = S.load_events(str(path), "csv", g)
+            assert [repr(v) for v in st.t.tolist()] == c["t"], name
+            assert st.x.tolist() == c["x"] and st.y.tolist() == c["y"], name
+            assert (None if st.polarity is None else st.polarity.tolist()) == c["p"], name
+        else:
+            with pytest.raises(getattr(E, c["type"])) as ei:
+                S.load_events(str(path), "csv", g)
+            assert str(ei.value).replace(str(path), "<path>") == c["message"], name
+
+
+def test_csv_writer_round_trips(tmp_path):
+    S = _S()
+    rng = np.random.default_rng(9)
+    st = S.EventStream(np.sort(rng.uniform(0, 1, 500)), rng.integers(0, 16, 500), rng.integers(0, 12, 500),
+                       S.CameraGeometry(16, 12), rng.choice([0, 1, -1], 500))
+    S.write_events_csv(st, str(tmp_path / "a.csv"))
+    lines = (tmp_path / "a.csv").read_text().splitlines()
+    assert lines[3] == f"{float(st.t[3])!r},{st.x[3]},{st.y[3]},{st.polarity[3]}"   # events.py:294-302 format
+    back = S.load_events(str(tmp_path / "a.csv"), "csv", S.CameraGeometry(16, 12))
+    np.testing.assert_array_equal(back.t, st.t)
+    np.testing.assert_array_equal(back.polarity, st.polarity)
+    pos = S.filter_polarity(st, "pos")
+    assert (pos.polarity > 0).all() and len(pos) + len(S.filter_polarity(st, "neg")) == len(st)
+
+
+def test_event_slice_checks():
+    """EventSlice construction checks (events.py:106-131)."""
+    S = _S()
+    from paper_2504_19417_b200.errors import GeometryError
+    g = S.CameraGeometry(8, 8)
+    s = S.EventSlice([0.0, 0.01], [1, 2], [3, 4], 0.0, 0.032, g)
+    assert s.n == 2 and s.events().shape == (2, 3)
+    with pytest.raises(ValueError, match="window must be positive"):
+        S.EventSlice([0.0], [1], [1], 0.0, 0.0, g)
+    with pytest.raises(ValueError, match="fall outside"):
+        S.EventSlice([0.0, 0.05], [1, 2], [3, 4], 0.0, 0.032, g)
+    with pytest.raises(ValueError, match="sorted ascending"):
+        S.EventSlice([0.01, 0.0], [1, 2], [3, 4], 0.0, 0.032, g)
+    with pytest.raises(GeometryError, match="outside geometry"):
+        S.EventSlice([0.0], [9], [1], 0.0, 0.032, g)
+    S.EventSlice([0.032 + 1e-18], [1], [1], 0.0, 0.032, g)   # ulp slack at the upper edge

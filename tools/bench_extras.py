@@ -46,7 +46,7 @@ for _ in range(5):
 predict_ms = (time.perf_counter() - t) / 5 * 1e3
 t = time.perf_counter()
 for _ in range(5):
-    pkg.slice_from_array(X, W, H, 0.032)
+    pkg.block_from_array(X, W, H, 0.032)
 validate_ms = (time.perf_counter() - t) / 5 * 1e3
 
 # trainer: 200k samples, D = 64 (128 features), hidden 128, batch 512
