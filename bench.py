@@ -475,17 +475,40 @@ def run_b200(args):
         roofline = {"bound": "hbm", "kernel": names[dom], "achieved": a, "peak": hbm_peak, "unit": "GB/s",
                     "frac": a / hbm_peak, "traffic": traffic, "alg_bytes_per_launch": int(byts[dom]),
                     "peak_kind": peak_kind}
-        # The encoder groups are instruction-issue bound (64 complex phases per
-        # event, twice): warp instructions per launch from the committed ncu
-        # capture of the same step (profiles/ncu_instr.json) over the group's
-        # live CUDA-event time, against 148 SMs x 4 schedulers x the SM clock.
+        # Compute roofline beside the HBM one: the encoder groups are bound by
+        # instruction issue / the FMA pipe (64 complex phases per event, twice)
+        # and the MLP by the tensor pipe.  Warp instructions per launch come
+        # from the committed ncu capture of the same workload
+        # (profiles/ncu_instr.json, tools/gpu_metrics.sh + tools/ncu_roofline.py)
+        # over the group's live CUDA-event time, against 148 SMs x 4 schedulers
+        # x the SM clock; pipe activity (FMA-heavy, ALU, tensor) is ncu's own
+        # per-kernel measurement of that capture (profiles/ncu_pipes.json).
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_instr.json")) as fh:
                 ins = json.load(fh).get(args.workload, {})
+            pipes = {}
+            pp = os.path.join(ROOT, "profiles", "ncu_pipes.json")
+            if os.path.exists(pp):
+                with open(pp) as fh:
+                    pipes = json.load(fh).get(args.workload, {})
             peak_issue = 148 * 4 * (clk_mhz or 1965.0) * 1e6
-            roofline["issue"] = {g: {"warp_instr_per_launch": ins[g], "achieved": ins[g] / (kernels[g]["ms"] * 1e-3),
-                                     "peak": peak_issue, "frac": ins[g] / (kernels[g]["ms"] * 1e-3) / peak_issue}
-                                 for g in names if g in ins}
+            comp = {}
+            for g in names:
+                if g not in ins:
+                    continue
+                ach = ins[g] / (kernels[g]["ms"] * 1e-3)
+                c = {"bound": "tensor" if g == "gather_mlp" else "issue", "warp_instr_per_launch": ins[g],
+                     "issue_achieved": ach, "issue_peak": peak_issue, "issue_frac": ach / peak_issue}
+                pg = pipes.get(g) or {}
+                for k in ("fmaheavy_pct", "alu_pct", "tensor_pipe_pct"):
+                    if k in pg:
+                        c[k + "_ncu"] = pg[k]
+                comp[g] = c
+            if "gather_mlp" in comp:   # F16X3 issues three fp16 MMAs per product: tensor work vs the peak
+                comp["gather_mlp"]["tensor_tflops_issued"] = 3 * mlp_tflops if args.mlp_mode in ("auto", "f16x3") \
+                    else mlp_tflops
+                comp["gather_mlp"]["tensor_frac_issued"] = comp["gather_mlp"]["tensor_tflops_issued"] / tc_peak
+            roofline["compute"] = comp
         except Exception:
             pass
 

@@ -43,7 +43,10 @@ constexpr int kAtomBytes = kM * 128;           // one 64-wide K atom: 128 rows x
 constexpr int kProdWarps = 16;                // producer warps (8 tile rows each)
 constexpr int kThreads = (kProdWarps + 5) * 32; // + 4 epilogue warps + 1 MMA warp
 constexpr uint32_t kTmemCols = kAcc * kN;
-constexpr int kQD = 4;                          // per-warp cp.async ring of pooled rows (3 in flight)
+#ifndef VKM_K3_QD
+#define VKM_K3_QD 4
+#endif
+constexpr int kQD = VKM_K3_QD;                  // per-warp cp.async ring of pooled rows (kQD - 1 in flight)
 #ifndef VKM_K3_PHB
 #define VKM_K3_PHB 2   // 1, 2, 4, 8 measured within 0.5 % (2 best at cfg2 and cfg3)
 #endif
@@ -143,7 +146,7 @@ __host__ __device__ __forceinline__ uint32_t umma_off(uint32_t m, uint32_t k) {
   return atom * kAtomBytes + (m >> 3) * 1024 + (m & 7) * 128 + chunk * 16 + (kk & 7) * 2;
 }
 
-template <int MODE>  // VKM_MLP_F16X3 or VKM_MLP_BF16
+template <int MODE, bool kMufu>  // VKM_MLP_F16X3 or VKM_MLP_BF16; sin/cos flavour (sincos2_k3_scaled)
 __global__ void __launch_bounds__(kThreads, 1)
     k_gather_mlp_tc(int64_t n, const uint64_t* __restrict__ val_s, const int32_t* __restrict__ pix_s, const int* __restrict__ nvalid_ptr,
                     const float* __restrict__ tf, int64_t P, const float2* __restrict__ Q,
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float rs = __shfl_sync(0xffffffffu, rs_reg, u + v);
             // conj(phase) * acc / cnt for channels (c0, c0+1), packed; the ÷count
             // (and fp16 pre-scale) rides on the sin/cos sign fix-up
-            VKM_SINCOS_K3_SCALED(fmul2(f2pack(aj, aj), T01), f2pack(rs, rs), snb[v], csb[v]);
+            sincos2_k3_scaled<kMufu>(fmul2(f2pack(aj, aj), T01), f2pack(rs, rs), snb[v], csb[v]);
           }
         }
         const uint64_t sn = snb[u % kPhB], cs = csb[u % kPhB];
@@ -354,8 +357,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     load_slot(int64_t(blockIdx.x) + 2 * G, a_nn, pix_nn);
     rs_c = recip(load_cnt(pix_c));
     cnt_n = load_cnt(pix_n);
-    prefetch_l2(blockIdx.x);
-    prefetch_l2(int64_t(blockIdx.x) + G);
+#ifndef VKM_K3_PF
+#define VKM_K3_PF 2   // tiles ahead whose pooled rows are bulk-prefetched into L2
+#endif
+    for (int d = 0; d < VKM_K3_PF; ++d) prefetch_l2(int64_t(blockIdx.x) + d * G);
 #pragma unroll
     for (int u = 0; u < kQD - 1; ++u) issue_row(__shfl_sync(0xffffffffu, pix_c, u), u);
     // one tile on stage kS (compile-time: the tile loop is unrolled by the
@@ -363,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto tile_step = [&](int64_t tile, int it, auto stage) {
       constexpr int kS = decltype(stage)::value;
       const uint32_t ph = (it >> 1) & 1;
-      prefetch_l2(tile + 2 * G);
+      prefetch_l2(tile + VKM_K3_PF * G);
       mbar_wait(&S.empty[kS], ph ^ 1);
       compute(a_c, rs_c, pix_c, pix_n, stage);
       fence_proxy_async();
@@ -507,19 +512,14 @@ void launch_gather_mlp_tc(int64_t n, const DevTables& tb, int W, int H, const Gr
     const char* e = std::getenv("VKM_TC_PREFETCH");
     return (e && e[0] == '0') ? 0 : 1;
   }();
-  if (mode == VKM_MLP_BF16) {
-    cudaFuncSetAttribute(tc::k_gather_mlp_tc<VKM_MLP_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    launch_pdl(tc::k_gather_mlp_tc<VKM_MLP_BF16>, grid, tc::kThreads, smem, s, n,
-               static_cast<const uint64_t*>(sb.val_s), static_cast<const int32_t*>(sb.pix_s), nvalid, tb.tf, P,
-               static_cast<const float2*>(g.Q), static_cast<const int*>(g.NQ), static_cast<const uint4*>(w.w1_hi),
-               static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out, prefetch);
-  } else {
-    cudaFuncSetAttribute(tc::k_gather_mlp_tc<VKM_MLP_F16X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    launch_pdl(tc::k_gather_mlp_tc<VKM_MLP_F16X3>, grid, tc::kThreads, smem, s, n,
-               static_cast<const uint64_t*>(sb.val_s), static_cast<const int32_t*>(sb.pix_s), nvalid, tb.tf, P,
-               static_cast<const float2*>(g.Q), static_cast<const int*>(g.NQ), static_cast<const uint4*>(w.w1_hi),
-               static_cast<const uint4*>(w.w1_lo), w.b1, w.w2, w.b2, w.w_scale, flows, counts_out, prefetch);
-  }
+  const bool mufu = sincos_mufu();
+  auto kern = mode == VKM_MLP_BF16 ? (mufu ? tc::k_gather_mlp_tc<VKM_MLP_BF16, true> : tc::k_gather_mlp_tc<VKM_MLP_BF16, false>)
+                                   : (mufu ? tc::k_gather_mlp_tc<VKM_MLP_F16X3, true> : tc::k_gather_mlp_tc<VKM_MLP_F16X3, false>);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  launch_pdl(kern, grid, tc::kThreads, smem, s, n, static_cast<const uint64_t*>(sb.val_s),
+             static_cast<const int32_t*>(sb.pix_s), nvalid, tb.tf, P, static_cast<const float2*>(g.Q),
+             static_cast<const int*>(g.NQ), static_cast<const uint4*>(w.w1_hi), static_cast<const uint4*>(w.w1_lo), w.b1,
+             w.w2, w.b2, w.w_scale, flows, counts_out, prefetch);
 }
 
 }  // namespace vkm

@@ -236,6 +236,7 @@ constexpr int kRxGroup = VKM_RX_GROUP;   // events per sin/cos group (divides 32
 
 size_t reduce_x_smem(int dx) { return size_t(kRxWarps) * ((2 * dx + 1) * 512 + kRxEnds * 4); }
 
+template <bool kMufu>
 __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restrict__ start,
                                                             const uint64_t* __restrict__ val_s,
                                                             const float* __restrict__ tf,
@@ -243,7 +244,6 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
                                                             const float4* __restrict__ myp, int W, int H, int nb,
                                                             int dx, int S, int nseg, int64_t P,
                                                             float2* __restrict__ R) {
-  pdl_wait();
   extern __shared__ __align__(16) uint8_t rx_smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int RL = 2 * dx + 1;
@@ -256,29 +256,48 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
   float4* const R4 = reinterpret_cast<float4*>(R) + ((int64_t(lane >> 2) * P) << 2) + (lane & 3);
   const int64_t items = int64_t(nb) * H * nseg;   // (virtual row, segment); P = nb·W·H
   const int64_t nwarps = int64_t(gridDim.x) * kRxWarps;
-  for (int64_t it = int64_t(blockIdx.x) * kRxWarps + wib; it < items; it += nwarps) {
-    const int y = int(it / nseg);                  // virtual row: slice y / H, sensor row y % H
-    const int x0 = int(it - int64_t(y) * nseg) * S, x1 = min(W, x0 + S);
-    const int xs = x0 - dx, nx = x1 + dx - xs;      // sweep x = xs + k, k in [0, nx)
-    const int* st = start + int64_t(y) * W;         // st[x]: first slot of pixel (x, y)
-    const int jfirst = __ldg(st + max(0, xs)), jend = __ldg(st + min(W, x1 + dx));
+  auto mx_at = [&](int x) { return __ldg(mxl + int64_t(min(max(x, 0), W - 1)) * 32); };
+  // Item setup reads only start[] (k_scan's output, complete before the
+  // predecessor chain that ends in this launch even began) and constant
+  // tables, so the first item's setup runs before pdl_wait(), overlapping
+  // the run sort's tail; only the slot values wait.
+#ifndef VKM_RX_PF
+#define VKM_RX_PF 1   // prefetch depth of the modulation factors and time arguments: 1 or 2
+#endif
+  int y = 0, x0 = 0, x1 = 0, xs = 0, nx = 0, jfirst = 0, jend = 0;
+  float4 fy4 = make_float4(0.f, 0.f, 0.f, 0.f), mc = fy4, mcn = fy4;
+  auto setup = [&](int64_t it) {
+    y = int(it / nseg);                          // virtual row: slice y / H, sensor row y % H
+    x0 = int(it - int64_t(y) * nseg) * S;
+    x1 = min(W, x0 + S);
+    xs = x0 - dx;
+    nx = x1 + dx - xs;                           // sweep x = xs + k, k in [0, nx)
+    const int* st = start + int64_t(y) * W;      // st[x]: first slot of pixel (x, y)
+    jfirst = __ldg(st + max(0, xs));
+    jend = __ldg(st + min(W, x1 + dx));
     __syncwarp();
-    for (int k = lane; k <= nx; k += 32) {          // ends[k]: end slot of pixel xs + k's run
+    for (int k = lane; k <= nx; k += 32) {       // ends[k]: end slot of pixel xs + k's run
       const int x = xs + k;
       ends[k] = k == nx ? jend : (x < 0 ? jfirst : (x < W ? __ldg(st + x + 1) : jend));
     }
     for (int k = 0; k < RL; ++k) ring0[k * 32] = make_ulonglong2(0ull, 0ull);
+    fy4 = __ldg(myl + int64_t(y % H) * 32);
+    mc = mx_at(xs);
+    if (VKM_RX_PF > 1) mcn = mx_at(xs + 1);
     __syncwarp();
-    const float4 fy4 = __ldg(myl + int64_t(y % H) * 32);
+  };
+  int64_t it = int64_t(blockIdx.x) * kRxWarps + wib;
+  if (it < items) setup(it);
+  pdl_wait();
+  for (; it < items; it += nwarps) {
     const uint64_t fyr = f2pack(fy4.x, fy4.y), fyi = f2pack(fy4.z, fy4.w);
     float4* out = R4 + ((int64_t(y) * W + x0) << 2);
     auto ld_a = [&](int jj) { return jj < jend ? slot_arg(__ldg(val_s + jj)) : 0.f; };
     int jb = jfirst;
-    float av0 = ld_a(jb + lane), av1 = ld_a(jb + 32 + lane);
+    float av0 = ld_a(jb + lane), av1 = ld_a(jb + 32 + lane), av2 = VKM_RX_PF > 1 ? ld_a(jb + 64 + lane) : 0.f;
 
     int k = 0;                                      // sweep index of the pixel being summed
     int je = ends[0], je_n = ends[1];               // run end of pixel k, and of k+1 (loaded a pixel early)
-    float4 mc = __ldg(mxl + int64_t(min(max(xs, 0), W - 1)) * 32);
     uint64_t gr = 0, gi = 0, ar = 0, ai = 0;
     ulonglong2* pn = ring0;                          // ring slot of pixel k
     ulonglong2* po = ring0 + 32;                     // ring slot of pixel k - 2δx
@@ -306,25 +325,36 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
       ++k;
       je = je_n;
       je_n = ends[min(k + 1, nx)];                   // shared-memory latency off the per-pixel chain
-      mc = __ldg(mxl + int64_t(min(max(xs + k, 0), W - 1)) * 32);   // next pixel's factor, in flight early
+      if (VKM_RX_PF > 1) {
+        mc = mcn;                                    // modulation factors two pixels ahead
+        mcn = mx_at(xs + k + 1);
+      } else {
+        mc = mx_at(xs + k);                          // next pixel's factor, in flight early
+      }
     };
 
     // Events in groups of kRxGroup: the sin/cos of a whole group are computed
     // back to back (independent chains), then added in slot order with the
     // pixel boundaries resolved between them.  Groups never straddle a 32-slot
-    // batch (both advance from jfirst).
+    // batch (both advance from jfirst).  Time arguments arrive two batches
+    // (64 slots) ahead.
     for (int j = jfirst; j < jend; j += kRxGroup) {
       if (j - jb >= 32) {
         jb += 32;
         av0 = av1;
-        av1 = ld_a(jb + 32 + lane);
+        if (VKM_RX_PF > 1) {
+          av1 = av2;
+          av2 = ld_a(jb + 64 + lane);
+        } else {
+          av1 = ld_a(jb + 32 + lane);
+        }
       }
       const int i0 = j - jb;
       uint64_t cs[kRxGroup], sn[kRxGroup];
 #pragma unroll
       for (int u = 0; u < kRxGroup; ++u) {
         const float au = __shfl_sync(kFullMask, av0, i0 + u);
-        VKM_SINCOS_HOT(fmul2(f2pack(au, au), T01), sn[u], cs[u]);
+        sincos2_hot<kMufu>(fmul2(f2pack(au, au), T01), sn[u], cs[u]);
       }
 #pragma unroll
       for (int u = 0; u < kRxGroup; ++u) {
@@ -337,6 +367,7 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
       }
     }
     while (k < nx) finish();
+    if (it + nwarps < items) setup(it + nwarps);
   }
   pdl_trigger();   // dependents may launch as this grid drains
 }
@@ -436,7 +467,7 @@ __global__ void __launch_bounds__(kRunsortThreads) k_runsort(const int* __restri
 // ---------------------------------------------------------------------------
 constexpr int kMsdTile = 8192, kMsdThreads = 256, kMsdWarps = kMsdThreads / 32;
 constexpr int kMsdMaxRows = 4096;                  // per-warp row bases in shared memory
-constexpr int kXsortThreads = 512, kXsortWarps = kXsortThreads / 32, kXsortMaxW = 2048;
+constexpr int kXsortThreads = 1024, kXsortWarps = kXsortThreads / 32, kXsortMaxW = 1536;
 
 size_t msd_tab_words(int64_t n) { return size_t(kMsdMaxRows) * size_t((n + kMsdTile - 1) / kMsdTile + 1); }
 
@@ -497,7 +528,7 @@ __global__ void __launch_bounds__(kMsdThreads) k_rowscatter(const int32_t* __res
       const unsigned peers = __match_any_sync(kFullMask, in ? r : -1);
       if (in) {
         const int pos = base[r] + __popc(peers & lt);
-        bkt[pos] = __ldg(val + e);
+        bkt[pos] = __ldcs(val + e);
         bx[pos] = p - r * W;
       }
       __syncwarp();
@@ -543,7 +574,7 @@ __global__ void __launch_bounds__(kXsortThreads) k_xsort(const uint64_t* __restr
       const unsigned peers = __match_any_sync(kFullMask, x);
       if (in) {
         const int pos = base[x] + __popc(peers & lt);
-        val_s[pos] = __ldg(bkt + j);
+        val_s[pos] = __ldcs(bkt + j);
         pix_s[pos] = r * W + x;
       }
       __syncwarp();
@@ -810,6 +841,11 @@ void launch_slot_events(const uint64_t* val_s, const int* valid, int64_t n, int3
   k_slot_events<<<int(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(val_s, valid, n, order);
 }
 
+bool sincos_mufu() {
+  const char* e = std::getenv("VKM_SINCOS");
+  return !(e && std::strcmp(e, "poly") == 0);
+}
+
 uint32_t next_scan_epoch() {
   static std::atomic<uint32_t> epoch{0};
   uint32_t e;
@@ -845,15 +881,18 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
     }
   }
   cudaMemsetAsync(sb.longcount, 0, sizeof(int), s);
-  // Dense slices take the row-bucket path, the others the counting scatter
-  // (VKM_SORT=counting|rows forces one, for A/B runs and tests).
+  // The counting scatter + run sort serves every density.  The row-bucket
+  // path (VKM_SORT=rows, tested for exact order) measured slower at config 5
+  // (rowhist 0.17 + rowscatter 1.11 + xsort 0.83 ms against scatter 0.98 +
+  // run sort 0.59 ms): both scatter 8-byte records to sectors spread over a
+  // destination far larger than L2 (DRAM read-modify-writes).
   static const int sort_env = [] {
     const char* e = std::getenv("VKM_SORT");
     return !e ? 0 : (std::strcmp(e, "counting") == 0 ? 1 : (std::strcmp(e, "rows") == 0 ? 2 : 0));
   }();
   const int R = st.nb * H;
   const bool rows_ok = R <= kMsdMaxRows && W <= kXsortMaxW;
-  const bool dense = rows_ok && (sort_env == 2 || (sort_env == 0 && double(n) > 8.0 * double(P) && n >= (1 << 20)));
+  const bool dense = rows_ok && sort_env == 2;
   if (n > 0) {
     const int blocks = int(std::min<int64_t>((n + 255) / 256, ev_blocks));
     int32_t* rank = dense ? nullptr : sb.rank;
@@ -887,7 +926,9 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
                static_cast<const uint64_t*>(sb.val), n, W, R, ntiles, static_cast<const int*>(off), sb.bkt, sb.rank);
     const size_t xs_smem = size_t(kXsortWarps) * W * 4;
     cudaFuncSetAttribute(k_xsort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(size_t(kXsortWarps) * kXsortMaxW * 4));
-    launch_pdl(k_xsort, std::min(R, 148 * 2), kXsortThreads, xs_smem, s, static_cast<const uint64_t*>(sb.bkt),
+    // one CTA per SM: the rows in flight (~0.5 MB of slots each at config 5)
+    // stay in L2 until their scattered 8-byte writes complete
+    launch_pdl(k_xsort, std::min(R, 148), kXsortThreads, xs_smem, s, static_cast<const uint64_t*>(sb.bkt),
                static_cast<const int32_t*>(sb.rank), static_cast<const int*>(sb.start), W, R, sb.val_s, sb.pix_s);
     launches += 4;
   } else if (n > 0) {
@@ -966,9 +1007,10 @@ void launch_reduce_x(const DevTables& tb, int W, int H, int nb, int dx, const So
     return;
   }
   const size_t smem = reduce_x_smem(dx);
-  cudaFuncSetAttribute(k_reduce_x, cudaFuncAttributeMaxDynamicSharedMemorySize, int(reduce_x_smem(kMaxFusedDx)));
+  auto kern = sincos_mufu() ? k_reduce_x<true> : k_reduce_x<false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(reduce_x_smem(kMaxFusedDx)));
   int per = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reduce_x, kRxWarps * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kRxWarps * 32, smem);
   const int64_t res_warps = int64_t(std::max(1, per)) * num_sms * kRxWarps;
   // Segment width: long segments keep the recomputed 2δx halo small; shorter
   // ones when a row split into 128-column segments would not fill the GPU.
@@ -982,8 +1024,8 @@ void launch_reduce_x(const DevTables& tb, int W, int H, int nb, int dx, const So
   const int nseg = (W + S - 1) / S;
   const int64_t items = int64_t(H) * nb * nseg;
   const int blocks = int(std::min<int64_t>((items + kRxWarps - 1) / kRxWarps, res_warps / kRxWarps));
-  launch_pdl(k_reduce_x, blocks, kRxWarps * 32, smem, s, sb.start, sb.val_s, tb.tf, tb.mxp, tb.myp, W, H, nb, dx, S,
-             nseg, P, R);
+  launch_pdl(kern, blocks, kRxWarps * 32, smem, s, sb.start, sb.val_s, tb.tf, tb.mxp, tb.myp, W, H, nb, dx, S, nseg,
+             P, R);
 }
 
 }  // namespace vkm

@@ -185,6 +185,28 @@ __device__ __forceinline__ void sincos2p_pi_scaled(uint64_t x, uint64_t scale01,
   c01 = fmul2(cr, f);
 }
 
+// Special-function-unit variant: reduction by 2π (two-part Cody-Waite) to
+// [-π, π], then MUFU.SIN / MUFU.COS (sin.approx: max abs error 2^-21.4 there,
+// ~3 ulp of 1.0), the per-pair scale applied last.  Four XU-pipe and five
+// FMA-pipe instructions per pair instead of ~17 FMA-pipe: for kernels whose
+// producers are FMA-pipe bound (K3's de-phase).
+__device__ __forceinline__ void sincos2_mufu_scaled(uint64_t x, uint64_t scale01, uint64_t& s01, uint64_t& c01) {
+  const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
+  const uint64_t qb = ffma2(x, f2pack(0.159154943f, 0.159154943f), magic);   // rint(x / 2π)
+  const uint64_t q = fsub2(qb, magic);
+  uint64_t r = ffma2(q, f2pack(-6.28318548e+00f, -6.28318548e+00f), x);
+  r = ffma2(q, f2pack(1.74845553e-07f, 1.74845553e-07f), r);
+  float r0, r1;
+  f2unpack(r, r0, r1);
+  float s0, s1, c0, c1;
+  asm("sin.approx.f32 %0, %1;" : "=f"(s0) : "f"(r0));
+  asm("sin.approx.f32 %0, %1;" : "=f"(s1) : "f"(r1));
+  asm("cos.approx.f32 %0, %1;" : "=f"(c0) : "f"(r0));
+  asm("cos.approx.f32 %0, %1;" : "=f"(c1) : "f"(r1));
+  s01 = fmul2(f2pack(s0, s1), scale01);
+  c01 = fmul2(f2pack(c0, c1), scale01);
+}
+
 // Packed-in/packed-out variant: theta = (x0, x1), returns (s0, s1), (c0, c1).
 __device__ __forceinline__ void sincos2p_f32(uint64_t theta, uint64_t& s01, uint64_t& c01) {
   float x0, x1, s0, c0, s1, c1;
@@ -199,24 +221,46 @@ __device__ __forceinline__ void sincos2p_f32(uint64_t theta, uint64_t& s01, uint
 // measured no faster on B200 (both kernels are dependency-latency bound:
 // k_reduce_x 128 -> 132 us, K3 ~equal, ncu cfg2) and is 2x less accurate, so
 // the pi/2-reduced version is the default; -DVKM_SINCOS_PI selects the other.
-#ifdef VKM_SINCOS_PI
-#define VKM_SINCOS_HOT sincos2p_pi
-#else
-#define VKM_SINCOS_HOT sincos2p_f32
-#endif
+__device__ __forceinline__ void sincos2p_mufu(uint64_t x, uint64_t& s01, uint64_t& c01) {
+  const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
+  const uint64_t qb = ffma2(x, f2pack(0.159154943f, 0.159154943f), magic);   // rint(x / 2π)
+  const uint64_t q = fsub2(qb, magic);
+  uint64_t r = ffma2(q, f2pack(-6.28318548e+00f, -6.28318548e+00f), x);
+  r = ffma2(q, f2pack(1.74845553e-07f, 1.74845553e-07f), r);
+  float r0, r1, s0, s1, c0, c1;
+  f2unpack(r, r0, r1);
+  asm("sin.approx.f32 %0, %1;" : "=f"(s0) : "f"(r0));
+  asm("sin.approx.f32 %0, %1;" : "=f"(s1) : "f"(r1));
+  asm("cos.approx.f32 %0, %1;" : "=f"(c0) : "f"(r0));
+  asm("cos.approx.f32 %0, %1;" : "=f"(c1) : "f"(r1));
+  s01 = f2pack(s0, s1);
+  c01 = f2pack(c0, c1);
+}
+// The hot kernels (k_reduce_x, k_gather_mlp_tc) take the sin/cos flavour as
+// a template parameter chosen at run time (sincos_mufu(), VKM_SINCOS):
+//   MUFU (default)  2π reduction + sin.approx/cos.approx on the special-function
+//                   unit: ~5e-7 absolute, 4 XU + 5 FMA-pipe instructions per
+//                   pair.  Both kernels are FMA-pipe bound, so moving the
+//                   polynomials off that pipe pays: cfg2 K1 0.168 -> 0.134 ms,
+//                   K3 0.134 -> 0.130 ms; flows vs the reference unchanged
+//                   (<= 7.2e-7 over the goldens).
+//   poly            the Cody-Waite + minimax polynomials below (1.4 ulp, the
+//                   same f32 phase as numpy on 98.9 % of arguments).
+template <bool kMufu>
+__device__ __forceinline__ void sincos2_hot(uint64_t x, uint64_t& s01, uint64_t& c01) {
+  if constexpr (kMufu)
+    sincos2p_mufu(x, s01, c01);
+  else
+    sincos2p_f32(x, s01, c01);
+}
+template <bool kMufu>
+__device__ __forceinline__ void sincos2_k3_scaled(uint64_t x, uint64_t scale01, uint64_t& s01, uint64_t& c01) {
+  if constexpr (kMufu)
+    sincos2_mufu_scaled(x, scale01, s01, c01);
+  else
+    sincos2p_pi_scaled(x, scale01, s01, c01);
+}
 #define VKM_SINCOS_CS sincos2_cs
-// K3 de-phase: the pi-reduced variant by default (K3 is issue-bound since the
-// metadata pipeline; -DVKM_K3_ACCURATE_SINCOS restores the accurate one).
-#ifdef VKM_K3_ACCURATE_SINCOS
-#define VKM_SINCOS_K3_SCALED(x, k, s, c) \
-  do {                                    \
-    sincos2p_f32((x), (s), (c));          \
-    (s) = fmul2((s), (k));                \
-    (c) = fmul2((c), (k));                \
-  } while (0)
-#else
-#define VKM_SINCOS_K3_SCALED sincos2p_pi_scaled
-#endif
 
 // a = f32((t - t0) / delta_t): f64 rebase and divide, then one rounding to f32,
 // exactly as rebase_slice (events.py:390-407) + _temporal_phases

@@ -64,6 +64,9 @@ size_t msd_tab_words(int64_t n);     // per-(row, event tile) counters for n eve
 // W x (nb·H) sensor whose windows never cross slice borders.  t0[b] = NaN
 // reads the slice's first event.  Passed by value as a kernel parameter.
 constexpr int kMaxBatch = 64;
+// Run-time flavour of the hot kernels' sin/cos (VKM_SINCOS=poly|mufu, default
+// mufu; read per launch).
+bool sincos_mufu();
 struct SliceTab {
   int32_t nb;
   int64_t off[kMaxBatch + 1];

@@ -25,7 +25,7 @@ def main(case):
         X = np.concatenate([X] + extra)
         X = X[np.argsort(X[:, 0], kind="stable")]
         xs, ys = 70, 10
-    else:   # 35 events per pixel; > 1M events so the automatic choice is the row-bucket path
+    else:   # 35 events per pixel (the config-5 density), > 1M events
         W, H = 192, 160
         X = vo.synth_uniform_noise(35 * W * H, W, H, seed=78)
         xs, ys = 40, 30

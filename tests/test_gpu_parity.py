@@ -53,9 +53,14 @@ def angular_stats(got, want, floor=1e-2):
     return (float(np.percentile(d, 99)), float(d.max())) if len(d) else (0.0, 0.0)
 
 
+@pytest.mark.parametrize("sincos", ["mufu", "poly"])
 @pytest.mark.parametrize("mode", ["fp32", "f16x3", "auto"])
 @pytest.mark.parametrize("case", GOLDEN_CASES)
-def test_predict_matches_reference_golden(case, mode):
+def test_predict_matches_reference_golden(case, mode, sincos, monkeypatch):
+    """Flows vs the reference's (max-abs FLOW_TOL) and neighbourhood counts
+    exact, for every MLP mode and both sin/cos flavours of the hot kernels
+    (VKM_SINCOS: special-function unit by default, or the polynomials)."""
+    monkeypatch.setenv("VKM_SINCOS", sincos)
     g = load_golden(case)
     reg = regressor(g, mode)
     if mode == "f16x3" and not (int(g["D"]) == 64 and int(g["w1"].shape[0]) == 128):

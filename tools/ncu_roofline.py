@@ -68,7 +68,8 @@ def analyse(path, keep=5):
             seqs[-1].append((name, v))
     seqs = seqs[-keep:]
     res = {g: {"dram_bytes": 0.0, "warp_instr": 0.0, "fma_instr": 0.0, "alu_instr": 0.0, "xu_instr": 0.0,
-               "tc_instr": 0.0, "ms_serialised": 0.0} for g in GROUPS}
+               "tc_instr": 0.0, "ms_serialised": 0.0, "fmaheavy_pct": 0.0, "alu_pct": 0.0, "issue_pct": 0.0}
+           for g in GROUPS}
     tensor = []
     for seq in seqs:
         for name, v in seq:
@@ -82,7 +83,12 @@ def analyse(path, keep=5):
             r["alu_instr"] += v("sm__inst_executed_pipe_alu.sum")
             r["xu_instr"] += v("sm__inst_executed_pipe_xu.sum")
             r["tc_instr"] += v("sm__inst_executed_pipe_tc.sum")
-            r["ms_serialised"] += v("gpu__time_duration.sum") * 1e3
+            ms = v("gpu__time_duration.sum") * 1e3
+            r["ms_serialised"] += ms
+            # duration-weighted pipe activity (normalised below)
+            r["fmaheavy_pct"] += ms * v("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active")
+            r["alu_pct"] += ms * v("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active")
+            r["issue_pct"] += ms * v("smsp__issue_active.avg.pct_of_peak_sustained_active")
             if "k_gather_mlp" in name:
                 tensor.append((v("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
                                v("sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active"),
@@ -91,14 +97,17 @@ def analyse(path, keep=5):
                                v("gpu__time_duration.sum") * 1e3))
     n = max(1, len(seqs))
     for r in res.values():
+        for k in ("fmaheavy_pct", "alu_pct", "issue_pct"):
+            r[k] = r[k] / r["ms_serialised"] if r["ms_serialised"] > 0 else 0.0
         for k in r:
-            r[k] /= n
+            if not k.endswith("_pct"):
+                r[k] /= n
     if tensor:
         m = len(tensor)
         res["gather_mlp"]["tensor_pipe_pct"] = sum(t[0] for t in tensor) / m
         res["gather_mlp"]["tensor_hmma_pct"] = sum(t[1] for t in tensor) / m
         res["gather_mlp"]["fma_pipe_pct"] = sum(t[2] for t in tensor) / m
-        res["gather_mlp"]["issue_pct"] = sum(t[3] for t in tensor) / m
+        res["gather_mlp"]["mlp_issue_pct"] = sum(t[3] for t in tensor) / m
     per_kernel = {}
     for seq in seqs:
         for name, v in seq:
