@@ -24,6 +24,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "../../include/veckm.h"
@@ -37,11 +38,33 @@ constexpr int kM = 128;             // events per tile (UMMA M)
 constexpr int kN = 128;             // hidden units (UMMA N)
 constexpr int kK = 128;             // features 2D (UMMA K total)
 constexpr int kStages = 2;
-constexpr int kAcc = 4;                // TMEM accumulators (4 x 128 columns = all 512)
+constexpr int kAcc = 4;                // TMEM accumulators (4 x 128 columns = all 512), row-per-warp producers
+// one-event-per-lane producers keep the A operand in TMEM: 2 accumulators
+// (columns 0..255) and 2 stages of A (hi | lo, 128 columns each) from kLeA
+constexpr int kAccLE = 2;
+constexpr int kLeA = kAccLE * 128;
 constexpr int kTileBytes = kM * kK * 2;        // 32 KB per fp16 operand image
 constexpr int kAtomBytes = kM * 128;           // one 64-wide K atom: 128 rows x 128 B
 constexpr int kProdWarps = 16;                // producer warps (8 tile rows each)
 constexpr int kThreads = (kProdWarps + 5) * 32; // + 4 epilogue warps + 1 MMA warp
+// One-event-per-lane producers: 16 warps (four per TMEM lane quarter, 8
+// channel pairs each), then 4 epilogue warps, the MMA warp and the gather
+// (TMA) warp: 22 warps (1024 threads per CTA cap the producers at 16 for an
+// even split of the 32 channel pairs).
+#ifndef VKM_K3_LEPROD
+#define VKM_K3_LEPROD 16   // 8 measured 1.4x slower (cfg2 K3 0.181 vs 0.127 ms): the producers need the warps
+#endif
+constexpr int kLEProd = VKM_K3_LEPROD;
+constexpr int kLEPairs = 32 * 4 / kLEProd;       // channel pairs per producer lane
+constexpr int kThreadsLE = (kLEProd + 6) * 32;
+template <bool kLaneEvent>
+struct Roles {
+  static constexpr int prod = kLaneEvent ? kLEProd : kProdWarps;
+  static constexpr int epi0 = prod;                // 4 epilogue warps
+  static constexpr int mma = prod + 4;
+  static constexpr int loader = prod + 5;          // lane-event variant only
+  static constexpr int threads = kLaneEvent ? kThreadsLE : kThreads;
+};
 constexpr uint32_t kTmemCols = kAcc * kN;
 #ifndef VKM_K3_QD
 #define VKM_K3_QD 4
@@ -58,7 +81,11 @@ struct Smem {
   uint8_t bl[kTileBytes];
   uint8_t ah[kStages][kTileBytes];
   uint8_t al[kStages][kTileBytes];
+#ifdef VKM_K3_REGQ
+  float4 qring[kProdWarps][1][32];     // unused: the rows live in registers
+#else
   float4 qring[kProdWarps][kQD][32];   // per producer warp: pooled rows of its next kQD-1 events
+#endif
   // head constants with the power-of-two operand scale s = w_scale·f_scale
   // folded in: relu(acc/s + b1)·w2 == relu(acc + s·b1)·(w2/s) exactly
   float b1s[kN];    // s·b1
@@ -68,7 +95,16 @@ struct Smem {
   float scale;
   uint32_t tmem_base;
   unsigned long long full[kStages], empty[kStages], tfull[kAcc], tempty[kAcc];
+  // one-event-per-lane variant: pooled-grid rows of a tile's pixel range,
+  // bulk-copied (TMA) into slots carved from the (then unused) A images + ring
+  int gp0[3];                                   // first pixel of the slot's range, -1: load directly
+  unsigned long long gfull[3], gempty[3];
 };
+constexpr int kGSlots = 3;
+constexpr int kGSpan = 96;                        // pixels per plane a slot holds
+constexpr int kGSlotBytes = 8 * kGSpan * 64;      // 48 KB
+static_assert(kGSlots * kGSlotBytes <= int(2 * kStages * kTileBytes + sizeof(float4) * kProdWarps * kQD * 32),
+              "gather slots exceed the A images + ring");
 
 static_assert(sizeof(Smem) + 1024 <= 232448, "K3 shared memory exceeds the 227 KB opt-in limit");
 
@@ -84,21 +120,34 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
 }
 // Bounded parity wait: a descriptor or protocol bug traps (kernel error)
 // instead of hanging the device.
+#ifndef VKM_K3_HINT
+#define VKM_K3_HINT 20000   // try_wait suspend-time hint (ns); 0 = plain try_wait
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
   const uint32_t a = smem_u32(b);
   uint32_t done = 0;
   for (uint32_t it = 0;; ++it) {
-    // suspend-time hint: a waiting warp sleeps in the barrier unit (up to
-    // ~20 us per try) instead of spinning on issue slots the producers need
+#if VKM_K3_HINT > 0
+    // suspend-time hint: a waiting warp sleeps in the barrier unit instead of
+    // spinning on issue slots the producers need
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
-        : "r"(a), "r"(parity), "r"(20000u)
+        : "r"(a), "r"(parity), "r"(uint32_t(VKM_K3_HINT))
         : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+#endif
     if (done) return;
-    if (it > (1u << 20)) __trap();
+    if (it > (1u << 24)) __trap();
   }
 }
 
@@ -133,6 +182,29 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t da, uint64_t 
       "l"(da), "l"(db), "r"(idesc), "r"(acc)
       : "memory");
 }
+// A operand from tensor memory (row m = TMEM lane m, K packed two fp16 per column)
+__device__ __forceinline__ void umma_f16_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+// global -> shared bulk copy (TMA engine), completion counted on an mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
 __device__ __forceinline__ void umma_commit(unsigned long long* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
                : "memory");
@@ -146,8 +218,8 @@ __host__ __device__ __forceinline__ uint32_t umma_off(uint32_t m, uint32_t k) {
   return atom * kAtomBytes + (m >> 3) * 1024 + (m & 7) * 128 + chunk * 16 + (kk & 7) * 2;
 }
 
-template <int MODE, bool kMufu>  // VKM_MLP_F16X3 or VKM_MLP_BF16; sin/cos flavour (sincos2_k3_scaled)
-__global__ void __launch_bounds__(kThreads, 1)
+template <int MODE, bool kMufu, bool kLaneEvent>  // VKM_MLP_F16X3 or VKM_MLP_BF16; sin/cos flavour; producer layout
+__global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
     k_gather_mlp_tc(int64_t n, const uint64_t* __restrict__ val_s, const int32_t* __restrict__ pix_s, const int* __restrict__ nvalid_ptr,
                     const float* __restrict__ tf, int64_t P, const float2* __restrict__ Q,
                     const int* __restrict__ NQ, const uint4* __restrict__ w1h, const uint4* __restrict__ w1l,
@@ -166,12 +238,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nvec = kTileBytes / 16;
     uint4* dh = reinterpret_cast<uint4*>(S.bh);
     uint4* dl = reinterpret_cast<uint4*>(S.bl);
-    for (int i = threadIdx.x; i < nvec; i += kThreads) {
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
       dh[i] = __ldg(w1h + i);
       if (kSplit) dl[i] = __ldg(w1l + i);
     }
     const float sc = w_scale * f_scale;   // a power of two: exact scaling
-    for (int i = threadIdx.x; i < kN; i += kThreads) {
+    for (int i = threadIdx.x; i < kN; i += blockDim.x) {
       S.b1s[i] = b1[i] * sc;
       S.w2a[i] = w2[i] / sc;
       S.w2b[i] = w2[kN + i] / sc;
@@ -181,16 +253,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       S.b2[1] = b2[1];
       S.scale = 1.f / (w_scale * f_scale);
       for (int s = 0; s < kStages; ++s) {
-        mbar_init(&S.full[s], kProdWarps * 32);
+        mbar_init(&S.full[s], Roles<kLaneEvent>::prod * 32);
         mbar_init(&S.empty[s], 1);
       }
       for (int a = 0; a < kAcc; ++a) {
         mbar_init(&S.tfull[a], 1);
         mbar_init(&S.tempty[a], 128);
       }
+      for (int g = 0; g < kGSlots; ++g) {
+        mbar_init(&S.gfull[g], 1);
+        mbar_init(&S.gempty[g], Roles<kLaneEvent>::prod);
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == kProdWarps + 4) {
+    if (warp == Roles<kLaneEvent>::mma) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
                    "r"(kTmemCols)
                    : "memory");
@@ -206,7 +282,154 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t ntiles = (n + kM - 1) / kM;
   const int64_t nv = __ldg(nvalid_ptr);   // slots [0, nv) hold the in-sensor events
 
-  if (warp < kProdWarps) {
+  if (kLaneEvent && warp < kLEProd) {
+    // ================ producers, one event per lane ================
+    // Warp (q, j) = (warp & 3, warp >> 2) fills tile rows 32q + lane (one event
+    // per lane) with channel pairs 8j .. 8j+7 (K positions 32j .. 32j+31 of the
+    // feature order of feature_kpos, i.e. four 16-byte chunks of the
+    // SWIZZLE_128B image per lane: 8 lanes of a row group hit 8 distinct
+    // chunk columns, so the 16-byte stores are conflict-free).  Each lane
+    // gathers its own pooled row (two 64-byte pieces, planes 2j and 2j+1),
+    // de-phases by its own event's phase, divides by the count and splits -
+    // no shuffles and no per-row shared-memory ring: the pooled rows of the
+    // next tile are loaded into the registers freed by the current tile's
+    // first pairs, so a tile of gathers stays in flight across the stage wait.
+    const int qq = warp & 3, jg = warp >> 2;      // lane quarter, channel-pair group
+    const int m = 32 * qq + lane;                 // tile row of this lane's event
+    uint64_t T01[kLEPairs];
+#pragma unroll
+    for (int u = 0; u < kLEPairs; ++u) {
+      const int c = 2 * (kLEPairs * jg + u);
+      T01[u] = f2pack(__ldg(tf + c), __ldg(tf + c + 1));
+    }
+    const float4* Q4 = reinterpret_cast<const float4*>(Q);
+    // The A operand lives in tensor memory: row m = TMEM lane m (this warp's
+    // lane quarter is qq = warp % 4, as tcgen05.st requires), K packed two
+    // fp16 per 32-bit column; pairs 8jg.. are K 32jg.. = columns 16jg..16jg+15
+    // of the stage's hi and lo regions (columns kLeA + 128 s + {0, 64}).
+    const uint32_t ta_lane = tmem + (uint32_t(32 * qq) << 16) + uint32_t(kLeA + 2 * kLEPairs * jg);
+    auto meta = [&](int64_t tl, float& a, int& pix) {
+      const int64_t slot = tl * kM + m;
+      a = 0.f;
+      pix = -1;
+      if (tl < ntiles && slot < nv) {
+        pix = __ldg(pix_s + slot);
+        a = slot_arg(__ldg(val_s + slot));
+      }
+    };
+    auto recip = [&](int cnt) {
+      float r;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(float(cnt)));
+      return cnt > 0 ? r * f_scale : 0.f;
+    };
+    // pooled row of pixel pix, pairs u of the group: plane 2jg + (u >> 2),
+    // q4 = u & 3; from the tile's bulk-copied slot (gp0 >= 0: pixel range
+    // [gp0, gp0 + kGSpan)) or, for tiles whose pixel range does not fit a
+    // slot, straight from global memory
+    const uint32_t gslots = smem_u32(S.ah[0]);
+    auto gather = [&](int pix, int u, int gp0, uint32_t slot_base) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (pix >= 0) {
+        if (gp0 >= 0) {
+          const uint32_t a = slot_base + uint32_t((((kLEPairs / 4) * jg + (u >> 2)) * kGSpan + (pix - gp0)) * 64 +
+                                                  (u & 3) * 16);
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+        } else {
+          const float4* src = Q4 + ((int64_t((kLEPairs / 4) * jg + (u >> 2)) * P + pix) << 2) + (u & 3);
+          asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                       : "l"(src));
+        }
+      }
+      return v;
+    };
+    const int64_t G = gridDim.x;
+    float a_c, a_n, a_nn;
+    int pix_c, pix_n, pix_nn, cnt_n;
+    meta(blockIdx.x, a_c, pix_c);
+    meta(int64_t(blockIdx.x) + G, a_n, pix_n);
+    meta(int64_t(blockIdx.x) + 2 * G, a_nn, pix_nn);
+    float rs_c = recip(pix_c >= 0 ? __ldg(NQ + pix_c) : 0);
+    cnt_n = pix_n >= 0 ? __ldg(NQ + pix_n) : 0;
+    int gslot = 0, gph = 0;   // gather slot of the current tile and its phase
+    auto tile_step = [&](int64_t tile, int it, auto stage) {
+      constexpr int kS = decltype(stage)::value;
+      const uint32_t ph = (it >> 1) & 1;
+      const uint64_t rs2 = f2pack(rs_c, rs_c);
+      const uint64_t aa = f2pack(a_c, a_c);
+      mbar_wait(&S.gfull[gslot], gph);   // this tile's pooled rows have landed (or gp0 = -1)
+      const int gp0 = S.gp0[gslot];
+      const uint32_t slot_base = gslots + uint32_t(gslot * kGSlotBytes);
+      float4 v[kLEPairs];
+#pragma unroll
+      for (int u = 0; u < kLEPairs; ++u) v[u] = gather(pix_c, u, gp0, slot_base);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.gempty[gslot]);   // reads are done (registers hold the rows)
+      if (++gslot == kGSlots) {
+        gslot = 0;
+        gph ^= 1;
+      }
+#pragma unroll
+      for (int half = 0; half < kLEPairs / 4; ++half) {   // pairs 4·half .. 4·half+3 -> 8 columns per image
+        uint32_t hw[8], lw[8];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int u = 4 * half + h;
+          uint64_t sn, cs;
+          sincos2_k3_scaled<kMufu>(fmul2(aa, T01[u]), rs2, sn, cs);
+          const float4 q = v[u];
+          const uint64_t ar = f2pack(q.x, q.y), ai = f2pack(q.z, q.w);
+          const uint64_t re = ffma2(sn, ai, fmul2(cs, ar));
+          const uint64_t im = fsub2(fmul2(cs, ai), fmul2(sn, ar));
+          if (kSplit) {
+            const uint64_t tmask = 0xFFFFE000FFFFE000ull;
+            const uint64_t tre = re & tmask, tim = im & tmask;
+            float h0, h1, h2, h3, l0, l1, l2, l3;
+            f2unpack(tre, h0, h1);
+            f2unpack(tim, h2, h3);
+            f2unpack(fsub2(re, tre), l0, l1);
+            f2unpack(fsub2(im, tim), l2, l3);
+            const __half2 hre = __floats2half2_rn(h0, h1), him = __floats2half2_rn(h2, h3);
+            const __half2 lre = __floats2half2_rn(l0, l1), lim = __floats2half2_rn(l2, l3);
+            hw[2 * h] = *reinterpret_cast<const uint32_t*>(&hre);
+            hw[2 * h + 1] = *reinterpret_cast<const uint32_t*>(&him);
+            lw[2 * h] = *reinterpret_cast<const uint32_t*>(&lre);
+            lw[2 * h + 1] = *reinterpret_cast<const uint32_t*>(&lim);
+          } else {
+            float re0, re1, im0, im1;
+            f2unpack(re, re0, re1);
+            f2unpack(im, im0, im1);
+            const __nv_bfloat162 bre = __floats2bfloat162_rn(re0, re1), bim = __floats2bfloat162_rn(im0, im1);
+            hw[2 * h] = *reinterpret_cast<const uint32_t*>(&bre);
+            hw[2 * h + 1] = *reinterpret_cast<const uint32_t*>(&bim);
+          }
+        }
+        if (half == 0) {   // the stage is needed only from the first store on
+          mbar_wait(&S.empty[kS], ph ^ 1);
+          tc_fence_after();
+        }
+        const uint32_t ta = ta_lane + uint32_t(kS * 128 + 8 * half);
+        tmem_st8(ta, hw);
+        if (kSplit) tmem_st8(ta + 64, lw);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(&S.full[kS]);
+      a_c = a_n;
+      pix_c = pix_n;
+      rs_c = recip(cnt_n);
+      a_n = a_nn;
+      pix_n = pix_nn;
+      cnt_n = pix_nn >= 0 ? __ldg(NQ + pix_nn) : 0;
+      meta(tile + 3 * G, a_nn, pix_nn);
+    };
+    static_assert(kStages == 2, "the producer loop is unrolled by the two stages");
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += 2 * G, it += 2) {
+      tile_step(tile, it, std::integral_constant<int, 0>{});
+      if (tile + G >= ntiles) break;
+      tile_step(tile + G, it + 1, std::integral_constant<int, 1>{});
+    }
+  } else if (!kLaneEvent && warp < kProdWarps) {
     // ======================= producers =======================
     // Warp w fills tile rows [8w, 8w+8) (pixel-sorted slots).  Its pooled-
     // grid rows stream through a cp.async ring (3 rows in flight), the slot
@@ -263,11 +486,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (cp.async, 16 B per lane, zero-filled for empty slots), so the
     // L2/HBM latency of the gathers overlaps the de-phase/split work.
     float4* const ring = &S.qring[warp][0][lane];
+#ifdef VKM_K3_REGQ
+    // pooled rows prefetched into registers (kQD - 1 rows ahead) instead of
+    // the shared-memory ring: no cp.async writes / LDS reads of shared memory
+    float4 rq[kQD];
+#pragma unroll
+    for (int i = 0; i < kQD; ++i) rq[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#endif
     // lane-constant parts of the gather (global plane base, shared ring slot 0)
     // hoisted: per row only the pixel offset and the slot offset are added
     const float4* const qlane = Q4 + ((int64_t(plane) * P) << 2) + q4;
     const uint32_t ring_s = smem_u32(ring);
     auto issue_row = [&](int pj, int slot) {
+#ifdef VKM_K3_NOGATHER   // A/B skeleton: no pooled-row gathers (the ring keeps stale rows)
+      return;
+#endif
+#ifdef VKM_K3_REGQ
+      {
+        const float4* src = qlane + (int64_t(pj >= 0 ? pj : 0) << 2);
+        float4 v;
+        asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(src));
+        rq[slot] = pj >= 0 ? v : make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+      }
+#endif
       const float4* src = qlane + (int64_t(pj >= 0 ? pj : 0) << 2);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n\tcp.async.commit_group;" ::"r"(
                        ring_s + uint32_t(slot) * 512u),
@@ -303,12 +545,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float rs = __shfl_sync(0xffffffffu, rs_reg, u + v);
             // conj(phase) * acc / cnt for channels (c0, c0+1), packed; the ÷count
             // (and fp16 pre-scale) rides on the sin/cos sign fix-up
+#ifdef VKM_K3_NOMATH   // A/B skeleton: no de-phase sin/cos
+            snb[v] = f2pack(aj, rs);
+            csb[v] = f2pack(rs, aj);
+#else
             sincos2_k3_scaled<kMufu>(fmul2(f2pack(aj, aj), T01), f2pack(rs, rs), snb[v], csb[v]);
+#endif
           }
         }
         const uint64_t sn = snb[u % kPhB], cs = csb[u % kPhB];
+#ifdef VKM_K3_REGQ
+        const float4 src_u = rq[u & (kQD - 1)];
+#else
         asm volatile("cp.async.wait_group %0;" ::"n"(kQD - 2) : "memory");
         const float4 src_u = ring[(u & (kQD - 1)) * 32];
+#endif
         {   // refill the slot read one row ago with the row kQD-1 ahead
           const int un = u + kQD - 1;
           const int pj = un < kRows ? __shfl_sync(0xffffffffu, pix_c, un) : __shfl_sync(0xffffffffu, pix_n, un - kRows);
@@ -369,7 +620,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr int kS = decltype(stage)::value;
       const uint32_t ph = (it >> 1) & 1;
       prefetch_l2(tile + VKM_K3_PF * G);
+#ifndef VKM_K3_NOWAIT   // A/B skeleton: producers do not wait for the MMA to free the stage (racy)
       mbar_wait(&S.empty[kS], ph ^ 1);
+#endif
       compute(a_c, rs_c, pix_c, pix_n, stage);
       fence_proxy_async();
       mbar_arrive(&S.full[kS]);
@@ -389,13 +642,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_step(tile + G, it + 1, std::integral_constant<int, 1>{});
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
-  } else if (warp < kProdWarps + 4) {
+  } else if (kLaneEvent && warp == Roles<kLaneEvent>::loader) {
+    // ================ gather loader (TMA) ================
+    // Slots are pixel-sorted, so a tile's pooled rows are one contiguous
+    // pixel range per channel plane: eight bulk copies (one per plane) move
+    // them into a shared-memory slot, three tiles ahead of the producers.
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int g = it % kGSlots;
+        const uint32_t ph = (it / kGSlots) & 1;
+        mbar_wait(&S.gempty[g], ph ^ 1);
+        const int64_t f = tile * kM;
+        int p0 = -1, span = 0;
+        if (f < nv) {
+          const int64_t l = (f + kM < nv ? f + kM : nv) - 1;
+          p0 = __ldg(pix_s + f);
+          span = __ldg(pix_s + l) - p0 + 1;
+          if (span > kGSpan) p0 = -1;
+        }
+        S.gp0[g] = p0;
+        if (p0 >= 0) {
+          const uint32_t bytes = uint32_t(span) * 64u;
+          mbar_expect_tx(&S.gfull[g], 8u * bytes);
+          const uint32_t dst = smem_u32(S.ah[0]) + uint32_t(g * kGSlotBytes);
+#pragma unroll
+          for (int pl = 0; pl < 8; ++pl)
+            bulk_g2s(dst + uint32_t(pl * kGSpan * 64), Q + (int64_t(pl) * P + p0) * 8, bytes, &S.gfull[g]);
+        } else {
+          mbar_arrive(&S.gfull[g]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= Roles<kLaneEvent>::epi0 && warp < Roles<kLaneEvent>::epi0 + 4) {
     // ======================= epilogue =======================
     const int q = warp & 3;   // TMEM lane quadrant = warp id % 4
     int it = 0;
+    constexpr int kA = kLaneEvent ? kAccLE : kAcc;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const int acc = it & (kAcc - 1);
-      const uint32_t ph = (it / kAcc) & 1;
+      const int acc = it & (kA - 1);
+      const uint32_t ph = (it / kA) & 1;
       const int64_t slot = tile * kM + q * 32 + lane;
       int cnt = 1;
       int64_t e = -1;
@@ -407,6 +694,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       uint64_t oa = 0, ob = 0;   // (even, odd) hidden partial sums of the two outputs
       const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * kN);
+#ifdef VKM_K3_NOEPI   // A/B skeleton: no epilogue math
+      if (false)
+#endif
 #pragma unroll
       for (int cb = 0; cb < kN; cb += 32) {
         uint32_t r[32];
@@ -449,27 +739,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (counts_out) counts_out[e] = cnt;
       }
     }
-  } else {
+  } else if (warp == Roles<kLaneEvent>::mma) {
     // ======================= MMA issuer =======================
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc(kSplit ? 0u : 1u);
       const uint32_t bh = smem_u32(S.bh), bl = smem_u32(S.bl);
       int it = 0;
+      constexpr int kA = kLaneEvent ? kAccLE : kAcc;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int s = it & 1, acc = it & (kAcc - 1);
-        const uint32_t ph = (it >> 1) & 1, pha = (it / kAcc) & 1;
+        const int s = it & 1, acc = it & (kA - 1);
+        const uint32_t ph = (it >> 1) & 1, pha = (it / kA) & 1;
         mbar_wait(&S.tempty[acc], pha ^ 1);
         mbar_wait(&S.full[s], ph);
         tc_fence_after();
         const uint32_t d = tmem + uint32_t(acc * kN);
-        const uint32_t ah = smem_u32(S.ah[s]), al = smem_u32(S.al[s]);
+        if (kLaneEvent) {
+          const uint32_t ta = tmem + uint32_t(kLeA + s * 128);   // A hi | lo of stage s (TMEM lane 0)
 #pragma unroll
-        for (int ks = 0; ks < kK / 16; ++ks) {
-          const uint32_t off = (ks >> 2) * kAtomBytes + (ks & 3) * 32;
-          umma_f16(d, umma_desc(ah + off), umma_desc(bh + off), idesc, ks > 0);
-          if (kSplit) {
-            umma_f16(d, umma_desc(ah + off), umma_desc(bl + off), idesc, 1);
-            umma_f16(d, umma_desc(al + off), umma_desc(bh + off), idesc, 1);
+          for (int ks = 0; ks < kK / 16; ++ks) {
+            const uint32_t off = (ks >> 2) * kAtomBytes + (ks & 3) * 32;
+#ifdef VKM_K3_NOMMA
+            continue;
+#endif
+            umma_f16_ta(d, ta + 8 * ks, umma_desc(bh + off), idesc, ks > 0);
+            if (kSplit) {
+              umma_f16_ta(d, ta + 8 * ks, umma_desc(bl + off), idesc, 1);
+              umma_f16_ta(d, ta + 64 + 8 * ks, umma_desc(bh + off), idesc, 1);
+            }
+          }
+        } else {
+          const uint32_t ah = smem_u32(S.ah[s]), al = smem_u32(S.al[s]);
+#pragma unroll
+          for (int ks = 0; ks < kK / 16; ++ks) {
+            const uint32_t off = (ks >> 2) * kAtomBytes + (ks & 3) * 32;
+#ifdef VKM_K3_NOMMA   // A/B skeleton: no tensor-core work
+            continue;
+#endif
+            umma_f16(d, umma_desc(ah + off), umma_desc(bh + off), idesc, ks > 0);
+            if (kSplit) {
+              umma_f16(d, umma_desc(ah + off), umma_desc(bl + off), idesc, 1);
+              umma_f16(d, umma_desc(al + off), umma_desc(bh + off), idesc, 1);
+            }
           }
         }
         umma_commit(&S.empty[s]);
@@ -481,7 +791,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == kProdWarps + 4) {
+  if (warp == Roles<kLaneEvent>::mma) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
   }
@@ -513,10 +823,20 @@ void launch_gather_mlp_tc(int64_t n, const DevTables& tb, int W, int H, const Gr
     return (e && e[0] == '0') ? 0 : 1;
   }();
   const bool mufu = sincos_mufu();
-  auto kern = mode == VKM_MLP_BF16 ? (mufu ? tc::k_gather_mlp_tc<VKM_MLP_BF16, true> : tc::k_gather_mlp_tc<VKM_MLP_BF16, false>)
-                                   : (mufu ? tc::k_gather_mlp_tc<VKM_MLP_F16X3, true> : tc::k_gather_mlp_tc<VKM_MLP_F16X3, false>);
+  const bool rows = [] {   // VKM_K3=rows: the row-per-warp producers (A/B and tests; read per launch)
+    const char* e = std::getenv("VKM_K3");
+    return e && std::strcmp(e, "rows") == 0;
+  }();
+  using K = decltype(&tc::k_gather_mlp_tc<VKM_MLP_F16X3, true, true>);
+  K kern;
+  if (mode == VKM_MLP_BF16)
+    kern = mufu ? (rows ? tc::k_gather_mlp_tc<VKM_MLP_BF16, true, false> : tc::k_gather_mlp_tc<VKM_MLP_BF16, true, true>)
+                : (rows ? tc::k_gather_mlp_tc<VKM_MLP_BF16, false, false> : tc::k_gather_mlp_tc<VKM_MLP_BF16, false, true>);
+  else
+    kern = mufu ? (rows ? tc::k_gather_mlp_tc<VKM_MLP_F16X3, true, false> : tc::k_gather_mlp_tc<VKM_MLP_F16X3, true, true>)
+                : (rows ? tc::k_gather_mlp_tc<VKM_MLP_F16X3, false, false> : tc::k_gather_mlp_tc<VKM_MLP_F16X3, false, true>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  launch_pdl(kern, grid, tc::kThreads, smem, s, n, static_cast<const uint64_t*>(sb.val_s),
+  launch_pdl(kern, grid, rows ? tc::kThreads : tc::kThreadsLE, smem, s, n, static_cast<const uint64_t*>(sb.val_s),
              static_cast<const int32_t*>(sb.pix_s), nvalid, tb.tf, P, static_cast<const float2*>(g.Q),
              static_cast<const int*>(g.NQ), static_cast<const uint4*>(w.w1_hi), static_cast<const uint4*>(w.w1_lo), w.b1,
              w.w2, w.b2, w.w_scale, flows, counts_out, prefetch);

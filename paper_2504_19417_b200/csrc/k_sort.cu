@@ -726,6 +726,7 @@ constexpr int kRx1Warps = 4;   // two items per block
 constexpr int kRx1Group = 4;   // events per group: one float4 of time arguments
 size_t reduce_x1_smem(int dx) { return size_t(kRx1Warps) * ((2 * dx + 1) * 256 + kRxEnds * 4); }
 
+template <bool kMufu>
 __global__ void __launch_bounds__(kRx1Warps * 32) k_reduce_x1(const int* __restrict__ start,
                                                               const uint64_t* __restrict__ val_s,
                                                               const float* __restrict__ tf,
@@ -813,8 +814,8 @@ __global__ void __launch_bounds__(kRx1Warps * 32) k_reduce_x1(const int* __restr
       }
       const float4 a4 = *reinterpret_cast<const float4*>(abuf + (j - jb));
       uint64_t cs[kRx1Group];
-      VKM_SINCOS_CS(fmul2(f2pack(a4.x, a4.y), TT), cs[0], cs[1]);
-      VKM_SINCOS_CS(fmul2(f2pack(a4.z, a4.w), TT), cs[2], cs[3]);
+      sincos2_cs_hot<kMufu>(fmul2(f2pack(a4.x, a4.y), TT), cs[0], cs[1]);
+      sincos2_cs_hot<kMufu>(fmul2(f2pack(a4.z, a4.w), TT), cs[2], cs[3]);
 #pragma unroll
       for (int u = 0; u < kRx1Group; ++u) {
         if (j + u >= je) {
@@ -989,20 +990,23 @@ void launch_reduce_x(const DevTables& tb, int W, int H, int nb, int dx, const So
   // k_reduce_x1 issues ~35 % more instructions but runs twice the warps: it
   // wins where the (2δx+1)-pixel ring limits occupancy (cfg3, δ = 20: -3.6 %),
   // loses slightly at δ = 10 (cfg2: +2 %).
-  const int variant = variant_env >= 0 ? variant_env : (dx >= 16 ? 1 : 0);
+  // (With the MUFU sin/cos, k_reduce_x is also the faster one at δ = 20:
+  // cfg3 accumulate 0.57 vs 0.67 ms; the x1 variant stays behind VKM_RX=1.)
+  const int variant = variant_env >= 0 ? variant_env : 0;
   if (variant == 1) {   // one channel per lane, two warps per item
     const size_t smem = reduce_x1_smem(dx);
+    auto kern1 = sincos_mufu() ? k_reduce_x1<true> : k_reduce_x1<false>;
     // per call: the attribute is per device, and one process may drive several
-    cudaFuncSetAttribute(k_reduce_x1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(reduce_x1_smem(kMaxFusedDx)));
+    cudaFuncSetAttribute(kern1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(reduce_x1_smem(kMaxFusedDx)));
     int per = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_reduce_x1, kRx1Warps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern1, kRx1Warps * 32, smem);
     const int64_t res_items = int64_t(std::max(1, per)) * num_sms * (kRx1Warps / 2);
     int S = kRxMaxSeg;
     while (S > 32 && 4 * int64_t(H) * nb * ((W + S - 1) / S) < 3 * res_items) S >>= 1;
     const int nseg = (W + S - 1) / S;
     const int64_t items = int64_t(H) * nb * nseg;
     const int blocks = int(std::min<int64_t>((items + 1) / 2, res_items / 2));
-    launch_pdl(k_reduce_x1, blocks, kRx1Warps * 32, smem, s, sb.start, sb.val_s, tb.tf, tb.mx, tb.my, W, H, nb, dx,
+    launch_pdl(kern1, blocks, kRx1Warps * 32, smem, s, sb.start, sb.val_s, tb.tf, tb.mx, tb.my, W, H, nb, dx,
                S, nseg, P, R);
     return;
   }

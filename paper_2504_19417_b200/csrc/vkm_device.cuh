@@ -254,6 +254,20 @@ __device__ __forceinline__ void sincos2_hot(uint64_t x, uint64_t& s01, uint64_t&
     sincos2p_f32(x, s01, c01);
 }
 template <bool kMufu>
+__device__ __forceinline__ void sincos2_cs_hot(uint64_t theta, uint64_t& cs0, uint64_t& cs1) {
+  if constexpr (kMufu) {   // (cos, sin) pairs of the two arguments
+    uint64_t s01, c01;
+    sincos2p_mufu(theta, s01, c01);
+    float s0, s1, c0, c1;
+    f2unpack(s01, s0, s1);
+    f2unpack(c01, c0, c1);
+    cs0 = f2pack(c0, s0);
+    cs1 = f2pack(c1, s1);
+  } else {
+    sincos2_cs(theta, cs0, cs1);
+  }
+}
+template <bool kMufu>
 __device__ __forceinline__ void sincos2_k3_scaled(uint64_t x, uint64_t scale01, uint64_t& s01, uint64_t& c01) {
   if constexpr (kMufu)
     sincos2_mufu_scaled(x, scale01, s01, c01);

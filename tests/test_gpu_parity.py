@@ -53,21 +53,27 @@ def angular_stats(got, want, floor=1e-2):
     return (float(np.percentile(d, 99)), float(d.max())) if len(d) else (0.0, 0.0)
 
 
-@pytest.mark.parametrize("sincos", ["mufu", "poly"])
-@pytest.mark.parametrize("mode", ["fp32", "f16x3", "auto"])
+@pytest.mark.parametrize("variant", ["mufu", "poly", "rows"])
+@pytest.mark.parametrize("mode", ["fp32", "f16x3", "auto", "bf16"])
 @pytest.mark.parametrize("case", GOLDEN_CASES)
-def test_predict_matches_reference_golden(case, mode, sincos, monkeypatch):
-    """Flows vs the reference's (max-abs FLOW_TOL) and neighbourhood counts
-    exact, for every MLP mode and both sin/cos flavours of the hot kernels
-    (VKM_SINCOS: special-function unit by default, or the polynomials)."""
-    monkeypatch.setenv("VKM_SINCOS", sincos)
+def test_predict_matches_reference_golden(case, mode, variant, monkeypatch):
+    """Flows vs the reference's (max-abs FLOW_TOL; BF16: 3.5e-3, its angular
+    bound is tested below) and neighbourhood counts exact, for every MLP mode,
+    both sin/cos flavours of the hot kernels (VKM_SINCOS: special-function
+    unit by default, or the polynomials) and both K3 producer layouts
+    (one event per lane by default, VKM_K3=rows: one row per warp)."""
+    monkeypatch.setenv("VKM_SINCOS", "poly" if variant == "poly" else "mufu")
+    if variant == "rows":
+        monkeypatch.setenv("VKM_K3", "rows")
     g = load_golden(case)
     reg = regressor(g, mode)
     if mode == "f16x3" and not (int(g["D"]) == 64 and int(g["w1"].shape[0]) == 128):
         pytest.skip("tensor-core head needs D=64, hidden=128")
+    if mode == "bf16" and not (int(g["D"]) == 64 and int(g["w1"].shape[0]) == 128):
+        pytest.skip("tensor-core head needs D=64, hidden=128")
     flows = reg.predict(g["X"])
     assert flows.dtype == np.float64 and flows.shape == g["flows"].shape
-    np.testing.assert_allclose(flows, g["flows"], rtol=0, atol=FLOW_TOL)
+    np.testing.assert_allclose(flows, g["flows"], rtol=0, atol=3.5e-3 if mode == "bf16" else FLOW_TOL)
     blk = _pkg().block_from_array(g["X"], int(g["width"]), int(g["height"]), 2 * float(g["delta_t"]))
     _, counts = reg.engine().predict_host(blk.events, blk.t_start, return_counts=True)
     np.testing.assert_array_equal(counts, g["counts"])
