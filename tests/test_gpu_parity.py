@@ -367,7 +367,7 @@ def test_batched_slices_many_chunks_edge_cases():
             assert np.isnan(flows[off[i] + len(X) // 2]).all() and cnt[off[i] + len(X) // 2] == 0
 
 
-@pytest.mark.parametrize("sort", ["auto", "counting", "rows"])
+@pytest.mark.parametrize("sort", ["auto", "counting", "rows", "radix"])
 @pytest.mark.parametrize("case", ["hot", "dense"])
 def test_pixel_order_is_the_stable_argsort(case, sort):
     """K1's event order equals accumulate_grid's np.argsort(flat,
