@@ -589,113 +589,77 @@ __global__ void __launch_bounds__(kXsortThreads) k_xsort(const uint64_t* __restr
 
 // ---------------------------------------------------------------------------
 // Dense slices: stable LSD radix sort of (pixel key, slot value), 8-bit
-// digits, one kernel per digit pass in the onesweep style.  A 4096-item tile
-// ranks its items by digit in shared memory (warps walk their 512 items 32 at
-// a time in input order; __match_any_sync gives the in-step order), takes its
-// per-digit global offsets by decoupled look-back over the tiles before it
-// (one thread per digit; the digit totals of every pass come from one
-// histogram kernel), stages the items in digit order in shared memory and
-// writes each digit's run contiguously - so the scattered writes of the
-// counting scatter become ~16-item runs.  Stable, so each pixel's run stays in
-// time order and no run sort is needed.
+// digits.  Per digit pass: k_rs_tilehist counts each 4096-item tile's digits
+// into a digit-major table, k_scan turns it into every (digit, tile)'s global
+// first slot, and k_rs_scatter ranks the tile's items by digit in shared
+// memory (warps walk their 512 items 32 at a time in input order;
+// __match_any_sync gives the in-step order, so the sort is stable), stages
+// them in digit order and writes each digit's run contiguously - ~16-item
+// runs instead of the counting scatter's single 8-byte writes.  Stable, so
+// each pixel's run stays in time order and no run sort is needed.
 // ---------------------------------------------------------------------------
 constexpr int kRsThreads = 256, kRsItems = 16, kRsTile = kRsThreads * kRsItems, kRsWarps = kRsThreads / 32;
 constexpr int kRsBins = 256;
 
-size_t radix_state_words(int64_t n) { return size_t((n + kRsTile - 1) / kRsTile) * kRsBins; }
-
-// digit histograms of every pass (hist[pass][256]) in one read of the keys
-__global__ void __launch_bounds__(256) k_rs_hist(const int32_t* __restrict__ keys, int64_t n, int passes,
-                                                 unsigned int* __restrict__ hist) {
-  __shared__ unsigned int h[4][kRsBins];
-  for (int i = threadIdx.x; i < 4 * kRsBins; i += blockDim.x) (&h[0][0])[i] = 0;
-  __syncthreads();
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
-    const uint32_t k = uint32_t(__ldg(keys + e));
-    for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xFF], 1u);
+__global__ void __launch_bounds__(256) k_rs_tilehist(const int32_t* __restrict__ keys, int64_t n, int shift,
+                                                     int ntiles, int* __restrict__ tab) {
+  pdl_wait();
+  __shared__ int h[kRsBins];
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t e0 = int64_t(t) * kRsTile, e1 = min(n, e0 + kRsTile);
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(h + ((uint32_t(__ldg(keys + e)) >> shift) & 0xFF), 1);
+    __syncthreads();
+    tab[int64_t(threadIdx.x) * ntiles + t] = h[threadIdx.x];   // digit-major: the scan gives global offsets
+    __syncthreads();
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < passes * kRsBins; i += blockDim.x) {
-    const unsigned int v = (&h[0][0])[i];
-    if (v) atomicAdd(hist + i, v);
-  }
+  pdl_trigger();
 }
 
-// exclusive scan of each pass's 256 digit totals (one warp per pass)
-__global__ void k_rs_hist_scan(unsigned int* __restrict__ hist, int passes) {
-  const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (p >= passes) return;
-  unsigned int* h = hist + p * kRsBins;
-  unsigned int v[8], sum = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    v[i] = h[lane * 8 + i];
-    sum += v[i];
-  }
-  unsigned int incl = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned int u = __shfl_up_sync(kFullMask, incl, o);
-    if (lane >= o) incl += u;
-  }
-  unsigned int run = incl - sum;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    h[lane * 8 + i] = run;
-    run += v[i];
-  }
-}
-
-__global__ void __launch_bounds__(kRsThreads) k_rs_pass(const int32_t* __restrict__ kin,
-                                                        const uint64_t* __restrict__ vin, int64_t n, int shift,
-                                                        const unsigned int* __restrict__ digit_start,
-                                                        unsigned long long* __restrict__ state, uint32_t epoch,
-                                                        unsigned int* __restrict__ tile_ticket,
-                                                        int32_t* __restrict__ kout, uint64_t* __restrict__ vout) {
+__global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const int32_t* __restrict__ kin,
+                                                           const uint64_t* __restrict__ vin, int64_t n, int shift,
+                                                           int ntiles, const int* __restrict__ off,
+                                                           int32_t* __restrict__ kout, uint64_t* __restrict__ vout) {
   pdl_wait();
   extern __shared__ __align__(16) uint8_t rs_smem[];
   uint64_t* sval = reinterpret_cast<uint64_t*>(rs_smem);                      // [kRsTile] staged values
   int32_t* skey = reinterpret_cast<int32_t*>(sval + kRsTile);                  // [kRsTile] staged keys
   unsigned int* wcnt = reinterpret_cast<unsigned int*>(skey + kRsTile);       // [kRsWarps][256]
-  unsigned int* tbase = wcnt + kRsWarps * kRsBins;                            // [256] tile digit start (local)
-  unsigned int* gofs = tbase + kRsBins;                                       // [256] global start of the tile's run
-  __shared__ unsigned int tile_id;
+  unsigned int* tbase = wcnt + kRsWarps * kRsBins;                            // [256] tile-local digit start
+  int* gofs = reinterpret_cast<int*>(tbase + kRsBins);                        // [256] global start of the tile's run
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  const int64_t ntiles = (n + kRsTile - 1) / kRsTile;
-  const uint32_t ep = epoch & 0x3fffffffu;
-  volatile unsigned long long* vs = state;
-  for (;;) {
-    if (threadIdx.x == 0) tile_id = atomicAdd(tile_ticket, 1u);   // tiles in start order: look-back never waits on an unstarted tile
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     for (int i = threadIdx.x; i < kRsWarps * kRsBins; i += blockDim.x) wcnt[i] = 0;
+    gofs[threadIdx.x] = __ldg(off + int64_t(threadIdx.x) * ntiles + t);
     __syncthreads();
-    const int64_t t = tile_id;
-    if (t >= ntiles) break;
-    const int64_t base = t * kRsTile + int64_t(w) * (kRsTile / kRsWarps);   // this warp's 512 items
-    // pass 1: digits and warp-local stable ranks (warp-striped: step k covers items base + 32k .. +31)
+    const int64_t base = int64_t(t) * kRsTile + int64_t(w) * (kRsTile / kRsWarps);   // this warp's 512 items
     uint32_t key[kRsItems];
     uint64_t val[kRsItems];
     unsigned int wrank[kRsItems];
     unsigned int* wc = wcnt + w * kRsBins;
 #pragma unroll
-    for (int k = 0; k < kRsItems; ++k) {
+    for (int k = 0; k < kRsItems; ++k) {   // warp-striped: step k covers items base + 32k .. +31
       const int64_t e = base + k * 32 + lane;
       const bool ok = e < n;
       key[k] = ok ? uint32_t(__ldcs(kin + e)) : 0xFFFFFFFFu;
       val[k] = ok ? __ldcs(vin + e) : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < kRsItems; ++k) {
+      const bool ok = base + k * 32 + lane < n;
       const unsigned d = ok ? (key[k] >> shift) & 0xFF : 0x100u;
       const unsigned peers = __match_any_sync(kFullMask, d);
       const unsigned before = __popc(peers & lt);
-      unsigned c = 0;
-      if (ok) c = wc[d];
+      const unsigned c = ok ? wc[d] : 0u;
       wrank[k] = c + before;
       __syncwarp();
       if (ok && before == 0) wc[d] = c + __popc(peers);
       __syncwarp();
     }
     __syncthreads();
-    // per digit: exclusive over warps, tile total; publish, look back
-    {
+    {   // per digit: exclusive over warps, tile total
       const int d = threadIdx.x;   // kRsThreads == kRsBins
       unsigned int run = 0;
       for (int v2 = 0; v2 < kRsWarps; ++v2) {
@@ -703,29 +667,10 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_pass(const int32_t* __restric
         wcnt[v2 * kRsBins + d] = run;
         run += c;
       }
-      const unsigned int total = run;
-      unsigned long long* st = state + t * kRsBins + d;
-      // aggregate (flag 1) then the inclusive prefix (flag 2) once known
-      if (t == 0) {
-        *reinterpret_cast<volatile unsigned long long*>(st) = (uint64_t(ep) << 34) | (2ull << 32) | total;
-        gofs[d] = __ldg(digit_start + d);
-      } else {
-        *reinterpret_cast<volatile unsigned long long*>(st) = (uint64_t(ep) << 34) | (1ull << 32) | total;
-        unsigned int excl = 0;
-        for (int64_t q = t - 1; q >= 0; --q) {
-          uint64_t wd;
-          do wd = vs[q * kRsBins + d]; while (uint32_t(wd >> 34) != ep || ((wd >> 32) & 3) == 0);
-          excl += uint32_t(wd);
-          if (((wd >> 32) & 3) == 2) break;
-        }
-        *reinterpret_cast<volatile unsigned long long*>(st) = (uint64_t(ep) << 34) | (2ull << 32) | (excl + total);
-        gofs[d] = __ldg(digit_start + d) + excl;
-      }
-      tbase[d] = total;   // replaced by the exclusive scan below
+      tbase[d] = run;
     }
     __syncthreads();
-    // exclusive scan of the tile's digit totals (one warp, 8 digits per lane)
-    if (w == 0) {
+    if (w == 0) {   // exclusive scan of the tile's digit totals (8 digits per lane)
       unsigned int v8[8], sum = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -746,11 +691,9 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_pass(const int32_t* __restric
       }
     }
     __syncthreads();
-    // stage in digit order
 #pragma unroll
-    for (int k = 0; k < kRsItems; ++k) {
-      const int64_t e = base + k * 32 + lane;
-      if (e < n) {
+    for (int k = 0; k < kRsItems; ++k) {   // stage in digit order
+      if (base + k * 32 + lane < n) {
         const unsigned d = (key[k] >> shift) & 0xFF;
         const unsigned pos = tbase[d] + wcnt[w * kRsBins + d] + wrank[k];
         skey[pos] = int32_t(key[k]);
@@ -758,12 +701,11 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_pass(const int32_t* __restric
       }
     }
     __syncthreads();
-    // write each digit's run contiguously
-    const int valid = int(min(int64_t(kRsTile), n - t * kRsTile));
-    for (int i = threadIdx.x; i < valid; i += blockDim.x) {
+    const int valid = int(min(int64_t(kRsTile), n - int64_t(t) * kRsTile));
+    for (int i = threadIdx.x; i < valid; i += blockDim.x) {   // each digit's run contiguously
       const uint32_t k = uint32_t(skey[i]);
       const unsigned d = (k >> shift) & 0xFF;
-      const uint64_t dst = uint64_t(gofs[d]) + (i - tbase[d]);
+      const int64_t dst = int64_t(gofs[d]) + (i - int(tbase[d]));
       kout[dst] = int32_t(k);
       vout[dst] = sval[i];
     }
@@ -1108,29 +1050,32 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
     int bits = 1;
     while ((int64_t(1) << bits) <= P) ++bits;   // keys in [0, P] (P: outside the sensor)
     const int passes = (bits + 7) / 8;
-    const int64_t ntiles = (n + kRsTile - 1) / kRsTile;
-    cudaMemsetAsync(sb.rs_hist, 0, sizeof(unsigned int) * (4 * kRsBins + 4), s);
-    k_rs_hist<<<int(std::min<int64_t>((n + 255) / 256, ev_blocks)), 256, 0, s>>>(sb.pix, n, passes, sb.rs_hist);
-    k_rs_hist_scan<<<1, 32 * passes, 0, s>>>(sb.rs_hist, passes);
+    const int ntiles = int((n + kRsTile - 1) / kRsTile);
+    const int64_t m = int64_t(kRsBins) * ntiles;
+    int* tab = sb.msd_tab;                        // msd_tab_words(n) >= 256 * ntiles per half
+    int* off = sb.msd_tab + m;
     const size_t smem = radix_smem_bytes();
-    cudaFuncSetAttribute(k_rs_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per = 1, dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rs_pass, kRsThreads, smem);
-    const int grid = int(std::min<int64_t>(ntiles, int64_t(std::max(1, per)) * sms));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rs_scatter, kRsThreads, smem);
+    const int grid = std::min(ntiles, std::max(1, per) * sms);
+    const int mt = int((m + kScanTile - 1) / kScanTile);
     const int32_t* kin = sb.pix;
     const uint64_t* vin = sb.val;
     for (int p = 0; p < passes; ++p) {
       int32_t* kout = p == passes - 1 ? sb.pix_s : (p % 2 == 0 ? sb.rank : sb.pix);
       uint64_t* vout = p == passes - 1 ? sb.val_s : (p % 2 == 0 ? sb.bkt : sb.val);
-      launch_pdl(k_rs_pass, grid, kRsThreads, smem, s, kin, vin, n, 8 * p,
-                 static_cast<const unsigned int*>(sb.rs_hist + p * kRsBins), sb.rs_state, next_scan_epoch(),
-                 sb.rs_hist + 4 * kRsBins + p, kout, vout);
+      launch_pdl(k_rs_tilehist, std::min(ntiles, ev_blocks), 256, 0, s, kin, n, 8 * p, ntiles, tab);
+      launch_pdl(k_scan, std::min(mt, 148 * 4), kScanThreads, 0, s, static_cast<const int*>(tab), off, m, mt,
+                 sb.msd_state, next_scan_epoch());
+      launch_pdl(k_rs_scatter, grid, kRsThreads, smem, s, kin, vin, n, 8 * p, ntiles, static_cast<const int*>(off),
+                 kout, vout);
       kin = kout;
       vin = vout;
     }
-    launches += 3 + passes;
+    launches += 3 * passes;
   } else if (n > 0 && dense) {
     const int ntiles = int((n + kMsdTile - 1) / kMsdTile);
     const int64_t m = int64_t(R) * ntiles;

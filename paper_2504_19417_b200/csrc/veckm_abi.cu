@@ -172,12 +172,11 @@ int ensure_sort(vkm_handle* h, int64_t n, int64_t Pv) {
   (void)Pv;
   if (h->sort_cap >= cap) return VKM_OK;
   void* arrs[] = {h->sb.pix, h->sb.val, h->sb.val_s, h->sb.pix_s, h->sb.rank, h->sb.bkt, h->sb.msd_tab,
-                  h->sb.msd_state, h->sb.rs_state, h->sb.rs_hist};
+                  h->sb.msd_state};
   for (void* p : arrs)
     if (p) cudaFree(p);
   h->sb.pix = nullptr; h->sb.val = nullptr; h->sb.val_s = nullptr; h->sb.pix_s = nullptr; h->sb.rank = nullptr;
   h->sb.bkt = nullptr; h->sb.msd_tab = nullptr; h->sb.msd_state = nullptr;
-  h->sb.rs_state = nullptr; h->sb.rs_hist = nullptr;
   h->sort_cap = 0;
   VKM_CK(cudaMalloc(&h->sb.pix, 4 * cap));
   VKM_CK(cudaMalloc(&h->sb.rank, 4 * cap));
@@ -190,10 +189,6 @@ int ensure_sort(vkm_handle* h, int64_t n, int64_t Pv) {
     VKM_CK(cudaMalloc(&h->sb.msd_tab, 2 * sizeof(int) * tw));
     VKM_CK(cudaMalloc(&h->sb.msd_state, sizeof(unsigned long long) * sw));
     VKM_CK(cudaMemset(h->sb.msd_state, 0, sizeof(unsigned long long) * sw));   // epoch 0: never published
-    const size_t rw = vkm::radix_state_words(int64_t(cap));
-    VKM_CK(cudaMalloc(&h->sb.rs_state, sizeof(unsigned long long) * rw));
-    VKM_CK(cudaMemset(h->sb.rs_state, 0, sizeof(unsigned long long) * rw));
-    VKM_CK(cudaMalloc(&h->sb.rs_hist, sizeof(unsigned int) * (4 * 256 + 4)));
   }
   h->sort_cap = cap;
   return VKM_OK;
@@ -725,7 +720,7 @@ void vkm_destroy(vkm_handle* h) {
   void* ptrs[] = {h->tf, h->my, h->mx, h->mxp, h->myp, h->xyz64, h->t64, h->mx64, h->my64, h->g64a, h->g64b, h->out64, h->win_ev, h->win_aux, h->w1p, h->b1, h->w2, h->b2, h->w64, h->w1_f16_hi, h->w1_f16_lo, h->w1_bf16,
                   h->G, h->C, h->Q, h->NQ, h->feats, h->cnt_scratch, h->ev_stage, h->out_stage, h->cnt_stage,
                   h->sb.pix, h->sb.val, h->sb.start, h->sb.val_s, h->sb.pix_s, h->sb.scan_state,
-                  h->sb.rank, h->sb.longlist, h->sb.longcount, h->sb.bkt, h->sb.msd_tab, h->sb.msd_state, h->sb.rs_state, h->sb.rs_hist};
+                  h->sb.rank, h->sb.longlist, h->sb.longcount, h->sb.bkt, h->sb.msd_tab, h->sb.msd_state};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->evt)

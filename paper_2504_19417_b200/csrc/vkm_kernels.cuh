@@ -51,17 +51,13 @@ struct SortBufs {
   int32_t* rank;     // [n]   event's arrival rank inside its pixel (k_prep's histogram atomic)
   int* longlist;     // [P]   pixels whose run is longer than one warp sort
   int* longcount;    // [1]   long-run count
-  // dense slices (row-bucket path, k_sort.cu): row buckets of (event, a) and x,
-  // the per-(row, tile) count table + its scan, and the table scan's tile states
+  // dense slices (radix and row-bucket paths, k_sort.cu): the second key/value
+  // buffers, the per-(digit | row, tile) count table + its scan, and the
+  // table scan's tile states
   uint64_t* bkt;                     // [n]
   int* msd_tab;                      // [2 * msd_tab_words(n)]
   unsigned long long* msd_state;     // [scan_state_words(msd_tab_words(n))]
-  // dense slices (radix path): per-(tile, digit) look-back words (zeroed once),
-  // digit histograms of up to 4 passes + their tile tickets
-  unsigned long long* rs_state;      // [radix_state_words(n)]
-  unsigned int* rs_hist;             // [4 * 256 + 4]
 };
-size_t radix_state_words(int64_t n);
 size_t msd_tab_words(int64_t n);     // per-(row, event tile) counters for n events, rows <= kMsdMaxRows
 
 // Slices processed by one launch sequence (batched fused path): slice b owns
