@@ -201,6 +201,17 @@ typedef struct vkm_event_check {
 int vkm_check_events(const double* events_host, int64_t n, int64_t ld, int32_t width, int32_t height,
                      vkm_event_check* out);
 
+/* NormalFlowRegressor.predict's fast path (estimators.py:192-206): one host
+ * pass checks the (n, 3) f64 rows exactly like vkm_check_events and packs
+ * them for the upload; if the rows are valid, time-sorted and span at most
+ * `window` (validation.py:49-65), the slice runs as vkm_predict_host_wide
+ * (t_start = the first row's time) and *ran = 1; otherwise nothing runs,
+ * *ran = 0 and *check holds the checks, so the caller raises the reference's
+ * error (or sorts an unsorted slice and predicts).  Also *ran = 0 for slices
+ * below the packed single-slice size. */
+int vkm_predict_host_checked(vkm_handle* h, const double* events_host, int64_t n, double window,
+                             double* flows_host, vkm_event_check* check, int32_t* ran);
+
 /* Host utility: dst[i] = (double)src[i] for n values, split over the host
  * pool with streaming stores (the float64 results of the batch APIs). */
 int vkm_widen_f32(const float* src, double* dst, int64_t n);

@@ -47,6 +47,7 @@ SIGNATURES = {
     "vkm_set_mlp_mode": (C.c_int, [_P, C.c_int32]),
     "vkm_set_weights_f64": (C.c_int, [_P, _P, _P, _P, _P]),
     "vkm_pixel_order": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P, _P]),
+    "vkm_predict_host_checked": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P, _P]),
     "vkm_predict": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P, _P]),
     "vkm_encode": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P, _P]),
     "vkm_predict_host": (C.c_int, [_P, _P, C.c_int64, C.c_double, _P, _P]),

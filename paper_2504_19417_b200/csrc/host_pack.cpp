@@ -233,6 +233,9 @@ __attribute__((target("avx512f,avx512vl,avx512dq"))) int64_t check_avx512(const 
   if (bad_ord) c.sorted = 0;
   return i;
 }
+}  // namespace
+
+namespace vkm_host {
 // One serial pass over rows [0, n) (X already offset): the flags, the
 // first outside pixel (index relative to X), t of the first and last rows.
 void check_range(const double* X, int64_t n, int64_t ld, int32_t W, int32_t H, vkm_event_check& out) {
@@ -277,7 +280,20 @@ void check_range(const double* X, int64_t n, int64_t ld, int32_t W, int32_t H, v
   out = c;
 }
 
-}  // namespace
+void merge_check(vkm_event_check& c, const vkm_event_check& q) {
+  c.nonfinite |= q.nonfinite;
+  c.negative_t |= q.negative_t;
+  c.nonint |= q.nonint;
+  c.sorted &= q.sorted & !(q.t_first < c.t_last);
+  if (c.first_outside < 0 && q.first_outside >= 0) {
+    c.first_outside = q.first_outside;
+    c.outside_x = q.outside_x;
+    c.outside_y = q.outside_y;
+  }
+  c.t_last = q.t_last;
+}
+}  // namespace vkm_host
+using vkm_host::check_range;
 
 // The host pool of the handle-free host utilities (validation, widening):
 // created on first use, never torn down; one user at a time (try_lock, else
@@ -310,19 +326,7 @@ int vkm_check_events(const double* X, int64_t n, int64_t ld, int32_t W, int32_t 
       if (pc[p].first_outside >= 0) pc[p].first_outside += lo;
     });
     vkm_event_check c = pc[0];
-    for (int p = 1; p < parts; ++p) {
-      const vkm_event_check& q = pc[p];
-      c.nonfinite |= q.nonfinite;
-      c.negative_t |= q.negative_t;
-      c.nonint |= q.nonint;
-      c.sorted &= q.sorted & !(q.t_first < c.t_last);
-      if (c.first_outside < 0 && q.first_outside >= 0) {
-        c.first_outside = q.first_outside;
-        c.outside_x = q.outside_x;
-        c.outside_y = q.outside_y;
-      }
-      c.t_last = q.t_last;
-    }
+    for (int p = 1; p < parts; ++p) vkm_host::merge_check(c, pc[p]);
     *out = c;
     return 0;
   }

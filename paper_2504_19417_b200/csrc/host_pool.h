@@ -13,7 +13,15 @@
 #include <thread>
 #include <vector>
 
+#include "../../include/veckm.h"
+
 namespace vkm_host {
+
+// host_pack.cpp: the input checks of check_event_array over rows [0, n) of
+// (n, ld) f64 rows (first outside pixel relative to X), and the in-order merge
+// of two consecutive ranges' results
+void check_range(const double* X, int64_t n, int64_t ld, int32_t W, int32_t H, vkm_event_check& out);
+void merge_check(vkm_event_check& c, const vkm_event_check& q);
 
 class HostPool {
  public:

@@ -98,6 +98,7 @@ struct Smem {
   // one-event-per-lane variant: pooled-grid rows of a tile's pixel range,
   // bulk-copied (TMA) into slots carved from the (then unused) A images + ring
   int gp0[3];                                   // first pixel of the slot's range, -1: load directly
+  unsigned long long tpair[32];                 // (f32 T_c, f32 T_c+1) of each channel pair, packed
   unsigned long long gfull[3], gempty[3];
 };
 constexpr int kGSlots = 3;
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       if (kSplit) dl[i] = __ldg(w1l + i);
     }
     const float sc = w_scale * f_scale;   // a power of two: exact scaling
+    for (int i = threadIdx.x; i < 32; i += blockDim.x) S.tpair[i] = f2pack(__ldg(tf + 2 * i), __ldg(tf + 2 * i + 1));
     for (int i = threadIdx.x; i < kN; i += blockDim.x) {
       S.b1s[i] = b1[i] * sc;
       S.w2a[i] = w2[i] / sc;
@@ -359,6 +361,7 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       mbar_wait(&S.gfull[gslot], gph);   // this tile's pooled rows have landed (or gp0 = -1)
       const int gp0 = S.gp0[gslot];
       const uint32_t slot_base = gslots + uint32_t(gslot * kGSlotBytes);
+#ifndef VKM_K3_LATE
       float4 v[kLEPairs];
 #pragma unroll
       for (int u = 0; u < kLEPairs; ++u) v[u] = gather(pix_c, u, gp0, slot_base);
@@ -368,6 +371,7 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
         gslot = 0;
         gph ^= 1;
       }
+#endif
 #pragma unroll
       for (int half = 0; half < kLEPairs / 4; ++half) {   // pairs 4·half .. 4·half+3 -> 8 columns per image
         uint32_t hw[8], lw[8];
@@ -375,8 +379,14 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
         for (int h = 0; h < 4; ++h) {
           const int u = 4 * half + h;
           uint64_t sn, cs;
+#ifdef VKM_K3_LATE   // rows and frequencies read at their use: fewer live registers, more chains in flight
+          const uint64_t Tu = S.tpair[kLEPairs * jg + u];
+          const float4 q = gather(pix_c, u, gp0, slot_base);
+          sincos2_k3_scaled<kMufu>(fmul2(aa, Tu), rs2, sn, cs);
+#else
           sincos2_k3_scaled<kMufu>(fmul2(aa, T01[u]), rs2, sn, cs);
           const float4 q = v[u];
+#endif
           const uint64_t ar = f2pack(q.x, q.y), ai = f2pack(q.z, q.w);
           const uint64_t re = ffma2(sn, ai, fmul2(cs, ar));
           const uint64_t im = fsub2(fmul2(cs, ai), fmul2(sn, ar));
@@ -411,6 +421,14 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
         tmem_st8(ta, hw);
         if (kSplit) tmem_st8(ta + 64, lw);
       }
+#ifdef VKM_K3_LATE
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.gempty[gslot]);   // this warp's slot reads are done
+      if (++gslot == kGSlots) {
+        gslot = 0;
+        gph ^= 1;
+      }
+#endif
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       mbar_arrive(&S.full[kS]);

@@ -880,6 +880,80 @@ int vkm_predict_host_wide(vkm_handle* h, const double* ev_host, int64_t n, doubl
   return predict_host_impl(h, ev_host, n, t_start, nullptr, flows_host, counts_host);
 }
 
+int vkm_predict_host_checked(vkm_handle* h, const double* ev_host, int64_t n, double window, double* flows_host,
+                             vkm_event_check* check, int32_t* ran) {
+  if (int rc = check_handle(h)) return rc;
+  if (!ran || !check) return fail(VKM_EINVAL, "null output");
+  *ran = 0;
+  if (h->hidden <= 0) return fail(VKM_EINVAL, "handle has no flow head (hidden == 0)");
+  if (n <= 0 || !ev_host || !flows_host || !single_pack(h, n)) return VKM_OK;   // caller takes the checked path
+  DeviceGuard dg(h->p.device);
+  if (h->hpack_cap[0] < size_t(n)) {
+    if (h->hpack[0]) cudaFreeHost(h->hpack[0]);
+    h->hpack[0] = nullptr;
+    h->hpack_cap[0] = 0;
+    VKM_CK(cudaHostAlloc(&h->hpack[0], sizeof(uint2) * size_t(n), cudaHostAllocDefault));
+    h->hpack_cap[0] = size_t(n);
+  }
+  int rc = grow(&h->ev_stage, &h->ev_cap, size_t(n) * 3);
+  if (!rc) rc = grow(&h->out_stage, &h->out_cap, size_t(n) * 2);
+  if (rc) return rc;
+  if (!h->pool) h->pool = new vkm_host::HostPool(vkm_host::default_pool_threads());
+  cudaStream_t s = h->stream;
+  const double t0 = ev_host[0];   // sorted input: the window start (checked below)
+  uint2* d = reinterpret_cast<uint2*>(h->ev_stage);
+  // One pass over the rows: each host-pool part checks its rows
+  // (check_event_array's predicates, sortedness, first/last time) and packs
+  // them while they are in its cache; piece i+1 is checked and packed while
+  // piece i crosses PCIe.  Kernels run only for valid, sorted input within the
+  // window - otherwise the caller's validation raises the reference's error.
+  const int pieces = int(std::min<int64_t>(4, (n + (1 << 17) - 1) >> 17));
+  vkm_event_check c{0, 0, 0, 1, -1, 0, 0, 0.0, 0.0};
+  bool first = true;
+  for (int i = 0; i < pieces; ++i) {
+    const int64_t lo = n * i / pieces, hi = n * (i + 1) / pieces, m = hi - lo;
+    const int parts = std::max(1, std::min<int>(h->pool->size(), int((m + 32767) / 32768)));
+    std::vector<vkm_event_check> pcv(static_cast<size_t>(parts));
+    vkm_event_check* pc = pcv.data();
+    h->pool->run(parts, [&](int part) {
+      const int64_t a = lo + m * part / parts, b = lo + m * (part + 1) / parts;
+      vkm_event_check& q = pc[part];
+      vkm_host::check_range(ev_host + 3 * a, b - a, 3, h->p.width, h->p.height, q);
+      if (q.first_outside >= 0) q.first_outside += a;
+      vkm_host::pack_events(ev_host + 3 * a, b - a, t0, h->p.delta_t, h->p.width, h->p.height,
+                            reinterpret_cast<uint32_t*>(h->hpack[0] + a));
+    });
+    for (int part = 0; part < parts; ++part) {
+      if (first) {
+        c = pc[part];
+        first = false;
+      } else {
+        vkm_host::merge_check(c, pc[part]);
+      }
+    }
+    VKM_CK(cudaMemcpyAsync(d + lo, h->hpack[0] + lo, sizeof(uint2) * (hi - lo), cudaMemcpyHostToDevice, s));
+  }
+  *check = c;
+  const bool ok = !c.nonfinite && !c.negative_t && !c.nonint && c.first_outside < 0 && c.sorted &&
+                  !(c.t_last - c.t_first > window);
+  if (!ok) {
+    VKM_CK(cudaStreamSynchronize(s));   // the staging is reused by the next call
+    return VKM_OK;
+  }
+  int launches = 0;
+  rec(h, 0, s);
+  rc = predict_chunk(h, h->ev_stage, one_slice(n, t0), h->out_stage, nullptr, s, &launches, d);
+  if (rc) return rc;
+  rec(h, 3, s);
+  rc = download_f32(h, h->out_stage, 2 * n, s, nullptr, flows_host);
+  if (rc) return rc;
+  VKM_CK(cudaStreamSynchronize(s));
+  h->have_timing = h->profiling;
+  h->last_launches = launches;
+  *ran = 1;
+  return VKM_OK;
+}
+
 int vkm_encode_host(vkm_handle* h, const double* ev_host, int64_t n, double t_start, float* feats_host,
                     int32_t* counts_host) {
   if (int rc = check_handle(h)) return rc;
@@ -1006,6 +1080,15 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
         VKM_CK(cudaHostAlloc(&h->hpack[i], sizeof(uint2) * size_t(std::max<int64_t>(nmax, 1)), cudaHostAllocDefault));
         h->hpack_cap[i] = size_t(nmax);
       }
+  // Mixed transfer (VKM_PACK_RAW_EVERY = m > 0): every m-th chunk goes over
+  // PCIe as the caller's raw 24-byte rows (the DMA reads them straight from
+  // pinned host memory), the others host-packed: packing costs host DRAM
+  // traffic (read 24 + write 8 + DMA read 8 B/event), raw rows cost PCIe
+  // bytes (24 B/event), so a mix can balance the two when both bind.
+  static const int raw_every = [] {
+    const char* e = std::getenv("VKM_PACK_RAW_EVERY");
+    return e ? std::max(0, std::atoi(e)) : 0;
+  }();
   cudaStream_t sc = h->stream;
   // slot k = chunk % 2.  copy-in(c) waits until compute(c-2) stopped reading the
   // slot; compute(c) waits for copy-in(c) and for copy-out(c-2) to drain its output;
@@ -1015,12 +1098,13 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
     const vkm::SliceTab& st = chunks[c].second;
     const int64_t lo = offsets[chunks[c].first], n = st.off[st.nb];
     const int k = int(c & 1);
-    if (pack) {
+    const bool pack_c = pack && !(raw_every > 0 && (c % size_t(raw_every)) == size_t(raw_every - 1));
+    if (pack_c) {
       if (c >= 2) VKM_CK(cudaEventSynchronize(h->in_ready[k]));
       pack_chunk(h, ev_host, offsets, t_starts, chunks[c].first, st, h->hpack[k]);
     }
     if (c >= 2) VKM_CK(cudaStreamWaitEvent(h->s_in, h->computed[k], 0));
-    if (pack)
+    if (pack_c)
       VKM_CK(cudaMemcpyAsync(h->pev[k], h->hpack[k], sizeof(uint2) * n, cudaMemcpyHostToDevice, h->s_in));
     else
       VKM_CK(cudaMemcpyAsync(h->pev[k], ev_host + 3 * lo, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, h->s_in));
@@ -1028,7 +1112,7 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
     VKM_CK(cudaStreamWaitEvent(sc, h->in_ready[k], 0));
     if (c >= 2) VKM_CK(cudaStreamWaitEvent(sc, h->out_done[k], 0));
     int rc = predict_chunk(h, h->pev[k], st, h->pout[k], counts_host ? h->pcnt[k] : nullptr, sc, &launches,
-                           pack ? reinterpret_cast<const uint2*>(h->pev[k]) : nullptr);
+                           pack_c ? reinterpret_cast<const uint2*>(h->pev[k]) : nullptr);
     if (rc) return rc;
     VKM_CK(cudaEventRecord(h->computed[k], sc));
     VKM_CK(cudaStreamWaitEvent(h->s_out, h->computed[k], 0));

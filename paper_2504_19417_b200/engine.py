@@ -154,6 +154,23 @@ class FlowEngine:
                                                        counts.ctypes.data if counts is not None else None))
         return (flows, counts) if return_counts else flows
 
+    def predict_host_checked(self, events: np.ndarray, window: float):
+        """vkm_predict_host_checked: one host pass validates and packs the
+        (n, 3) f64 rows; for valid, time-sorted rows within `window` returns
+        the (n, 2) float64 flows (t_start = first row), else None (nothing
+        ran: the caller validates, raises or sorts, and predicts)."""
+        from .validation import _EventCheck
+        ev = events
+        if ev.dtype != np.float64 or ev.ndim != 2 or ev.shape[1] != 3 or not ev.flags.c_contiguous:
+            return None
+        n = len(ev)
+        flows = np.empty((n, 2), dtype=np.float64)
+        chk = _EventCheck()
+        ran = C.c_int32(0)
+        with self._lock: _lib.check(self._lib.vkm_predict_host_checked(self._h, ev.ctypes.data, n, float(window),
+                                                                     flows.ctypes.data, C.byref(chk), C.byref(ran)))
+        return flows if ran.value else None
+
     def predict_batch_host(self, events: np.ndarray, offsets: Sequence[int], t_starts=None,
                            flows: Optional[np.ndarray] = None, return_counts: bool = False):
         """Many slices from host memory in one pipelined call (copy-in of slice

@@ -193,6 +193,13 @@ class NormalFlowRegressor(BaseEstimator):
         """(n, 2) float64 flows in pixels/s; rows in stable time-sorted order
         (input order for sorted input); NaN rows for empty neighbourhoods."""
         eng = self.engine()
+        if self.precision == "f32" and isinstance(X, np.ndarray):
+            # one host pass validates and packs a sorted, valid slice for the
+            # upload (vkm_predict_host_checked); anything else - errors to
+            # raise, unsorted rows, small slices - takes the path below
+            flows = eng.predict_host_checked(X, 2.0 * self.delta_t)
+            if flows is not None:
+                return flows
         block = block_from_array(X, self.width, self.height, 2.0 * self.delta_t)
         if len(block) == 0:
             return np.full((0, 2), np.nan)

@@ -621,3 +621,41 @@ def test_strips_host_matches_unsplit_slice():
         assert np.isnan(f[[5, 6]]).all() and np.isnan(f_ref[[5, 6]]).all()
         good = np.isfinite(f_ref[:, 0])
         np.testing.assert_allclose(f[good], f_ref[good], rtol=0, atol=1e-5)
+
+
+def test_checked_fast_path_equals_validated_path():
+    """predict(X) on a large sorted slice runs vkm_predict_host_checked (one
+    host pass validates and packs); its flows equal the validated path's
+    bitwise, and every input the checks reject (NaN, negative time,
+    non-integer or outside pixels, span > window) raises the reference's
+    error exactly as before; unsorted input falls back to the sorting path."""
+    pkg = _pkg()
+    W, H = 346, 260
+    b = pkg.generate_bases(64)
+    w = pkg.init_weights(64, 128, b, seed=0, dtype=np.float32)
+    reg = pkg.NormalFlowRegressor(width=W, height=H, weights=w)
+    X = vo.synth_uniform_noise(300_000, W, H, seed=12)
+    eng = reg.engine()
+    fast = eng.predict_host_checked(X, 0.032)
+    assert fast is not None
+    blk = pkg.block_from_array(X, W, H, 0.032)
+    np.testing.assert_array_equal(fast, eng.predict_host_wide(blk.events, blk.t_start))
+    np.testing.assert_array_equal(reg.predict(X), fast)
+    cases = [("nan", lambda Y: Y.__setitem__((5, 0), np.nan), "non-finite"),
+             ("neg", lambda Y: Y.__setitem__((0, 0), -1.0), "non-negative"),
+             ("frac", lambda Y: Y.__setitem__((9, 1), 3.5), "integer-valued"),
+             ("out", lambda Y: Y.__setitem__((200_000, 2), H), "outside geometry"),
+             ("span", lambda Y: Y.__setitem__((len(Y) - 1, 0), 1.0), "exceeds the slice window")]
+    for name, mutate, msg in cases:
+        Y = X.copy()
+        mutate(Y)
+        assert eng.predict_host_checked(Y, 0.032) is None, name
+        with pytest.raises(ValueError, match=msg):
+            reg.predict(Y)
+    Y = X.copy()
+    Y[[10, 11]] = Y[[11, 10]]
+    Y[10, 0], Y[11, 0] = X[11, 0] + 1e-9, X[10, 0]        # unsorted pair
+    assert eng.predict_host_checked(Y, 0.032) is None
+    got = reg.predict(Y)
+    order = np.argsort(Y[:, 0], kind="stable")
+    np.testing.assert_allclose(got, reg.predict(Y[order]), rtol=0, atol=0)
