@@ -41,8 +41,13 @@ constexpr int kStages = 2;
 constexpr int kAcc = 4;                // TMEM accumulators (4 x 128 columns = all 512), row-per-warp producers
 // one-event-per-lane producers keep the A operand in TMEM: 2 accumulators
 // (columns 0..255) and 2 stages of A (hi | lo, 128 columns each) from kLeA
-constexpr int kAccLE = 2;
+#ifndef VKM_K3_LE_ACC
+#define VKM_K3_LE_ACC 2   // accumulators; stages of A fill the rest of the 512 columns
+#endif
+constexpr int kAccLE = VKM_K3_LE_ACC;
 constexpr int kLeA = kAccLE * 128;
+constexpr int kStagesLE = (512 - kLeA) / 128;
+static_assert(kStagesLE >= 2 && kStagesLE <= 3, "lane-event TMEM layout");
 constexpr int kTileBytes = kM * kK * 2;        // 32 KB per fp16 operand image
 constexpr int kAtomBytes = kM * 128;           // one 64-wide K atom: 128 rows x 128 B
 constexpr int kProdWarps = 16;                // producer warps (8 tile rows each)
@@ -94,16 +99,19 @@ struct Smem {
   float b2[2];
   float scale;
   uint32_t tmem_base;
-  unsigned long long full[kStages], empty[kStages], tfull[kAcc], tempty[kAcc];
+  unsigned long long full[3], empty[3], tfull[kAcc], tempty[kAcc];
   // one-event-per-lane variant: pooled-grid rows of a tile's pixel range,
   // bulk-copied (TMA) into slots carved from the (then unused) A images + ring
-  int gp0[3];                                   // first pixel of the slot's range, -1: load directly
+  int gp0[4];                                   // first pixel of the slot's range, -1: load directly
   unsigned long long tpair[32];                 // (f32 T_c, f32 T_c+1) of each channel pair, packed
-  unsigned long long gfull[3], gempty[3];
+  unsigned long long gfull[4], gempty[4];
 };
-constexpr int kGSlots = 3;
-constexpr int kGSpan = 96;                        // pixels per plane a slot holds
-constexpr int kGSlotBytes = 8 * kGSpan * 64;      // 48 KB
+#ifndef VKM_K3_GSLOTS
+#define VKM_K3_GSLOTS 3
+#endif
+constexpr int kGSlots = VKM_K3_GSLOTS;
+constexpr int kGSpan = kGSlots == 3 ? 96 : 80;    // pixels per plane a slot holds
+constexpr int kGSlotBytes = 8 * kGSpan * 64;      // 48 KB (40 KB for 4 slots)
 static_assert(kGSlots * kGSlotBytes <= int(2 * kStages * kTileBytes + sizeof(float4) * kProdWarps * kQD * 32),
               "gather slots exceed the A images + ring");
 
@@ -151,6 +159,18 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
     if (it > (1u << 24)) __trap();
   }
 }
+
+#ifdef VKM_K3_WAITPROF   // A/B instrumentation: cycles spent in each kind of barrier wait, per role
+__device__ unsigned long long g_k3_wait[8];
+#define K3_TIMED_WAIT(slot, call)                                  \
+  do {                                                             \
+    const long long t0_ = clock64();                               \
+    call;                                                          \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_k3_wait[slot], (unsigned long long)(clock64() - t0_)); \
+  } while (0)
+#else
+#define K3_TIMED_WAIT(slot, call) call
+#endif
 
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -254,7 +274,7 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       S.b2[0] = b2[0];
       S.b2[1] = b2[1];
       S.scale = 1.f / (w_scale * f_scale);
-      for (int s = 0; s < kStages; ++s) {
+      for (int s = 0; s < 3; ++s) {
         mbar_init(&S.full[s], Roles<kLaneEvent>::prod * 32);
         mbar_init(&S.empty[s], 1);
       }
@@ -353,12 +373,12 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
     float rs_c = recip(pix_c >= 0 ? __ldg(NQ + pix_c) : 0);
     cnt_n = pix_n >= 0 ? __ldg(NQ + pix_n) : 0;
     int gslot = 0, gph = 0;   // gather slot of the current tile and its phase
-    auto tile_step = [&](int64_t tile, int it, auto stage) {
-      constexpr int kS = decltype(stage)::value;
-      const uint32_t ph = (it >> 1) & 1;
+    auto tile_step = [&](int64_t tile, int it) {
+      const int kS = it % kStagesLE;                 // A stage in TMEM
+      const uint32_t ph = (it / kStagesLE) & 1;
       const uint64_t rs2 = f2pack(rs_c, rs_c);
       const uint64_t aa = f2pack(a_c, a_c);
-      mbar_wait(&S.gfull[gslot], gph);   // this tile's pooled rows have landed (or gp0 = -1)
+      K3_TIMED_WAIT(0, mbar_wait(&S.gfull[gslot], gph));   // this tile's pooled rows have landed (or gp0 = -1)
       const int gp0 = S.gp0[gslot];
       const uint32_t slot_base = gslots + uint32_t(gslot * kGSlotBytes);
 #ifndef VKM_K3_LATE
@@ -414,7 +434,7 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
           }
         }
         if (half == 0) {   // the stage is needed only from the first store on
-          mbar_wait(&S.empty[kS], ph ^ 1);
+          K3_TIMED_WAIT(1, mbar_wait(&S.empty[kS], ph ^ 1));
           tc_fence_after();
         }
         const uint32_t ta = ta_lane + uint32_t(kS * 128 + 8 * half);
@@ -440,13 +460,8 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       cnt_n = pix_nn >= 0 ? __ldg(NQ + pix_nn) : 0;
       meta(tile + 3 * G, a_nn, pix_nn);
     };
-    static_assert(kStages == 2, "the producer loop is unrolled by the two stages");
     int it = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += 2 * G, it += 2) {
-      tile_step(tile, it, std::integral_constant<int, 0>{});
-      if (tile + G >= ntiles) break;
-      tile_step(tile + G, it + 1, std::integral_constant<int, 1>{});
-    }
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++it) tile_step(tile, it);
   } else if (!kLaneEvent && warp < kProdWarps) {
     // ======================= producers =======================
     // Warp w fills tile rows [8w, 8w+8) (pixel-sorted slots).  Its pooled-
@@ -666,19 +681,30 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
     // pixel range per channel plane: eight bulk copies (one per plane) move
     // them into a shared-memory slot, three tiles ahead of the producers.
     if (lane == 0) {
+      // the pixel range of the next tile is loaded while this one waits for
+      // its slot, so the global-load latency is off the loader's chain
+      auto range = [&](int64_t tl, int& a, int& b) {
+        a = b = -1;
+        const int64_t f = tl * kM;
+        if (tl < ntiles && f < nv) {
+          const int64_t l = (f + kM < nv ? f + kM : nv) - 1;
+          a = __ldg(pix_s + f);
+          b = __ldg(pix_s + l);
+        }
+      };
+      int pa, pb;
+      range(blockIdx.x, pa, pb);
       int it = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int g = it % kGSlots;
         const uint32_t ph = (it / kGSlots) & 1;
-        mbar_wait(&S.gempty[g], ph ^ 1);
-        const int64_t f = tile * kM;
-        int p0 = -1, span = 0;
-        if (f < nv) {
-          const int64_t l = (f + kM < nv ? f + kM : nv) - 1;
-          p0 = __ldg(pix_s + f);
-          span = __ldg(pix_s + l) - p0 + 1;
-          if (span > kGSpan) p0 = -1;
-        }
+        int na, nb;
+        range(tile + gridDim.x, na, nb);
+        K3_TIMED_WAIT(2, mbar_wait(&S.gempty[g], ph ^ 1));
+        int p0 = pa, span = pb - pa + 1;
+        if (pa < 0 || span > kGSpan) p0 = -1;
+        pa = na;
+        pb = nb;
         S.gp0[g] = p0;
         if (p0 >= 0) {
           const uint32_t bytes = uint32_t(span) * 64u;
@@ -708,7 +734,7 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
         e = slot_event(__ldg(val_s + slot));
         cnt = __ldg(NQ + __ldg(pix_s + slot));
       }
-      mbar_wait(&S.tfull[acc], ph);
+      K3_TIMED_WAIT(3, mbar_wait(&S.tfull[acc], ph));
       tc_fence_after();
       uint64_t oa = 0, ob = 0;   // (even, odd) hidden partial sums of the two outputs
       const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * kN);
@@ -764,11 +790,12 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       const uint32_t bh = smem_u32(S.bh), bl = smem_u32(S.bl);
       int it = 0;
       constexpr int kA = kLaneEvent ? kAccLE : kAcc;
+      constexpr int kSt = kLaneEvent ? kStagesLE : kStages;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int s = it & 1, acc = it & (kA - 1);
-        const uint32_t ph = (it >> 1) & 1, pha = (it / kA) & 1;
-        mbar_wait(&S.tempty[acc], pha ^ 1);
-        mbar_wait(&S.full[s], ph);
+        const int s = it % kSt, acc = it & (kA - 1);
+        const uint32_t ph = (it / kSt) & 1, pha = (it / kA) & 1;
+        K3_TIMED_WAIT(4, mbar_wait(&S.tempty[acc], pha ^ 1));
+        K3_TIMED_WAIT(5, mbar_wait(&S.full[s], ph));
         tc_fence_after();
         const uint32_t d = tmem + uint32_t(acc * kN);
         if (kLaneEvent) {
@@ -816,6 +843,17 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
 }
 
 }  // namespace tc
+
+#ifdef VKM_K3_WAITPROF
+}  // namespace vkm
+extern "C" int vkm_debug_k3_waits(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, vkm::tc::g_k3_wait, sizeof(unsigned long long) * 8);
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(vkm::tc::g_k3_wait, z, sizeof(z));
+  return 0;
+}
+namespace vkm {
+#endif
 
 int feature_kpos(int f) {   // [Re(0..63) | Im(0..63)] -> per channel pair (Re c, Re c+1, Im c, Im c+1)
   const int c = f & 63, im = f >> 6;
