@@ -3,10 +3,15 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl b200|reference]
 
-A step = one pass of the hot path (accumulate -> pool -> gather+MLP) over one
-synthetic slice per rank, inputs resident in HBM, L2 flushed between steps.
-Multi-GPU (torchrun, one rank per GPU): every rank processes its own slices,
-no data-path collective (weak scaling); timing is the max over ranks.
+A step = one pass of the hot path (accumulate -> pool -> gather+MLP) over the
+workload's synthetic slices, inputs resident in HBM, L2 flushed between steps.
+Multi-GPU (torchrun, one rank per GPU), timing the max over ranks:
+  default / cfg1-cfg3  every rank its own slice (weak scaling, no collective)
+  --workload cfg4      BASELINE's 1000 back-to-back slices split over the ranks
+                       (strong scaling, no collective)
+  --split spatial      one slice resident on GPU 0, split into row strips inside
+                       the step (device partition, NCCL strips, flows gathered
+                       back; strong scaling)
 `--impl reference` times the reference algorithm's CPU restatement
 (oracle/veckm_oracle.py, all host threads) on a bounded sample of the same
 workload; on N>1 only rank 0 runs it.
@@ -164,6 +169,12 @@ def cpu_reference(wl, steps, warmup, budget_s=90.0):
     return value, cores, sample, statistics.median(times)
 
 
+def fixed_slice_set(args):
+    """Config 4 (BASELINE: 1000 back-to-back slices sharded over the GPUs):
+    a fixed slice set split over the ranks, i.e. strong scaling."""
+    return args.workload == "cfg4" and not args.slices and args.split != "spatial"
+
+
 def bench_config(args, world):
     """The `config` of both arms' JSON lines (identical by construction, so
     the driver can match the reference arm to this one)."""
@@ -171,11 +182,17 @@ def bench_config(args, world):
     if args.slices:
         slices = args.slices
     spatial = args.split == "spatial"
+    extra = {}
     if spatial:
         par = f"spatial{world} (row strips + {d}-row event halo, device partition + gather of owned flows)"
+    elif fixed_slice_set(args):
+        total = int(os.environ.get("VKM_BENCH_CFG4_SLICES", "1000"))
+        slices = -(-total // world)
+        extra = {"slices_total_per_step": total}
+        par = f"dp{world} (the {total} slices split over the ranks, no collective)"
     else:
         par = f"dp{world} (independent slices per rank, no collective)"
-    return {"workload": desc, "sensor": f"{W}x{H}", "events_per_slice": n, "delta": d,
+    return {"workload": desc, "sensor": f"{W}x{H}", "events_per_slice": n, "delta": d, **extra,
             "slices_per_rank_per_step": 1 if spatial else slices, "embed_dim": 64, "hidden": 128,
             "mlp_mode": args.mlp_mode, "l2": "flushed between steps (512 MiB write, outside step events)",
             "parallelism": par}
@@ -189,7 +206,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-        "scaling": "strong" if args.split == "spatial" else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if (args.split == "spatial" or fixed_slice_set(args)) else "weak", "vs_baseline": None,
+        "dtype": "f32",
         "data": "synthetic (uniform noise, seeded per rank), random-init weights D=64/hidden=128",
         "config": bench_config(args, args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
@@ -264,7 +282,8 @@ def run_b200(args):
         # back-to-back slices of BASELINE split over the ranks (strong scaling)
         from paper_2504_19417_b200.sharding import slice_range
         if args.workload == "cfg4" and not args.slices:
-            mine = slice_range(1000, rank, world)
+            total = int(os.environ.get("VKM_BENCH_CFG4_SLICES", "1000"))   # tests shrink it
+            mine = slice_range(total, rank, world)
         else:
             mine = range(1000 * rank, 1000 * rank + slices)
         host = [_synth(n, W, H, seed=s) for s in mine]
@@ -520,7 +539,7 @@ def run_b200(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong" if spatial else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if (spatial or fixed_slice_set(args)) else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (uniform noise, seeded per rank), random-init weights D=64/hidden=128",
         "config": bench_config(args, world),
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "kernels": kernels,

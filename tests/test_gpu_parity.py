@@ -269,19 +269,26 @@ def test_bench_multirank_shared_gpu(tmp_path):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, VKM_BENCH_SHARED_GPU="1")
-    for split in ("slices", "spatial"):
+    env = dict(os.environ, VKM_BENCH_SHARED_GPU="1", VKM_BENCH_CFG4_SLICES="6")
+    runs = [("cfg1", "slices", 0), ("cfg1", "spatial", 1), ("cfg4", "slices", 2)]
+    for wl, split, k in runs:
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-               "--master-addr", "127.0.0.1", "--master-port", str(29500 + (split == "spatial")),
-               os.path.join(root, "bench.py"), "--gpus", "2", "--workload", "cfg1", "--steps", "3",
-               "--warmup", "3", "--no-e2e", "--no-cpu-baseline", "--split", split]
-        out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=root)
+               "--master-addr", "127.0.0.1", "--master-port", str(29500 + k),
+               os.path.join(root, "bench.py"), "--gpus", "2", "--workload", wl, "--steps", "3",
+               "--warmup", "3", "--no-cpu-baseline", "--split", split]
+        if wl == "cfg4":
+            cmd.append("--no-e2e")
+        out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900, cwd=root)
         assert out.returncode == 0, out.stderr[-2000:]
         lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
         assert len(lines) == 1, out.stdout
         rec = json.loads(lines[0])
         assert rec["n_gpus"] == 2 and rec["value"] > 0
-        assert rec["scaling"] == ("strong" if split == "spatial" else "weak")
+        assert rec["scaling"] == ("strong" if (split == "spatial" or wl == "cfg4") else "weak")
+        if wl == "cfg4":   # the fixed slice set split over the ranks: 3 slices each
+            assert rec["config"]["slices_per_rank_per_step"] == 3
+        if split == "spatial":   # e2e: pinned slice -> GPU 0 -> strips -> flows back
+            assert rec["e2e"]["value"] > 0 and rec["e2e"]["h2d_bytes_per_step"] == 24 * 100_000
 
 
 def test_predict_slices_pipelined_host_batch():

@@ -436,3 +436,6 @@ def test_bench_reference_arm_line_matches_b200_config():
     import bench
     args = argparse.Namespace(workload="cfg1", slices=0, split="slices", mlp_mode="auto")
     assert line["config"] == bench.bench_config(args, 1)
+    a4 = argparse.Namespace(workload="cfg4", slices=0, split="slices", mlp_mode="auto")
+    c4 = bench.bench_config(a4, 8)   # config 4: the 1000 slices split over 8 ranks
+    assert c4["slices_total_per_step"] == 1000 and c4["slices_per_rank_per_step"] == 125
