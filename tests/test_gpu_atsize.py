@@ -3,12 +3,12 @@
 * configs[0]: 346x260, 100k events, delta 10 — every one of the 100k flows
   and neighbourhood counts against the golden frozen from the REAL reference
   (tests/golden/make_golden_cfg1.py), through the drop-in `predict(X)`.
-* configs[2]: 1280x720, 4M events, delta 20 (the long-window k_reduce_x1
-  path) — counts of all 4M events exact (box sums of the pixel histogram),
+* configs[2]: 1280x720, 4M events, delta 20 (41-pixel windows, the longest
+  sliding-window segments) — counts of all 4M events exact (box sums of the pixel histogram),
   flows of 2000 strided queries against the oracle (vo.accumulate_near: the
   reference's per-pixel order over every pixel a query window touches).
 * configs[4] density: the full 1280x720 slice of 32M events (35 ev/px, the
-  dense ordering path) — all counts exact, 200 strided oracle queries; and a
+  dense slices' radix-sort path) — all counts exact, 200 strided oracle queries; and a
   1280x96 band at the same density with 2000 queries.
 * configs[3]: 125 slices of 200k events (346x260) batched through
   predict_slices — all counts exact per slice against box sums, flows of
