@@ -145,6 +145,94 @@ void widen_f32(const float* src, double* dst, int64_t m) {
   for (int64_t i = 0; i < m; ++i) dst[i] = double(src[i]);
 }
 
+// Reads of write-combining staging (the DMA engine's destination; uncached for
+// the CPU, so a D2H never waits on snoops of CPU-cached lines): MOVNTDQA
+// streaming loads of 64-byte lines, scalar reads only up to src's alignment.
+__attribute__((target("avx512f"))) static void widen_wc_avx512(const float* src, double* dst, int64_t m) {
+  int64_t i = 0;
+  for (; i < m && (reinterpret_cast<uintptr_t>(src + i) & 63); ++i) dst[i] = double(src[i]);
+  const bool dal = (reinterpret_cast<uintptr_t>(dst + i) & 63) == 0;
+  // eight lines in flight before the first conversion (WC reads are not
+  // prefetched: each line is a memory round trip)
+  for (; i + 128 <= m; i += 128) {
+    __m512 v[8];
+#pragma GCC unroll 8
+    for (int k = 0; k < 8; ++k) v[k] = _mm512_castsi512_ps(_mm512_stream_load_si512(const_cast<float*>(src + i + 16 * k)));
+#pragma GCC unroll 8
+    for (int k = 0; k < 8; ++k) {
+      const __m512d lo = _mm512_cvtps_pd(_mm512_castps512_ps256(v[k]));
+      const __m512d hi = _mm512_cvtps_pd(_mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castps_pd(v[k]), 1)));
+      if (dal) {
+        _mm512_stream_pd(dst + i + 16 * k, lo);
+        _mm512_stream_pd(dst + i + 16 * k + 8, hi);
+      } else {
+        _mm512_storeu_pd(dst + i + 16 * k, lo);
+        _mm512_storeu_pd(dst + i + 16 * k + 8, hi);
+      }
+    }
+  }
+  for (; i + 16 <= m; i += 16) {
+    const __m512 v = _mm512_castsi512_ps(_mm512_stream_load_si512(const_cast<float*>(src + i)));
+    const __m512d lo = _mm512_cvtps_pd(_mm512_castps512_ps256(v));
+    const __m512d hi = _mm512_cvtps_pd(_mm256_castpd_ps(_mm512_extractf64x4_pd(_mm512_castps_pd(v), 1)));
+    if (dal) {
+      _mm512_stream_pd(dst + i, lo);
+      _mm512_stream_pd(dst + i + 8, hi);
+    } else {
+      _mm512_storeu_pd(dst + i, lo);
+      _mm512_storeu_pd(dst + i + 8, hi);
+    }
+  }
+  _mm_sfence();
+  for (; i < m; ++i) dst[i] = double(src[i]);
+}
+
+__attribute__((target("avx512f"))) static void copy_wc_avx512(const uint8_t* src, uint8_t* dst, size_t bytes) {
+  size_t i = 0;
+  for (; i < bytes && (reinterpret_cast<uintptr_t>(src + i) & 63); ++i) dst[i] = src[i];
+  const bool dal = (reinterpret_cast<uintptr_t>(dst + i) & 63) == 0;
+  for (; i + 512 <= bytes; i += 512) {   // eight lines in flight
+    __m512i v[8];
+#pragma GCC unroll 8
+    for (int k = 0; k < 8; ++k) v[k] = _mm512_stream_load_si512(const_cast<uint8_t*>(src + i + 64 * k));
+#pragma GCC unroll 8
+    for (int k = 0; k < 8; ++k) {
+      if (dal)
+        _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i + 64 * k), v[k]);
+      else
+        _mm512_storeu_si512(dst + i + 64 * k, v[k]);
+    }
+  }
+  if (dal) _mm_sfence();
+  for (; i + 64 <= bytes; i += 64)
+    _mm512_storeu_si512(dst + i, _mm512_stream_load_si512(const_cast<uint8_t*>(src + i)));
+  for (; i < bytes; ++i) dst[i] = src[i];
+}
+
+static bool have_avx512f() {
+  static const bool v = [] {
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx512f");
+  }();
+  return v;
+}
+
+void widen_f32_wc(const float* src, double* dst, int64_t m) {
+  if (have_avx512f()) {
+    widen_wc_avx512(src, dst, m);
+    return;
+  }
+  for (int64_t i = 0; i < m; ++i) dst[i] = double(src[i]);
+}
+
+void copy_wc(const void* src, void* dst, size_t bytes) {
+  if (have_avx512f()) {
+    copy_wc_avx512(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), bytes);
+    return;
+  }
+  std::memcpy(dst, src, bytes);
+}
+
 // out: 2 uint32 per event (the device's uint2 record)
 void pack_events(const double* rows, int64_t m, double t0, double dt, int W, int H, uint32_t* out) {
   static const int isa = [] {
@@ -233,6 +321,74 @@ __attribute__((target("avx512f,avx512vl,avx512dq"))) int64_t check_avx512(const 
   if (bad_ord) c.sorted = 0;
   return i;
 }
+
+// check_avx512's predicates and pack_avx512's records in one pass (rows
+// already in registers once): for contiguous rows, out 32-byte aligned.
+// Returns the first row not processed; c.first_outside is relative to X.
+__attribute__((target("avx512f,avx512vl,avx512dq"))) int64_t check_pack_avx512(const double* X, int64_t n, double t0,
+                                                                                double dt, int W, int H, uint32_t* out,
+                                                                                vkm_event_check& c, double& prev) {
+  const __m512i t01 = _mm512_setr_epi64(0, 3, 6, 9, 12, 15, 0, 0), t2 = _mm512_setr_epi64(0, 1, 2, 3, 4, 5, 10, 13);
+  const __m512i x01 = _mm512_setr_epi64(1, 4, 7, 10, 13, 0, 0, 0), x2 = _mm512_setr_epi64(0, 1, 2, 3, 4, 8, 11, 14);
+  const __m512i y01 = _mm512_setr_epi64(2, 5, 8, 11, 14, 0, 0, 0), y2 = _mm512_setr_epi64(0, 1, 2, 3, 4, 9, 12, 15);
+  const __m512i rot = _mm512_setr_epi64(7, 0, 1, 2, 3, 4, 5, 6);
+  const __m512d dmax = _mm512_set1_pd(1.7976931348623157e308), big = _mm512_set1_pd(4503599627370496.0);
+  const __m512d z = _mm512_setzero_pd(), vt0 = _mm512_set1_pd(t0), vdt = _mm512_set1_pd(dt);
+  const __m256i vW = _mm256_set1_epi32(W), vH = _mm256_set1_epi32(H), z32 = _mm256_setzero_si256();
+  __mmask8 bad_fin = 0, bad_neg = 0, bad_int = 0, bad_ord = 0;
+  int64_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    const double* p = X + 3 * i;
+    const __m512d a0 = _mm512_loadu_pd(p), a1 = _mm512_loadu_pd(p + 8), a2 = _mm512_loadu_pd(p + 16);
+    const __m512d t = _mm512_permutex2var_pd(_mm512_permutex2var_pd(a0, t01, a1), t2, a2);
+    const __m512d x = _mm512_permutex2var_pd(_mm512_permutex2var_pd(a0, x01, a1), x2, a2);
+    const __m512d y = _mm512_permutex2var_pd(_mm512_permutex2var_pd(a0, y01, a1), y2, a2);
+    const __mmask8 fin = _mm512_cmp_pd_mask(_mm512_abs_pd(t), dmax, _CMP_LE_OQ) &
+                         _mm512_cmp_pd_mask(_mm512_abs_pd(x), dmax, _CMP_LE_OQ) &
+                         _mm512_cmp_pd_mask(_mm512_abs_pd(y), dmax, _CMP_LE_OQ);
+    bad_fin |= __mmask8(~fin);
+    bad_neg |= _mm512_cmp_pd_mask(t, z, _CMP_LT_OQ);
+    const __mmask8 xint = _mm512_cmp_pd_mask(_mm512_abs_pd(x), big, _CMP_NLT_UQ) |
+                          _mm512_cmp_pd_mask(_mm512_roundscale_pd(x, _MM_FROUND_TO_ZERO | _MM_FROUND_NO_EXC), x, _CMP_EQ_OQ);
+    const __mmask8 yint = _mm512_cmp_pd_mask(_mm512_abs_pd(y), big, _CMP_NLT_UQ) |
+                          _mm512_cmp_pd_mask(_mm512_roundscale_pd(y, _MM_FROUND_TO_ZERO | _MM_FROUND_NO_EXC), y, _CMP_EQ_OQ);
+    bad_int |= __mmask8(fin & ~(xint & yint));
+    const __m512d tp = _mm512_mask_blend_pd(1, _mm512_permutexvar_pd(rot, t), _mm512_set1_pd(prev));
+    bad_ord |= _mm512_cmp_pd_mask(t, tp, _CMP_LT_OQ);
+    prev = p[21];
+    // truncation (INT_MIN for NaN / out of int32 range): the bounds check and
+    // the record's pixel; the record is valid for in-image integral values
+    const __m256i xi = _mm512_cvttpd_epi32(x), yi = _mm512_cvttpd_epi32(y);
+    const __mmask8 in = _mm256_cmpge_epi32_mask(xi, z32) & _mm256_cmplt_epi32_mask(xi, vW) &
+                        _mm256_cmpge_epi32_mask(yi, z32) & _mm256_cmplt_epi32_mask(yi, vH);
+    if (c.first_outside < 0) {
+      const __mmask8 outm = __mmask8(fin & ~in);
+      if (outm) {
+        const int k = __builtin_ctz(unsigned(outm));
+        alignas(32) int32_t xs[8], ys[8];
+        _mm256_store_si256(reinterpret_cast<__m256i*>(xs), xi);
+        _mm256_store_si256(reinterpret_cast<__m256i*>(ys), yi);
+        c.first_outside = i + k;
+        c.outside_x = xs[k];
+        c.outside_y = ys[k];
+      }
+    }
+    const __mmask8 ok = in & _mm512_cmp_pd_mask(_mm512_cvtepi32_pd(xi), x, _CMP_EQ_OQ) &
+                        _mm512_cmp_pd_mask(_mm512_cvtepi32_pd(yi), y, _CMP_EQ_OQ);
+    const __m256 a = _mm512_cvtpd_ps(_mm512_div_pd(_mm512_sub_pd(t, vt0), vdt));
+    const __m256i xy = _mm256_mask_blend_epi32(ok, _mm256_set1_epi32(-1), _mm256_or_si256(xi, _mm256_slli_epi32(yi, 16)));
+    const __m256i ab = _mm256_castps_si256(a);
+    const __m256i lo = _mm256_unpacklo_epi32(ab, xy), hi = _mm256_unpackhi_epi32(ab, xy);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(out + 2 * i), _mm256_permute2x128_si256(lo, hi, 0x20));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(out + 2 * i + 8), _mm256_permute2x128_si256(lo, hi, 0x31));
+  }
+  _mm_sfence();
+  c.nonfinite |= bad_fin != 0;
+  c.negative_t |= bad_neg != 0;
+  c.nonint |= bad_int != 0;
+  if (bad_ord) c.sorted = 0;
+  return i;
+}
 }  // namespace
 
 namespace vkm_host {
@@ -278,6 +434,59 @@ void check_range(const double* X, int64_t n, int64_t ld, int32_t W, int32_t H, v
     c.t_last = X[(n - 1) * ld];
   }
   out = c;
+}
+
+// check_range + pack_events over contiguous rows [0, n) in one pass: the
+// AVX-512 body between a scalar head (to the records' 32-byte alignment) and
+// a scalar tail, the three parts' checks merged in row order.
+void check_pack(const double* X, int64_t n, double t0, double dt, int32_t W, int32_t H, uint32_t* out,
+                vkm_event_check& res) {
+  static const bool fused = [] {
+    __builtin_cpu_init();
+    const char* e = std::getenv("VKM_CHECK_PACK");
+    return !(e && e[0] == '0') && __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512vl") &&
+           __builtin_cpu_supports("avx512dq");
+  }();
+  if (!fused || n < 64) {
+    check_range(X, n, 3, W, H, res);
+    pack_events(X, n, t0, dt, W, H, out);
+    return;
+  }
+  const int64_t head = std::min<int64_t>(n, int64_t((32 - (reinterpret_cast<uintptr_t>(out) & 31)) & 31) / 8);
+  vkm_event_check c{0, 0, 0, 1, -1, 0, 0, 0.0, 0.0};
+  bool have = false;
+  auto add = [&](const vkm_event_check& q) {
+    if (have) {
+      merge_check(c, q);
+    } else {
+      c = q;
+      have = true;
+    }
+  };
+  if (head > 0) {
+    vkm_event_check q;
+    check_range(X, head, 3, W, H, q);
+    pack_scalar(X, head, t0, dt, W, H, out);
+    add(q);
+  }
+  vkm_event_check b{0, 0, 0, 1, -1, 0, 0, 0.0, 0.0};
+  double prev = X[3 * head];
+  const int64_t body = check_pack_avx512(X + 3 * head, n - head, t0, dt, W, H, out + 2 * head, b, prev);
+  if (body > 0) {
+    if (b.first_outside >= 0) b.first_outside += head;
+    b.t_first = X[3 * head];
+    b.t_last = X[3 * (head + body - 1)];
+    add(b);
+  }
+  const int64_t e = head + body;
+  if (e < n) {
+    vkm_event_check q;
+    check_range(X + 3 * e, n - e, 3, W, H, q);
+    if (q.first_outside >= 0) q.first_outside += e;
+    pack_scalar(X + 3 * e, n - e, t0, dt, W, H, out + 2 * e);
+    add(q);
+  }
+  res = c;
 }
 
 void merge_check(vkm_event_check& c, const vkm_event_check& q) {
@@ -331,6 +540,15 @@ int vkm_check_events(const double* X, int64_t n, int64_t ld, int32_t W, int32_t 
     return 0;
   }
   check_range(X, n, ld, W, H, *out);
+  return 0;
+}
+
+// Test hook (not part of the ABI header): vkm_host::check_pack on
+// contiguous (n, 3) rows, records into out (2 uint32 per event).
+int vkm_debug_check_pack(const double* X, int64_t n, double t0, double dt, int32_t W, int32_t H, uint32_t* out,
+                         vkm_event_check* c) {
+  if (!c || n < 0 || (n > 0 && (!X || !out))) return 1;
+  vkm_host::check_pack(X, n, t0, dt, W, H, out, *c);
   return 0;
 }
 

@@ -21,6 +21,9 @@ namespace vkm_host {
 // (n, ld) f64 rows (first outside pixel relative to X), and the in-order merge
 // of two consecutive ranges' results
 void check_range(const double* X, int64_t n, int64_t ld, int32_t W, int32_t H, vkm_event_check& out);
+// check_range and pack_events of contiguous rows in one pass
+void check_pack(const double* X, int64_t n, double t0, double dt, int32_t W, int32_t H, uint32_t* out,
+                vkm_event_check& res);
 void merge_check(vkm_event_check& c, const vkm_event_check& q);
 
 class HostPool {

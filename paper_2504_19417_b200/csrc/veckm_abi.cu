@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
 #include <functional>
 #include <limits>
@@ -166,6 +167,58 @@ vkm::GridBufs bufs(const vkm_handle* h) { return vkm::GridBufs{h->G, h->C, h->Q,
 void rec(vkm_handle* h, int i, cudaStream_t s) {
   if (h->profiling) cudaEventRecord(h->evt[i], s);
 }
+
+struct HostTrace;
+thread_local HostTrace* g_trace = nullptr;   // the running call's trace (download pieces mark into it)
+
+// VKM_TRACE=1: the drop-in host call prints its host-side stage times and the
+// device span of its copies and kernels to stderr (diagnostics only).
+struct HostTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  std::string out;
+  cudaEvent_t ev[12] = {};
+  const char* ev_name[12] = {};
+  int nev = 0;
+  HostTrace() : on([] {
+    const char* e = std::getenv("VKM_TRACE");
+    return e && *e == '1';
+  }()) {
+    if (on) {
+      t0 = std::chrono::steady_clock::now();
+      g_trace = this;
+    }
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    char b[96];
+    std::snprintf(b, sizeof b, " %s=%.0f", what, us);
+    out += b;
+  }
+  void dev(const char* what, cudaStream_t s) {
+    if (!on || nev == 12) return;
+    cudaEventCreate(&ev[nev]);
+    cudaEventRecord(ev[nev], s);
+    ev_name[nev++] = what;
+  }
+  ~HostTrace() {
+    if (!on) return;
+    std::string d;
+    for (int i = 1; i < nev; ++i) {
+      float ms = 0.f;
+      cudaEventSynchronize(ev[i]);
+      cudaEventElapsedTime(&ms, ev[0], ev[i]);
+      char b[96];
+      std::snprintf(b, sizeof b, " %s=%.0f", ev_name[i], ms * 1e3f);
+      d += b;
+    }
+    for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
+    g_trace = nullptr;
+    std::fprintf(stderr, "[vkm trace] host us:%s | device us from %s:%s\n", out.c_str(), nev ? ev_name[0] : "-",
+                 d.c_str());
+  }
+};
 
 int ensure_sort(vkm_handle* h, int64_t n, int64_t Pv) {
   const size_t cap = size_t(std::max<int64_t>(n, 1));
@@ -353,6 +406,8 @@ namespace vkm_host {
 // host_pack.cpp: vectorised packing of f64 [t, x, y] rows into 8-byte records
 void pack_events(const double* rows, int64_t m, double t0, double dt, int W, int H, uint32_t* out);
 void widen_f32(const float* src, double* dst, int64_t m);
+void widen_f32_wc(const float* src, double* dst, int64_t m);
+void copy_wc(const void* src, void* dst, size_t bytes);
 }  // namespace vkm_host
 namespace {
 
@@ -383,10 +438,26 @@ void pack_chunk(vkm_handle* h, const double* ev, const int64_t* offsets, const d
 }
 
 // Pack events [lo, hi) of one slice (time origin t0) on the host pool.
+// host-pool granularity of the single-slice packing: events per part
+// (VKM_PACK_GRAIN) and pieces per upload (VKM_SINGLE_PIECES)
+int64_t pack_grain() {
+  static const int64_t g = [] {
+    const char* e = std::getenv("VKM_PACK_GRAIN");
+    return e ? std::max<int64_t>(1024, std::atoll(e)) : int64_t(8192);
+  }();
+  return g;
+}
+int single_pieces(int64_t n) {
+  static const int p = [] {
+    const char* e = std::getenv("VKM_SINGLE_PIECES");
+    return e ? std::max(1, std::min(16, std::atoi(e))) : 4;
+  }();
+  return int(std::min<int64_t>(p, (n + (1 << 17) - 1) >> 17));
+}
 void pack_range(vkm_handle* h, const double* ev, int64_t lo, int64_t hi, double t0, uint2* out) {
   if (!h->pool) h->pool = new vkm_host::HostPool(vkm_host::default_pool_threads());
   const int64_t m = hi - lo;
-  const int parts = std::max(1, std::min<int>(h->pool->size(), int((m + 32767) / 32768)));
+  const int parts = std::max(1, std::min<int>(h->pool->size(), int((m + pack_grain() - 1) / pack_grain())));
   h->pool->run(parts, [&](int part) {
     const int64_t a = lo + m * part / parts, b = lo + m * (part + 1) / parts;
     if (b > a)
@@ -434,29 +505,47 @@ int upload_packed(vkm_handle* h, const double* ev_host, int64_t n, double t0, cu
 // D2H of `bytes` bytes through page-locked staging, in up to four pieces:
 // consume(lo, hi) (on the host pool, byte range of the result) runs for
 // piece i while piece i+1 is in flight.  Returns with every piece consumed.
+// The result staging is write-combining memory, read back with streaming
+// loads: the CPU never caches its lines, so the next call's D2H does not wait
+// on snoops of lines the widening left in the cores' caches (first 2-MB piece
+// 46 instead of 110-160 us).  VKM_HOUT_WC=0: ordinary page-locked memory.
+bool hout_wc() {
+  static const bool v = [] {
+    const char* e = std::getenv("VKM_HOUT_WC");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 template <class Consume>
 int download_staged(vkm_handle* h, const void* dev, size_t bytes, size_t align, cudaStream_t s, Consume consume) {
   if (h->hout_cap < bytes) {
     if (h->hout) cudaFreeHost(h->hout);
     h->hout = nullptr;
     h->hout_cap = 0;
-    VKM_CK(cudaHostAlloc(&h->hout, bytes, cudaHostAllocDefault));
+    VKM_CK(cudaHostAlloc(&h->hout, bytes, hout_wc() ? cudaHostAllocWriteCombined : cudaHostAllocDefault));
     h->hout_cap = bytes;
   }
   for (auto& e : h->dl_ev)
     if (!e) VKM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   const size_t units = bytes / align;
-  const int pieces = int(std::max<size_t>(1, std::min<size_t>(4, (bytes + (size_t(1) << 20) - 1) >> 20)));
+  static const size_t max_pieces = [] {   // VKM_DL_PIECES (A/B)
+    const char* e = std::getenv("VKM_DL_PIECES");
+    return e ? size_t(std::max(1, std::min(4, std::atoi(e)))) : size_t(4);
+  }();
+  const int pieces = int(std::max<size_t>(1, std::min<size_t>(max_pieces, (bytes + (size_t(1) << 20) - 1) >> 20)));
   auto edge = [&](int i) { return units * size_t(i) / size_t(pieces) * align; };
   for (int i = 0; i < pieces; ++i) {
     VKM_CK(cudaMemcpyAsync(h->hout + edge(i), static_cast<const uint8_t*>(dev) + edge(i), edge(i + 1) - edge(i),
                            cudaMemcpyDeviceToHost, s));
     VKM_CK(cudaEventRecord(h->dl_ev[i], s));
+    if (g_trace) g_trace->dev("d2h", s);
   }
   if (!h->pool) h->pool = new vkm_host::HostPool(vkm_host::default_pool_threads());
   for (int i = 0; i < pieces; ++i) {
     const size_t lo = edge(i) / align, len = edge(i + 1) / align - lo;
     VKM_CK(cudaEventSynchronize(h->dl_ev[i]));
+    if (g_trace) g_trace->mark("dl");
     const int parts = int(std::max<size_t>(1, std::min<size_t>(size_t(h->pool->size()), (len * align) >> 18)));
     h->pool->run(parts, [&](int part) {
       consume((lo + len * size_t(part) / size_t(parts)) * align, (lo + len * size_t(part + 1) / size_t(parts)) * align);
@@ -470,7 +559,9 @@ int download_f32(vkm_handle* h, const float* dev, int64_t m, cudaStream_t s, flo
   return download_staged(h, dev, sizeof(float) * size_t(m), sizeof(float), s, [&](size_t a, size_t b) {
     const float* st = reinterpret_cast<const float*>(h->hout);   // (re)allocated by download_staged
     if (out64)
-      vkm_host::widen_f32(st + a / 4, out64 + a / 4, int64_t((b - a) / 4));
+      (hout_wc() ? vkm_host::widen_f32_wc : vkm_host::widen_f32)(st + a / 4, out64 + a / 4, int64_t((b - a) / 4));
+    else if (hout_wc())
+      vkm_host::copy_wc(h->hout + a, reinterpret_cast<uint8_t*>(out32) + a, b - a);
     else
       std::memcpy(reinterpret_cast<uint8_t*>(out32) + a, h->hout + a, b - a);
   });
@@ -479,7 +570,10 @@ int download_f32(vkm_handle* h, const float* dev, int64_t m, cudaStream_t s, flo
 // bytes copied as they are (float64 results)
 int download_raw(vkm_handle* h, const void* dev, size_t bytes, cudaStream_t s, void* out) {
   return download_staged(h, dev, bytes, 8, s, [&](size_t a, size_t b) {
-    std::memcpy(static_cast<uint8_t*>(out) + a, h->hout + a, b - a);
+    if (hout_wc())
+      vkm_host::copy_wc(h->hout + a, static_cast<uint8_t*>(out) + a, b - a);
+    else
+      std::memcpy(static_cast<uint8_t*>(out) + a, h->hout + a, b - a);
   });
 }
 
@@ -907,21 +1001,22 @@ int vkm_predict_host_checked(vkm_handle* h, const double* ev_host, int64_t n, do
   // them while they are in its cache; piece i+1 is checked and packed while
   // piece i crosses PCIe.  Kernels run only for valid, sorted input within the
   // window - otherwise the caller's validation raises the reference's error.
-  const int pieces = int(std::min<int64_t>(4, (n + (1 << 17) - 1) >> 17));
+  const int pieces = single_pieces(n);
   vkm_event_check c{0, 0, 0, 1, -1, 0, 0, 0.0, 0.0};
   bool first = true;
+  HostTrace tr;
+  tr.dev("start", s);
   for (int i = 0; i < pieces; ++i) {
     const int64_t lo = n * i / pieces, hi = n * (i + 1) / pieces, m = hi - lo;
-    const int parts = std::max(1, std::min<int>(h->pool->size(), int((m + 32767) / 32768)));
+    const int parts = std::max(1, std::min<int>(h->pool->size(), int((m + pack_grain() - 1) / pack_grain())));
     std::vector<vkm_event_check> pcv(static_cast<size_t>(parts));
     vkm_event_check* pc = pcv.data();
     h->pool->run(parts, [&](int part) {
       const int64_t a = lo + m * part / parts, b = lo + m * (part + 1) / parts;
       vkm_event_check& q = pc[part];
-      vkm_host::check_range(ev_host + 3 * a, b - a, 3, h->p.width, h->p.height, q);
+      vkm_host::check_pack(ev_host + 3 * a, b - a, t0, h->p.delta_t, h->p.width, h->p.height,
+                           reinterpret_cast<uint32_t*>(h->hpack[0] + a), q);
       if (q.first_outside >= 0) q.first_outside += a;
-      vkm_host::pack_events(ev_host + 3 * a, b - a, t0, h->p.delta_t, h->p.width, h->p.height,
-                            reinterpret_cast<uint32_t*>(h->hpack[0] + a));
     });
     for (int part = 0; part < parts; ++part) {
       if (first) {
@@ -931,8 +1026,10 @@ int vkm_predict_host_checked(vkm_handle* h, const double* ev_host, int64_t n, do
         vkm_host::merge_check(c, pc[part]);
       }
     }
+    tr.mark("packed");
     VKM_CK(cudaMemcpyAsync(d + lo, h->hpack[0] + lo, sizeof(uint2) * (hi - lo), cudaMemcpyHostToDevice, s));
   }
+  tr.dev("uploaded", s);
   *check = c;
   const bool ok = !c.nonfinite && !c.negative_t && !c.nonint && c.first_outside < 0 && c.sorted &&
                   !(c.t_last - c.t_first > window);
@@ -945,8 +1042,12 @@ int vkm_predict_host_checked(vkm_handle* h, const double* ev_host, int64_t n, do
   rc = predict_chunk(h, h->ev_stage, one_slice(n, t0), h->out_stage, nullptr, s, &launches, d);
   if (rc) return rc;
   rec(h, 3, s);
+  tr.dev("computed", s);
+  tr.mark("launched");
   rc = download_f32(h, h->out_stage, 2 * n, s, nullptr, flows_host);
   if (rc) return rc;
+  tr.dev("downloaded", s);
+  tr.mark("widened");
   VKM_CK(cudaStreamSynchronize(s));
   h->have_timing = h->profiling;
   h->last_launches = launches;

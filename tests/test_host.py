@@ -300,6 +300,66 @@ def test_native_event_check_parallel_parts():
         _assert_check_matches(lib, X, W, H)
 
 
+def test_fused_check_pack_matches_check_and_records():
+    """vkm_host::check_pack (the drop-in call's one pass: checks + 8-byte
+    records, AVX-512 body between a scalar head and tail) gives
+    vkm_check_events' answer and the records k_prep would build: f32 bits of
+    (t - t0)/dt and x | y << 16, or 0xFFFFFFFF for rows outside the image or
+    not integral; records written at every alignment of the output."""
+    import ctypes
+    from paper_2504_19417_b200 import _lib, validation as v
+    lib = _lib.load()
+    fn = lib.vkm_debug_check_pack
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
+                   ctypes.c_void_p, ctypes.c_void_p]
+    rng = np.random.default_rng(21)
+    W, H = 40, 30
+    for trial in range(200):
+        n = int(rng.integers(0, 400)) if trial % 4 else int(rng.integers(1000, 5000))
+        X = np.stack([np.sort(rng.uniform(0, 0.03, n)), rng.integers(-2, W + 2, n), rng.integers(-2, H + 2, n)],
+                     1).astype(np.float64)
+        for _ in range(int(rng.integers(0, 4))):
+            if n == 0:
+                break
+            i, kind = int(rng.integers(0, n)), int(rng.integers(0, 7))
+            if kind == 0:
+                X[i, 1 + int(rng.integers(0, 2))] = np.nan
+            elif kind == 1:
+                X[i, 1] = -np.inf
+            elif kind == 2:
+                X[i, 0] = -1e-3
+            elif kind == 3:
+                X[i, 1 + int(rng.integers(0, 2))] += 0.5
+            elif kind == 4:
+                X[i, 1] = 3e9
+            elif kind == 5:
+                X[i, 0] = 0.05 * rng.uniform()
+            else:
+                X[i, 2] = -0.0
+        t0, dt = (X[0, 0] if n else 0.0), 1e-3
+        shift = trial % 4                                  # record alignment: 8-byte steps inside a 32-byte line
+        buf = np.zeros(2 * (n + 8), dtype=np.uint32)
+        out = buf[2 * shift: 2 * (shift + n)]
+        c = v._EventCheck()
+        assert fn(X.ctypes.data, n, t0, dt, W, H, out.ctypes.data, ctypes.byref(c)) == 0
+        ref = v._EventCheck()
+        assert lib.vkm_check_events(X.ctypes.data, n, 3, W, H, ctypes.byref(ref)) == 0
+        for f in ("nonfinite", "negative_t", "nonint", "sorted", "first_outside", "outside_x", "outside_y"):
+            assert getattr(c, f) == getattr(ref, f), (trial, f)
+        if n:
+            assert (c.t_first, c.t_last) == (ref.t_first, ref.t_last)
+        rec = out.reshape(-1, 2)
+        with np.errstate(invalid="ignore"):
+            a = ((X[:, 0] - t0) / dt).astype(np.float32).view(np.uint32)
+            x, y = X[:, 1], X[:, 2]
+            ok = (x >= 0) & (x < W) & (y >= 0) & (y < H) & (x == np.floor(x)) & (y == np.floor(y))
+            xy = np.where(ok, np.nan_to_num(x).astype(np.int64) | (np.nan_to_num(y).astype(np.int64) << 16),
+                          0xFFFFFFFF).astype(np.uint32)
+        assert np.array_equal(rec[:, 0], a), trial
+        assert np.array_equal(rec[:, 1], xy), trial
+
+
 def test_product_path_does_not_import_the_oracle():
     """oracle/ is test infrastructure only: importing the package and building
     an estimator pulls in nothing from it (run in a fresh interpreter)."""
