@@ -589,27 +589,55 @@ __global__ void __launch_bounds__(kXsortThreads) k_xsort(const uint64_t* __restr
 
 // ---------------------------------------------------------------------------
 // Dense slices: stable LSD radix sort of (pixel key, slot value), 8-bit
-// digits.  Per digit pass: k_rs_tilehist counts each 4096-item tile's digits
+// digits.  Per digit pass: k_rs_tilehist counts each 3072-item tile's digits
 // into a digit-major table, k_scan turns it into every (digit, tile)'s global
 // first slot, and k_rs_scatter ranks the tile's items by digit in shared
 // memory (warps walk their 512 items 32 at a time in input order;
 // __match_any_sync gives the in-step order, so the sort is stable), stages
-// them in digit order and writes each digit's run contiguously - ~16-item
-// runs instead of the counting scatter's single 8-byte writes.  Stable, so
+// them in digit order and writes each digit's run contiguously - ~12-item
+// runs instead of the counting scatter's single 8-byte writes.  12 items per
+// thread measured best at config 5 (16: 2 x 114 KB blocks per SM waited on
+// shared memory; 8: a 2x larger digit table to scan; 4: 1.4x slower).  Stable, so
 // each pixel's run stays in time order and no run sort is needed.
 // ---------------------------------------------------------------------------
-constexpr int kRsThreads = 256, kRsItems = 16, kRsTile = kRsThreads * kRsItems, kRsWarps = kRsThreads / 32;
+#ifndef VKM_RS_ITEMS
+#define VKM_RS_ITEMS 12
+#endif
+constexpr int kRsThreads = 256, kRsItems = VKM_RS_ITEMS, kRsTile = kRsThreads * kRsItems, kRsWarps = kRsThreads / 32;
 constexpr int kRsBins = 256;
 
 __global__ void __launch_bounds__(256) k_rs_tilehist(const int32_t* __restrict__ keys, int64_t n, int shift,
                                                      int ntiles, int* __restrict__ tab) {
   pdl_wait();
   __shared__ int h[kRsBins];
+  static_assert(kRsItems % 4 == 0, "one thread = kRsItems / 4 16-byte key loads");
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     h[threadIdx.x] = 0;
+    const int64_t e0 = int64_t(t) * kRsTile;
+    uint32_t k[kRsItems];
+    if (e0 + kRsTile <= n) {   // full tile: independent 16-byte loads per thread, issued together
+      const int4* src = reinterpret_cast<const int4*>(keys + e0);
+#pragma unroll
+      for (int j = 0; j < kRsItems / 4; ++j) {
+        const int4 v = __ldcs(src + threadIdx.x + 256 * j);
+        k[4 * j] = uint32_t(v.x);
+        k[4 * j + 1] = uint32_t(v.y);
+        k[4 * j + 2] = uint32_t(v.z);
+        k[4 * j + 3] = uint32_t(v.w);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kRsItems; ++j) {
+        const int64_t e = e0 + 4 * (threadIdx.x + 256 * (j >> 2)) + (j & 3);
+        k[j] = e < n ? uint32_t(__ldcs(keys + e)) : 0xFFFFFFFFu;
+      }
+    }
     __syncthreads();
-    const int64_t e0 = int64_t(t) * kRsTile, e1 = min(n, e0 + kRsTile);
-    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicAdd(h + ((uint32_t(__ldg(keys + e)) >> shift) & 0xFF), 1);
+#pragma unroll
+    for (int j = 0; j < kRsItems; ++j) {
+      const int64_t e = e0 + 4 * (threadIdx.x + 256 * (j >> 2)) + (j & 3);
+      if (e < n) atomicAdd(h + ((k[j] >> shift) & 0xFF), 1);
+    }
     __syncthreads();
     tab[int64_t(threadIdx.x) * ntiles + t] = h[threadIdx.x];   // digit-major: the scan gives global offsets
     __syncthreads();
@@ -617,45 +645,103 @@ __global__ void __launch_bounds__(256) k_rs_tilehist(const int32_t* __restrict__
   pdl_trigger();
 }
 
-__global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const int32_t* __restrict__ kin,
+// The tile's keys and values arrive by two bulk copies (TMA engine) into an
+// input buffer, issued for the block's next tile as soon as the current one
+// is in registers, so the loads' DRAM latency overlaps the ranking, staging
+// and writing of the current tile.  (Loading with per-thread loads at the top
+// of each tile left the 16 resident warps per SM waiting on DRAM: 22 % of
+// HBM, 0.36 ms per pass at config 5.)
+#ifndef VKM_RS_MINB
+#define VKM_RS_MINB 2
+#endif
+template <bool kMatch>
+__global__ void __launch_bounds__(kRsThreads, VKM_RS_MINB) k_rs_scatter(const int32_t* __restrict__ kin,
                                                            const uint64_t* __restrict__ vin, int64_t n, int shift,
                                                            int ntiles, const int* __restrict__ off,
                                                            int32_t* __restrict__ kout, uint64_t* __restrict__ vout) {
-  pdl_wait();
-  extern __shared__ __align__(16) uint8_t rs_smem[];
-  uint64_t* sval = reinterpret_cast<uint64_t*>(rs_smem);                      // [kRsTile] staged values
-  int32_t* skey = reinterpret_cast<int32_t*>(sval + kRsTile);                  // [kRsTile] staged keys
+  extern __shared__ __align__(128) uint8_t rs_smem[];
+  uint64_t* ival = reinterpret_cast<uint64_t*>(rs_smem);                      // [kRsTile] input values (TMA)
+  uint64_t* sval = ival + kRsTile;                                            // [kRsTile] staged values
+  int32_t* ikey = reinterpret_cast<int32_t*>(sval + kRsTile);                 // [kRsTile] input keys (TMA)
+  int32_t* skey = ikey + kRsTile;                                             // [kRsTile] staged keys
   unsigned int* wcnt = reinterpret_cast<unsigned int*>(skey + kRsTile);       // [kRsWarps][256]
   unsigned int* tbase = wcnt + kRsWarps * kRsBins;                            // [256] tile-local digit start
   int* gofs = reinterpret_cast<int*>(tbase + kRsBins);                        // [256] global start of the tile's run
+  unsigned int* wmask = reinterpret_cast<unsigned int*>(gofs + kRsBins);     // [kRsWarps][256] digit lane masks
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wmask + kRsWarps * kRsBins);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
+  // bytes of tile t the bulk copies bring (16-byte multiples; the rest of a
+  // ragged last tile is read from global memory)
+  auto kbytes = [&](int t) { return uint32_t(min(int64_t(kRsTile), n - int64_t(t) * kRsTile) * 4) & ~15u; };
+  auto vbytes = [&](int t) { return uint32_t(min(int64_t(kRsTile), n - int64_t(t) * kRsTile) * 8) & ~15u; };
+  auto issue = [&](int t) {   // one thread
+    if (t >= ntiles) return;
+    const uint32_t kb = kbytes(t), vb = vbytes(t);
+    fence_async_smem();   // the buffer's previous contents were read through the generic proxy
+    mbar_arrive_tx(bar, kb + vb);
+    if (kb) bulk_g2s(ikey, kin + int64_t(t) * kRsTile, kb, bar);
+    if (vb) bulk_g2s(ival, vin + int64_t(t) * kRsTile, vb, bar);
+  };
+  for (int i = threadIdx.x; i < kRsWarps * kRsBins; i += blockDim.x) wmask[i] = 0u;   // kept zero between steps
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  if (threadIdx.x == 0) issue(blockIdx.x);
+  uint32_t phase = 0;
+  // the digit's global start for the block's next tile, loaded a tile ahead
+  // (256 scattered words of the digit-major table: an L2 round trip)
+  int gnext = blockIdx.x < ntiles ? __ldg(off + int64_t(threadIdx.x) * ntiles + blockIdx.x) : 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     for (int i = threadIdx.x; i < kRsWarps * kRsBins; i += blockDim.x) wcnt[i] = 0;
-    gofs[threadIdx.x] = __ldg(off + int64_t(threadIdx.x) * ntiles + t);
-    __syncthreads();
-    const int64_t base = int64_t(t) * kRsTile + int64_t(w) * (kRsTile / kRsWarps);   // this warp's 512 items
+    gofs[threadIdx.x] = gnext;
+    if (t + int(gridDim.x) < ntiles) gnext = __ldg(off + int64_t(threadIdx.x) * ntiles + t + gridDim.x);
+    const int64_t t0 = int64_t(t) * kRsTile;
+    const int valid = int(min(int64_t(kRsTile), n - t0));
+    const int kfull = int(kbytes(t) >> 2), vfull = int(vbytes(t) >> 3);
+    const int wb = w * (kRsTile / kRsWarps);   // this warp's 512 items (tile-local)
     uint32_t key[kRsItems];
     uint64_t val[kRsItems];
     unsigned int wrank[kRsItems];
     unsigned int* wc = wcnt + w * kRsBins;
+    unsigned int* wm = wmask + w * kRsBins;
+    mbar_wait(bar, phase);
+    phase ^= 1u;
 #pragma unroll
-    for (int k = 0; k < kRsItems; ++k) {   // warp-striped: step k covers items base + 32k .. +31
-      const int64_t e = base + k * 32 + lane;
-      const bool ok = e < n;
-      key[k] = ok ? uint32_t(__ldcs(kin + e)) : 0xFFFFFFFFu;
-      val[k] = ok ? __ldcs(vin + e) : 0ull;
+    for (int k = 0; k < kRsItems; ++k) {   // warp-striped: step k covers items wb + 32k .. +31
+      const int i = wb + k * 32 + lane;
+      key[k] = i < kfull ? uint32_t(ikey[i]) : (i < valid ? uint32_t(__ldg(kin + t0 + i)) : 0xFFFFFFFFu);
+      val[k] = i < vfull ? ival[i] : (i < valid ? __ldg(vin + t0 + i) : 0ull);
     }
+    __syncthreads();   // input buffer consumed, counters zeroed
+    if (threadIdx.x == 0) issue(t + gridDim.x);
 #pragma unroll
     for (int k = 0; k < kRsItems; ++k) {
-      const bool ok = base + k * 32 + lane < n;
-      const unsigned d = ok ? (key[k] >> shift) & 0xFF : 0x100u;
-      const unsigned peers = __match_any_sync(kFullMask, d);
+      const bool ok = wb + k * 32 + lane < valid;
+      unsigned d, peers;
+      if (kMatch) {   // few distinct digits (the top pass): MATCH.ANY
+        d = ok ? (key[k] >> shift) & 0xFF : 0x100u;
+        peers = __match_any_sync(kFullMask, d);
+      } else {
+        // lanes with equal digits: each ORs its bit into the digit's mask
+        // word (shared atomics; MATCH.ANY over up to 32 distinct 8-bit digits
+        // was the kernel's main stall: 0.36 -> 0.31 ms per pass at config 5)
+        d = (key[k] >> shift) & 0xFF;
+        if (ok) atomicOr(wm + d, 1u << lane);
+        __syncwarp();
+        peers = ok ? wm[d] : 0u;
+      }
       const unsigned before = __popc(peers & lt);
       const unsigned c = ok ? wc[d] : 0u;
       wrank[k] = c + before;
       __syncwarp();
-      if (ok && before == 0) wc[d] = c + __popc(peers);
+      if (ok && before == 0) {
+        wc[d] = c + __popc(peers);
+        if (!kMatch) wm[d] = 0u;
+      }
       __syncwarp();
     }
     __syncthreads();
@@ -693,7 +779,7 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const int32_t* __rest
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kRsItems; ++k) {   // stage in digit order
-      if (base + k * 32 + lane < n) {
+      if (wb + k * 32 + lane < valid) {
         const unsigned d = (key[k] >> shift) & 0xFF;
         const unsigned pos = tbase[d] + wcnt[w * kRsBins + d] + wrank[k];
         skey[pos] = int32_t(key[k]);
@@ -701,7 +787,6 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const int32_t* __rest
       }
     }
     __syncthreads();
-    const int valid = int(min(int64_t(kRsTile), n - int64_t(t) * kRsTile));
     for (int i = threadIdx.x; i < valid; i += blockDim.x) {   // each digit's run contiguously
       const uint32_t k = uint32_t(skey[i]);
       const unsigned d = (k >> shift) & 0xFF;
@@ -714,7 +799,7 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const int32_t* __rest
   pdl_trigger();
 }
 
-size_t radix_smem_bytes() { return size_t(kRsTile) * 12 + size_t(kRsWarps + 2) * kRsBins * 4; }
+size_t radix_smem_bytes() { return size_t(kRsTile) * 24 + size_t(2 * kRsWarps + 2) * kRsBins * 4 + 16; }
 
 // ---------------------------------------------------------------------------
 // Exclusive scan of the per-pixel counts, one pass: each 4096-count tile
@@ -1055,11 +1140,12 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
     int* tab = sb.msd_tab;                        // msd_tab_words(n) >= 256 * ntiles per half
     int* off = sb.msd_tab + m;
     const size_t smem = radix_smem_bytes();
-    cudaFuncSetAttribute(k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_rs_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_rs_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int per = 1, dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rs_scatter, kRsThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rs_scatter<false>, kRsThreads, smem);
     const int grid = std::min(ntiles, std::max(1, per) * sms);
     const int mt = int((m + kScanTile - 1) / kScanTile);
     const int32_t* kin = sb.pix;
@@ -1070,8 +1156,14 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
       launch_pdl(k_rs_tilehist, std::min(ntiles, ev_blocks), 256, 0, s, kin, n, 8 * p, ntiles, tab);
       launch_pdl(k_scan, std::min(mt, 148 * 4), kScanThreads, 0, s, static_cast<const int*>(tab), off, m, mt,
                  sb.msd_state, next_scan_epoch());
-      launch_pdl(k_rs_scatter, grid, kRsThreads, smem, s, kin, vin, n, 8 * p, ntiles, static_cast<const int*>(off),
-                 kout, vout);
+      // a top digit of <= 4 bits has <= 16 values: MATCH.ANY ranks it faster
+      // than the shared-atomic masks (few words, many lanes each)
+      if (bits - 8 * p <= 4)
+        launch_pdl(k_rs_scatter<true>, grid, kRsThreads, smem, s, kin, vin, n, 8 * p, ntiles,
+                   static_cast<const int*>(off), kout, vout);
+      else
+        launch_pdl(k_rs_scatter<false>, grid, kRsThreads, smem, s, kin, vin, n, 8 * p, ntiles,
+                   static_cast<const int*>(off), kout, vout);
       kin = kout;
       vin = vout;
     }
