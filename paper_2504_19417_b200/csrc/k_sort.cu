@@ -613,10 +613,14 @@ __global__ void __launch_bounds__(256) k_run_starts(const int32_t* __restrict__ 
 #pragma unroll
       for (int j = 0; j < 4; ++j) k[j + 1] = i0 + j < n ? __ldg(pix_s + i0 + j) : int32_t(P + 1);
     }
+    if (k[0] != k[4]) {   // a run boundary among these slots (1 in 35 at config 5)
+      const int Pi = int(P), i0i = int(i0), ni = int(n);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (i0 + j > n) break;
-      for (int64_t p = int64_t(k[j]) + 1; p <= min(int64_t(k[j + 1]), P); ++p) start[p] = int(i0 + j);
+      for (int j = 0; j < 4; ++j) {
+        if (i0i + j > ni) break;
+        const int hi = min(k[j + 1], Pi);
+        for (int p = k[j] + 1; p <= hi; ++p) start[p] = i0i + j;
+      }
     }
   }
   pdl_trigger();

@@ -19,5 +19,5 @@ for args in "--workload cfg5 --split spatial" "--workload cfg4"; do
   echo "rc n2 $name $?"
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gather|k_reduce_x|k_box_y" -s 12 -c 3 -o gpurun_out/prof_full_${T}_cfg2 python bench.py --workload cfg2 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_${T}_cfg2.log 2>&1; echo "rc ncu-full cfg2 $?"
-timeout 900 ncu --set full --clock-control none -k regex:"k_gather|k_reduce_x" -s 6 -c 2 -o gpurun_out/prof_full_${T}_cfg5 python bench.py --workload cfg5 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_${T}_cfg5.log 2>&1; echo "rc ncu-full cfg5 $?"
+timeout 900 ncu --set full --clock-control none -k regex:"k_gather|k_reduce_x|k_rs_scatter" -s 8 -c 3 -o gpurun_out/prof_full_${T}_cfg5 python bench.py --workload cfg5 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_${T}_cfg5.log 2>&1; echo "rc ncu-full cfg5 $?"
 for f in gpurun_out/bench_${T}_*.jsonl; do python -c "import json,sys;d=json.loads(open('$f').readlines()[-1]);print('$f',d.get('config',{}).get('workload','')[:30],'%.3e'%d['value'],'e2e %.3e'%(d.get('e2e') or {}).get('value',0),(d.get('clocks') or {}).get('reasons'))" 2>/dev/null; done
