@@ -93,7 +93,7 @@ struct Smem {
 #endif
   // head constants with the power-of-two operand scale s = w_scale·f_scale
   // folded in: relu(acc/s + b1)·w2 == relu(acc + s·b1)·(w2/s) exactly
-  float b1s[kN];    // s·b1
+  float b1s[kN];    // -s·b1 (relu(h + b1) = max(h, -b1) + b1; the + b1 part is folded into b2)
   float w2a[kN];    // w2[0][n] / s
   float w2b[kN];    // w2[1][n] / s
   float b2[2];
@@ -266,13 +266,20 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
     const float sc = w_scale * f_scale;   // a power of two: exact scaling
     for (int i = threadIdx.x; i < 32; i += blockDim.x) S.tpair[i] = f2pack(__ldg(tf + 2 * i), __ldg(tf + 2 * i + 1));
     for (int i = threadIdx.x; i < kN; i += blockDim.x) {
-      S.b1s[i] = b1[i] * sc;
+      S.b1s[i] = -b1[i] * sc;
       S.w2a[i] = w2[i] / sc;
       S.w2b[i] = w2[kN + i] / sc;
     }
     if (threadIdx.x == 0) {
-      S.b2[0] = b2[0];
-      S.b2[1] = b2[1];
+      // W2·relu(h + b1) + b2 = W2·max(h, -b1) + (b2 + W2·b1): the epilogue
+      // skips the bias add (two FADD2 per four hidden units)
+      double c0 = b2[0], c1 = b2[1];
+      for (int i = 0; i < kN; ++i) {
+        c0 += double(w2[i]) * double(b1[i]);
+        c1 += double(w2[kN + i]) * double(b1[i]);
+      }
+      S.b2[0] = float(c0);
+      S.b2[1] = float(c1);
       S.scale = 1.f / (w_scale * f_scale);
       for (int s = 0; s < 3; ++s) {
         mbar_init(&S.full[s], Roles<kLaneEvent>::prod * 32);
@@ -756,14 +763,12 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
             : "r"(taddr + cb));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {   // 4 hidden units: 3 LDS.128, 2 FADD2, 4 FMNMX, 4 FFMA2
-          const float4 bb = *reinterpret_cast<const float4*>(S.b1s + cb + i);
+        for (int i = 0; i < 32; i += 4) {   // 4 hidden units: 3 LDS.128, 4 FMNMX, 4 FFMA2
+          const float4 nb = *reinterpret_cast<const float4*>(S.b1s + cb + i);
           const float4 wa = *reinterpret_cast<const float4*>(S.w2a + cb + i);
           const float4 wb = *reinterpret_cast<const float4*>(S.w2b + cb + i);
-          float h0, h1, h2, h3;
-          f2unpack(fadd2(f2pack(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), f2pack(bb.x, bb.y)), h0, h1);
-          f2unpack(fadd2(f2pack(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])), f2pack(bb.z, bb.w)), h2, h3);
-          const uint64_t h01 = f2pack(fmaxf(h0, 0.f), fmaxf(h1, 0.f)), h23 = f2pack(fmaxf(h2, 0.f), fmaxf(h3, 0.f));
+          const uint64_t h01 = f2pack(fmaxf(__uint_as_float(r[i]), nb.x), fmaxf(__uint_as_float(r[i + 1]), nb.y));
+          const uint64_t h23 = f2pack(fmaxf(__uint_as_float(r[i + 2]), nb.z), fmaxf(__uint_as_float(r[i + 3]), nb.w));
           oa = ffma2(h01, f2pack(wa.x, wa.y), oa);
           oa = ffma2(h23, f2pack(wa.z, wa.w), oa);
           ob = ffma2(h01, f2pack(wb.x, wb.y), ob);
