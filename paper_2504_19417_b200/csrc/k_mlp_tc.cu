@@ -270,16 +270,26 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       S.w2a[i] = w2[i] / sc;
       S.w2b[i] = w2[kN + i] / sc;
     }
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
       // W2·relu(h + b1) + b2 = W2·max(h, -b1) + (b2 + W2·b1): the epilogue
-      // skips the bias add (two FADD2 per four hidden units)
-      double c0 = b2[0], c1 = b2[1];
-      for (int i = 0; i < kN; ++i) {
+      // skips the bias add (two FADD2 per four hidden units); the dot
+      // products in f64, spread over the warp
+      double c0 = 0.0, c1 = 0.0;
+      for (int i = lane; i < kN; i += 32) {
         c0 += double(w2[i]) * double(b1[i]);
         c1 += double(w2[kN + i]) * double(b1[i]);
       }
-      S.b2[0] = float(c0);
-      S.b2[1] = float(c1);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+      }
+      if (lane == 0) {
+        S.b2[0] = float(double(b2[0]) + c0);
+        S.b2[1] = float(double(b2[1]) + c1);
+      }
+    }
+    if (threadIdx.x == 0) {
       S.scale = 1.f / (w_scale * f_scale);
       for (int s = 0; s < 3; ++s) {
         mbar_init(&S.full[s], Roles<kLaneEvent>::prod * 32);
