@@ -1191,6 +1191,7 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
     return e ? std::max(0, std::atoi(e)) : 0;
   }();
   cudaStream_t sc = h->stream;
+  HostTrace tr;   // VKM_TRACE=1: per chunk, when the host finished waiting (w) and packing (p)
   // slot k = chunk % 2.  copy-in(c) waits until compute(c-2) stopped reading the
   // slot; compute(c) waits for copy-in(c) and for copy-out(c-2) to drain its output;
   // packing chunk c waits until copy-in(c-2) has drained the host staging slot.
@@ -1202,7 +1203,9 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
     const bool pack_c = pack && !(raw_every > 0 && (c % size_t(raw_every)) == size_t(raw_every - 1));
     if (pack_c) {
       if (c >= 2) VKM_CK(cudaEventSynchronize(h->in_ready[k]));
+      tr.mark("w");
       pack_chunk(h, ev_host, offsets, t_starts, chunks[c].first, st, h->hpack[k]);
+      tr.mark("p");
     }
     if (c >= 2) VKM_CK(cudaStreamWaitEvent(h->s_in, h->computed[k], 0));
     if (pack_c)
@@ -1222,8 +1225,10 @@ int vkm_predict_batch_host(vkm_handle* h, const double* ev_host, const int64_t* 
       VKM_CK(cudaMemcpyAsync(counts_host + lo, h->pcnt[k], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, h->s_out));
     VKM_CK(cudaEventRecord(h->out_done[k], h->s_out));
   }
+  tr.mark("enq");
   VKM_CK(cudaStreamSynchronize(h->s_out));
   VKM_CK(cudaStreamSynchronize(sc));
+  tr.mark("done");
   h->have_timing = false;
   h->last_launches = launches;
   return VKM_OK;
