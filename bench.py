@@ -570,6 +570,15 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=90.0,
                     help="--impl reference: seconds of host work the whole run is sized to")
     args = ap.parse_args()
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    if local_world > 1 and "VKM_HOST_THREADS" not in os.environ:
+        # one host pool per rank: share the node's cores instead of every rank
+        # starting min(16, cores) threads (read when the library creates its pool)
+        try:
+            cores = len(os.sched_getaffinity(0))
+        except AttributeError:
+            cores = os.cpu_count() or 1
+        os.environ["VKM_HOST_THREADS"] = str(max(2, min(16, cores // local_world)))
     if args.impl == "reference":
         run_reference(args)
     else:
