@@ -110,6 +110,12 @@ struct Smem {
 #define VKM_K3_GSLOTS 3
 #endif
 constexpr int kGSlots = VKM_K3_GSLOTS;
+#ifndef VKM_K3_LDSPLIT   // 1: the producers load the second half of their pooled rows mid-tile
+#define VKM_K3_LDSPLIT 1
+#endif
+#ifndef VKM_K3_LDAHEAD   // L > 0 (with LDSPLIT): pair u+L's row is loaded when pair u's math starts
+#define VKM_K3_LDAHEAD 0
+#endif
 constexpr int kGSpan = kGSlots == 3 ? 96 : 80;    // pixels per plane a slot holds
 constexpr int kGSlotBytes = 8 * kGSpan * 64;      // 48 KB (40 KB for 4 slots)
 static_assert(kGSlots * kGSlotBytes <= int(2 * kStages * kTileBytes + sizeof(float4) * kProdWarps * kQD * 32),
@@ -400,6 +406,51 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       const uint32_t slot_base = gslots + uint32_t(gslot * kGSlotBytes);
 #ifndef VKM_K3_LATE
       float4 v[kLEPairs];
+#ifndef VKM_K3_GATHER_PER_PAIR
+      // warp-uniform gp0 >= 0: one base address, the pieces at fixed offsets.
+      // Rows past the slice's events (pix -1) read pixel gp0: their outputs
+      // are never stored and MMA rows do not mix.
+      const bool blk = gp0 >= 0;
+      const uint32_t gbase =
+          slot_base + uint32_t(((kLEPairs / 4) * jg * kGSpan + (pix_c > gp0 ? pix_c - gp0 : 0)) * 64);
+      auto ld_half = [&](int half) {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int u = 4 * half + h;
+          const uint32_t a = gbase + uint32_t((u >> 2) * kGSpan * 64 + (u & 3) * 16);
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w) : "r"(a));
+        }
+      };
+      auto ld_one = [&](int u) {
+        const uint32_t a = gbase + uint32_t((u >> 2) * kGSpan * 64 + (u & 3) * 16);
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w) : "r"(a));
+      };
+      if (blk) {
+#if VKM_K3_LDAHEAD
+#pragma unroll
+        for (int u = 0; u < VKM_K3_LDAHEAD; ++u) ld_one(u);
+#else
+        ld_half(0);
+#endif
+#if VKM_K3_LDSPLIT == 0
+#pragma unroll
+        for (int half = 1; half < kLEPairs / 4; ++half) ld_half(half);
+#endif
+      } else {
+#pragma unroll
+        for (int u = 0; u < kLEPairs; ++u) v[u] = gather(pix_c, u, -1, slot_base);
+      }
+#if VKM_K3_LDSPLIT == 0
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.gempty[gslot]);   // reads are done (registers hold the rows)
+      if (++gslot == kGSlots) {
+        gslot = 0;
+        gph ^= 1;
+      }
+#endif
+#else
 #pragma unroll
       for (int u = 0; u < kLEPairs; ++u) v[u] = gather(pix_c, u, gp0, slot_base);
       __syncwarp();
@@ -409,13 +460,38 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
         gph ^= 1;
       }
 #endif
+#endif
 #pragma unroll
       for (int half = 0; half < kLEPairs / 4; ++half) {   // pairs 4·half .. 4·half+3 -> 8 columns per image
         uint32_t hw[8], lw[8];
+#if !defined(VKM_K3_LATE) && !defined(VKM_K3_GATHER_PER_PAIR) && VKM_K3_LDSPLIT && !VKM_K3_LDAHEAD
+        if (half > 0 && blk) ld_half(half);   // the second half's rows load under the first half's math
+        if (half == kLEPairs / 4 - 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.gempty[gslot]);   // reads issued (release orders them before the TMA refill)
+          if (++gslot == kGSlots) {
+            gslot = 0;
+            gph ^= 1;
+          }
+        }
+#endif
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           const int u = 4 * half + h;
           uint64_t sn, cs;
+#if !defined(VKM_K3_LATE) && !defined(VKM_K3_GATHER_PER_PAIR) && VKM_K3_LDSPLIT && VKM_K3_LDAHEAD
+          if (u + VKM_K3_LDAHEAD < kLEPairs) {   // pair u+L's row loads under pair u's math
+            if (blk) ld_one(u + VKM_K3_LDAHEAD);
+            if (u + VKM_K3_LDAHEAD == kLEPairs - 1) {
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&S.gempty[gslot]);
+              if (++gslot == kGSlots) {
+                gslot = 0;
+                gph ^= 1;
+              }
+            }
+          }
+#endif
 #ifdef VKM_K3_LATE   // rows and frequencies read at their use: fewer live registers, more chains in flight
           const uint64_t Tu = S.tpair[kLEPairs * jg + u];
           const float4 q = gather(pix_c, u, gp0, slot_base);

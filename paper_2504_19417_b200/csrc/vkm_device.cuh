@@ -185,17 +185,37 @@ __device__ __forceinline__ void sincos2p_pi_scaled(uint64_t x, uint64_t scale01,
   c01 = fmul2(cr, f);
 }
 
+// Argument reduction ahead of sin.approx / cos.approx (which scale by 1/2π
+// with round-toward-zero and take the fraction of a turn: the absolute error
+// of that scaled argument grows with |x|).  VKM_MUFU_RED selects
+//   2 (default) rint(x / 2π) and a two-part Cody-Waite step: 4 FMA-pipe ops
+//   1           one Cody-Waite term (error k·1.7e-7 more): 3 ops
+//   0           none (|x| <= ~14 here, so the turn fraction keeps ~22 bits)
+#ifndef VKM_MUFU_RED
+#define VKM_MUFU_RED 2
+#endif
+__device__ __forceinline__ uint64_t mufu_reduce2(uint64_t x) {
+#if VKM_MUFU_RED == 0
+  return x;
+#else
+  const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
+  const uint64_t qb = ffma2(x, f2pack(0.159154943f, 0.159154943f), magic);   // rint(x / 2π)
+  const uint64_t q = fsub2(qb, magic);
+  uint64_t r = ffma2(q, f2pack(-6.28318548e+00f, -6.28318548e+00f), x);
+#if VKM_MUFU_RED >= 2
+  r = ffma2(q, f2pack(1.74845553e-07f, 1.74845553e-07f), r);
+#endif
+  return r;
+#endif
+}
+
 // Special-function-unit variant: reduction by 2π (two-part Cody-Waite) to
 // [-π, π], then MUFU.SIN / MUFU.COS (sin.approx: max abs error 2^-21.4 there,
 // ~3 ulp of 1.0), the per-pair scale applied last.  Four XU-pipe and five
 // FMA-pipe instructions per pair instead of ~17 FMA-pipe: for kernels whose
 // producers are FMA-pipe bound (K3's de-phase).
 __device__ __forceinline__ void sincos2_mufu_scaled(uint64_t x, uint64_t scale01, uint64_t& s01, uint64_t& c01) {
-  const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
-  const uint64_t qb = ffma2(x, f2pack(0.159154943f, 0.159154943f), magic);   // rint(x / 2π)
-  const uint64_t q = fsub2(qb, magic);
-  uint64_t r = ffma2(q, f2pack(-6.28318548e+00f, -6.28318548e+00f), x);
-  r = ffma2(q, f2pack(1.74845553e-07f, 1.74845553e-07f), r);
+  const uint64_t r = mufu_reduce2(x);
   float r0, r1;
   f2unpack(r, r0, r1);
   float s0, s1, c0, c1;
@@ -222,11 +242,7 @@ __device__ __forceinline__ void sincos2p_f32(uint64_t theta, uint64_t& s01, uint
 // k_reduce_x 128 -> 132 us, K3 ~equal, ncu cfg2) and is 2x less accurate, so
 // the pi/2-reduced version is the default; -DVKM_SINCOS_PI selects the other.
 __device__ __forceinline__ void sincos2p_mufu(uint64_t x, uint64_t& s01, uint64_t& c01) {
-  const uint64_t magic = f2pack(12582912.0f, 12582912.0f);
-  const uint64_t qb = ffma2(x, f2pack(0.159154943f, 0.159154943f), magic);   // rint(x / 2π)
-  const uint64_t q = fsub2(qb, magic);
-  uint64_t r = ffma2(q, f2pack(-6.28318548e+00f, -6.28318548e+00f), x);
-  r = ffma2(q, f2pack(1.74845553e-07f, 1.74845553e-07f), r);
+  const uint64_t r = mufu_reduce2(x);
   float r0, r1, s0, s1, c0, c1;
   f2unpack(r, r0, r1);
   asm("sin.approx.f32 %0, %1;" : "=f"(s0) : "f"(r0));
