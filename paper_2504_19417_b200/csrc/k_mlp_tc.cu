@@ -113,6 +113,9 @@ constexpr int kGSlots = VKM_K3_GSLOTS;
 #ifndef VKM_K3_LDSPLIT   // 1: the producers load the second half of their pooled rows mid-tile
 #define VKM_K3_LDSPLIT 1
 #endif
+#ifndef VKM_K3_EPI_PIPE   // 1: double-buffered 16-column TMEM loads in the epilogue
+#define VKM_K3_EPI_PIPE 1
+#endif
 #ifndef VKM_K3_LDAHEAD   // L > 0 (with LDSPLIT): pair u+L's row is loaded when pair u's math starts
 #define VKM_K3_LDAHEAD 0
 #endif
@@ -831,6 +834,52 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       tc_fence_after();
       uint64_t oa = 0, ob = 0;   // (even, odd) hidden partial sums of the two outputs
       const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * kN);
+#if VKM_K3_EPI_PIPE
+      // 16-column chunks, double-buffered: the TMEM load of chunk c+1 is in
+      // flight while chunk c is reduced, and the accumulator is released as
+      // soon as its last chunk is in registers (before that chunk's math)
+      auto ld16 = [&](uint32_t (&r)[16], int cb) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr + cb));
+      };
+      auto red16 = [&](const uint32_t (&r)[16], int cb) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+          const float4 nb = *reinterpret_cast<const float4*>(S.b1s + cb + i);
+          const float4 wa = *reinterpret_cast<const float4*>(S.w2a + cb + i);
+          const float4 wb = *reinterpret_cast<const float4*>(S.w2b + cb + i);
+          const uint64_t h01 = f2pack(fmaxf(__uint_as_float(r[i]), nb.x), fmaxf(__uint_as_float(r[i + 1]), nb.y));
+          const uint64_t h23 = f2pack(fmaxf(__uint_as_float(r[i + 2]), nb.z), fmaxf(__uint_as_float(r[i + 3]), nb.w));
+          oa = ffma2(h01, f2pack(wa.x, wa.y), oa);
+          oa = ffma2(h23, f2pack(wa.z, wa.w), oa);
+          ob = ffma2(h01, f2pack(wb.x, wb.y), ob);
+          ob = ffma2(h23, f2pack(wb.z, wb.w), ob);
+        }
+      };
+      {
+        uint32_t ra[16], rb[16];
+        ld16(ra, 0);
+#pragma unroll
+        for (int cb = 0; cb < kN; cb += 32) {
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          ld16(rb, cb + 16);
+          red16(ra, cb);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (cb + 32 < kN) {
+            ld16(ra, cb + 32);
+          } else {
+            tc_fence_before();
+            mbar_arrive(&S.tempty[acc]);
+          }
+          red16(rb, cb + 16);
+        }
+      }
+      if (false)
+#endif
 #ifdef VKM_K3_NOEPI   // A/B skeleton: no epilogue math
       if (false)
 #endif
@@ -861,8 +910,10 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
           ob = ffma2(h23, f2pack(wb.z, wb.w), ob);
         }
       }
+#if !VKM_K3_EPI_PIPE
       tc_fence_before();
       mbar_arrive(&S.tempty[acc]);
+#endif
       float oa0, oa1, ob0, ob1;
       f2unpack(oa, oa0, oa1);
       f2unpack(ob, ob0, ob1);
