@@ -61,13 +61,20 @@ constexpr int kThreads = (kProdWarps + 5) * 32; // + 4 epilogue warps + 1 MMA wa
 #endif
 constexpr int kLEProd = VKM_K3_LEPROD;
 constexpr int kLEPairs = 32 * 4 / kLEProd;       // channel pairs per producer lane
-constexpr int kThreadsLE = (kLEProd + 6) * 32;
+#ifndef VKM_K3_EPIW
+#define VKM_K3_EPIW 4   // epilogue warps of the lane-event variant: 4, or 8 (two per TMEM lane quarter, half the
+                        // hidden units each: 72 registers with spills, K3 +18 % at cfg 5 - not used)
+#endif
+constexpr int kEpiLE = VKM_K3_EPIW;
+static_assert(kEpiLE == 4 || kEpiLE == 8, "epilogue warps");
+constexpr int kThreadsLE = (kLEProd + kEpiLE + 2) * 32;
 template <bool kLaneEvent>
 struct Roles {
   static constexpr int prod = kLaneEvent ? kLEProd : kProdWarps;
-  static constexpr int epi0 = prod;                // 4 epilogue warps
-  static constexpr int mma = prod + 4;
-  static constexpr int loader = prod + 5;          // lane-event variant only
+  static constexpr int epi = kLaneEvent ? kEpiLE : 4;
+  static constexpr int epi0 = prod;                // epilogue warps
+  static constexpr int mma = prod + epi;
+  static constexpr int loader = prod + epi + 1;    // lane-event variant only
   static constexpr int threads = kLaneEvent ? kThreadsLE : kThreads;
 };
 constexpr uint32_t kTmemCols = kAcc * kN;
@@ -123,6 +130,8 @@ constexpr int kGSpan = kGSlots == 3 ? 96 : 80;    // pixels per plane a slot hol
 constexpr int kGSlotBytes = 8 * kGSpan * 64;      // 48 KB (40 KB for 4 slots)
 static_assert(kGSlots * kGSlotBytes <= int(2 * kStages * kTileBytes + sizeof(float4) * kProdWarps * kQD * 32),
               "gather slots exceed the A images + ring");
+static_assert(kGSlots * kGSlotBytes + 2 * kM * 8 <= int(2 * kStages * kTileBytes + sizeof(float4) * kProdWarps * kQD * 32),
+              "gather slots + epilogue hand-over exceed the A images + ring");
 
 static_assert(sizeof(Smem) + 1024 <= 232448, "K3 shared memory exceeds the 227 KB opt-in limit");
 
@@ -306,7 +315,7 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       }
       for (int a = 0; a < kAcc; ++a) {
         mbar_init(&S.tfull[a], 1);
-        mbar_init(&S.tempty[a], 128);
+        mbar_init(&S.tempty[a], 32 * Roles<kLaneEvent>::epi);
       }
       for (int g = 0; g < kGSlots; ++g) {
         mbar_init(&S.gfull[g], 1);
@@ -815,9 +824,16 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= Roles<kLaneEvent>::epi0 && warp < Roles<kLaneEvent>::epi0 + 4) {
+  } else if (warp >= Roles<kLaneEvent>::epi0 && warp < Roles<kLaneEvent>::epi0 + Roles<kLaneEvent>::epi) {
     // ======================= epilogue =======================
     const int q = warp & 3;   // TMEM lane quadrant = warp id % 4
+    // 8 epilogue warps: warps q and q + 4 share lane quadrant q, each reducing
+    // half of the hidden units; the upper half hands its partial outputs over
+    // through shared memory (named barrier 1 + q per pair)
+    constexpr int kEh = Roles<kLaneEvent>::epi / 4;
+    static_assert(kEh == 1 || VKM_K3_EPI_PIPE, "8 epilogue warps need the pipelined epilogue");
+    const int eh = kEh == 1 ? 0 : (warp - Roles<kLaneEvent>::epi0) >> 2;
+    const int cbeg = eh * (kN / kEh);
     int it = 0;
     constexpr int kA = kLaneEvent ? kAccLE : kAcc;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -826,7 +842,7 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       const int64_t slot = tile * kM + q * 32 + lane;
       int cnt = 1;
       int64_t e = -1;
-      if (slot < nv) {
+      if (slot < nv && eh == 0) {
         e = slot_event(__ldg(val_s + slot));
         cnt = __ldg(NQ + __ldg(pix_s + slot));
       }
@@ -862,14 +878,15 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       };
       {
         uint32_t ra[16], rb[16];
-        ld16(ra, 0);
+        ld16(ra, cbeg);
 #pragma unroll
-        for (int cb = 0; cb < kN; cb += 32) {
+        for (int c = 0; c < kN / kEh; c += 32) {
+          const int cb = cbeg + c;
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           ld16(rb, cb + 16);
           red16(ra, cb);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (cb + 32 < kN) {
+          if (c + 32 < kN / kEh) {
             ld16(ra, cb + 32);
           } else {
             tc_fence_before();
@@ -917,7 +934,18 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       float oa0, oa1, ob0, ob1;
       f2unpack(oa, oa0, oa1);
       f2unpack(ob, ob0, ob1);
-      const float o0 = oa0 + oa1, o1 = ob0 + ob1;
+      float o0 = oa0 + oa1, o1 = ob0 + ob1;
+      if (kEh == 2) {
+        // 2 x 128 float2 past the gather slots (the A-image region's unused tail)
+        float2* part = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(S.ah[0]) + kGSlots * kGSlotBytes) +
+                       (it & 1) * kM + q * 32 + lane;
+        if (eh == 1) *part = make_float2(o0, o1);
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+        if (eh == 1) continue;
+        const float2 pu = *part;
+        o0 += pu.x;
+        o1 += pu.y;
+      }
       if (e >= 0) {
         float2 r2 = make_float2(o0 + S.b2[0], o1 + S.b2[1]);
         if (cnt <= 0) r2 = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
