@@ -396,11 +396,13 @@ __global__ void __launch_bounds__(kRxWarps * 32) k_reduce_x(const int* __restric
 // up to the order of the atomics; the
 // runs are then put back into event (= time) order, which is exactly the
 // stable pixel-major order of np.argsort(kind="stable") (encoder.py:255-257):
-//   k_runsort   one thread per pixel, insertion sort of runs <= 32 events;
-//               longer runs go to a list
-//   k_longsort  one CTA per listed run: bitonic sort (ascending-only network,
-//               so the virtual +inf padding never moves) in shared memory for
-//               runs <= 4096, in global memory beyond (pathological hot pixels)
+//   k_runsort   one thread per pixel, insertion sort of runs <= 256 events;
+//               the block then sorts each of its longer runs with a bitonic
+//               network (ascending-only, so the virtual +inf padding never
+//               moves) in the staged slots, or in global memory when the
+//               block's range is not staged (pathological hot pixels).
+//               VKM_RUNSORT_LONG_INBLOCK=0 lists them for k_longsort instead
+//               (one CTA per run, a separate launch).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_scatter(const int32_t* __restrict__ pix, const uint64_t* __restrict__ val,
                                                  const int32_t* __restrict__ rank, int64_t n, int64_t P,
@@ -422,7 +424,42 @@ __global__ void __launch_bounds__(256) k_scatter(const int32_t* __restrict__ pix
 // insertion-sorts its run there by event index.  Runs too long for the stage
 // go to a list sorted by k_longsort.  ppb is chosen on the host from the mean
 // run length so the range usually fits (dense slices: 35 events per pixel).
+__device__ __forceinline__ void cas_slot(uint64_t& a, uint64_t& b) {
+  if (uint32_t(a) > uint32_t(b)) {
+    const uint64_t t = a;
+    a = b;
+    b = t;
+  }
+}
+
+// Ascending-only bitonic network over a[0, L) by the calling block (the
+// virtual padding to N = 2^k behaves as +inf and never moves): merge stage k
+// first compares i with its mirror in the 2k block, then half-cleaners.
+__device__ void block_bitonic(uint64_t* a, int L) {
+  int N = 1;
+  while (N < L) N <<= 1;
+  for (int k = 2; k <= N; k <<= 1) {
+    for (int i = threadIdx.x; i < N / 2; i += blockDim.x) {
+      const int lo = (i / (k / 2)) * k + (i % (k / 2));
+      const int hi = (i / (k / 2)) * k + k - 1 - (i % (k / 2));
+      if (hi < L) cas_slot(a[lo], a[hi]);
+    }
+    __syncthreads();
+    for (int j = k / 4; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < N / 2; i += blockDim.x) {
+        const int lo = (i / j) * 2 * j + (i % j), hi = lo + j;
+        if (hi < L) cas_slot(a[lo], a[hi]);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+#ifndef VKM_RUNSORT_LONG_INBLOCK   // 1: k_runsort sorts its long runs itself (no k_longsort launch)
+#define VKM_RUNSORT_LONG_INBLOCK 1
+#endif
 constexpr int kRunsortThreads = 128;
+constexpr int kLongCap = 32;           // long runs a block step sorts cooperatively (more: per thread)
 constexpr int kRunsortStage = 6144;    // most slots staged per block (48 KB)
 constexpr int kInsertRun = 256;        // longer runs: k_longsort (bitonic)
 constexpr int kSmemRun = 4096;         // k_longsort sorts runs up to this in shared memory
@@ -433,19 +470,29 @@ __global__ void __launch_bounds__(kRunsortThreads) k_runsort(const int* __restri
                                                              int* __restrict__ longcount) {
   pdl_wait();
   extern __shared__ uint64_t stage[];   // stage_cap slots
+  __shared__ int nlong, longp[kLongCap];
   for (int64_t p0 = int64_t(blockIdx.x) * ppb; p0 < P; p0 += int64_t(gridDim.x) * ppb) {
     const int64_t pe = min(P, p0 + int64_t(ppb));
     const int b0 = __ldg(start + p0), b1 = __ldg(start + pe);
     const bool staged = b1 - b0 <= stage_cap;
+    if (threadIdx.x == 0) nlong = 0;
     if (staged)
       for (int i = threadIdx.x; i < b1 - b0; i += blockDim.x) stage[i] = val_s[b0 + i];
     __syncthreads();
     for (int64_t p = p0 + threadIdx.x; p < pe; p += blockDim.x) {
       const int s = __ldg(start + p), L = __ldg(start + p + 1) - s;
       for (int j = 0; j < L; ++j) pix_s[s + j] = int32_t(p);   // slot -> pixel (K3's gather key)
+      int li = -1;
+#if VKM_RUNSORT_LONG_INBLOCK
+      if (L > kInsertRun) li = atomicAdd(&nlong, 1);
+      if (li >= 0 && li < kLongCap) {
+        longp[li] = int(p);   // sorted below by the whole block
+      } else if (L > 1) {     // (beyond kLongCap long runs per step: insertion sort, nearly sorted runs)
+#else
       if (L > kInsertRun) {
         longlist[atomicAdd(longcount, 1)] = int(p);
       } else if (L > 1) {
+#endif
         uint64_t* r = staged ? stage + (s - b0) : val_s + s;
         for (int i = 1; i < L; ++i) {   // by event index (low 32 bits), unique within a run
           const uint64_t v = r[i];
@@ -460,6 +507,14 @@ __global__ void __launch_bounds__(kRunsortThreads) k_runsort(const int* __restri
       }
     }
     __syncthreads();
+#if VKM_RUNSORT_LONG_INBLOCK
+    const int nl = min(nlong, kLongCap);
+    for (int li = 0; li < nl; ++li) {
+      const int p = longp[li];
+      const int s = __ldg(start + p), L = __ldg(start + p + 1) - s;
+      block_bitonic(staged ? stage + (s - b0) : val_s + s, L);
+    }
+#endif
     if (staged)
       for (int i = threadIdx.x; i < b1 - b0; i += blockDim.x) val_s[b0 + i] = stage[i];
     __syncthreads();
@@ -946,13 +1001,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const int* __restrict__ i
   pdl_trigger();
 }
 
-__device__ __forceinline__ void cas_slot(uint64_t& a, uint64_t& b) {
-  if (uint32_t(a) > uint32_t(b)) {
-    const uint64_t t = a;
-    a = b;
-    b = t;
-  }
-}
 
 __global__ void __launch_bounds__(512) k_longsort(const int* __restrict__ start, uint64_t* __restrict__ val_s,
                                                   const int* __restrict__ longlist,
@@ -1161,7 +1209,9 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
       dev_cached = dev;
     }
   }
+#if !VKM_RUNSORT_LONG_INBLOCK
   cudaMemsetAsync(sb.longcount, 0, sizeof(int), s);
+#endif
   // The counting scatter + run sort serves every density.  The row-bucket
   // path (VKM_SORT=rows, tested for exact order) measured slower at config 5
   // (rowhist 0.17 + rowscatter 1.11 + xsort 0.83 ms against scatter 0.98 +
@@ -1275,8 +1325,12 @@ int launch_sort_events(const double* ev, const uint2* packed, const SliceTab& st
     cudaFuncSetAttribute(k_runsort, cudaFuncAttributeMaxDynamicSharedMemorySize, kRunsortStage * 8);
     launch_pdl(k_runsort, pb, kRunsortThreads, size_t(cap) * 8, s, static_cast<const int*>(sb.start), P, ppb, cap,
                sb.val_s, sb.pix_s, sb.longlist, sb.longcount);
+#if VKM_RUNSORT_LONG_INBLOCK
+    launches += 2;
+#else
     launch_pdl(k_longsort, 148, 512, 0, s, sb.start, sb.val_s, sb.longlist, sb.longcount);
     launches += 3;
+#endif
   }
   return launches;
 }
