@@ -1,6 +1,6 @@
 """Subprocess body of test_gpu_parity.test_pixel_order_is_the_stable_argsort:
 K1's pixel-major event order vs np.argsort(kind="stable") (encoder.py:255-259)
-and the hottest pixel's flows vs the oracle.  Usage: python _order_check.py hot|dense"""
+and the hottest pixel's flows vs the oracle.  Usage: python _order_check.py hot|hotrow|dense"""
 import os
 import sys
 
@@ -25,6 +25,12 @@ def main(case):
         X = np.concatenate([X] + extra)
         X = X[np.argsort(X[:, 0], kind="stable")]
         xs, ys = 70, 10
+    elif case == "hotrow":   # 64 adjacent runs of 300 events: more long runs than one run-sort block step sorts together
+        X = vo.synth_uniform_noise(20000, W, H, seed=79)
+        extra = [np.stack([rng.uniform(0.0, 0.032, 300), np.full(300, x), np.full(300, 40)], 1) for x in range(16, 80)]
+        X = np.concatenate([X] + extra)
+        X = X[np.argsort(X[:, 0], kind="stable")]
+        xs, ys = 47, 40
     else:   # 35 events per pixel (the config-5 density), > 1M events
         W, H = 192, 160
         X = vo.synth_uniform_noise(35 * W * H, W, H, seed=78)

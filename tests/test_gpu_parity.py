@@ -375,15 +375,17 @@ def test_batched_slices_many_chunks_edge_cases():
 
 
 @pytest.mark.parametrize("sort", ["auto", "counting", "rows", "radix"])
-@pytest.mark.parametrize("case", ["hot", "dense"])
+@pytest.mark.parametrize("case", ["hot", "hotrow", "dense"])
 def test_pixel_order_is_the_stable_argsort(case, sort):
     """K1's event order equals accumulate_grid's np.argsort(flat,
     kind="stable") and bincount run starts (encoder.py:255-259) exactly, on
     both sort paths: the counting scatter + run ordering (k_prep arrival ranks
-    -> k_scan -> k_scatter -> k_runsort / k_longsort) and the dense slices'
-    row-bucket counting sort (k_rowhist -> k_scan -> k_rowscatter -> k_xsort).
-    "hot": runs of 1, 2..256, 257..4096 and > 4096 events; "dense": 35 events
-    per pixel (the config-5 density).  The sort switch (VKM_SORT) is read once
+    -> k_scan -> k_scatter -> k_runsort, long runs sorted in-block) and the
+    dense slices' sorts (radix; row-bucket k_rowhist -> k_scan -> k_rowscatter
+    -> k_xsort).  "hot": runs of 1, 2..256, 257..4096 and > 4096 events;
+    "hotrow": 64 adjacent 300-event runs (more long runs than k_runsort's
+    block step sorts together: the rest take the per-thread insertion sort);
+    "dense": 35 events per pixel (the config-5 density).  The sort switch (VKM_SORT) is read once
     per process, so each case runs in a fresh interpreter (tests/_order_check.py)."""
     import os, subprocess, sys
     env = dict(os.environ)
