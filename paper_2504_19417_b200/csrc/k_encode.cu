@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) k_features(const double* __restrict__ ev,
       const int pj = __shfl_sync(kFull, pix, src & 31);
       const int cj = __shfl_sync(kFull, cnt, src & 31);
       if (src >= nv) continue;
-      const float4 acc = __ldg(Q4 + ((int64_t(plane) * P + pj) << 2) + q4);
+      const float4 acc = __ldg(Q4 + ((int64_t(plane) * P + pj) << 2) + (q4 ^ qswz(pj)));
       float s0, k0, s1, k1;
       sincos2_f32(__fmul_rn(aj, T0), __fmul_rn(aj, T1), s0, k0, s1, k1);
       const float den = float(max(cj, 1));
@@ -257,7 +257,8 @@ __global__ void k_grid_to_ref(const float2* __restrict__ G, const int* __restric
   const int64_t pix = int64_t(y) * W + x;
   float2 v;
   if (packed) {
-    const float* f = reinterpret_cast<const float*>(G + (int64_t(c >> 3) * P + pix) * 8) + ((c & 7) >> 1) * 4 + (c & 1);
+    const float* f = reinterpret_cast<const float*>(G + (int64_t(c >> 3) * P + pix) * 8) +
+                     (((c & 7) >> 1) ^ qswz(pix)) * 4 + (c & 1);   // packed = the pooled grid Q
     v = make_float2(f[0], f[2]);
   } else {
     v = G[(int64_t(c >> 3) * P + pix) * 8 + (c & 7)];

@@ -389,10 +389,10 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       if (pix >= 0) {
         if (gp0 >= 0) {
           const uint32_t a = slot_base + uint32_t((((kLEPairs / 4) * jg + (u >> 2)) * kGSpan + (pix - gp0)) * 64 +
-                                                  (u & 3) * 16);
+                                                  ((u & 3) ^ qswz(pix)) * 16);
           asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
         } else {
-          const float4* src = Q4 + ((int64_t((kLEPairs / 4) * jg + (u >> 2)) * P + pix) << 2) + (u & 3);
+          const float4* src = Q4 + ((int64_t((kLEPairs / 4) * jg + (u >> 2)) * P + pix) << 2) + ((u & 3) ^ qswz(pix));
           asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                        : "l"(src));
         }
@@ -425,17 +425,18 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       const bool blk = gp0 >= 0;
       const uint32_t gbase =
           slot_base + uint32_t(((kLEPairs / 4) * jg * kGSpan + (pix_c > gp0 ? pix_c - gp0 : 0)) * 64);
+      const int gsw = qswz(pix_c > 0 ? pix_c : 0);   // chunk slot swizzle of this lane's pixel
       auto ld_half = [&](int half) {
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           const int u = 4 * half + h;
-          const uint32_t a = gbase + uint32_t((u >> 2) * kGSpan * 64 + (u & 3) * 16);
+          const uint32_t a = gbase + uint32_t((u >> 2) * kGSpan * 64 + ((u & 3) ^ gsw) * 16);
           asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
                        : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w) : "r"(a));
         }
       };
       auto ld_one = [&](int u) {
-        const uint32_t a = gbase + uint32_t((u >> 2) * kGSpan * 64 + (u & 3) * 16);
+        const uint32_t a = gbase + uint32_t((u >> 2) * kGSpan * 64 + ((u & 3) ^ gsw) * 16);
         asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
                      : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w) : "r"(a));
       };
@@ -641,14 +642,16 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
 #endif
 #ifdef VKM_K3_REGQ
       {
-        const float4* src = qlane + (int64_t(pj >= 0 ? pj : 0) << 2);
+        const int pjc = pj >= 0 ? pj : 0;
+        const float4* src = qlane + (int64_t(pjc) << 2) + ((q4 ^ qswz(pjc)) - q4);
         float4 v;
         asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(src));
         rq[slot] = pj >= 0 ? v : make_float4(0.f, 0.f, 0.f, 0.f);
         return;
       }
 #endif
-      const float4* src = qlane + (int64_t(pj >= 0 ? pj : 0) << 2);
+      const int pjc = pj >= 0 ? pj : 0;
+      const float4* src = qlane + (int64_t(pjc) << 2) + ((q4 ^ qswz(pjc)) - q4);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n\tcp.async.commit_group;" ::"r"(
                        ring_s + uint32_t(slot) * 512u),
                    "l"(src), "r"(pj >= 0 ? 16 : 0)

@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(256) k_box_y_demod(const float4* __restrict__ 
         const uint64_t oi = fsub2(fmul2(ai, fr), fmul2(ar, fi));
         // Q with evict_first: its 158 MB (cfg 2) must not push out the lead
         // rows of R kept for the trailing re-read (pool -7 % at cfg 3 and 4)
-        asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(Qp + int64_t(y) * rs),
+        const int c4 = idx & 3, cs = c4 ^ qswz(int64_t(slice) * H * W + int64_t(y) * W + (idx >> 2));
+        asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(Qp + int64_t(y) * rs + (cs - c4)),
                      "l"(orr), "l"(oi), "l"(drop)
                      : "memory");
         ar = fsub2(ar, tv[u].x);
@@ -164,8 +165,7 @@ __global__ void __launch_bounds__(256) k_box_x(const float2* __restrict__ R, flo
   const int x0 = blockIdx.x * CS, x1 = min(W, x0 + CS);
   const int c = plane * 8 + ch;
   const float2* Rr = R + int64_t(plane) * P * 8 + int64_t(y) * W * 8 + ch;
-  float2* Qr = Q + int64_t(plane) * P * 8 + int64_t(y) * W * 8 + (ch >> 1) * 2;   // + (ch & 1) floats below
-  Qr = reinterpret_cast<float2*>(reinterpret_cast<float*>(Qr) + (ch & 1));
+  float2* Qr = Q + int64_t(plane) * P * 8 + int64_t(y) * W * 8;   // pixel x: chunk (ch >> 1) ^ qswz, + (ch & 1) floats
   float2 dmy = __ldg(my + int64_t(y) * D8 + c);
   dmy.y = -dmy.y;
   const float2 zero = make_float2(0.f, 0.f);
@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(256) k_box_x(const float2* __restrict__ R, flo
       if (x + u >= x1) break;
       acc = cadd(acc, ld[u]);
       const float2 o = cmulc(cmul(acc, dmy), m[u]);   // · conj(e^{iyY}) · conj(e^{ixX})
-      float* qo = reinterpret_cast<float*>(Qr + int64_t(x + u) * 8);   // packed pairs: re at +0, im at +2
+      const int64_t px = int64_t(y) * W + x + u;
+      float* qo = reinterpret_cast<float*>(Qr + int64_t(x + u) * 8 + ((ch >> 1) ^ qswz(px)) * 2) + (ch & 1);   // re +0, im +2
       qo[0] = o.x;
       qo[2] = o.y;
       acc = csub(acc, tr[u]);

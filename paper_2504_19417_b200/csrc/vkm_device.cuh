@@ -299,6 +299,20 @@ __device__ __forceinline__ float time_arg(double t, double t0, double delta_t) {
   return __double2float_rn((t - t0) / delta_t);
 }
 
+// Pooled-grid (Q) layout: per channel plane, 64 bytes per pixel = four
+// 16-byte chunks (channel pairs).  Chunk c of pixel p is stored in slot
+// c ^ qswz(p), so lanes reading the same chunk of consecutive pixels (K3's
+// gathers of a pixel-sorted tile) hit eight distinct 16-byte bank groups
+// instead of two.  Every writer (y pass, split x pass) and reader (K3, the
+// encoder features, the grid export) goes through qswz.  Measured (v29,
+// profiles/r02/q_swizzle_ab_v29.txt): correct, but K3 15 % slower at cfg 2
+// (run-time chunk offsets: more registers, spills) and the y pass +3 %, so
+// the linear layout (0) is the default; qswz then folds to 0.
+#ifndef VKM_Q_SWZ
+#define VKM_Q_SWZ 0
+#endif
+__host__ __device__ __forceinline__ int qswz(int64_t p) { return VKM_Q_SWZ ? int((p >> 1) & 3) : 0; }
+
 // Complex product with explicit rounding (no FMA contraction): numpy's
 // complex64 multiply order (encoder.py:334, 345).
 __device__ __forceinline__ float2 cmul_rn(float2 a, float2 b) {
