@@ -478,8 +478,8 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
       for (int half = 0; half < kLEPairs / 4; ++half) {   // pairs 4·half .. 4·half+3 -> 8 columns per image
         uint32_t hw[8], lw[8];
 #if !defined(VKM_K3_LATE) && !defined(VKM_K3_GATHER_PER_PAIR) && VKM_K3_LDSPLIT && !VKM_K3_LDAHEAD
-        if (half > 0 && blk) ld_half(half);   // the second half's rows load under the first half's math
-        if (half == kLEPairs / 4 - 1) {
+        if (VKM_K3_LDSPLIT == 1 && half > 0 && blk) ld_half(half);   // the second half's rows load under the first half's math
+        if (VKM_K3_LDSPLIT == 1 && half == kLEPairs / 4 - 1) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&S.gempty[gslot]);   // reads issued (release orders them before the TMA refill)
           if (++gslot == kGSlots) {
@@ -539,6 +539,17 @@ __global__ void __launch_bounds__(Roles<kLaneEvent>::threads, 1)
             hw[2 * h + 1] = *reinterpret_cast<const uint32_t*>(&bim);
           }
         }
+#if !defined(VKM_K3_LATE) && !defined(VKM_K3_GATHER_PER_PAIR) && VKM_K3_LDSPLIT == 2 && !VKM_K3_LDAHEAD
+        if (half == 0) {   // the second half's rows load before the stage wait (in flight across it)
+          if (blk) ld_half(1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.gempty[gslot]);
+          if (++gslot == kGSlots) {
+            gslot = 0;
+            gph ^= 1;
+          }
+        }
+#endif
         if (half == 0) {   // the stage is needed only from the first store on
           K3_TIMED_WAIT(1, mbar_wait(&S.empty[kS], ph ^ 1));
           tc_fence_after();
