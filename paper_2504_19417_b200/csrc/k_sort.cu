@@ -458,7 +458,10 @@ __device__ void block_bitonic(uint64_t* a, int L) {
 #ifndef VKM_RUNSORT_LONG_INBLOCK   // 1: k_runsort sorts its long runs itself (no k_longsort launch)
 #define VKM_RUNSORT_LONG_INBLOCK 1
 #endif
-constexpr int kRunsortThreads = 128;
+#ifndef VKM_RUNSORT_THREADS
+#define VKM_RUNSORT_THREADS 128
+#endif
+constexpr int kRunsortThreads = VKM_RUNSORT_THREADS;
 constexpr int kLongCap = 32;           // long runs a block step sorts cooperatively (more: per thread)
 constexpr int kRunsortStage = 6144;    // most slots staged per block (48 KB)
 constexpr int kInsertRun = 256;        // longer runs: k_longsort (bitonic)
@@ -931,7 +934,10 @@ size_t radix_smem_bytes() { return size_t(kRsTile) * 24 + size_t(2 * kRsWarps + 
 // taken in increasing order by a grid no larger than what is co-resident, so
 // every predecessor a tile waits on is being processed.
 // ---------------------------------------------------------------------------
-constexpr int kScanThreads = 256, kScanItems = 16, kScanTile = kScanThreads * kScanItems;
+#ifndef VKM_SCAN_ITEMS
+#define VKM_SCAN_ITEMS 16
+#endif
+constexpr int kScanThreads = 256, kScanItems = VKM_SCAN_ITEMS, kScanTile = kScanThreads * kScanItems;
 __global__ void __launch_bounds__(kScanThreads) k_scan(const int* __restrict__ in, int* __restrict__ out, int64_t m,
                                                        int ntiles, unsigned long long* __restrict__ state,
                                                        uint32_t epoch) {
