@@ -130,7 +130,8 @@ constexpr int kGSpan = kGSlots == 3 ? 96 : 80;    // pixels per plane a slot hol
 constexpr int kGSlotBytes = 8 * kGSpan * 64;      // 48 KB (40 KB for 4 slots)
 static_assert(kGSlots * kGSlotBytes <= int(2 * kStages * kTileBytes + sizeof(float4) * kProdWarps * kQD * 32),
               "gather slots exceed the A images + ring");
-static_assert(kGSlots * kGSlotBytes + 2 * kM * 8 <= int(2 * kStages * kTileBytes + sizeof(float4) * kProdWarps * kQD * 32),
+static_assert(kEpiLE == 4 ||
+                  kGSlots * kGSlotBytes + 2 * kM * 8 <= int(2 * kStages * kTileBytes + sizeof(float4) * kProdWarps * kQD * 32),
               "gather slots + epilogue hand-over exceed the A images + ring");
 
 static_assert(sizeof(Smem) + 1024 <= 232448, "K3 shared memory exceeds the 227 KB opt-in limit");
